@@ -1,0 +1,21 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (CUDA) — run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running CPU oracle pin")
+
+
+@pytest.fixture(scope="session")
+def orc():
+    from oracle import fus_oracle
+
+    fus_oracle.build()
+    return fus_oracle
