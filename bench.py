@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: volume-potential apply throughput (grid points/s, complex128) on B200.
+
+Workload (BASELINE.json configs[1], "cfg2"): one GreenKernel::apply on a 256^3 grid with a
+512^3 circulant embedding, k = 2k_1 at f = 1.1 MHz, c = 1540 m/s, h = lambda_2/6; the source
+is a seeded iid complex U[-1,1] field (libstdc++ mt19937, tests/acceptance.cpp:30-36) times a
+Gaussian envelope of std 0.2 x box width centred in the box.  A "step" is one apply with the
+kernel spectrum cached (include/fus/potential.hpp:25-27); the spectrum build is reported
+separately.  Inputs and workspaces (0.27 + 1.6 GB) exceed the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W]       # this framework (libfusg.so)
+  python bench.py --impl reference ...                   # the CPU reference path (oracle port)
+
+N > 1 (torchrun): every rank applies its own independent cfg2 volume potential (independent
+harmonics/sources: weak scaling, no data-path collective); time = max over ranks.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "volume-potential grid pts/s (c128)"
+UNIT = "grid_pts/s"
+WORKLOAD = ("cfg2: single volume-potential apply, 256^3 grid, 512^3 circulant embedding, complex128, "
+            "k2=2k at f=1.1MHz c=1540, h=lambda2/6, iid U[-1,1] (mt19937 seed 2024) x Gaussian "
+            "envelope sigma=0.2*box")
+N_SIDE = 256
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cfg2_inputs():
+    from paper_2011_03009_b200 import fus
+
+    c, f0 = 1540.0, 1.1e6
+    h = (c / (2 * f0)) / 6.0
+    g = fus.make_grid([0, 0, 0], [N_SIDE * h] * 3, h, 2)
+    k = fus.Wavenumber(complex(2 * 2 * math.pi * f0 / c, 0.0), 2, 2 * math.pi * f0)
+    f = fus.random_vector(g.count(), 2024).reshape(g.dims[2], g.dims[1], g.dims[0])
+    cen = 0.5 * (g.lo + g.hi)
+    sig = 0.2 * (g.hi[0] - g.lo[0])
+    ax = [g.lo[a] + (np.arange(g.dims[a]) + 0.5) * g.dx - cen[a] for a in range(3)]
+    r2 = (ax[0] ** 2)[None, None, :] + (ax[1] ** 2)[None, :, None] + (ax[2] ** 2)[:, None, None]
+    f = (f * np.exp(-r2 / (2 * sig * sig))).reshape(-1)
+    return g, k, f
+
+
+def algorithmic_bytes(N, P):
+    """pruned fused 5-pass pipeline, 16 B per complex128 element."""
+    Nx, Ny, Nz = N
+    Px, Py, Pz = P
+    n = Nx * Ny * Nz
+    k_oct = (Px // 2 + 1) * (Py // 2 + 1) * (Pz // 2 + 1)
+    per_pass = {
+        "A_fwd_x": 16 * (n + Px * Ny * Nz),
+        "B_fwd_y": 16 * (Px * Ny * Nz + Px * Py * Nz),
+        "C_fwd_z_mul_inv_z": 16 * (2 * Px * Py * Nz + k_oct),
+        "D_inv_y": 16 * (Px * Py * Nz + Px * Ny * Nz),
+        "E_inv_x_crop": 16 * (Px * Ny * Nz + n),
+    }
+    return per_pass, sum(per_pass.values())
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world, local):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = f"cuda:{local}" if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------- CPU reference arm
+def cpu_apply_seconds(g, k, f, workers, max_steps, warmup, budget_s):
+    """Oracle port of GreenKernel::apply (src/potential.cpp:120-151) on the host: pocketfft
+    on exactly the reference's 2N box. Returns (seconds/apply, steps run)."""
+    from oracle import fus_oracle as orc
+
+    orc.build()
+    go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 2)
+    K = orc.GreenKernel(go, orc.Wavenumber(k.k, 2, k.omega), workers=workers)
+    for _ in range(warmup):
+        K.apply(f)
+    times = []
+    t_all = time.perf_counter()
+    while len(times) < max_steps:
+        t0 = time.perf_counter()
+        K.apply(f)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all > budget_s:
+            break
+    return statistics.mean(times), len(times)
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return 0
+    g, k, f = cfg2_inputs()
+    cores = os.cpu_count() or 1
+    orc_lib = None
+    try:
+        from oracle import fus_oracle as orc
+        orc_lib = orc.lib()
+        orc_lib.orc_set_num_threads(cores)
+    except Exception:
+        pass
+    sec, steps = cpu_apply_seconds(g, k, f, cores, args.steps, min(args.warmup, 1), 150.0)
+    v = g.count() / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid": [N_SIDE] * 3, "padded": [2 * N_SIDE] * 3,
+                   "parallelism": "host cores"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{steps} full cfg2 applies (oracle/fus_oracle: pocketfft on the "
+                                   f"reference's 2N box, {cores} FFT workers; spectrum prebuilt)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------- GPU arm
+def run_gpu(args, world, rank, local):
+    import torch
+
+    from paper_2011_03009_b200 import _lib, fus
+
+    torch.cuda.set_device(local)
+    ctx = fus.context(local)
+    g, k, f = cfg2_inputs()
+    N = g.count()
+    t0 = time.perf_counter()
+    K = fus.GreenKernel(g, k, ctx=ctx)
+    build_s = time.perf_counter() - t0
+    P = K.padded
+    fd = torch.from_numpy(f).to(f"cuda:{local}")
+    ud = torch.empty_like(fd)
+    torch.cuda.synchronize()
+    L = _lib.lib()
+    stream = ctx.stream_ptr
+
+    def step():
+        _lib.check(L.fusg_kernel_apply(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, None))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    ctx.synchronize()
+
+    # ---- timed region: K back-to-back applies on the library stream, CUDA events
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cs = torch.cuda.ExternalStream(stream)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier(world)
+    ctx.synchronize()
+    launches0 = ctx.launch_count()
+    ev0.record(cs)
+    for _ in range(args.steps):
+        step()
+    ev1.record(cs)
+    ev1.synchronize()
+    launches = ctx.launch_count() - launches0
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    barrier(world)
+    clocks = sampler.stop()
+    ms = max_over_ranks(ms_local, world, local)
+    value = world * N / (ms * 1e-3)
+
+    # ---- per-pass durations (CUDA events between the passes, same stream)
+    pass_ms = (__import__("ctypes").c_double * 5)()
+    _lib.check(L.fusg_kernel_apply_timed(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, 20, pass_ms))
+    pass_ms = list(pass_ms)
+    per_pass, total_bytes = algorithmic_bytes(g.dims, P)
+    names = list(per_pass)
+    dom = int(np.argmax(pass_ms))
+    hbm, hbm_kind = peaks()
+    dom_gbs = per_pass[names[dom]] / (pass_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(names[dom])
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the C-ABI host-vector call (pinned host buffers, H2D+D2H inside)
+    fh = torch.from_numpy(f).pin_memory()
+    uh = torch.empty_like(fh).pin_memory()
+    for _ in range(2):
+        _lib.check(L.fusg_kernel_apply_host(K.handle, fh.data_ptr(), uh.data_ptr(), 1.0))
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        _lib.check(L.fusg_kernel_apply_host(K.handle, fh.data_ptr(), uh.data_ptr(), 1.0))
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, local)
+
+    # parity spot check of the timed output against the host path (same kernels)
+    ctx.synchronize()
+    assert torch.equal(ud.cpu(), uh), "device and host-vector applies disagree"
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        try:
+            from oracle import fus_oracle as orc
+            orc.lib().orc_set_num_threads(cores)
+            sec, nst = cpu_apply_seconds(g, k, f, cores, 3, 0, 20.0)
+            cpu_baseline = {"value": N / sec, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": f"{nst} full cfg2 apply(s) by oracle/fus_oracle (pocketfft on the "
+                                      f"reference's 2N box, {cores} FFT workers; spectrum prebuilt)"}
+        except Exception as e:  # reported, never silently replaced
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "grid": list(g.dims), "padded": list(P),
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs+workspace (1.9 GB) > 126 MB L2; no flush"},
+            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": dom_gbs, "peak": hbm,
+                         "peak_kind": hbm_kind, "unit": "GB/s", "frac": dom_gbs / hbm,
+                         "traffic": traffic,
+                         "algorithmic_bytes_per_launch": per_pass[names[dom]]},
+            "apply_roofline": {"algorithmic_bytes": total_bytes,
+                               "achieved_gbs": total_bytes / (ms * 1e-3) / 1e9,
+                               "frac": total_bytes / (ms * 1e-3) / 1e9 / hbm},
+            "passes_ms": dict(zip(names, pass_ms)),
+            "kernel_build_s": build_s,
+            "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
+                    "d2h_bytes_per_step": 16 * N},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fusg", choices=["fusg", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            return run_reference(args, world, rank)
+        return run_gpu(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

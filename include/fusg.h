@@ -1,0 +1,190 @@
+/* fusg.h — C-ABI of the B200-native volume-potential harmonic solver (arXiv 2011.03009).
+ *
+ * Drop-in boundary for the reference's hot path (the public headers under
+ * /root/reference/proj/include/fus/).
+ * Plain C types only: fields are interleaved complex128 (re, im) arrays, x fastest,
+ * index = ix + Nx*(iy + Ny*iz) (include/fus/grid.hpp:41-43).  Functions whose pointer
+ * arguments are named *_dev take device pointers (CUDA global memory); *_host take host
+ * pointers.  Every function returns fusg_status; exceptions never cross this boundary and
+ * fusg_last_error() returns the thread-local message of the last failure.  Error classes
+ * mirror the reference's exception types (std::invalid_argument, std::out_of_range,
+ * std::runtime_error).
+ *
+ * Each entry cites the reference interface it replaces.
+ */
+#ifndef FUSG_H_
+#define FUSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fusg_status {
+  FUSG_OK = 0,
+  FUSG_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  FUSG_OUT_OF_RANGE = 2,     /* std::out_of_range     */
+  FUSG_RUNTIME = 3,          /* std::runtime_error    */
+  FUSG_CUDA = 4,             /* CUDA runtime failure  */
+  FUSG_NCCL = 5,             /* NCCL failure          */
+  FUSG_OOM = 6               /* device allocation     */
+} fusg_status;
+
+/* VoxelGrid (include/fus/grid.hpp:30-50): covered box, spacing, voxel counts, harmonic. */
+typedef struct fusg_grid {
+  double lo[3];
+  double hi[3];
+  double dx;
+  int32_t dims[3];
+  int32_t harmonic;
+} fusg_grid;
+
+/* Wavenumber (include/fus/medium.hpp:26-30). */
+typedef struct fusg_wavenumber {
+  double k_re, k_im;
+  int32_t harmonic;
+  double omega;
+} fusg_wavenumber;
+
+/* Medium (include/fus/medium.hpp:12-23), name omitted. */
+typedef struct fusg_medium {
+  double rho0, c0, beta, alpha0, eta;
+} fusg_medium;
+
+/* BowlTransducer (include/fus/transducer.hpp:15-28); points_host is n_points x 3. */
+typedef struct fusg_bowl {
+  double f0, focal_length, outer_radius, power;
+  int32_t n_points;
+  const double* points_host;
+} fusg_bowl;
+
+/* StageTiming (include/fus/cascade.hpp:25-32) plus the stages the reference leaves
+ * untimed (p1 evaluation, rhs assembly); seconds, measured with CUDA events. */
+typedef struct fusg_stage_timing {
+  int32_t harmonic;
+  uint64_t voxels;
+  double meshing_s, interpolation_s, kernel_s, potential_s;
+  double p1_s, rhs_s;
+} fusg_stage_timing;
+
+typedef struct fusg_ctx fusg_ctx;       /* one CUDA device + stream + workspace */
+typedef struct fusg_kernel fusg_kernel; /* GreenKernel: cached octant spectrum */
+
+const char* fusg_last_error(void);
+const char* fusg_version(void);
+
+/* ---------------------------------------------------------------- host arithmetic
+ * Bit-exact restatements (compiled without FMA contraction, like the reference). */
+
+/* make_grid (src/grid.cpp:12-34); anchor_or_null may be NULL. */
+fusg_status fusg_make_grid(const double req_lo[3], const double req_hi[3], double dx,
+                           int32_t harmonic, const double* anchor_or_null, fusg_grid* out);
+/* complex_wavenumber (src/medium.cpp:31-45). */
+fusg_status fusg_complex_wavenumber(const fusg_medium* m, double f0, int32_t n,
+                                    fusg_wavenumber* out);
+/* self_weight / equivalent_sphere_radius (src/potential.cpp:55-70). */
+fusg_status fusg_self_weight(const fusg_wavenumber* k, double dx, double out[2]);
+double fusg_equivalent_sphere_radius(double dx);
+/* next_fast_size (src/potential.cpp:36-43) and the padded box the device path uses. */
+int32_t fusg_next_fast_size(int32_t n);
+fusg_status fusg_padded_dims(const fusg_grid* g, int32_t pad_small_primes, int32_t out[3]);
+/* distribute_points (src/transducer.cpp:22-70): out_host is n_points x 3. */
+fusg_status fusg_distribute_points(double focal_length, double outer_radius, int32_t n_points,
+                                   double* out_host);
+/* plan_nested_meshes (src/grid.cpp:81-112) / plan_single_mesh (src/cascade.cpp:109-118).
+ * out_grids[i] is the grid of harmonic i+2 (n_harmonics-1 entries); domains_lo/hi are the
+ * planned domains D_i (3 doubles each); reference receives the fine reference mesh. */
+fusg_status fusg_plan_nested_meshes(const fusg_bowl* t, const fusg_medium* m, double d,
+                                    int32_t n_w, int32_t n_harmonics, double width_scale,
+                                    int32_t single_mesh, fusg_grid* out_grids,
+                                    double* domains_lo, double* domains_hi,
+                                    fusg_grid* reference, double* w_out);
+/* rhs coefficient beta omega^2 n^2 / (2 rho0 c0^4) (src/cascade.cpp:32-34). */
+double fusg_rhs_coefficient(const fusg_medium* m, double omega, int32_t n);
+/* Seeded test input (tests/acceptance.cpp:30-36): std::mt19937 + U(-1,1), re then im. */
+fusg_status fusg_random_vector(int64_t n, uint32_t seed, double* out_host);
+
+/* ---------------------------------------------------------------- device context */
+fusg_status fusg_ctx_create(int32_t device, fusg_ctx** out);
+fusg_status fusg_ctx_destroy(fusg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t); NULL stream arguments below mean this one. */
+void* fusg_ctx_stream(fusg_ctx* ctx);
+fusg_status fusg_ctx_synchronize(fusg_ctx* ctx);
+/* Number of kernels of this library launched on the context so far. */
+uint64_t fusg_ctx_launch_count(fusg_ctx* ctx);
+
+/* ---------------------------------------------------------------- volume potential
+ * GreenKernel (include/fus/potential.hpp:28-48, src/potential.cpp:72-159). */
+
+/* GreenKernel::GreenKernel (src/potential.cpp:72-118): builds the octant spectrum on the
+ * device. The padded box is the smallest {2,3,5,7}-smooth size >= 2N-1 per axis (or
+ * next_fast_size(2N) with pad_small_primes): the same discrete operator (offset_of,
+ * src/potential.cpp:88-94) as the reference's 2N box. */
+fusg_status fusg_kernel_create(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenumber* k,
+                               int32_t pad_small_primes, fusg_kernel** out);
+fusg_status fusg_kernel_destroy(fusg_kernel* kernel);
+fusg_status fusg_kernel_padded(const fusg_kernel* kernel, int32_t out[3]);
+/* Device bytes held by the kernel (spectrum + apply workspace). */
+uint64_t fusg_kernel_device_bytes(const fusg_kernel* kernel);
+/* GreenKernel::apply (src/potential.cpp:120-151) times `scale` (1 for apply, -1 for the
+ * cascade's p_n = -apply(f_n), src/cascade.cpp:100). f_dev/u_dev: N complex128 on device;
+ * u_dev must not alias f_dev. stream may be NULL (context stream). Asynchronous. */
+fusg_status fusg_kernel_apply(fusg_kernel* kernel, const double* f_dev, double* u_dev,
+                              double scale, void* stream);
+/* Measurement hook: `reps` back-to-back applies on the context stream with CUDA events
+ * between the five passes (A: fwd x, B: fwd y, C: fwd z * K^ inv z, D: inv y, E: inv x);
+ * pass_ms receives the mean duration of each pass. */
+fusg_status fusg_kernel_apply_timed(fusg_kernel* kernel, const double* f_dev, double* u_dev,
+                                    double scale, int32_t reps, double pass_ms[5]);
+/* Host-vector drop-in for GreenKernel::apply(const VectorXcd&): host->device copy, apply,
+ * device->host copy, synchronous. */
+fusg_status fusg_kernel_apply_host(fusg_kernel* kernel, const double* f_host, double* u_host,
+                                   double scale);
+
+/* ---------------------------------------------------------------- incident field
+ * Equal-area monopole (Rayleigh-type) sum amp * sum_i e^{ikd}/(4 pi d)
+ * (src/transducer.cpp:107-132,179-196). Fails with FUSG_INVALID_ARGUMENT when an
+ * evaluation point coincides with a source (d < 1e-12, :112-113). */
+fusg_status fusg_monopole_grid(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                               const fusg_grid* grid, double k_re, double k_im, double amp,
+                               double* out_dev, void* stream);
+fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                                 const double* pts_dev, int64_t n_pts, double k_re, double k_im,
+                                 double amp, double* out_dev, void* stream);
+/* radiated_power (src/transducer.cpp:134-155): deterministic fixed-order reduction. */
+fusg_status fusg_radiated_power(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                                double x_disc, double R, double k_re, double k_im, double amp,
+                                double rho0, double c0, int32_t n_r, int32_t n_theta,
+                                double* out_host);
+
+/* ---------------------------------------------------------------- source / transfer */
+/* rhs_source (src/cascade.cpp:21-40): out = coeff * sum_{m=1}^{n-1} p_m p_{n-m};
+ * lower_dev holds n-1 device pointers (p_1 .. p_{n-1}), each `count` complex128. */
+fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower_dev,
+                            int64_t count, const fusg_medium* m, double omega, double* out_dev,
+                            void* stream);
+/* interpolate (src/grid.cpp:141-195): trilinear transfer onto target voxel centres. */
+fusg_status fusg_interpolate(fusg_ctx* ctx, const fusg_grid* src, const double* f_dev,
+                             const fusg_grid* target, double* out_dev, void* stream);
+
+/* ---------------------------------------------------------------- recursion
+ * run_cascade (src/cascade.cpp:42-107), device resident. grids[i] is the planned grid of
+ * harmonic i+2; out_dev[n] receives p_{n+1} (p_1 lives on grids[0]) and must hold
+ * grids[max(n-1,0)].count complex128. timings has n_harmonics-1 rows (harmonics 2..n). */
+typedef struct fusg_cascade_desc {
+  fusg_medium medium;
+  fusg_bowl transducer;
+  const fusg_grid* grids;
+  int32_t n_harmonics;
+  int32_t recompute_p1_each_grid;
+  int32_t pad_small_primes;
+} fusg_cascade_desc;
+fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* desc, double* const* out_dev,
+                             fusg_stage_timing* timings, double* source_normalization);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FUSG_H_ */

@@ -1,0 +1,344 @@
+// C-ABI entry points for the device context, the GreenKernel (volume potential) and the
+// device-resident harmonic recursion (run_cascade, src/cascade.cpp:42-107).
+#include <chrono>
+#include <cstring>
+#include <iostream>
+#include <memory>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace fusg {
+fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s);
+fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
+                          double kre, double kim, double amp, double2* out, cudaStream_t s);
+fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
+                            const fusg_grid& tgt, double2* out, cudaStream_t s);
+fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
+                    double2* out, cudaStream_t s);
+fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s);
+fusg_status radiated_power_dev(fusg_ctx* ctx, const double* src_dev, int n_src, double x_disc,
+                               double R, double kre, double kim, double amp, double rho0, double c0,
+                               int n_r, int n_theta, double* out_host, cudaStream_t s);
+fusg_status check_monopole_flag(fusg_ctx* ctx, cudaStream_t s);
+}  // namespace fusg
+
+using namespace fusg;
+
+namespace {
+
+int64_t count_of(const fusg_grid& g) { return int64_t(g.dims[0]) * g.dims[1] * g.dims[2]; }
+
+bool same_grid(const fusg_grid& a, const fusg_grid& b) {  // src/cascade.cpp:15-17
+  return a.dims[0] == b.dims[0] && a.dims[1] == b.dims[1] && a.dims[2] == b.dims[2] &&
+         a.dx == b.dx && a.lo[0] == b.lo[0] && a.lo[1] == b.lo[1] && a.lo[2] == b.lo[2];
+}
+
+void free_kernel(fusg_kernel* K) {
+  if (!K) return;
+  cudaSetDevice(K->ctx->device);
+  cudaFree(K->bufA);
+  cudaFree(K->bufB);
+  cudaFree(K->koct);
+  for (auto* t : K->tw) cudaFree(t);
+  delete K;
+}
+
+// CUDA-event stopwatch on a stream
+struct EvTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit EvTimer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EvTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void start() { cudaEventRecord(a, s); }
+  double stop() {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e-3;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+fusg_status fusg_ctx_create(int32_t device, fusg_ctx** out) {
+  if (!out) return set_error(FUSG_INVALID_ARGUMENT, "ctx_create: null out");
+  int n = 0;
+  FUSG_CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return set_error(FUSG_INVALID_ARGUMENT, "ctx_create: no such device");
+  FUSG_CUDA_TRY(cudaSetDevice(device));
+  auto ctx = std::make_unique<fusg_ctx>();
+  ctx->device = device;
+  FUSG_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  FUSG_CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  FUSG_CUDA_TRY(cudaMalloc(&ctx->dev_flag, sizeof(int)));
+  FUSG_CUDA_TRY(cudaMemset(ctx->dev_flag, 0, sizeof(int)));
+  *out = ctx.release();
+  return FUSG_OK;
+}
+
+fusg_status fusg_ctx_destroy(fusg_ctx* ctx) {
+  if (!ctx) return FUSG_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->dev_flag);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return FUSG_OK;
+}
+
+void* fusg_ctx_stream(fusg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+fusg_status fusg_ctx_synchronize(fusg_ctx* ctx) {
+  if (!ctx) return set_error(FUSG_INVALID_ARGUMENT, "ctx_synchronize: null ctx");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return FUSG_OK;
+}
+
+uint64_t fusg_ctx_launch_count(fusg_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+// GreenKernel::GreenKernel (src/potential.cpp:72-118)
+fusg_status fusg_kernel_create(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenumber* k,
+                               int32_t pad_small_primes, fusg_kernel** out) {
+  if (!ctx || !grid || !k || !out) return set_error(FUSG_INVALID_ARGUMENT, "kernel_create: null argument");
+  for (int a = 0; a < 3; ++a)
+    if (grid->dims[a] < 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_create: empty grid");
+  if (grid->dx <= 0.0) return set_error(FUSG_INVALID_ARGUMENT, "self_weight: delta_x must be positive");
+  (void)pad_small_primes;  // any smooth P >= 2N-1 is the same operator; see fusg_padded_dims
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  double w0[2];
+  fusg_status st = fusg_self_weight(k, grid->dx, w0);
+  if (st != FUSG_OK) return st;
+  auto* K = new fusg_kernel;
+  K->ctx = ctx;
+  K->grid = *grid;
+  K->k = *k;
+  st = volume_potential_build(K, make_double2(w0[0], w0[1]));
+  if (st != FUSG_OK) {
+    free_kernel(K);
+    return st;
+  }
+  *out = K;
+  return FUSG_OK;
+}
+
+fusg_status fusg_kernel_destroy(fusg_kernel* K) {
+  free_kernel(K);
+  return FUSG_OK;
+}
+
+fusg_status fusg_kernel_padded(const fusg_kernel* K, int32_t out[3]) {
+  if (!K) return set_error(FUSG_INVALID_ARGUMENT, "kernel_padded: null kernel");
+  for (int a = 0; a < 3; ++a) out[a] = K->P[a];
+  return FUSG_OK;
+}
+
+uint64_t fusg_kernel_device_bytes(const fusg_kernel* K) { return K ? K->bytes : 0; }
+
+// GreenKernel::apply (src/potential.cpp:120-151)
+fusg_status fusg_kernel_apply(fusg_kernel* K, const double* f_dev, double* u_dev, double scale,
+                              void* stream) {
+  if (!K || !f_dev || !u_dev) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: null argument");
+  if (static_cast<const void*>(f_dev) == static_cast<const void*>(u_dev))
+    return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: output aliases input");
+  FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
+  std::lock_guard<std::mutex> lock(K->mu);
+  return volume_potential_apply(K, reinterpret_cast<const double2*>(f_dev),
+                                reinterpret_cast<double2*>(u_dev), scale, K->ctx->pick(stream));
+}
+
+fusg_status fusg_kernel_apply_timed(fusg_kernel* K, const double* f_dev, double* u_dev,
+                                    double scale, int32_t reps, double pass_ms[5]) {
+  if (!K || !f_dev || !u_dev || !pass_ms || reps < 1)
+    return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_timed: bad argument");
+  FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
+  std::lock_guard<std::mutex> lock(K->mu);
+  cudaStream_t s = K->ctx->stream;
+  std::vector<cudaEvent_t> ev(6 * size_t(reps));
+  for (auto& e : ev) FUSG_CUDA_TRY(cudaEventCreate(&e));
+  fusg_status st = FUSG_OK;
+  for (int r = 0; r < reps && st == FUSG_OK; ++r)
+    st = volume_potential_apply(K, reinterpret_cast<const double2*>(f_dev),
+                                reinterpret_cast<double2*>(u_dev), scale, s, &ev[6 * size_t(r)]);
+  if (st == FUSG_OK) {
+    FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+    for (int p = 0; p < 5; ++p) {
+      double acc = 0.0;
+      for (int r = 0; r < reps; ++r) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[6 * size_t(r) + p], ev[6 * size_t(r) + p + 1]);
+        acc += ms;
+      }
+      pass_ms[p] = acc / reps;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return st;
+}
+
+fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double* u_host,
+                                   double scale) {
+  if (!K || !f_host || !u_host) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
+  const size_t bytes = size_t(count_of(K->grid)) * 16;
+  cudaStream_t s = K->ctx->stream;
+  double *f = nullptr, *u = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&f, bytes, s));
+  FUSG_CUDA_TRY(cudaMallocAsync(&u, bytes, s));
+  FUSG_CUDA_TRY(cudaMemcpyAsync(f, f_host, bytes, cudaMemcpyHostToDevice, s));
+  fusg_status st;
+  {
+    std::lock_guard<std::mutex> lock(K->mu);
+    st = volume_potential_apply(K, reinterpret_cast<const double2*>(f), reinterpret_cast<double2*>(u),
+                                scale, s);
+  }
+  if (st == FUSG_OK) FUSG_CUDA_TRY(cudaMemcpyAsync(u_host, u, bytes, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(f, s);
+  cudaFreeAsync(u, s);
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return st;
+}
+
+// run_cascade (src/cascade.cpp:42-107), device resident.
+fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* const* out_dev,
+                             fusg_stage_timing* timings, double* source_normalization) {
+  if (!ctx || !d || !out_dev) return set_error(FUSG_INVALID_ARGUMENT, "run_cascade: null argument");
+  const int n = d->n_harmonics;
+  if (n < 2) return set_error(FUSG_INVALID_ARGUMENT, "run_cascade: n_harmonics must be >= 2");
+  if (!d->grids) return set_error(FUSG_INVALID_ARGUMENT, "run_cascade: no planned grids");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const fusg_bowl& t = d->transducer;
+  const fusg_medium& med = d->medium;
+  auto grid_of = [&](int harmonic) -> const fusg_grid& {  // p1 lives on D_2's grid
+    return d->grids[harmonic <= 2 ? 0 : harmonic - 2];
+  };
+
+  double* src = nullptr;
+  fusg_status st = upload_sources(t.points_host, t.n_points, &src, s);
+  if (st != FUSG_OK) return st;
+  std::unique_ptr<double, void (*)(double*)> src_guard(src, [](double* p) { cudaFree(p); });
+  const double l = t.focal_length, R = t.outer_radius;
+  const double cap_area = 2.0 * M_PI * l * (l - std::sqrt(l * l - R * R));
+  const double x_disc = l - std::sqrt(l * l - R * R);
+
+  // p1 on the D_2 grid: evaluate_source_field (src/transducer.cpp:198-206)
+  EvTimer tm(s);
+  tm.start();
+  fusg_wavenumber k1{};
+  st = fusg_complex_wavenumber(&med, t.f0, 1, &k1);
+  if (st != FUSG_OK) return st;
+  double scale = 0.0;
+  if (t.power != 0.0) {  // power_scale_factor (src/transducer.cpp:157-163)
+    double pw = 0.0;
+    st = radiated_power_dev(ctx, src, t.n_points, x_disc, R, k1.k_re, k1.k_im,
+                            1.0 * cap_area / double(t.n_points), med.rho0, med.c0, 384, 256, &pw, s);
+    if (st != FUSG_OK) return st;
+    if (pw <= 0.0) return set_error(FUSG_RUNTIME, "power normalization: degenerate field, Pi(p) = 0");
+    scale = std::sqrt(t.power / pw);
+  }
+  const double norm = scale > 0.0 ? scale : 1.0;
+  if (source_normalization) *source_normalization = norm;
+  const double amp1 = scale * cap_area / double(t.n_points);
+  st = monopole_grid(ctx, src, t.n_points, grid_of(1), k1.k_re, k1.k_im, amp1,
+                     reinterpret_cast<double2*>(out_dev[0]), s);
+  if (st != FUSG_OK) return st;
+  st = check_monopole_flag(ctx, s);
+  if (st != FUSG_OK) return st;
+  const double p1_s = tm.stop();
+  double peak = 0.0;
+  st = max_abs_dev(ctx, reinterpret_cast<const double2*>(out_dev[0]), count_of(grid_of(1)), &peak, s);
+  if (st != FUSG_OK) return st;
+  if (peak > 15e6)
+    std::cerr << "warning: peak pressure " << peak / 1e6
+              << " MPa exceeds the 15 MPa weakly-nonlinear bound; the truncated cascade"
+                 " may be inaccurate\n";
+
+  for (int i = 2; i <= n; ++i) {
+    fusg_stage_timing row{};
+    row.harmonic = i;
+    auto t0 = std::chrono::steady_clock::now();
+    const fusg_grid& grid = grid_of(i);
+    const int64_t count = count_of(grid);
+    row.voxels = uint64_t(count);
+    row.meshing_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (i == 2) row.p1_s = p1_s;
+
+    // bring p_1 .. p_{i-1} onto this grid
+    tm.start();
+    std::vector<double2*> temps;
+    std::vector<const double2*> lower;
+    for (int m = 1; m <= i - 1; ++m) {
+      const fusg_grid& gm = grid_of(m);
+      const double2* pm = reinterpret_cast<const double2*>(out_dev[m - 1]);
+      if (same_grid(gm, grid)) {
+        lower.push_back(pm);
+        continue;
+      }
+      double2* tmp = nullptr;
+      if (cudaMallocAsync(&tmp, size_t(count) * 16, s) != cudaSuccess) {
+        for (auto* p : temps) cudaFreeAsync(p, s);
+        cudaGetLastError();
+        return set_error(FUSG_OOM, "run_cascade: temporary field allocation failed");
+      }
+      temps.push_back(tmp);
+      if (m == 1 && d->recompute_p1_each_grid)
+        st = monopole_grid(ctx, src, t.n_points, grid, k1.k_re, k1.k_im, amp1, tmp, s);
+      else
+        st = interpolate_dev(ctx, gm, pm, grid, tmp, s);
+      if (st != FUSG_OK) break;
+      lower.push_back(tmp);
+    }
+    if (st == FUSG_OK) row.interpolation_s = tm.stop();
+
+    // rhs_source (untimed in the reference; timed separately here)
+    fusg_wavenumber ki{};
+    double2* f = nullptr;
+    if (st == FUSG_OK) st = fusg_complex_wavenumber(&med, t.f0, i, &ki);
+    if (st == FUSG_OK) {
+      tm.start();
+      if (cudaMallocAsync(&f, size_t(count) * 16, s) != cudaSuccess) {
+        cudaGetLastError();
+        st = set_error(FUSG_OOM, "run_cascade: source allocation failed");
+      } else {
+        st = rhs_dev(ctx, i, lower.data(), count, fusg_rhs_coefficient(&med, ki.omega, i), f, s);
+        if (st == FUSG_OK) row.rhs_s = tm.stop();
+      }
+    }
+    for (auto* p : temps) cudaFreeAsync(p, s);
+
+    // GreenKernel(grid_i, k_i) -> "Evaluate G_k"
+    fusg_kernel* K = nullptr;
+    if (st == FUSG_OK) {
+      tm.start();
+      fusg_grid gi = grid;
+      gi.harmonic = i;
+      st = fusg_kernel_create(ctx, &gi, &ki, d->pad_small_primes, &K);
+      if (st == FUSG_OK) row.kernel_s = tm.stop();
+    }
+    // p_i = -apply(f)
+    if (st == FUSG_OK) {
+      tm.start();
+      st = volume_potential_apply(K, f, reinterpret_cast<double2*>(out_dev[i - 1]), -1.0, s);
+      if (st == FUSG_OK) row.potential_s = tm.stop();
+    }
+    if (f) cudaFreeAsync(f, s);
+    if (K) fusg_kernel_destroy(K);
+    if (st != FUSG_OK) return st;
+    if (timings) timings[i - 2] = row;
+  }
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return FUSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,450 @@
+// Incident field (equal-area monopole / Rayleigh-type sum), radiated-power integral,
+// Westervelt quadratic source and trilinear nested-grid transfer.
+//
+//  * monopole sum  (src/transducer.cpp:107-132,179-196): FP64 CUDA-core kernel, one voxel per
+//    thread, sources broadcast from shared memory in the reference's summation order.
+//  * radiated power (src/transducer.cpp:134-155): per-node |amp S|^2, then a fixed-order
+//    two-level reduction (rings in order, then rings summed in order): deterministic.
+//  * rhs_source (src/cascade.cpp:21-40) and interpolate (src/grid.cpp:141-195): elementwise
+//    and gather kernels written with explicit round-to-nearest intrinsics, so they round
+//    exactly like the reference's non-FMA x86-64 build (bit-identical outputs).
+#include <cmath>
+#include <vector>
+
+#include "internal.hpp"
+
+namespace fusg {
+
+constexpr int kSrcChunk = 1024;
+
+struct GridDev {
+  double lo[3];
+  double dx;
+  int dims[3];
+};
+
+static GridDev to_dev(const fusg_grid& g) {
+  GridDev d;
+  for (int a = 0; a < 3; ++a) {
+    d.lo[a] = g.lo[a];
+    d.dims[a] = g.dims[a];
+  }
+  d.dx = g.dx;
+  return d;
+}
+
+// centre coordinate lo + (i + 0.5) dx, rounded like include/fus/grid.hpp:44-46
+__device__ __forceinline__ double centre(double lo, int i, double dx) {
+  return __dadd_rn(lo, __dmul_rn(double(i) + 0.5, dx));
+}
+
+// One monopole term e^{-Im k d}/(4 pi d) e^{i Re k d} accumulated into acc
+// (src/transducer.cpp:110-117).  Returns false on coincidence.
+__device__ __forceinline__ void monopole_term(double x, double y, double z, double sx, double sy,
+                                              double sz, double kre, double kim, double2& acc,
+                                              bool& bad) {
+  const double ddx = x - sx, ddy = y - sy, ddz = z - sz;
+  const double dist = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(ddx, ddx), __dmul_rn(ddy, ddy)),
+                                     __dmul_rn(ddz, ddz)));
+  if (dist < 1e-12) bad = true;
+  const double mag = exp(-kim * dist) / (4.0 * M_PI * dist);
+  double s, c;
+  sincos(kre * dist, &s, &c);
+  acc.x += mag * c;
+  acc.y += mag * s;
+}
+
+__device__ __forceinline__ void stage_sources(const double* src, int n_src, int base, double* sx,
+                                              double* sy, double* sz) {
+  for (int j = threadIdx.x; j < kSrcChunk && base + j < n_src; j += blockDim.x) {
+    sx[j] = src[3 * (base + j)];
+    sy[j] = src[3 * (base + j) + 1];
+    sz[j] = src[3 * (base + j) + 2];
+  }
+}
+
+__global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __restrict__ src, int n_src,
+                                                            GridDev g, double kre, double kim,
+                                                            double amp, double2* __restrict__ out,
+                                                            int* flag) {
+  __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
+  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = idx < count;
+  double x = 0, y = 0, z = 0;
+  if (active) {
+    const int ix = int(idx % g.dims[0]);
+    const int64_t r = idx / g.dims[0];
+    const int iy = int(r % g.dims[1]);
+    const int iz = int(r / g.dims[1]);
+    x = centre(g.lo[0], ix, g.dx);
+    y = centre(g.lo[1], iy, g.dx);
+    z = centre(g.lo[2], iz, g.dx);
+  }
+  double2 acc = make_double2(0.0, 0.0);
+  bool bad = false;
+  for (int base = 0; base < n_src; base += kSrcChunk) {
+    __syncthreads();
+    stage_sources(src, n_src, base, sx, sy, sz);
+    __syncthreads();
+    if (active) {
+      const int n = min(kSrcChunk, n_src - base);
+      for (int j = 0; j < n; ++j) monopole_term(x, y, z, sx[j], sy[j], sz[j], kre, kim, acc, bad);
+    }
+  }
+  if (active) {
+    if (bad) atomicExch(flag, 1);
+    out[idx] = make_double2(amp * acc.x, amp * acc.y);
+  }
+}
+
+__global__ void __launch_bounds__(256) monopole_points_kernel(const double* __restrict__ src,
+                                                              int n_src,
+                                                              const double* __restrict__ pts,
+                                                              int64_t n_pts, double kre, double kim,
+                                                              double amp, double2* __restrict__ out,
+                                                              int* flag) {
+  __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = idx < n_pts;
+  double x = 0, y = 0, z = 0;
+  if (active) {
+    x = pts[3 * idx];
+    y = pts[3 * idx + 1];
+    z = pts[3 * idx + 2];
+  }
+  double2 acc = make_double2(0.0, 0.0);
+  bool bad = false;
+  for (int base = 0; base < n_src; base += kSrcChunk) {
+    __syncthreads();
+    stage_sources(src, n_src, base, sx, sy, sz);
+    __syncthreads();
+    if (active) {
+      const int n = min(kSrcChunk, n_src - base);
+      for (int j = 0; j < n; ++j) monopole_term(x, y, z, sx[j], sy[j], sz[j], kre, kim, acc, bad);
+    }
+  }
+  if (active) {
+    if (bad) atomicExch(flag, 1);
+    out[idx] = make_double2(amp * acc.x, amp * acc.y);
+  }
+}
+
+// Disc nodes of radiated_power: node (j, m) at (x_disc, r cos th, r sin th).
+__global__ void __launch_bounds__(256) power_nodes_kernel(const double* __restrict__ src, int n_src,
+                                                          double x_disc, double dr, double dth,
+                                                          int n_r, int n_theta, double kre,
+                                                          double kim, double amp,
+                                                          double* __restrict__ node_out, int* flag) {
+  __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool active = idx < int64_t(n_r) * n_theta;
+  double y = 0, z = 0;
+  if (active) {
+    const int j = int(idx / n_theta), m = int(idx % n_theta);
+    const double r = (j + 0.5) * dr;
+    const double th = (m + 0.5) * dth;
+    y = r * cos(th);
+    z = r * sin(th);
+  }
+  double2 acc = make_double2(0.0, 0.0);
+  bool bad = false;
+  for (int base = 0; base < n_src; base += kSrcChunk) {
+    __syncthreads();
+    stage_sources(src, n_src, base, sx, sy, sz);
+    __syncthreads();
+    if (active) {
+      const int n = min(kSrcChunk, n_src - base);
+      for (int j = 0; j < n; ++j) monopole_term(x_disc, y, z, sx[j], sy[j], sz[j], kre, kim, acc, bad);
+    }
+  }
+  if (active) {
+    if (bad) atomicExch(flag, 1);
+    const double re = amp * acc.x, im = amp * acc.y;
+    node_out[idx] = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+  }
+}
+
+// Fixed-order reduction: ring j sums its n_theta nodes in order, times r_j; then rings in
+// order. One block; deterministic for any launch configuration.
+__global__ void power_reduce_kernel(const double* __restrict__ nodes, int n_r, int n_theta,
+                                    double dr, double* __restrict__ rings, double* out,
+                                    double factor) {
+  for (int j = threadIdx.x; j < n_r; j += blockDim.x) {
+    double ring = 0.0;
+    for (int m = 0; m < n_theta; ++m) ring = __dadd_rn(ring, nodes[int64_t(j) * n_theta + m]);
+    rings[j] = __dmul_rn(ring, (j + 0.5) * dr);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int j = 0; j < n_r; ++j) total = __dadd_rn(total, rings[j]);
+    *out = total * factor;
+  }
+}
+
+// rhs_source: out = coeff * sum_{m=1}^{n-1} p_m p_{n-m}, complex products as (ac-bd, ad+bc)
+struct LowerPtrs {
+  const double2* p[32];
+};
+
+__global__ void rhs_kernel(LowerPtrs lp, int n, int64_t count, double coeff,
+                           double2* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int m = 1; m <= n - 1; ++m) {
+      const double2 a = lp.p[m - 1][i], b = lp.p[n - m - 1][i];
+      const double pr = __dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y));
+      const double pi = __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x));
+      re = __dadd_rn(re, pr);
+      im = __dadd_rn(im, pi);
+    }
+    out[i] = make_double2(__dmul_rn(coeff, re), __dmul_rn(coeff, im));
+  }
+}
+
+// interpolate (src/grid.cpp:141-195), exact rounding
+__global__ void interp_kernel(GridDev s, const double2* __restrict__ f, GridDev t,
+                              double2* __restrict__ out) {
+  const int64_t count = int64_t(t.dims[0]) * t.dims[1] * t.dims[2];
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < count;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int ix = int(idx % t.dims[0]);
+    const int64_t r = idx / t.dims[0];
+    const int iy = int(r % t.dims[1]);
+    const int iz = int(r / t.dims[1]);
+    const int ii[3] = {ix, iy, iz};
+    int i0[3];
+    double tt[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double p = centre(t.lo[a], ii[a], t.dx);
+      const double q = __dsub_rn(__ddiv_rn(__dsub_rn(p, s.lo[a]), s.dx), 0.5);
+      int base = int(floor(q));
+      const int hi = max(0, s.dims[a] - 2);
+      base = base < 0 ? 0 : (base > hi ? hi : base);
+      double frac = __dsub_rn(q, double(base));
+      if (frac < 0.0) frac = 0.0;
+      if (frac > 1.0) frac = s.dims[a] > 1 ? 1.0 : 0.0;
+      i0[a] = base;
+      tt[a] = frac;
+    }
+    double re = 0.0, im = 0.0;
+#pragma unroll
+    for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < 2; ++cx) {
+          const double wx = cx ? tt[0] : __dsub_rn(1.0, tt[0]);
+          const double wy = cy ? tt[1] : __dsub_rn(1.0, tt[1]);
+          const double wz = cz ? tt[2] : __dsub_rn(1.0, tt[2]);
+          const double wgt = __dmul_rn(__dmul_rn(wx, wy), wz);
+          if (wgt == 0.0) continue;
+          const int jx = min(max(i0[0] + cx, 0), s.dims[0] - 1);
+          const int jy = min(max(i0[1] + cy, 0), s.dims[1] - 1);
+          const int jz = min(max(i0[2] + cz, 0), s.dims[2] - 1);
+          const double2 v = f[jx + int64_t(s.dims[0]) * (jy + int64_t(s.dims[1]) * jz)];
+          re = __dadd_rn(re, __dmul_rn(wgt, v.x));
+          im = __dadd_rn(im, __dmul_rn(wgt, v.y));
+        }
+    out[idx] = make_double2(re, im);
+  }
+}
+
+// max |v| (for the 15 MPa weak-nonlinearity warning, src/cascade.cpp:56-60)
+__global__ void max_abs_kernel(const double2* __restrict__ v, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    m = fmax(m, hypot(v[i].x, v[i].y));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// ---------------------------------------------------------------------------- launchers
+static int grid_stride_blocks(const fusg_ctx* ctx, int64_t n, int threads) {
+  const int64_t need = (n + threads - 1) / threads;
+  const int64_t cap = int64_t(ctx->num_sms) * 16;
+  return int(std::max<int64_t>(1, std::min(need, cap)));
+}
+
+fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s) {
+  if (n_src < 1) return set_error(FUSG_INVALID_ARGUMENT, "monopole sum: no source points");
+  FUSG_CUDA_TRY(cudaMallocAsync(dev, sizeof(double) * 3 * n_src, s));
+  FUSG_CUDA_TRY(cudaMemcpyAsync(*dev, src_host, sizeof(double) * 3 * n_src,
+                                cudaMemcpyHostToDevice, s));
+  return FUSG_OK;
+}
+
+static fusg_status check_flag(fusg_ctx* ctx, cudaStream_t s) {
+  int h = 0;
+  FUSG_CUDA_TRY(cudaMemcpyAsync(&h, ctx->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h) {
+    FUSG_CUDA_TRY(cudaMemsetAsync(ctx->dev_flag, 0, sizeof(int), s));
+    return set_error(FUSG_INVALID_ARGUMENT, "evaluation point coincides with a monopole source");
+  }
+  return FUSG_OK;
+}
+
+fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
+                          double kre, double kim, double amp, double2* out, cudaStream_t s) {
+  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  const int threads = 256;
+  monopole_grid_kernel<<<unsigned((count + threads - 1) / threads), threads, 0, s>>>(
+      src_dev, n_src, to_dev(g), kre, kim, amp, out, ctx->dev_flag);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("monopole_grid_kernel");
+  return FUSG_OK;
+}
+
+fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
+                            const fusg_grid& tgt, double2* out, cudaStream_t s) {
+  for (int a = 0; a < 3; ++a)
+    if (tgt.lo[a] < src.lo[a] - src.dx || tgt.hi[a] > src.hi[a] + src.dx)
+      return set_error(FUSG_INVALID_ARGUMENT,
+                       "interpolate: target extends more than one source voxel beyond the source domain");
+  const int64_t count = int64_t(tgt.dims[0]) * tgt.dims[1] * tgt.dims[2];
+  interp_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(to_dev(src), f, to_dev(tgt), out);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("interp_kernel");
+  return FUSG_OK;
+}
+
+fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
+                    double2* out, cudaStream_t s) {
+  if (n < 2) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source: harmonic index must be >= 2");
+  if (n - 1 > 32) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source: at most 33 harmonics");
+  LowerPtrs lp{};
+  for (int m = 0; m < n - 1; ++m) {
+    if (!lower[m]) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source: null lower harmonic");
+    lp.p[m] = lower[m];
+  }
+  rhs_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(lp, n, count, coeff, out);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("rhs_kernel");
+  return FUSG_OK;
+}
+
+fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s) {
+  unsigned long long* d = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long), s));
+  FUSG_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
+  max_abs_kernel<<<grid_stride_blocks(ctx, n, 256), 256, 0, s>>>(v, n, d);
+  ctx->launches++;
+  unsigned long long h = 0;
+  FUSG_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FUSG_CUDA_TRY(cudaFreeAsync(d, s));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  double m;
+  memcpy(&m, &h, sizeof(m));
+  *out = m;
+  return FUSG_OK;
+}
+
+fusg_status radiated_power_dev(fusg_ctx* ctx, const double* src_dev, int n_src, double x_disc,
+                               double R, double kre, double kim, double amp, double rho0, double c0,
+                               int n_r, int n_theta, double* out_host, cudaStream_t s) {
+  if (n_r < 1 || n_theta < 1) return set_error(FUSG_INVALID_ARGUMENT, "radiated_power: empty disc");
+  const double dr = R / n_r;
+  const double dth = 2.0 * M_PI / n_theta;
+  const int64_t nn = int64_t(n_r) * n_theta;
+  double* nodes = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&nodes, sizeof(double) * (nn + n_r + 1), s));
+  power_nodes_kernel<<<unsigned((nn + 255) / 256), 256, 0, s>>>(src_dev, n_src, x_disc, dr, dth, n_r,
+                                                                 n_theta, kre, kim, amp, nodes,
+                                                                 ctx->dev_flag);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("power_nodes_kernel");
+  // the final total * dr * dth / (2 rho0 c0) is applied on the host in the reference's order
+  power_reduce_kernel<<<1, 256, 0, s>>>(nodes, n_r, n_theta, dr, nodes + nn, nodes + nn + n_r, 1.0);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("power_reduce_kernel");
+  double total = 0.0;
+  FUSG_CUDA_TRY(cudaMemcpyAsync(&total, nodes + nn + n_r, sizeof(double), cudaMemcpyDeviceToHost, s));
+  FUSG_CUDA_TRY(cudaFreeAsync(nodes, s));
+  fusg_status st = check_flag(ctx, s);
+  if (st != FUSG_OK) return st;
+  *out_host = total * dr * dth / (2.0 * rho0 * c0);
+  return FUSG_OK;
+}
+
+fusg_status check_monopole_flag(fusg_ctx* ctx, cudaStream_t s) { return check_flag(ctx, s); }
+
+}  // namespace fusg
+
+using namespace fusg;
+
+extern "C" {
+
+fusg_status fusg_monopole_grid(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                               const fusg_grid* grid, double k_re, double k_im, double amp,
+                               double* out_dev, void* stream) {
+  if (!ctx || !grid || !out_dev) return set_error(FUSG_INVALID_ARGUMENT, "monopole_grid: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->pick(stream);
+  double* src = nullptr;
+  fusg_status st = upload_sources(src_host, n_src, &src, s);
+  if (st != FUSG_OK) return st;
+  st = monopole_grid(ctx, src, n_src, *grid, k_re, k_im, amp, reinterpret_cast<double2*>(out_dev), s);
+  cudaFreeAsync(src, s);
+  if (st != FUSG_OK) return st;
+  return check_flag(ctx, s);
+}
+
+fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                                 const double* pts_dev, int64_t n_pts, double k_re, double k_im,
+                                 double amp, double* out_dev, void* stream) {
+  if (!ctx || (n_pts > 0 && (!pts_dev || !out_dev)))
+    return set_error(FUSG_INVALID_ARGUMENT, "monopole_points: null argument");
+  if (n_pts == 0) return FUSG_OK;
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->pick(stream);
+  double* src = nullptr;
+  fusg_status st = upload_sources(src_host, n_src, &src, s);
+  if (st != FUSG_OK) return st;
+  monopole_points_kernel<<<unsigned((n_pts + 255) / 256), 256, 0, s>>>(
+      src, n_src, pts_dev, n_pts, k_re, k_im, amp, reinterpret_cast<double2*>(out_dev), ctx->dev_flag);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("monopole_points_kernel");
+  cudaFreeAsync(src, s);
+  return check_flag(ctx, s);
+}
+
+fusg_status fusg_radiated_power(fusg_ctx* ctx, const double* src_host, int32_t n_src, double x_disc,
+                                double R, double k_re, double k_im, double amp, double rho0,
+                                double c0, int32_t n_r, int32_t n_theta, double* out_host) {
+  if (!ctx || !out_host) return set_error(FUSG_INVALID_ARGUMENT, "radiated_power: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  double* src = nullptr;
+  fusg_status st = upload_sources(src_host, n_src, &src, s);
+  if (st != FUSG_OK) return st;
+  st = radiated_power_dev(ctx, src, n_src, x_disc, R, k_re, k_im, amp, rho0, c0, n_r, n_theta,
+                          out_host, s);
+  cudaFreeAsync(src, s);
+  return st;
+}
+
+fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower_dev, int64_t count,
+                            const fusg_medium* m, double omega, double* out_dev, void* stream) {
+  if (!ctx || !m || !lower_dev || !out_dev)
+    return set_error(FUSG_INVALID_ARGUMENT, "rhs_source: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  const double coeff = fusg_rhs_coefficient(m, omega, n);
+  return rhs_dev(ctx, n, reinterpret_cast<const double2* const*>(lower_dev), count, coeff,
+                 reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
+}
+
+fusg_status fusg_interpolate(fusg_ctx* ctx, const fusg_grid* src, const double* f_dev,
+                             const fusg_grid* target, double* out_dev, void* stream) {
+  if (!ctx || !src || !target || !f_dev || !out_dev)
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  return interpolate_dev(ctx, *src, reinterpret_cast<const double2*>(f_dev), *target,
+                         reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Internal (non-ABI) declarations shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <mutex>
+#include <string>
+
+#include "../../include/fusg.h"
+#include "plan.hpp"
+
+namespace fusg {
+
+fusg_status set_error(fusg_status st, const std::string& msg);
+fusg_status cuda_error(cudaError_t e, const char* what);
+
+#define FUSG_CUDA_TRY(expr)                                   \
+  do {                                                        \
+    cudaError_t e_ = (expr);                                  \
+    if (e_ != cudaSuccess) return ::fusg::cuda_error(e_, #expr); \
+  } while (0)
+
+#define FUSG_TRY(expr)            \
+  do {                            \
+    fusg_status s_ = (expr);      \
+    if (s_ != FUSG_OK) return s_; \
+  } while (0)
+
+// Reports the first launch error of the preceding kernel(s).
+#define FUSG_LAUNCH_CHECK(what)                               \
+  do {                                                        \
+    cudaError_t e_ = cudaGetLastError();                      \
+    if (e_ != cudaSuccess) return ::fusg::cuda_error(e_, what); \
+  } while (0)
+
+int smooth_padded_size(int n, bool pad_small_primes);
+bool make_plan_radices(int L, AxisPlan& pl);
+
+}  // namespace fusg
+
+struct fusg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int* dev_flag = nullptr;  // device error flag (monopole coincidence)
+  std::atomic<uint64_t> launches{0};
+  std::mutex mu;
+  cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+};
+
+struct fusg_kernel {
+  fusg_ctx* ctx = nullptr;
+  fusg_grid grid{};
+  fusg_wavenumber k{};
+  int P[3] = {0, 0, 0};  // padded box
+  int H[3] = {0, 0, 0};  // octant extents P/2 + 1
+  fusg::AxisPlan plan[3]{};
+  double2* tw[3] = {nullptr, nullptr, nullptr};
+  double2* koct = nullptr;  // kernel spectrum octant [Hz][Hy][Hx]
+  double2* bufA = nullptr;  // [Nz][Ny][Px]
+  double2* bufB = nullptr;  // [Nz][Py][Px]
+  uint64_t bytes = 0;
+  std::mutex mu;  // serialises applies sharing the workspace
+};
+
+namespace fusg {
+fusg_status volume_potential_build(fusg_kernel* K, double2 self);
+// ev (optional): 6 events recorded before passes A..E and after E
+fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
+                                   cudaStream_t st, cudaEvent_t* ev = nullptr);
+}  // namespace fusg

@@ -1,0 +1,353 @@
+// Volume-potential operator on the device: GreenKernel construction ("Evaluate G_k") and
+// GreenKernel::apply (src/potential.cpp:72-151) as pruned, fused FP64 Stockham passes.
+//
+// apply(f) = crop_N( IDFT_P( K^ . DFT_P( pad_P(f) ) ) ) / |P|   (src/potential.cpp:128-149)
+//
+//   pass A  forward x : f [Nz][Ny][Nx]      -> A [Nz][Ny][Px]   (zero padding fused: rows of Nx)
+//   pass B  forward y : A                    -> B [Nz][Py][Px]   (pruned input: Ny of Py)
+//   pass C  forward z, * K^, inverse z: B -> B in place          (pruned in/out: Nz of Pz)
+//   pass D  inverse y : B                    -> A               (pruned output: Ny)
+//   pass E  inverse x, * scale/|P|, crop : A -> u [Nz][Ny][Nx]
+//
+// The padded kernel tensor is even along every axis (K[P-m] = K[m], offset_of at :88-94),
+// so its spectrum is even too: only the octant [0,Px/2]x[0,Py/2]x[0,Pz/2] is built and
+// stored, and pass C folds its index.  The octant is built by the same pass machinery with
+// the kernel values generated in registers (no padded tensor is ever materialised).
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "fft_pass.cuh"
+#include "internal.hpp"
+
+namespace fusg {
+
+// ---------------------------------------------------------------------------- loaders
+struct GLoadF {
+  GLoad g;
+  __device__ __forceinline__ GLoadAt at(int i, int k, bool ok) const {
+    return GLoadAt{g.p + i * g.si + k * g.sk, g.sp, g.nvalid, ok};
+  }
+};
+struct GStoreF {
+  GStore g;
+  __device__ __forceinline__ GStoreAt at(int i, int k, bool ok) const {
+    return GStoreAt{g.p + i * g.si + k * g.sk, g.sp, g.nvalid, ok, g.scale};
+  }
+};
+
+// Kernel-tensor generator for the first build pass (src/potential.cpp:96-115): line i is
+// the non-negative offset pair (oy, oz) = (i mod Ny, i / Ny); position = x index of the
+// padded box.
+struct KGenAt {
+  static constexpr bool kSmem = false;
+  int Nx, Px, oy, oz;
+  double dx, vol, kre, kim;
+  double2 self;
+  bool ok;
+  __device__ __forceinline__ double2 load(int pos) const {
+    const int ox = offset_of(pos, Nx, Px);
+    if (!ok || ox == kExcluded) return make_double2(0.0, 0.0);
+    if (ox == 0 && oy == 0 && oz == 0) return self;
+    const double r = dx * sqrt(double(ox) * ox + double(oy) * oy + double(oz) * oz);
+    const double mag = exp(-kim * r) / (4.0 * M_PI * r);
+    double s, c;
+    sincos(kre * r, &s, &c);
+    return make_double2(vol * (mag * c), vol * (mag * s));
+  }
+};
+struct KGenF {
+  int Nx, Ny, Px;
+  double dx, vol, kre, kim;
+  double2 self;
+  __device__ __forceinline__ KGenAt at(int i, int, bool ok) const {
+    return KGenAt{Nx, Px, i % Ny, i / Ny, dx, vol, kre, kim, self, ok};
+  }
+};
+
+// Even extension of a half-range line: value at padded position = base[|offset|].
+struct FoldAt {
+  static constexpr bool kSmem = false;
+  const double2* base;
+  int64_t sp;
+  int N, P;
+  bool ok;
+  __device__ __forceinline__ double2 load(int pos) const {
+    const int o = offset_of(pos, N, P);
+    if (!ok || o == kExcluded) return make_double2(0.0, 0.0);
+    return __ldg(base + int64_t(o < 0 ? -o : o) * sp);
+  }
+};
+struct FoldF {
+  const double2* p;
+  int64_t si, sk, sp;
+  int N, P;
+  __device__ __forceinline__ FoldAt at(int i, int k, bool ok) const {
+    return FoldAt{p + i * si + k * sk, sp, N, P, ok};
+  }
+};
+
+// Spectral multiply between the forward and inverse z transforms of pass C: reads the
+// forward spectrum from shared memory and multiplies by the folded octant value.
+template <int T>
+struct KMulAt {
+  static constexpr bool kSmem = true;
+  const double2* sm;
+  int t;
+  const double2* kline;
+  int64_t sz;
+  int P;
+  bool ok;
+  __device__ __forceinline__ double2 load(int pos) const {
+    const double2 v = sm[pos * T + t];
+    if (!ok) return make_double2(0.0, 0.0);
+    return cmul(v, __ldg(kline + int64_t(fold_index(pos, P)) * sz));
+  }
+};
+struct KOct {
+  const double2* p;
+  int Hx, Hy, Px, Py, Pz;
+};
+
+// ---------------------------------------------------------------------------- kernels
+template <bool INV, int T, class LD, class ST>
+__global__ void __launch_bounds__(512) axis_pass(AxisPlan pl, LineGeom g, LD ld, ST st) {
+  extern __shared__ double2 sm[];
+  const int tile = blockIdx.x % g.ntiles;
+  const int k = blockIdx.x / g.ntiles;
+  const int t = threadIdx.x % T, jt = threadIdx.x / T;
+  const int i = tile * T + t;
+  const bool ok = i < g.n_inner;
+  auto src = ld.at(ok ? i : 0, k, ok);
+  auto dst = st.at(ok ? i : 0, k, ok);
+  fft_line<INV, T>(pl, sm, t, jt, src, dst);
+}
+
+template <int T>
+__global__ void __launch_bounds__(512) conv_pass(AxisPlan pl, LineGeom g, GLoadF ld, GStoreF st,
+                                                  KOct ko) {
+  extern __shared__ double2 sm[];
+  const int tile = blockIdx.x % g.ntiles;
+  const int k = blockIdx.x / g.ntiles;  // ky
+  const int t = threadIdx.x % T, jt = threadIdx.x / T;
+  const int i = tile * T + t;           // kx
+  const bool ok = i < g.n_inner;
+  const int ii = ok ? i : 0;
+  auto src = ld.at(ii, k, ok);
+  SmemIO<T> mid{sm, t};
+  fft_line<false, T>(pl, sm, t, jt, src, mid);
+  __syncthreads();
+  KMulAt<T> msrc{sm, t,
+                 ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px),
+                 int64_t(ko.Hx) * ko.Hy, ko.Pz, ok};
+  auto dst = st.at(ii, k, ok);
+  fft_line<true, T>(pl, sm, t, jt, msrc, dst);
+}
+
+// ---------------------------------------------------------------------------- planning
+static bool smooth7(int n) {
+  for (int p : {2, 3, 5, 7})
+    while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+int smooth_padded_size(int n, bool pad_small_primes) {
+  // Reference: 2N, or next_fast_size(2N) (src/potential.cpp:74-77). Any P >= 2N-1 gives
+  // the same discrete operator; the device path needs {2,3,5,7}-smooth lengths.
+  int p = pad_small_primes ? 2 * n : std::max(2, 2 * n - 1);
+  while (!smooth7(p)) ++p;
+  return p;
+}
+
+bool make_plan_radices(int L, AxisPlan& pl) {
+  int m = L, e2 = 0, e3 = 0, e5 = 0, e7 = 0;
+  while (m % 2 == 0) { m /= 2; ++e2; }
+  while (m % 3 == 0) { m /= 3; ++e3; }
+  while (m % 5 == 0) { m /= 5; ++e5; }
+  while (m % 7 == 0) { m /= 7; ++e7; }
+  if (m != 1 || L < 2) return false;
+  std::vector<int> r;
+  if (e2 > 0) {
+    const int n = (e2 + 3) / 4;  // stages for the power of two, <= 4 bits each, balanced
+    for (int s = 0; s < n; ++s) {
+      const int bits = e2 / n + (s < e2 % n ? 1 : 0);
+      r.push_back(1 << bits);
+    }
+  }
+  for (int i = 0; i < e7; ++i) r.push_back(7);
+  for (int i = 0; i < e5; ++i) r.push_back(5);
+  for (int i = 0; i < e3; ++i) r.push_back(3);
+  if (int(r.size()) > kMaxStages) return false;
+  pl.L = L;
+  pl.nst = int(r.size());
+  int ns = 1, tpl = 1;
+  for (int s = 0; s < pl.nst; ++s) {
+    pl.radix[s] = r[s];
+    pl.ns[s] = ns;
+    ns *= r[s];
+    const int nb = L / r[s];
+    const int bmax = kMaxElems / r[s];
+    tpl = std::max(tpl, (nb + bmax - 1) / bmax);
+  }
+  pl.tpl = tpl;
+  return true;
+}
+
+static fusg_status upload_twiddles(int L, double2** out) {
+  std::vector<double2> h(L);
+  for (int m = 0; m < L; ++m) {
+    // exp(-2 pi i m / L) with the angle reduced to the first octant for accuracy
+    const long double a = -2.0L * 3.141592653589793238462643383279502884L * m / L;
+    h[m] = make_double2(double(cosl(a)), double(sinl(a)));
+  }
+  FUSG_CUDA_TRY(cudaMalloc(out, sizeof(double2) * L));
+  FUSG_CUDA_TRY(cudaMemcpy(*out, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+  return FUSG_OK;
+}
+
+constexpr size_t kSmemBudget = 100 * 1024;
+
+static int choose_tile(const AxisPlan& pl, int n_inner) {
+  int T = 16;
+  while (T > 1 && (size_t(pl.L) * T * sizeof(double2) > kSmemBudget || T * pl.tpl > 512 ||
+                   (T / 2 >= n_inner)))
+    T /= 2;
+  return T;
+}
+
+template <bool INV, int T, class LD, class ST>
+static fusg_status launch_axis_t(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
+                                 const LD& ld, const ST& st, cudaStream_t s) {
+  LineGeom g{n_inner, n_outer, (n_inner + T - 1) / T};
+  const size_t smem = size_t(pl.L) * T * sizeof(double2);
+  auto fn = axis_pass<INV, T, LD, ST>;
+  FUSG_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int64_t blocks = int64_t(g.ntiles) * n_outer;
+  fn<<<unsigned(blocks), T * pl.tpl, smem, s>>>(pl, g, ld, st);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("axis_pass");
+  return FUSG_OK;
+}
+
+template <bool INV, class LD, class ST>
+static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
+                               const LD& ld, const ST& st, cudaStream_t s) {
+  if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
+    return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
+  switch (choose_tile(pl, n_inner)) {
+    case 16: return launch_axis_t<INV, 16>(ctx, pl, n_inner, n_outer, ld, st, s);
+    case 8: return launch_axis_t<INV, 8>(ctx, pl, n_inner, n_outer, ld, st, s);
+    case 4: return launch_axis_t<INV, 4>(ctx, pl, n_inner, n_outer, ld, st, s);
+    case 2: return launch_axis_t<INV, 2>(ctx, pl, n_inner, n_outer, ld, st, s);
+    default: return launch_axis_t<INV, 1>(ctx, pl, n_inner, n_outer, ld, st, s);
+  }
+}
+
+template <int T>
+static fusg_status launch_conv_t(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
+                                 const GLoadF& ld, const GStoreF& st, const KOct& ko,
+                                 cudaStream_t s) {
+  LineGeom g{n_inner, n_outer, (n_inner + T - 1) / T};
+  const size_t smem = size_t(pl.L) * T * sizeof(double2);
+  auto fn = conv_pass<T>;
+  FUSG_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int64_t blocks = int64_t(g.ntiles) * n_outer;
+  fn<<<unsigned(blocks), T * pl.tpl, smem, s>>>(pl, g, ld, st, ko);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("conv_pass");
+  return FUSG_OK;
+}
+
+static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
+                               const GLoadF& ld, const GStoreF& st, const KOct& ko,
+                               cudaStream_t s) {
+  if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
+    return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
+  switch (choose_tile(pl, n_inner)) {
+    case 16: return launch_conv_t<16>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
+    case 8: return launch_conv_t<8>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
+    case 4: return launch_conv_t<4>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
+    case 2: return launch_conv_t<2>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
+    default: return launch_conv_t<1>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
+  }
+}
+
+// ---------------------------------------------------------------------------- build
+fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  for (int a = 0; a < 3; ++a) {
+    K->P[a] = smooth_padded_size(K->grid.dims[a], false);
+    K->H[a] = K->P[a] / 2 + 1;
+    if (!make_plan_radices(K->P[a], K->plan[a]))
+      return set_error(FUSG_INVALID_ARGUMENT, "no FFT plan for padded length");
+    FUSG_TRY(upload_twiddles(K->P[a], &K->tw[a]));
+    K->plan[a].tw = K->tw[a];
+  }
+  const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
+  const int Hx = K->H[0], Hy = K->H[1], Hz = K->H[2];
+  const size_t nA = size_t(Px) * Ny * Nz, nB = size_t(Px) * Py * Nz;
+  const size_t nK = size_t(Hx) * Hy * Hz;
+  if (cudaMalloc(&K->bufA, nA * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc(&K->bufB, nB * sizeof(double2)) != cudaSuccess ||
+      cudaMalloc(&K->koct, nK * sizeof(double2)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(FUSG_OOM, "GreenKernel: device allocation failed");
+  }
+  K->bytes = (nA + nB + nK) * sizeof(double2);
+
+  fusg_ctx* ctx = K->ctx;
+  cudaStream_t s = ctx->stream;
+  const double dx = K->grid.dx;
+  // G1: generate K along x for offsets (oy, oz) >= 0, forward x, keep kx <= Px/2
+  KGenF gen{Nx, Ny, Px, dx, dx * dx * dx, K->k.k_re, K->k.k_im, self};
+  GStoreF s1{GStore{K->bufA, Hx, 0, 1, Hx, 1.0}};
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, gen, s1, s));
+  // G2: even extension along y, forward y, keep ky <= Py/2
+  FoldF l2{K->bufA, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
+  GStoreF s2{GStore{K->bufB, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Hx, Nz, l2, s2, s));
+  // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant
+  FoldF l3{K->bufB, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
+  GStoreF s3{GStore{K->koct, 1, Hx, int64_t(Hx) * Hy, Hz, 1.0}};
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[2], Hx, Hy, l3, s3, s));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return FUSG_OK;
+}
+
+// ---------------------------------------------------------------------------- apply
+fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
+                                   cudaStream_t s, cudaEvent_t* ev) {
+  auto mark = [&](int i) {
+    if (ev) cudaEventRecord(ev[i], s);
+  };
+  fusg_ctx* ctx = K->ctx;
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
+  const int64_t PxNy = int64_t(Px) * Ny, PxPy = int64_t(Px) * Py;
+  const double total = double(Px) * double(Py) * double(Pz);
+  mark(0);
+  // A: rows of f (stride Nx) -> rows of A (stride Px)
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{f, Nx, 0, 1, Nx}},
+                              GStoreF{GStore{K->bufA, Px, 0, 1, Px, 1.0}}, s));
+  mark(1);
+  // B: y lines of A (Ny valid) -> y lines of B
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Px, Nz, GLoadF{GLoad{K->bufA, 1, PxNy, Px, Ny}},
+                              GStoreF{GStore{K->bufB, 1, PxPy, Px, Py, 1.0}}, s));
+  mark(2);
+  // C: z lines of B: forward, * K^, inverse, keep Nz
+  FUSG_TRY(launch_conv(ctx, K->plan[2], Px, Py, GLoadF{GLoad{K->bufB, 1, Px, PxPy, Nz}},
+                       GStoreF{GStore{K->bufB, 1, Px, PxPy, Nz, 1.0}},
+                       KOct{K->koct, K->H[0], K->H[1], Px, Py, Pz}, s));
+  mark(3);
+  // D: inverse y, keep Ny -> A
+  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Px, Nz, GLoadF{GLoad{K->bufB, 1, PxPy, Px, Py}},
+                             GStoreF{GStore{K->bufA, 1, PxNy, Px, Ny, 1.0}}, s));
+  mark(4);
+  // E: inverse x, scale, crop -> u
+  FUSG_TRY(launch_axis<true>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{K->bufA, Px, 0, 1, Px}},
+                             GStoreF{GStore{u, Nx, 0, 1, Nx, scale / total}}, s));
+  mark(5);
+  return FUSG_OK;
+}
+
+}  // namespace fusg

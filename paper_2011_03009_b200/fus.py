@@ -1,0 +1,566 @@
+"""Python mirror of the reference's ``namespace fus`` API for the volume-potential path.
+
+Same names, argument meaning and error behaviour as ``/root/reference/proj/include/fus/*.hpp``
+(ValueError <-> std::invalid_argument, IndexError <-> std::out_of_range, RuntimeError <->
+std::runtime_error).  Numerics run in libfusg.so (hand-written sm_100a kernels); host-side
+grid/planner arithmetic runs in the same library's bit-exact C++.  Fields are
+complex128 torch tensors resident on the GPU; numpy arrays are accepted and copied over.
+There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field, replace
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+try:
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+# ------------------------------------------------------------------------ context
+class Context:
+    """One CUDA device + stream (fusg_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().fusg_ctx_create(device, C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    @property
+    def stream_ptr(self) -> int:
+        return lib().fusg_ctx_stream(self.handle) or 0
+
+    def synchronize(self):
+        check(lib().fusg_ctx_synchronize(self.handle))
+
+    def launch_count(self) -> int:
+        return int(lib().fusg_ctx_launch_count(self.handle))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().fusg_ctx_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+_contexts = {}
+
+
+def context(device: Optional[int] = None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device() if torch is not None and torch.cuda.is_available() else 0
+    if device not in _contexts:
+        _contexts[device] = Context(device)
+    return _contexts[device]
+
+
+def _on_device(a, ctx: Context):
+    """complex128 contiguous CUDA tensor view of a field (copies host arrays)."""
+    if torch is None:
+        raise _lib.FusgError("torch is required for device buffers")
+    if isinstance(a, np.ndarray):
+        a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128))
+    if not isinstance(a, torch.Tensor):
+        a = torch.as_tensor(np.asarray(a, dtype=np.complex128))
+    if a.dtype != torch.complex128:
+        a = a.to(torch.complex128)
+    return a.to(f"cuda:{ctx.device}").contiguous().reshape(-1)
+
+
+def _sync_torch_to(ctx: Context):
+    """Order the library's stream after torch's current stream (inputs produced by torch)."""
+    torch.cuda.current_stream(ctx.device).synchronize()
+
+
+# ------------------------------------------------------------------------ L1 types
+@dataclass
+class Medium:
+    """include/fus/medium.hpp:12-23"""
+    name: str
+    rho0: float
+    c0: float
+    beta: float
+    alpha0: float
+    eta: float
+
+    def c(self):
+        return _lib.MediumC(self.rho0, self.c0, self.beta, self.alpha0, self.eta)
+
+
+@dataclass
+class Wavenumber:
+    """include/fus/medium.hpp:26-30"""
+    k: complex
+    harmonic: int
+    omega: float
+
+    def c(self):
+        return _lib.Wave(self.k.real, self.k.imag, self.harmonic, self.omega)
+
+
+K_DB_PER_NEPER = 8.685889638065035
+
+
+def medium_preset(name: str) -> Medium:
+    """src/medium.cpp:47-52"""
+    table = {"water": (1000.0, 1480.0, 3.5, 0.2, 2.0), "liver": (1060.0, 1590.0, 4.4, 90.0, 1.1),
+             "kidney": (1050.0, 1570.0, 4.7, 10.0, 1.0)}
+    if name not in table:
+        raise ValueError(f"unknown medium preset '{name}'")
+    return Medium(name, *table[name])
+
+
+def is_medium_preset(name: str) -> bool:
+    return name in ("water", "liver", "kidney")
+
+
+def complex_wavenumber(m: Medium, f0: float, n: int) -> Wavenumber:
+    """src/medium.cpp:31-45"""
+    w = _lib.Wave()
+    mc = m.c()
+    check(lib().fusg_complex_wavenumber(C.byref(mc), float(f0), int(n), C.byref(w)))
+    return Wavenumber(complex(w.k_re, w.k_im), w.harmonic, w.omega)
+
+
+@dataclass
+class VoxelGrid:
+    """include/fus/grid.hpp:30-50 (x fastest)."""
+    lo: np.ndarray
+    hi: np.ndarray
+    dx: float
+    dims: tuple
+    harmonic: int = 1
+
+    def count(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+    def index(self, ix, iy, iz) -> int:
+        return ix + self.dims[0] * (iy + self.dims[1] * iz)
+
+    def center(self, ix, iy, iz) -> np.ndarray:
+        return np.array([self.lo[0] + (ix + 0.5) * self.dx, self.lo[1] + (iy + 0.5) * self.dx,
+                         self.lo[2] + (iz + 0.5) * self.dx])
+
+    def c(self) -> _lib.Grid:
+        g = _lib.Grid()
+        for a in range(3):
+            g.lo[a], g.hi[a], g.dims[a] = float(self.lo[a]), float(self.hi[a]), int(self.dims[a])
+        g.dx, g.harmonic = float(self.dx), int(self.harmonic)
+        return g
+
+    @staticmethod
+    def from_c(g: _lib.Grid) -> "VoxelGrid":
+        return VoxelGrid(np.array(list(g.lo)), np.array(list(g.hi)), g.dx, tuple(g.dims), g.harmonic)
+
+
+def same_grid(a: VoxelGrid, b: VoxelGrid) -> bool:
+    """src/cascade.cpp:15-17"""
+    return tuple(a.dims) == tuple(b.dims) and a.dx == b.dx and bool(np.all(a.lo == b.lo))
+
+
+def _d3(v):
+    return (C.c_double * 3)(*[float(x) for x in v])
+
+
+def make_grid(lo, hi, dx: float, harmonic: int, anchor=None) -> VoxelGrid:
+    """src/grid.cpp:12-34"""
+    g = _lib.Grid()
+    anc = _d3(anchor) if anchor is not None else None
+    check(lib().fusg_make_grid(_d3(lo), _d3(hi), float(dx), int(harmonic), anc, C.byref(g)))
+    return VoxelGrid.from_c(g)
+
+
+@dataclass
+class HarmonicField:
+    """include/fus/grid.hpp:57-61; values is a complex128 CUDA tensor (x fastest)."""
+    grid: VoxelGrid
+    values: "torch.Tensor"
+    wavenumber: Wavenumber
+
+
+def random_vector(n: int, seed: int) -> np.ndarray:
+    """Seeded input exactly like tests/acceptance.cpp:30-36 (host)."""
+    out = np.empty(2 * n, np.float64)
+    check(lib().fusg_random_vector(n, seed, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out.view(np.complex128)
+
+
+# ------------------------------------------------------------------------ potential
+def equivalent_sphere_radius(dx: float) -> float:
+    return float(lib().fusg_equivalent_sphere_radius(float(dx)))
+
+
+def self_weight(k: Wavenumber, dx: float) -> complex:
+    """src/potential.cpp:59-70"""
+    out = (C.c_double * 2)()
+    w = k.c()
+    check(lib().fusg_self_weight(C.byref(w), float(dx), out))
+    return complex(out[0], out[1])
+
+
+def green_function(x, y, k: Wavenumber) -> complex:
+    """src/potential.cpp:47-53 (scalar helper)"""
+    d = np.asarray(x, float) - np.asarray(y, float)
+    r = math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+    if r < 1e-300:
+        raise ValueError("green_function: singular at x == y")
+    mag = math.exp(-k.k.imag * r) / (4.0 * math.pi * r)
+    return complex(mag * math.cos(k.k.real * r), mag * math.sin(k.k.real * r))
+
+
+def next_fast_size(n: int) -> int:
+    return int(lib().fusg_next_fast_size(int(n)))
+
+
+class GreenKernel:
+    """GreenKernel (include/fus/potential.hpp:28-48): octant spectrum cached on the GPU."""
+
+    def __init__(self, grid: VoxelGrid, k: Wavenumber, pad_small_primes: bool = False,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or context()
+        self._grid, self._k = grid, k
+        h = C.c_void_p()
+        g, w = grid.c(), k.c()
+        check(lib().fusg_kernel_create(self.ctx.handle, C.byref(g), C.byref(w),
+                                       int(bool(pad_small_primes)), C.byref(h)))
+        self.handle = h
+        p = (C.c_int32 * 3)()
+        check(lib().fusg_kernel_padded(h, p))
+        self.padded = tuple(p)
+
+    def grid(self) -> VoxelGrid:
+        return self._grid
+
+    def wavenumber(self) -> Wavenumber:
+        return self._k
+
+    def device_bytes(self) -> int:
+        return int(lib().fusg_kernel_device_bytes(self.handle))
+
+    def apply(self, f, scale: float = 1.0, out=None):
+        """u = scale * apply(f) (src/potential.cpp:120-151); f: N complex128 (tensor/array).
+        Returns a CUDA tensor; synchronous with respect to torch's current stream."""
+        if isinstance(f, HarmonicField):
+            return HarmonicField(self._grid, self.apply(f.values, scale), self._k)
+        n = self._grid.count()
+        if (f.numel() if torch is not None and isinstance(f, torch.Tensor) else np.size(f)) != n:
+            raise ValueError("GreenKernel::apply: field size does not match kernel grid")
+        fd = _on_device(f, self.ctx)
+        u = out if out is not None else torch.empty(n, dtype=torch.complex128, device=fd.device)
+        _sync_torch_to(self.ctx)
+        check(lib().fusg_kernel_apply(self.handle, fd.data_ptr(), u.data_ptr(), float(scale), None))
+        self.ctx.synchronize()
+        return u
+
+    def apply_async(self, f_ptr: int, u_ptr: int, scale: float = 1.0, stream: int = 0):
+        """Raw device-pointer apply on `stream` (0 = context stream); no synchronisation."""
+        check(lib().fusg_kernel_apply(self.handle, f_ptr, u_ptr, float(scale), stream or None))
+
+    def apply_host(self, f: np.ndarray, scale: float = 1.0) -> np.ndarray:
+        """Host-vector drop-in (GreenKernel::apply(const VectorXcd&)): H2D, apply, D2H."""
+        f = np.ascontiguousarray(f, np.complex128).reshape(-1)
+        if f.size != self._grid.count():
+            raise ValueError("GreenKernel::apply: field size does not match kernel grid")
+        u = np.empty_like(f)
+        check(lib().fusg_kernel_apply_host(self.handle, f.ctypes.data, u.ctypes.data, float(scale)))
+        return u
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().fusg_kernel_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def padded_dims(grid: VoxelGrid, pad_small_primes: bool = False) -> tuple:
+    out = (C.c_int32 * 3)()
+    g = grid.c()
+    check(lib().fusg_padded_dims(C.byref(g), int(pad_small_primes), out))
+    return tuple(out)
+
+
+# ------------------------------------------------------------------------ transducer
+@dataclass
+class BowlTransducer:
+    """include/fus/transducer.hpp:15-28"""
+    name: str
+    f0: float
+    focal_length: float
+    outer_radius: float
+    power: float
+    source_points: np.ndarray
+
+    def focus(self):
+        return np.array([self.focal_length, 0.0, 0.0])
+
+    def cap_area(self) -> float:
+        l, R = self.focal_length, self.outer_radius
+        return 2.0 * math.pi * l * (l - math.sqrt(l * l - R * R))
+
+    def rim_plane_x(self) -> float:
+        l, R = self.focal_length, self.outer_radius
+        return l - math.sqrt(l * l - R * R)
+
+    def _src(self):
+        self._pts = np.ascontiguousarray(self.source_points, np.float64)
+        return self._pts.ctypes.data_as(C.POINTER(C.c_double)), len(self._pts)
+
+    def c(self) -> _lib.Bowl:
+        p, n = self._src()
+        return _lib.Bowl(self.f0, self.focal_length, self.outer_radius, self.power, n, p)
+
+
+def distribute_points(l: float, R: float, n: int) -> np.ndarray:
+    """src/transducer.cpp:22-70"""
+    out = np.empty(3 * int(n), np.float64)
+    check(lib().fusg_distribute_points(float(l), float(R), int(n),
+                                       out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out.reshape(-1, 3)
+
+
+def make_bowl(name, f0, l, R, power, n_points) -> BowlTransducer:
+    """src/transducer.cpp:72-84"""
+    if f0 <= 0.0:
+        raise ValueError("make_bowl: f0 must be positive")
+    if power < 0.0:
+        raise ValueError("make_bowl: power must be >= 0")
+    return BowlTransducer(name, f0, l, R, power, distribute_points(l, R, n_points))
+
+
+def transducer_preset(name: str, power: float = 100.0, n_points: int = 4096) -> BowlTransducer:
+    """src/transducer.cpp:86-92"""
+    if name == "H101":
+        return make_bowl("H101", 1.1e6, 63.2e-3, 32.0e-3, power, n_points)
+    if name == "H131":
+        return make_bowl("H131", 1.1e6, 35.0e-3, 16.5e-3, power, n_points)
+    raise ValueError(f"unknown transducer preset '{name}'")
+
+
+def unnormalized_field(t: BowlTransducer, pts, k: Wavenumber, amp: Optional[float] = None,
+                       ctx: Optional[Context] = None):
+    """src/transducer.cpp:123-132; returns a CUDA tensor."""
+    ctx = ctx or context()
+    if amp is None:
+        amp = t.cap_area() / float(len(t.source_points))
+    p = torch.as_tensor(np.ascontiguousarray(np.asarray(pts, float).reshape(-1, 3))).to(f"cuda:{ctx.device}")
+    out = torch.empty(p.shape[0], dtype=torch.complex128, device=p.device)
+    sp, n = t._src()
+    _sync_torch_to(ctx)
+    check(lib().fusg_monopole_points(ctx.handle, sp, n, p.data_ptr(), p.shape[0], k.k.real,
+                                     k.k.imag, float(amp), out.data_ptr(), None))
+    return out
+
+
+def radiated_power(t: BowlTransducer, m: Medium, k: Wavenumber, amplitude_scale: float,
+                   n_r: int = 384, n_theta: int = 256, ctx: Optional[Context] = None) -> float:
+    """src/transducer.cpp:134-155"""
+    ctx = ctx or context()
+    amp = amplitude_scale * t.cap_area() / float(len(t.source_points))
+    sp, n = t._src()
+    out = C.c_double()
+    check(lib().fusg_radiated_power(ctx.handle, sp, n, t.rim_plane_x(), t.outer_radius, k.k.real,
+                                    k.k.imag, amp, m.rho0, m.c0, int(n_r), int(n_theta),
+                                    C.byref(out)))
+    return out.value
+
+
+def power_scale_factor(t: BowlTransducer, m: Medium, k: Wavenumber) -> float:
+    """src/transducer.cpp:157-163"""
+    if t.power == 0.0:
+        return 0.0
+    pw = radiated_power(t, m, k, 1.0)
+    if pw <= 0.0:
+        raise RuntimeError("power normalization: degenerate field, Pi(p) = 0")
+    return math.sqrt(t.power / pw)
+
+
+def evaluate_first_harmonic(t: BowlTransducer, m: Medium, grid: VoxelGrid, amplitude_scale: float,
+                            ctx: Optional[Context] = None) -> HarmonicField:
+    """src/transducer.cpp:179-196"""
+    ctx = ctx or context()
+    k1 = complex_wavenumber(m, t.f0, 1)
+    amp = amplitude_scale * t.cap_area() / float(len(t.source_points))
+    out = torch.empty(grid.count(), dtype=torch.complex128, device=f"cuda:{ctx.device}")
+    sp, n = t._src()
+    g = grid.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_monopole_grid(ctx.handle, sp, n, C.byref(g), k1.k.real, k1.k.imag, amp,
+                                   out.data_ptr(), None))
+    return HarmonicField(grid, out, k1)
+
+
+def evaluate_source_field(t: BowlTransducer, m: Medium, grid: VoxelGrid):
+    """src/transducer.cpp:198-206 -> (field, normalization)"""
+    k1 = complex_wavenumber(m, t.f0, 1)
+    scale = power_scale_factor(t, m, k1)
+    f = evaluate_first_harmonic(t, m, grid, scale)
+    return f, (scale if scale > 0.0 else 1.0)
+
+
+# ------------------------------------------------------------------------ planner
+@dataclass
+class PlannedGrid:
+    harmonic: int
+    domain_lo: np.ndarray
+    domain_hi: np.ndarray
+    grid: VoxelGrid
+
+
+@dataclass
+class MeshPlan:
+    """include/fus/grid.hpp:71-84"""
+    grids: List[PlannedGrid]
+    reference: VoxelGrid
+    d: float
+    w: float
+    focus: np.ndarray
+    n_w: int
+
+    def for_harmonic(self, n: int) -> PlannedGrid:
+        for pg in self.grids:
+            if pg.harmonic == n:
+                return pg
+        raise IndexError(f"MeshPlan: no grid planned for harmonic {n}")
+
+    def reduction_factor(self, n: int) -> float:
+        return float(self.reference.count()) / float(self.for_harmonic(n).grid.count())
+
+
+def _plan(t, m, d, n_w, n_h, width_scale, single):
+    nh = max(int(n_h) - 1, 0)
+    grids = (_lib.Grid * max(nh, 1))()
+    lo = (C.c_double * (3 * max(nh, 1)))()
+    hi = (C.c_double * (3 * max(nh, 1)))()
+    ref = _lib.Grid()
+    w = C.c_double()
+    tb, mc = t.c(), m.c()
+    check(lib().fusg_plan_nested_meshes(C.byref(tb), C.byref(mc), float(d), int(n_w), int(n_h),
+                                        float(width_scale), int(single), grids, lo, hi,
+                                        C.byref(ref), C.byref(w)))
+    pgs = [PlannedGrid(i + 2, np.array(lo[3 * i:3 * i + 3]), np.array(hi[3 * i:3 * i + 3]),
+                       VoxelGrid.from_c(grids[i])) for i in range(nh)]
+    return MeshPlan(pgs, VoxelGrid.from_c(ref), float(d), w.value, t.focus(), int(n_w))
+
+
+def plan_nested_meshes(t, m, d, n_w, n_harmonics, width_scale=1.0) -> MeshPlan:
+    """src/grid.cpp:81-112"""
+    return _plan(t, m, d, n_w, n_harmonics, width_scale, False)
+
+
+def plan_single_mesh(t, m, d, n_w, n_harmonics, width_scale=1.0) -> MeshPlan:
+    """src/cascade.cpp:109-118"""
+    return _plan(t, m, d, n_w, n_harmonics, width_scale, True)
+
+
+def interpolate(fld: HarmonicField, target: VoxelGrid, ctx: Optional[Context] = None) -> HarmonicField:
+    """src/grid.cpp:141-195"""
+    ctx = ctx or context()
+    v = _on_device(fld.values, ctx)
+    if v.numel() != fld.grid.count():
+        raise ValueError("interpolate: field size does not match its grid")
+    out = torch.empty(target.count(), dtype=torch.complex128, device=v.device)
+    sg, tg = fld.grid.c(), target.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_interpolate(ctx.handle, C.byref(sg), v.data_ptr(), C.byref(tg), out.data_ptr(), None))
+    ctx.synchronize()
+    return HarmonicField(target, out, fld.wavenumber)
+
+
+# ------------------------------------------------------------------------ cascade
+def rhs_source(n: int, lower: Sequence[HarmonicField], m: Medium, omega: float,
+               ctx: Optional[Context] = None):
+    """src/cascade.cpp:21-40; returns a CUDA tensor."""
+    ctx = ctx or context()
+    if n < 2:
+        raise ValueError("rhs_source: harmonic index must be >= 2")
+    if len(lower) < n - 1:
+        raise ValueError(f"rhs_source: missing lower harmonics for n = {n}")
+    vals = [_on_device(h.values, ctx) for h in lower[: n - 1]]
+    count = vals[0].numel()
+    if any(v.numel() != count for v in vals):
+        raise ValueError("rhs_source: lower harmonics live on different grids")
+    ptrs = (C.c_void_p * len(vals))(*[v.data_ptr() for v in vals])
+    out = torch.empty(count, dtype=torch.complex128, device=vals[0].device)
+    mc = m.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_rhs_source(ctx.handle, int(n), ptrs, count, C.byref(mc), float(omega),
+                                out.data_ptr(), None))
+    ctx.synchronize()
+    return out
+
+
+@dataclass
+class CascadeConfig:
+    """include/fus/cascade.hpp:12-21"""
+    medium: Medium
+    transducer: BowlTransducer
+    plan: MeshPlan
+    n_harmonics: int = 5
+    recompute_p1_each_grid: bool = False
+    pad_small_primes: bool = False
+
+
+@dataclass
+class StageTiming:
+    """include/fus/cascade.hpp:25-32 (+ p1_s, rhs_s)"""
+    harmonic: int
+    voxels: int
+    meshing_s: float
+    interpolation_s: float
+    kernel_s: float
+    potential_s: float
+    p1_s: float = 0.0
+    rhs_s: float = 0.0
+
+
+@dataclass
+class CascadeResult:
+    """include/fus/cascade.hpp:34-40"""
+    harmonics: List[HarmonicField] = field(default_factory=list)
+    timings: List[StageTiming] = field(default_factory=list)
+    source_normalization: float = 1.0
+
+    def p(self, n: int) -> HarmonicField:
+        return self.harmonics[n - 1]
+
+
+def run_cascade(cfg: CascadeConfig, ctx: Optional[Context] = None) -> CascadeResult:
+    """src/cascade.cpp:42-107, device resident (fusg_run_cascade)."""
+    ctx = ctx or context()
+    n = int(cfg.n_harmonics)
+    if n < 2:
+        raise ValueError("run_cascade: n_harmonics must be >= 2")
+    grids = [cfg.plan.for_harmonic(i).grid for i in range(2, n + 1)]
+    cg = (_lib.Grid * len(grids))(*[g.c() for g in grids])
+    dev = f"cuda:{ctx.device}"
+    outs = [torch.empty(grids[max(i - 1, 0)].count(), dtype=torch.complex128, device=dev)
+            for i in range(n)]
+    ptrs = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    rows = (_lib.StageTiming * (n - 1))()
+    norm = C.c_double()
+    desc = _lib.CascadeDesc(cfg.medium.c(), cfg.transducer.c(), cg, n,
+                            int(cfg.recompute_p1_each_grid), int(cfg.pad_small_primes))
+    _sync_torch_to(ctx)
+    check(lib().fusg_run_cascade(ctx.handle, C.byref(desc), ptrs, rows, C.byref(norm)))
+    res = CascadeResult(source_normalization=norm.value)
+    for i in range(n):
+        g = grids[max(i - 1, 0)]
+        k = complex_wavenumber(cfg.medium, cfg.transducer.f0, i + 1)
+        res.harmonics.append(HarmonicField(g, outs[i], k))
+    for r in rows:
+        res.timings.append(StageTiming(r.harmonic, int(r.voxels), r.meshing_s, r.interpolation_s,
+                                       r.kernel_s, r.potential_s, r.p1_s, r.rhs_s))
+    return res

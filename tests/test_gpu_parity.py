@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the pinned CPU oracle.
+
+Tolerances: the reference's own (1e-12 / 1e-13 for the FFT-free known-answer tests) and
+north_star's relative L2 <= 1e-10 per complex128 field; integer/index work (grids, crop,
+interpolation, rhs) must be bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2011_03009_b200 import fus  # noqa: E402
+
+
+def rel_l2(a, b):
+    a = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    b = b.cpu().numpy() if hasattr(b, "cpu") else np.asarray(b)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return fus.context(0)
+
+
+def water():
+    return fus.medium_preset("water")
+
+
+# ------------------------------------------------------------------ volume potential KATs
+@pytest.mark.parametrize("seed,pad", [(1234, False), (1234, True), (2024, False)])
+def test_apply_matches_direct_20x18x16(ctx, orc, seed, pad):
+    # tests/test_potential.cpp:75-92, tests/acceptance.cpp:98-112 (< 1e-12 rel max-norm)
+    g = fus.make_grid([0, 0, 0], [20e-4, 18e-4, 16e-4], 1e-4, 2)
+    assert g.dims == (20, 18, 16)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), seed)
+    u = host(fus.GreenKernel(g, k, pad).apply(f))
+    go = orc.make_grid([0, 0, 0], [20e-4, 18e-4, 16e-4], 1e-4, 2)
+    ref = orc.direct_potential_oracle(orc.complex_wavenumber(orc.medium_preset("water"), 1.1e6, 2), go, f)
+    assert np.max(np.abs(u - ref)) < 1e-12 * np.max(np.abs(ref))
+
+
+def test_delta_reproduces_kernel_column(ctx):
+    # tests/test_potential.cpp:117-139 (1e-13 rel + 1e-20 abs; exact crop and indexing)
+    g = fus.make_grid([0, 0, 0], [9e-4, 8e-4, 7e-4], 1e-4, 1)
+    k = fus.complex_wavenumber(water(), 1.1e6, 1)
+    delta = np.zeros(g.count(), np.complex128)
+    j = g.index(4, 3, 2)
+    delta[j] = 1.0
+    col = host(fus.GreenKernel(g, k).apply(delta))
+    vol = g.dx ** 3
+    xj = g.center(4, 3, 2)
+    for iz in range(g.dims[2]):
+        for iy in range(g.dims[1]):
+            for ix in range(g.dims[0]):
+                i = g.index(ix, iy, iz)
+                want = fus.self_weight(k, g.dx) if i == j else vol * fus.green_function(g.center(ix, iy, iz), xj, k)
+                assert abs(col[i] - want) < 1e-13 * abs(want) + 1e-20
+
+
+def test_apply_linear_and_translation_covariant(ctx):
+    # tests/test_potential.cpp:94-115
+    g = fus.make_grid([-3e-3, 1e-3, 0], [2e-3, 6e-3, 4e-3], 5e-4, 1)
+    k = fus.complex_wavenumber(water(), 1.1e6, 1)
+    K = fus.GreenKernel(g, k)
+    f, h = fus.random_vector(g.count(), 7), fus.random_vector(g.count(), 8)
+    a = complex(0.3, -1.7)
+    lhs = host(K.apply(a * f + h))
+    rhs = a * host(K.apply(f)) + host(K.apply(h))
+    assert np.max(np.abs(lhs - rhs)) < 1e-12 * np.max(np.abs(rhs))
+    off = np.array([11e-3, -4e-3, 9e-3])
+    K2 = fus.GreenKernel(fus.VoxelGrid(g.lo + off, g.hi + off, g.dx, g.dims, 1), k)
+    u = host(K.apply(f))
+    assert np.max(np.abs(host(K2.apply(f)) - u)) < 1e-12 * np.max(np.abs(u))
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (1, 5, 3), (7, 6, 5), (13, 11, 2), (33, 1, 9),
+                                  (16, 16, 16), (25, 30, 7), (64, 3, 40)])
+def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
+    dx = 1e-4
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    assert g.dims == dims
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), 99)
+    u = host(fus.GreenKernel(g, k).apply(f))
+    go = orc.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    ko = orc.complex_wavenumber(orc.medium_preset("water"), 1.1e6, 2)
+    ref = orc.GreenKernel(go, ko).apply(f)
+    assert rel_l2(u, ref) <= 1e-12
+    if g.count() <= 4000:
+        d = orc.direct_potential_oracle(ko, go, f)
+        assert np.max(np.abs(u - d)) < 1e-12 * np.max(np.abs(d))
+
+
+def cfg1_grid():
+    c, f = 1540.0, 1.1e6
+    h = (c / f) / 6.0
+    return fus.make_grid([0, 0, 0], [64 * h, 64 * h, 64 * h], h, 1), fus.Wavenumber(
+        complex(2 * math.pi * f / c, 0.0), 1, 2 * math.pi * f)
+
+
+def test_config1_64cubed_vs_oracle(ctx, orc):
+    # BASELINE config 1: 64^3, h = lambda/6 at 1.1 MHz, c = 1540, iid U[-1,1] seed 1234
+    g, k = cfg1_grid()
+    assert g.dims == (64, 64, 64)
+    f = fus.random_vector(g.count(), 1234)
+    K = fus.GreenKernel(g, k)
+    assert K.padded == (128, 128, 128)
+    u = K.apply(f)
+    go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 1)
+    ref = orc.GreenKernel(go, orc.Wavenumber(k.k, 1, k.omega), workers=8).apply(f)
+    assert rel_l2(u, ref) <= 1e-10
+    # host-vector drop-in gives the same bits as the device apply
+    assert np.array_equal(K.apply_host(f), host(u))
+    # scale argument: -apply
+    assert np.array_equal(host(K.apply(f, -1.0)), -host(u))
+
+
+def cfg2_source(g, seed=2024):
+    f = fus.random_vector(g.count(), seed).reshape(g.dims[2], g.dims[1], g.dims[0])
+    c = 0.5 * (g.lo + g.hi)
+    sig = 0.2 * (g.hi[0] - g.lo[0])
+    x = g.lo[0] + (np.arange(g.dims[0]) + 0.5) * g.dx
+    y = g.lo[1] + (np.arange(g.dims[1]) + 0.5) * g.dx
+    z = g.lo[2] + (np.arange(g.dims[2]) + 0.5) * g.dx
+    r2 = ((x - c[0]) ** 2)[None, None, :] + ((y - c[1]) ** 2)[None, :, None] + ((z - c[2]) ** 2)[:, None, None]
+    return (f * np.exp(-r2 / (2 * sig * sig))).reshape(-1)
+
+
+def cfg2_grid():
+    c, f0 = 1540.0, 1.1e6
+    k2 = 2 * 2 * math.pi * f0 / c
+    h = (c / (2 * f0)) / 6.0
+    return fus.make_grid([0, 0, 0], [256 * h] * 3, h, 2), fus.Wavenumber(complex(k2, 0.0), 2, 2 * math.pi * f0)
+
+
+def test_config2_256cubed_vs_oracle(ctx, orc):
+    g, k = cfg2_grid()
+    assert g.dims == (256, 256, 256)
+    f = cfg2_source(g)
+    K = fus.GreenKernel(g, k)
+    assert K.padded == (512, 512, 512)
+    u = K.apply(f)
+    go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 2)
+    ref = orc.GreenKernel(go, orc.Wavenumber(k.k, 2, k.omega), workers=16).apply(f)
+    assert rel_l2(u, ref) <= 1e-10
+
+
+# ------------------------------------------------------------------ incident field
+def test_monopole_grid_and_points_vs_oracle(ctx, orc):
+    t = fus.transducer_preset("H131", 100.0, 4096)
+    to = orc.transducer_preset("H131", 100.0, 4096)
+    w, wo = water(), orc.medium_preset("water")
+    plan = fus.plan_nested_meshes(t, w, 6e-3, 2, 2, 0.3)
+    g = plan.for_harmonic(2).grid
+    p = fus.evaluate_first_harmonic(t, w, g, 3.0)
+    go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 2)
+    ref = orc.evaluate_first_harmonic(to, wo, go, 3.0).values
+    assert rel_l2(p.values, ref) <= 1e-12
+    k = fus.complex_wavenumber(w, t.f0, 1)
+    xs = [[10e-3 + i * (35e-3 / 400.0), 0, 0] for i in range(400)]
+    pp = fus.unnormalized_field(t, xs, k)
+    ref = orc.unnormalized_field(to, xs, orc.complex_wavenumber(wo, to.f0, 1))
+    assert rel_l2(pp, ref) <= 1e-12
+
+
+def test_monopole_coincidence_raises(ctx):
+    t = fus.transducer_preset("H131", 100.0, 16)
+    k = fus.complex_wavenumber(water(), t.f0, 1)
+    with pytest.raises(ValueError):
+        fus.unnormalized_field(t, [t.source_points[3]], k)
+    # the context stays usable afterwards
+    assert fus.unnormalized_field(t, [[20e-3, 0, 0]], k).shape[0] == 1
+
+
+def test_radiated_power_vs_oracle(ctx, orc):
+    t = fus.transducer_preset("H131", 40.0, 512)
+    to = orc.transducer_preset("H131", 40.0, 512)
+    w, wo = water(), orc.medium_preset("water")
+    k, ko = fus.complex_wavenumber(w, t.f0, 1), orc.complex_wavenumber(wo, to.f0, 1)
+    for (nr, nt) in ((96, 64), (384, 256)):
+        a = fus.radiated_power(t, w, k, 1.0, nr, nt)
+        b = orc.radiated_power(to, wo, ko, 1.0, nr, nt)
+        assert abs(a - b) <= 1e-12 * abs(b)
+    s = fus.power_scale_factor(t, w, k)
+    assert fus.radiated_power(t, w, k, s) == pytest.approx(40.0, rel=1e-12)
+    # deterministic: identical bits on repeat
+    assert fus.radiated_power(t, w, k, 1.0) == fus.radiated_power(t, w, k, 1.0)
+
+
+# ------------------------------------------------------------------ transfer + source (bit-exact)
+def test_interpolate_bit_exact(ctx, orc):
+    w = water()
+    k = fus.complex_wavenumber(w, 1.1e6, 1)
+    src = fus.make_grid([0, 0, 0], [8e-3] * 3, 1e-3, 1)
+    for tgt in (fus.make_grid([1e-3] * 3, [7e-3] * 3, 0.4e-3, 2),
+                fus.make_grid([-0.5e-3] * 3, [8.5e-3] * 3, 0.37e-3, 3),
+                fus.make_grid([0, 0, 0], [8e-3, 8e-3, 1e-3], 1e-3, 1)):
+        f = fus.random_vector(src.count(), 5)
+        out = fus.interpolate(fus.HarmonicField(src, f, k), tgt)
+        so = orc.VoxelGrid(src.lo, src.hi, src.dx, src.dims)
+        to = orc.VoxelGrid(tgt.lo, tgt.hi, tgt.dx, tgt.dims)
+        ref = orc.interpolate(orc.HarmonicField(so, f, None), to).values
+        assert np.array_equal(host(out.values), ref)
+    with pytest.raises(ValueError):
+        fus.interpolate(fus.HarmonicField(src, fus.random_vector(src.count(), 1), k),
+                        fus.make_grid([0, 0, 0], [20e-3, 8e-3, 8e-3], 1e-3, 1))
+
+
+def test_rhs_source_bit_exact(ctx, orc):
+    w, wo = water(), orc.medium_preset("water")
+    g = fus.make_grid([0, 0, 0], [10e-3, 7e-3, 5e-3], 1e-3, 1)
+    omega = 2 * math.pi * 1.1e6
+    fields = [fus.random_vector(g.count(), 10 + i) for i in range(5)]
+    for n in (2, 3, 4, 6):
+        lower = [fus.HarmonicField(g, fields[i], None) for i in range(n - 1)]
+        got = host(fus.rhs_source(n, lower, w, omega))
+        lo = [orc.HarmonicField(None, fields[i], None) for i in range(n - 1)]
+        assert np.array_equal(got, orc.rhs_source(n, lo, wo, omega))
+    with pytest.raises(ValueError):
+        fus.rhs_source(1, [], w, omega)
+
+
+# ------------------------------------------------------------------ recursion
+def tiny(n_h, power, lib):
+    w = lib.medium_preset("water")
+    t = lib.transducer_preset("H131", power, 128)
+    t.f0 = 0.25e6
+    return lib.CascadeConfig(w, t, lib.plan_nested_meshes(t, w, 6e-3, 3, n_h, 0.35), n_h)
+
+
+def test_cascade_vs_oracle_tiny(ctx, orc):
+    # tests/test_cascade.cpp:19-27 tiny_config, 3 harmonics: each field <= 1e-10 rel L2
+    r = fus.run_cascade(tiny(3, 20.0, fus))
+    ro = orc.run_cascade(tiny(3, 20.0, orc))
+    assert len(r.harmonics) == 3 and len(r.timings) == 2
+    for n in (1, 2, 3):
+        assert r.p(n).grid.dims == ro.p(n).grid.dims
+        assert rel_l2(r.p(n).values, ro.p(n).values) <= 1e-10, n
+    assert r.source_normalization == pytest.approx(ro.source_normalization, rel=1e-12)
+    assert [t.harmonic for t in r.timings] == [2, 3]
+    assert r.timings[0].voxels == r.p(2).grid.count()
+
+
+def test_cascade_homogeneity_and_determinism(ctx):
+    # tests/test_cascade.cpp:84-106 and acceptance criterion 7
+    r1 = fus.run_cascade(tiny(3, 10.0, fus))
+    r4 = fus.run_cascade(tiny(3, 40.0, fus))
+    for n, s in ((1, 2.0), (2, 4.0), (3, 8.0)):
+        a, b = host(r4.p(n).values), s * host(r1.p(n).values)
+        assert np.linalg.norm(a - b) / np.linalg.norm(host(r1.p(n).values)) < 1e-12
+    again = fus.run_cascade(tiny(3, 10.0, fus))
+    for n in (1, 2, 3):
+        assert torch.equal(again.p(n).values, r1.p(n).values)
+
+
+def test_cascade_recompute_p1_and_single_mesh(ctx, orc):
+    cfg, cfgo = tiny(3, 20.0, fus), tiny(3, 20.0, orc)
+    cfg.recompute_p1_each_grid = cfgo.recompute_p1_each_grid = True
+    r, ro = fus.run_cascade(cfg), orc.run_cascade(cfgo)
+    for n in (1, 2, 3):
+        assert rel_l2(r.p(n).values, ro.p(n).values) <= 1e-10
+    t, to = cfg.transducer, cfgo.transducer
+    cfg.plan = fus.plan_single_mesh(t, cfg.medium, 6e-3, 3, 3, 0.35)
+    cfgo.plan = orc.plan_single_mesh(to, cfgo.medium, 6e-3, 3, 3, 0.35)
+    r, ro = fus.run_cascade(cfg), orc.run_cascade(cfgo)
+    for n in (1, 2, 3):
+        assert rel_l2(r.p(n).values, ro.p(n).values) <= 1e-10
+
+
+def test_launch_counter_counts_library_kernels(ctx):
+    g, k = cfg1_grid()
+    K = fus.GreenKernel(g, k)
+    before = ctx.launch_count()
+    K.apply(fus.random_vector(g.count(), 3))
+    assert ctx.launch_count() - before == 5  # passes A..E
