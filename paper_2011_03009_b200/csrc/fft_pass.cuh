@@ -12,6 +12,10 @@
 // Stockham autosort, radix R, Ns = product of the radices already applied:
 //   j in [0, L/R): k = j mod Ns; v[r] = x[j + r L/R] * w_{Ns R}^{r k}; v = DFT_R(v);
 //   y[(j / Ns) Ns R + k + r Ns] = v[r]
+//
+// Endpoints see (pos, e): pos is the line position, e in [0, kMaxElems) the thread-local
+// element slot (compile-time after unrolling), so an endpoint may keep per-element state in
+// registers (pass C's spectral multiply does).
 #pragma once
 #include <cstdint>
 
@@ -21,44 +25,37 @@
 namespace fusg {
 
 // ------------------------------------------------------------------ stage
-// One Stockham stage of runtime radix R in {2,3,4,5,7,8,16}.  A thread owns up to
-// B = 16 / R butterflies (j = jt + b * tpl); their R*B <= 16 values live in one fixed
-// register array v[16] whose element e maps to (b, r) = (e / R, e % R).  Element indices are
+// One Stockham stage of runtime radix R in {2,3,4,5,7,8}.  A thread owns up to
+// B = kMaxElems / R butterflies (j = jt + b * tpl); their values live in one fixed register
+// array v[kMaxElems] whose element e maps to (b, r) = (e / R, e % R).  Element indices are
 // compile-time everywhere (unrolled loops, per-radix switch arms), so v stays in registers.
-// Src: double2 load(int pos) for the first stage; Dst: store(int pos, double2) for the last.
 template <bool INV>
 __device__ __forceinline__ void dft_block(int R, double2* v) {
+  static_assert(kMaxElems == 8, "dft_block is written for 8 elements per thread");
   switch (R) {
     case 2:
 #pragma unroll
-      for (int b = 0; b < 8; ++b) dft<2, INV>(v + 2 * b);
+      for (int b = 0; b < 4; ++b) dft<2, INV>(v + 2 * b);
       break;
     case 3:
 #pragma unroll
-      for (int b = 0; b < 5; ++b) dft<3, INV>(v + 3 * b);
+      for (int b = 0; b < 2; ++b) dft<3, INV>(v + 3 * b);
       break;
     case 4:
 #pragma unroll
-      for (int b = 0; b < 4; ++b) dft<4, INV>(v + 4 * b);
+      for (int b = 0; b < 2; ++b) dft<4, INV>(v + 4 * b);
       break;
-    case 5:
-#pragma unroll
-      for (int b = 0; b < 3; ++b) dft<5, INV>(v + 5 * b);
-      break;
-    case 7:
-#pragma unroll
-      for (int b = 0; b < 2; ++b) dft<7, INV>(v + 7 * b);
-      break;
-    case 8:
-#pragma unroll
-      for (int b = 0; b < 2; ++b) dft<8, INV>(v + 8 * b);
-      break;
-    case 16:
-      dft<16, INV>(v);
-      break;
-    default:
-      break;
+    case 5: dft<5, INV>(v); break;
+    case 7: dft<7, INV>(v); break;
+    case 8: dft<8, INV>(v); break;
+    default: break;
   }
+}
+
+// slot e -> (b, r) for radix R
+__device__ __forceinline__ void slot(int e, int R, int& b, int& r) {
+  b = e / R;
+  r = e - b * R;
 }
 
 template <bool INV, int T, bool FIRST, bool LAST, class Src, class Dst>
@@ -69,51 +66,43 @@ __device__ __forceinline__ void fft_stage(const AxisPlan& pl, int R, int Ns, dou
   const int B = kMaxElems / R;
   const int tws = L / (Ns * R);
   double2 v[kMaxElems];
-  int pos[kMaxElems];
-  bool val[kMaxElems];
-  {
-    int b = 0, r = 0;
-#pragma unroll
-    for (int e = 0; e < kMaxElems; ++e) {
-      const int j = jt + b * pl.tpl;
-      val[e] = (b < B) && (j < nb);
-      pos[e] = j + r * nb;
-      if (++r == R) { r = 0; ++b; }
-    }
-  }
 #pragma unroll
   for (int e = 0; e < kMaxElems; ++e) {
-    if (val[e]) v[e] = FIRST ? src.load(pos[e]) : sm[pos[e] * T + t];
-    else v[e] = make_double2(0.0, 0.0);
+    int b, r;
+    slot(e, R, b, r);
+    const int j = jt + b * pl.tpl;
+    v[e] = make_double2(0.0, 0.0);
+    if (b < B && j < nb) {
+      const int pos = j + r * nb;
+      v[e] = FIRST ? src.load(pos, e) : sm[pos * T + t];
+    }
   }
   // everyone has read this stage's shared-memory inputs before anyone overwrites them
   if ((!FIRST || Src::kSmem) && (!LAST || Dst::kSmem)) __syncthreads();
   if (Ns > 1) {
-    int b = 0, r = 0;
 #pragma unroll
     for (int e = 0; e < kMaxElems; ++e) {
-      if (val[e] && r > 0) {
-        const int j = jt + b * pl.tpl;
+      int b, r;
+      slot(e, R, b, r);
+      const int j = jt + b * pl.tpl;
+      if (r > 0 && b < B && j < nb) {
         const int k = j % Ns;
         const double2 w = __ldg(&pl.tw[r * k * tws]);
         v[e] = INV ? cmulc(v[e], w) : cmul(v[e], w);
       }
-      if (++r == R) { r = 0; ++b; }
     }
   }
   dft_block<INV>(R, v);
-  {
-    int b = 0, r = 0;
 #pragma unroll
-    for (int e = 0; e < kMaxElems; ++e) {
-      if (val[e]) {
-        const int j = jt + b * pl.tpl;
-        const int k = j % Ns;
-        const int p = (j - k) * R + k + r * Ns;  // (j / Ns) * Ns * R + k + r Ns
-        if (LAST) dst.store(p, v[e]);
-        else sm[p * T + t] = v[e];
-      }
-      if (++r == R) { r = 0; ++b; }
+  for (int e = 0; e < kMaxElems; ++e) {
+    int b, r;
+    slot(e, R, b, r);
+    const int j = jt + b * pl.tpl;
+    if (b < B && j < nb) {
+      const int k = j % Ns;
+      const int p = (j - k) * R + k + r * Ns;  // (j / Ns) * Ns * R + k + r Ns
+      if (LAST) dst.store(p, e, v[e]);
+      else sm[p * T + t] = v[e];
     }
   }
   if (!LAST) __syncthreads();  // outputs visible to the next stage (a smem-backed Dst syncs in the caller)
@@ -128,8 +117,19 @@ __device__ __forceinline__ void fft_line(const AxisPlan& pl, double2* sm, int t,
     return;
   }
   fft_stage<INV, T, true, false>(pl, pl.radix[0], 1, sm, t, jt, src, dst);
-  for (int s = 1; s < n - 1; ++s) fft_stage<INV, T, false, false>(pl, pl.radix[s], pl.ns[s], sm, t, jt, src, dst);
+  for (int s = 1; s < n - 1; ++s)
+    fft_stage<INV, T, false, false>(pl, pl.radix[s], pl.ns[s], sm, t, jt, src, dst);
   fft_stage<INV, T, false, true>(pl, pl.radix[n - 1], pl.ns[n - 1], sm, t, jt, src, dst);
+}
+
+// Position of element slot e in the first stage (its read position), or -1 if unused.
+__device__ __forceinline__ int first_stage_pos(const AxisPlan& pl, int jt, int e) {
+  const int R = pl.radix[0];
+  const int nb = pl.L / R;
+  int b, r;
+  slot(e, R, b, r);
+  const int j = jt + b * pl.tpl;
+  return (b < kMaxElems / R && j < nb) ? j + r * nb : -1;
 }
 
 // ------------------------------------------------------------------ line addressing
@@ -150,7 +150,7 @@ struct GLoadAt {
   int64_t sp;
   int nvalid;
   bool ok;
-  __device__ __forceinline__ double2 load(int pos) const {
+  __device__ __forceinline__ double2 load(int pos, int) const {
     if (ok && pos < nvalid) return __ldg(base + pos * sp);
     return make_double2(0.0, 0.0);
   }
@@ -170,7 +170,7 @@ struct GStoreAt {
   int nvalid;
   bool ok;
   double scale;
-  __device__ __forceinline__ void store(int pos, double2 v) const {
+  __device__ __forceinline__ void store(int pos, int, double2 v) const {
     if (ok && pos < nvalid) base[pos * sp] = (scale == 1.0) ? v : cscale(v, scale);
   }
 };
@@ -181,8 +181,17 @@ struct SmemIO {
   static constexpr bool kSmem = true;
   double2* sm;
   int t;
-  __device__ __forceinline__ double2 load(int pos) const { return sm[pos * T + t]; }
-  __device__ __forceinline__ void store(int pos, double2 v) const { sm[pos * T + t] = v; }
+  __device__ __forceinline__ double2 load(int pos, int) const { return sm[pos * T + t]; }
+  __device__ __forceinline__ void store(int pos, int, double2 v) const { sm[pos * T + t] = v; }
+};
+
+// Register endpoint: the last stage of one transform hands its outputs to the first stage
+// of the next in registers (valid when the first stage reads exactly the positions the last
+// stage wrote, i.e. equal first/last radix).
+struct RegIO {
+  static constexpr bool kSmem = false;
+  double2 v[kMaxElems];
+  __device__ __forceinline__ void store(int, int e, double2 x) { v[e] = x; }
 };
 
 __host__ __device__ __forceinline__ int fold_index(int k, int P) { return (2 * k <= P) ? k : P - k; }

@@ -5,7 +5,7 @@
 namespace fusg {
 
 constexpr int kMaxStages = 8;
-constexpr int kMaxElems = 16;  // complex values a thread holds per stage
+constexpr int kMaxElems = 8;  // complex values a thread holds per stage (radix <= 8)
 
 struct AxisPlan {
   int L;                     // transform length (padded size along this axis)

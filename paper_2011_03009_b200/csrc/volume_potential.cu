@@ -14,10 +14,13 @@
 // stored, and pass C folds its index.  The octant is built by the same pass machinery with
 // the kernel values generated in registers (no padded tensor is ever materialised).
 #include <cmath>
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <cstdio>
 #include <vector>
 
-#include "fft_pass.cuh"
+#include "fft_static.cuh"
 #include "internal.hpp"
 
 namespace fusg {
@@ -45,7 +48,7 @@ struct KGenAt {
   double dx, vol, kre, kim;
   double2 self;
   bool ok;
-  __device__ __forceinline__ double2 load(int pos) const {
+  __device__ __forceinline__ double2 load(int pos, int) const {
     const int ox = offset_of(pos, Nx, Px);
     if (!ok || ox == kExcluded) return make_double2(0.0, 0.0);
     if (ox == 0 && oy == 0 && oz == 0) return self;
@@ -72,7 +75,7 @@ struct FoldAt {
   int64_t sp;
   int N, P;
   bool ok;
-  __device__ __forceinline__ double2 load(int pos) const {
+  __device__ __forceinline__ double2 load(int pos, int) const {
     const int o = offset_of(pos, N, P);
     if (!ok || o == kExcluded) return make_double2(0.0, 0.0);
     return __ldg(base + int64_t(o < 0 ? -o : o) * sp);
@@ -87,22 +90,22 @@ struct FoldF {
   }
 };
 
-// Spectral multiply between the forward and inverse z transforms of pass C: reads the
-// forward spectrum from shared memory and multiplies by the folded octant value.
+// Spectral multiply between the forward and inverse z transforms of pass C.  The folded
+// octant values for this thread's first-stage slots are prefetched into registers (kv) before
+// the forward transform starts, so their latency hides behind it.
 template <int T>
-struct KMulAt {
+struct SmemMulAt {
   static constexpr bool kSmem = true;
   const double2* sm;
   int t;
-  const double2* kline;
-  int64_t sz;
-  int P;
-  bool ok;
-  __device__ __forceinline__ double2 load(int pos) const {
-    const double2 v = sm[pos * T + t];
-    if (!ok) return make_double2(0.0, 0.0);
-    return cmul(v, __ldg(kline + int64_t(fold_index(pos, P)) * sz));
-  }
+  const double2* kv;
+  __device__ __forceinline__ double2 load(int pos, int e) const { return cmul(sm[pos * T + t], kv[e]); }
+};
+struct RegMulAt {
+  static constexpr bool kSmem = false;
+  const double2* v;
+  const double2* kv;
+  __device__ __forceinline__ double2 load(int, int e) const { return cmul(v[e], kv[e]); }
 };
 struct KOct {
   const double2* p;
@@ -111,7 +114,7 @@ struct KOct {
 
 // ---------------------------------------------------------------------------- kernels
 template <bool INV, int T, class LD, class ST>
-__global__ void __launch_bounds__(512) axis_pass(AxisPlan pl, LineGeom g, LD ld, ST st) {
+__global__ void __launch_bounds__(512, 2) axis_pass(AxisPlan pl, LineGeom g, LD ld, ST st) {
   extern __shared__ double2 sm[];
   const int tile = blockIdx.x % g.ntiles;
   const int k = blockIdx.x / g.ntiles;
@@ -124,8 +127,8 @@ __global__ void __launch_bounds__(512) axis_pass(AxisPlan pl, LineGeom g, LD ld,
 }
 
 template <int T>
-__global__ void __launch_bounds__(512) conv_pass(AxisPlan pl, LineGeom g, GLoadF ld, GStoreF st,
-                                                  KOct ko) {
+__global__ void __launch_bounds__(512, 2) conv_pass(AxisPlan pl, LineGeom g, GLoadF ld, GStoreF st,
+                                                 KOct ko, int fuse_regs) {
   extern __shared__ double2 sm[];
   const int tile = blockIdx.x % g.ntiles;
   const int k = blockIdx.x / g.ntiles;  // ky
@@ -133,15 +136,30 @@ __global__ void __launch_bounds__(512) conv_pass(AxisPlan pl, LineGeom g, GLoadF
   const int i = tile * T + t;           // kx
   const bool ok = i < g.n_inner;
   const int ii = ok ? i : 0;
+  const double2* kline = ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px);
+  const int64_t sz = int64_t(ko.Hx) * ko.Hy;
+  double2 kv[kMaxElems];
+#pragma unroll
+  for (int e = 0; e < kMaxElems; ++e) {
+    const int p = first_stage_pos(pl, jt, e);
+    kv[e] = (ok && p >= 0) ? __ldg(kline + int64_t(fold_index(p, ko.Pz)) * sz) : make_double2(0.0, 0.0);
+  }
   auto src = ld.at(ii, k, ok);
-  SmemIO<T> mid{sm, t};
-  fft_line<false, T>(pl, sm, t, jt, src, mid);
-  __syncthreads();
-  KMulAt<T> msrc{sm, t,
-                 ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px),
-                 int64_t(ko.Hx) * ko.Hy, ko.Pz, ok};
   auto dst = st.at(ii, k, ok);
-  fft_line<true, T>(pl, sm, t, jt, msrc, dst);
+  if (fuse_regs) {
+    // last forward radix == first inverse radix: the spectrum never leaves registers
+    RegIO mid;
+    fft_line<false, T>(pl, sm, t, jt, src, mid);
+    __syncthreads();
+    RegMulAt msrc{mid.v, kv};
+    fft_line<true, T>(pl, sm, t, jt, msrc, dst);
+  } else {
+    SmemIO<T> mid{sm, t};
+    fft_line<false, T>(pl, sm, t, jt, src, mid);
+    __syncthreads();
+    SmemMulAt<T> msrc{sm, t, kv};
+    fft_line<true, T>(pl, sm, t, jt, msrc, dst);
+  }
 }
 
 // ---------------------------------------------------------------------------- planning
@@ -168,7 +186,7 @@ bool make_plan_radices(int L, AxisPlan& pl) {
   if (m != 1 || L < 2) return false;
   std::vector<int> r;
   if (e2 > 0) {
-    const int n = (e2 + 3) / 4;  // stages for the power of two, <= 4 bits each, balanced
+    const int n = (e2 + 2) / 3;  // stages for the power of two, <= 3 bits each, balanced
     for (int s = 0; s < n; ++s) {
       const int bits = e2 / n + (s < e2 % n ? 1 : 0);
       r.push_back(1 << bits);
@@ -177,6 +195,18 @@ bool make_plan_radices(int L, AxisPlan& pl) {
   for (int i = 0; i < e7; ++i) r.push_back(7);
   for (int i = 0; i < e5; ++i) r.push_back(5);
   for (int i = 0; i < e3; ++i) r.push_back(3);
+  // Put a repeated radix (largest first) at both ends: pass C then hands the forward
+  // spectrum to the inverse transform in registers (first/last radix equal).
+  std::sort(r.begin(), r.end(), [](int a, int b) { return a > b; });
+  for (size_t a = 0; a + 1 < r.size(); ++a) {
+    if (r[a] == r[a + 1]) {
+      const int rv = r[a];
+      r.erase(r.begin() + a, r.begin() + a + 2);
+      r.insert(r.begin(), rv);
+      r.push_back(rv);
+      break;
+    }
+  }
   if (int(r.size()) > kMaxStages) return false;
   pl.L = L;
   pl.nst = int(r.size());
@@ -215,6 +245,191 @@ static int choose_tile(const AxisPlan& pl, int n_inner) {
   return T;
 }
 
+// ---------------------------------------------------------------------------- static plans
+// Compile-time-planned kernels for the hot padded lengths (apply passes only; the one-off
+// kernel-spectrum build uses the runtime-planned kernels).  Register budget: 64 per thread
+// (minBlocks = 1024 threads / block size), i.e. 32 resident warps per SM.
+template <class RL, int T>
+struct SBounds {
+  static constexpr int threads = RL::tpl() * T;
+  static constexpr int min_blocks = threads >= 1024 ? 1 : 1024 / threads;
+  // pass C keeps the forward spectrum and the prefetched K^ slots live: allow ~96 registers
+  static constexpr int conv_min_blocks = threads >= 680 ? 1 : 680 / threads;
+};
+
+template <class RL, int T, bool INV>
+__global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_blocks)
+    axis_pass_s(LineGeom g, GLoadF ld, GStoreF st, const double2* __restrict__ tw) {
+  extern __shared__ double2 sm[];
+  const int tile = blockIdx.x % g.ntiles;
+  const int k = blockIdx.x / g.ntiles;
+  const int t = threadIdx.x % T, jt = threadIdx.x / T;
+  const int i = tile * T + t;
+  const bool ok = i < g.n_inner;
+  auto src = ld.at(ok ? i : 0, k, ok);
+  auto dst = st.at(ok ? i : 0, k, ok);
+  fft_line_s<RL, T, INV>(sm, t, jt, tw, src, dst);
+}
+
+// K^ read straight from global memory at the multiply (no register prefetch).
+struct RegMulGlobalAt {
+  static constexpr bool kSmem = false;
+  const double2* v;
+  const double2* kline;
+  int64_t sz;
+  int P;
+  bool ok;
+  __device__ __forceinline__ double2 load(int pos, int e) const {
+    return ok ? cmul(v[e], __ldg(kline + int64_t(fold_index(pos, P)) * sz)) : make_double2(0.0, 0.0);
+  }
+};
+
+// MINB: min resident blocks (register cap); KPREF: prefetch K^ into registers first.
+template <class RL, int T, int MINB, bool KPREF>
+__global__ void __launch_bounds__(SBounds<RL, T>::threads, MINB)
+    conv_pass_s(LineGeom g, GLoadF ld, GStoreF st, KOct ko, const double2* __restrict__ tw) {
+  extern __shared__ double2 sm[];
+  const int tile = blockIdx.x % g.ntiles;
+  const int k = blockIdx.x / g.ntiles;  // ky
+  const int t = threadIdx.x % T, jt = threadIdx.x / T;
+  const int i = tile * T + t;           // kx
+  const bool ok = i < g.n_inner;
+  const int ii = ok ? i : 0;
+  const double2* kline = ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px);
+  const int64_t sz = int64_t(ko.Hx) * ko.Hy;
+  double2 kv[kMaxElems];
+  if constexpr (KPREF) {
+#pragma unroll
+    for (int e = 0; e < kMaxElems; ++e) {
+      const int p = first_stage_pos_s<RL>(jt, e);
+      kv[e] = (ok && p >= 0) ? __ldg(kline + int64_t(fold_index(p, RL::len())) * sz)
+                             : make_double2(0.0, 0.0);
+    }
+  }
+  auto src = ld.at(ii, k, ok);
+  auto dst = st.at(ii, k, ok);
+  if constexpr (RL::at(0) == RL::at(RL::n - 1)) {
+    RegIO mid;
+    fft_line_s<RL, T, false>(sm, t, jt, tw, src, mid);
+    __syncthreads();
+    if constexpr (KPREF) {
+      RegMulAt msrc{mid.v, kv};
+      fft_line_s<RL, T, true>(sm, t, jt, tw, msrc, dst);
+    } else {
+      RegMulGlobalAt msrc{mid.v, kline, sz, RL::len(), ok};
+      fft_line_s<RL, T, true>(sm, t, jt, tw, msrc, dst);
+    }
+  } else {
+    static_assert(KPREF, "smem hand-off variant prefetches K^");
+    SmemIO<T> mid{sm, t};
+    fft_line_s<RL, T, false>(sm, t, jt, tw, src, mid);
+    __syncthreads();
+    SmemMulAt<T> msrc{sm, t, kv};
+    fft_line_s<RL, T, true>(sm, t, jt, tw, msrc, dst);
+  }
+}
+
+using AxisFn = void (*)(LineGeom, GLoadF, GStoreF, const double2*);
+using ConvFn = void (*)(LineGeom, GLoadF, GStoreF, KOct, const double2*);
+
+// One table per pass kind; per length the first entry is the default, FUSG_{ROW,COL,CONV}_VAR
+// selects another (tuning knob).  Row passes (x: A, E) and column passes (y: B, D) share the
+// axis kernels; conv is pass C.
+struct StaticEntry {
+  int L, T, threads;
+  AxisFn fwd, inv;
+  ConvFn conv;
+};
+
+#define FUSG_AX(TT, ...)                                                                   \
+  StaticEntry {                                                                            \
+    Radices<__VA_ARGS__>::len(), TT, Radices<__VA_ARGS__>::tpl() * TT,                     \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, false>, axis_pass_s<Radices<__VA_ARGS__>, TT, true>, \
+        nullptr                                                                            \
+  }
+#define FUSG_CV(TT, MINB, KPREF, ...)                                                      \
+  StaticEntry {                                                                            \
+    Radices<__VA_ARGS__>::len(), TT, Radices<__VA_ARGS__>::tpl() * TT, nullptr, nullptr,   \
+        conv_pass_s<Radices<__VA_ARGS__>, TT, MINB, KPREF>                                 \
+  }
+
+static const StaticEntry kRowTab[] = {
+    FUSG_AX(4, 8, 8, 8),        // 512  (cfg2)
+    FUSG_AX(8, 8, 8, 8),
+    FUSG_AX(16, 4, 8, 4),       // 128  (cfg1)
+    FUSG_AX(2, 8, 8, 3, 8),     // 1536 (cfg5)
+    FUSG_AX(2, 5, 7, 3, 2, 5),  // 1050 (cfg3 x)
+    FUSG_AX(2, 7, 4, 5, 7),     // 980  (cfg3 y, z)
+    FUSG_AX(4, 5, 5, 5, 5),     // 625  (desk cfg4)
+    FUSG_AX(4, 3, 8, 3, 3, 3),  // 648  (desk cfg4)
+    FUSG_AX(4, 8, 7, 4, 3),     // 672  (desk cfg4)
+};
+static const StaticEntry kColTab[] = {
+    FUSG_AX(8, 8, 8, 8),
+    FUSG_AX(4, 8, 8, 8),
+    FUSG_AX(16, 4, 8, 4),
+    FUSG_AX(2, 8, 8, 3, 8),
+    FUSG_AX(2, 5, 7, 3, 2, 5),
+    FUSG_AX(2, 7, 4, 5, 7),
+    FUSG_AX(4, 5, 5, 5, 5),
+    FUSG_AX(4, 3, 8, 3, 3, 3),
+    FUSG_AX(4, 8, 7, 4, 3),
+};
+static const StaticEntry kConvTab[] = {
+    FUSG_CV(8, 1, true, 8, 8, 8),
+    FUSG_CV(4, 3, true, 8, 8, 8),
+    FUSG_CV(4, 4, false, 8, 8, 8),
+    FUSG_CV(8, 2, false, 8, 8, 8),
+    FUSG_CV(4, 2, true, 8, 8, 8),
+    FUSG_CV(16, 1, true, 4, 8, 4),
+    FUSG_CV(2, 1, true, 8, 8, 3, 8),
+    FUSG_CV(2, 1, true, 5, 7, 3, 2, 5),
+    FUSG_CV(2, 1, true, 7, 4, 5, 7),
+    FUSG_CV(4, 1, true, 5, 5, 5, 5),
+    FUSG_CV(4, 1, true, 3, 8, 3, 3, 3),
+    FUSG_CV(4, 1, true, 8, 7, 4, 3),
+};
+
+enum StaticKind { kKindRow = 0, kKindCol = 1, kKindConv = 2 };
+
+// FUSG_STATIC=0 disables the compile-time-planned kernels.
+static const StaticEntry* find_static(int L, int kind) {
+  static const bool enabled = [] {
+    const char* e = getenv("FUSG_STATIC");
+    return !(e && atoi(e) == 0);
+  }();
+  static const int var[3] = {
+      getenv("FUSG_ROW_VAR") ? atoi(getenv("FUSG_ROW_VAR")) : 0,
+      getenv("FUSG_COL_VAR") ? atoi(getenv("FUSG_COL_VAR")) : 0,
+      getenv("FUSG_CONV_VAR") ? atoi(getenv("FUSG_CONV_VAR")) : 0};
+  if (!enabled) return nullptr;
+  const StaticEntry* tab = kind == kKindRow ? kRowTab : kind == kKindCol ? kColTab : kConvTab;
+  const size_t n = kind == kKindRow ? sizeof(kRowTab) / sizeof(StaticEntry)
+                   : kind == kKindCol ? sizeof(kColTab) / sizeof(StaticEntry)
+                                      : sizeof(kConvTab) / sizeof(StaticEntry);
+  const StaticEntry* first = nullptr;
+  int seen = 0;
+  for (size_t q = 0; q < n; ++q) {
+    if (tab[q].L != L) continue;
+    if (!first) first = &tab[q];
+    if (seen++ == var[kind]) return &tab[q];
+  }
+  return first;
+}
+
+template <class Fn, class... Args>
+static fusg_status launch_static(fusg_ctx* ctx, Fn fn, const StaticEntry& e, int n_inner, int n_outer,
+                                 cudaStream_t s, Args... args) {
+  LineGeom g{n_inner, n_outer, (n_inner + e.T - 1) / e.T};
+  const size_t smem = size_t(e.L) * e.T * sizeof(double2);
+  FUSG_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int64_t blocks = int64_t(g.ntiles) * n_outer;
+  fn<<<unsigned(blocks), e.threads, smem, s>>>(g, args...);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("static fft pass");
+  return FUSG_OK;
+}
+
 template <bool INV, int T, class LD, class ST>
 static fusg_status launch_axis_t(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
                                  const LD& ld, const ST& st, cudaStream_t s) {
@@ -231,9 +446,13 @@ static fusg_status launch_axis_t(fusg_ctx* ctx, const AxisPlan& pl, int n_inner,
 
 template <bool INV, class LD, class ST>
 static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, int n_outer,
-                               const LD& ld, const ST& st, cudaStream_t s) {
+                               const LD& ld, const ST& st, cudaStream_t s, int kind = kKindCol) {
   if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
     return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
+  if constexpr (std::is_same<LD, GLoadF>::value && std::is_same<ST, GStoreF>::value) {
+    if (const StaticEntry* e = find_static(pl.L, kind))
+      return launch_static(ctx, INV ? e->inv : e->fwd, *e, n_inner, n_outer, s, ld, st, pl.tw);
+  }
   switch (choose_tile(pl, n_inner)) {
     case 16: return launch_axis_t<INV, 16>(ctx, pl, n_inner, n_outer, ld, st, s);
     case 8: return launch_axis_t<INV, 8>(ctx, pl, n_inner, n_outer, ld, st, s);
@@ -252,7 +471,8 @@ static fusg_status launch_conv_t(fusg_ctx* ctx, const AxisPlan& pl, int n_inner,
   auto fn = conv_pass<T>;
   FUSG_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t blocks = int64_t(g.ntiles) * n_outer;
-  fn<<<unsigned(blocks), T * pl.tpl, smem, s>>>(pl, g, ld, st, ko);
+  const int fuse = pl.radix[0] == pl.radix[pl.nst - 1];
+  fn<<<unsigned(blocks), T * pl.tpl, smem, s>>>(pl, g, ld, st, ko, fuse);
   ctx->launches++;
   FUSG_LAUNCH_CHECK("conv_pass");
   return FUSG_OK;
@@ -263,6 +483,8 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
                                cudaStream_t s) {
   if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
     return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
+  if (const StaticEntry* e = find_static(pl.L, kKindConv))
+    return launch_static(ctx, e->conv, *e, n_inner, n_outer, s, ld, st, ko, pl.tw);
   switch (choose_tile(pl, n_inner)) {
     case 16: return launch_conv_t<16>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
     case 8: return launch_conv_t<8>(ctx, pl, n_inner, n_outer, ld, st, ko, s);
@@ -323,12 +545,13 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
   fusg_ctx* ctx = K->ctx;
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
-  const int64_t PxNy = int64_t(Px) * Ny, PxPy = int64_t(Px) * Py;
+  const int64_t PxNy = int64_t(Px) * Ny;
   const double total = double(Px) * double(Py) * double(Pz);
+  const int64_t PxPy = int64_t(Px) * Py;
   mark(0);
   // A: rows of f (stride Nx) -> rows of A (stride Px)
   FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{f, Nx, 0, 1, Nx}},
-                              GStoreF{GStore{K->bufA, Px, 0, 1, Px, 1.0}}, s));
+                              GStoreF{GStore{K->bufA, Px, 0, 1, Px, 1.0}}, s, kKindRow));
   mark(1);
   // B: y lines of A (Ny valid) -> y lines of B
   FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Px, Nz, GLoadF{GLoad{K->bufA, 1, PxNy, Px, Ny}},
@@ -340,12 +563,13 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
                        KOct{K->koct, K->H[0], K->H[1], Px, Py, Pz}, s));
   mark(3);
   // D: inverse y, keep Ny -> A
-  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Px, Nz, GLoadF{GLoad{K->bufB, 1, PxPy, Px, Py}},
+  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Px, Nz,
+                             GLoadF{GLoad{K->bufB, 1, PxPy, Px, Py}},
                              GStoreF{GStore{K->bufA, 1, PxNy, Px, Ny, 1.0}}, s));
   mark(4);
   // E: inverse x, scale, crop -> u
   FUSG_TRY(launch_axis<true>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{K->bufA, Px, 0, 1, Px}},
-                             GStoreF{GStore{u, Nx, 0, 1, Nx, scale / total}}, s));
+                             GStoreF{GStore{u, Nx, 0, 1, Nx, scale / total}}, s, kKindRow));
   mark(5);
   return FUSG_OK;
 }
