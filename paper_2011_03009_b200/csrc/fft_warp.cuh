@@ -1,0 +1,163 @@
+// Warp-per-line Stockham FFT engine for the hot padded lengths (L <= 512).
+//
+// A line of L points is owned by LANES lanes of one warp (32 / LANES lines per warp); each
+// lane holds E = L / LANES values in registers.  Stages exchange data through a shared-memory
+// line buffer with __syncwarp only (no CTA barriers inside a transform).  The buffer is
+// swizzled, addr(pos) = pos ^ ((pos >> 3) & 7) per 8-element row, which makes both Stockham
+// access patterns (lane-consecutive reads, stride-R writes) bank-conflict-free.
+//
+// Twiddles: one table load w^k per butterfly and stage; the powers w^{rk}, r < R, come from a
+// depth-3 multiply tree (<= 3 roundings), halving shared/L1 traffic versus loading all R-1.
+//
+// Stage s (radix R, NS = product of earlier radices, NB = L/R): butterfly j = lane + LANES*b,
+// slot e = b*R + r holds position j + r*NB on input and (j - j%NS)*R + j%NS + r*NS on output.
+#pragma once
+#include "fft_static.cuh"
+
+namespace fusg {
+
+__device__ __forceinline__ int swz(int p) { return p ^ ((p >> 3) & 7); }
+
+// w^r for r = 1..R-1 from w (compile-time R), INV -> conjugate handled by the caller
+template <int R>
+__device__ __forceinline__ void twiddle_powers(double2 w, double2* p) {
+  p[1] = w;
+  if constexpr (R > 2) p[2] = cmul(w, w);
+  if constexpr (R > 3) p[3] = cmul(p[2], w);
+  if constexpr (R > 4) p[4] = cmul(p[2], p[2]);
+  if constexpr (R > 5) p[5] = cmul(p[4], w);
+  if constexpr (R > 6) p[6] = cmul(p[3], p[3]);
+  if constexpr (R > 7) p[7] = cmul(p[4], p[3]);
+}
+
+template <class RL, int LANES>
+struct WarpGeom {
+  static constexpr int L = RL::len();
+  static constexpr int E = L / LANES;
+  static_assert(L % LANES == 0, "line must split evenly over its lanes");
+};
+
+// Input slot positions of stage S for lane `lane`.
+template <class RL, int LANES, int S>
+__device__ __forceinline__ int in_pos(int lane, int e) {
+  constexpr int R = RL::at(S);
+  constexpr int NB = RL::len() / R;
+  const int b = e / R, r = e % R;
+  return lane + LANES * b + r * NB;
+}
+
+template <class RL, int LANES, int S>
+__device__ __forceinline__ int out_pos(int lane, int e) {
+  constexpr int R = RL::at(S);
+  constexpr int NS = RL::ns(S);
+  const int b = e / R, r = e % R;
+  const int j = lane + LANES * b;
+  const int k = j % NS;
+  return (j - k) * R + k + r * NS;
+}
+
+// Twiddle + butterflies of stage S on the register array v (input slots -> output slots).
+template <class RL, int LANES, bool INV, int S>
+__device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const double2* __restrict__ tw) {
+  constexpr int R = RL::at(S);
+  constexpr int NS = RL::ns(S);
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  constexpr int B = E / R;
+  constexpr int TWS = L / (NS * R);
+  static_assert(E % R == 0, "each lane must own whole butterflies");
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    if constexpr (NS > 1) {
+      const int j = lane + LANES * b;
+      const int k = j % NS;
+      double2 p[8];
+      twiddle_powers<R>(__ldg(tw + k * TWS), p);
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[b * R + r] = INV ? cmulc(v[b * R + r], p[r]) : cmul(v[b * R + r], p[r]);
+    }
+    dft<R, INV>(v + b * R);
+  }
+}
+
+// Full transform of the LANES-lane line owned by this lane group.
+//   src.load(pos, e) feeds stage 0; dst.store(pos, e, v) receives the last stage's outputs.
+//   ex.at(pos): this line's swizzled shared exchange slot for position pos.
+template <class RL, int LANES, bool INV, int S = 0, class Ex, class Src, class Dst>
+__device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const double2* __restrict__ tw,
+                                         Src& src, Dst& dst) {
+  constexpr int E = RL::len() / LANES;
+  if constexpr (S == 0) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = src.load(in_pos<RL, LANES, 0>(lane, e), e);
+  }
+  warp_stage_compute<RL, LANES, INV, S>(v, lane, tw);
+  if constexpr (S + 1 < RL::n) {
+    __syncwarp();  // all lanes finished reading the buffer (previous stage / caller)
+#pragma unroll
+    for (int e = 0; e < E; ++e) ex.at(out_pos<RL, LANES, S>(lane, e)) = v[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = ex.at(in_pos<RL, LANES, S + 1>(lane, e));
+    warp_fft<RL, LANES, INV, S + 1>(v, ex, lane, tw, src, dst);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst.store(out_pos<RL, LANES, S>(lane, e), e, v[e]);
+  }
+}
+
+// ------------------------------------------------------------------ endpoints
+// Column of a swizzled [pos][8] tile: element (pos, t) lives at pos*8 + (t ^ swz-bits).
+__device__ __forceinline__ int tile_at(int pos, int t) { return pos * 8 + (t ^ ((pos ^ (pos >> 3)) & 7)); }
+
+struct PrivEx {  // private line buffer of L elements
+  double2* b;
+  __device__ __forceinline__ double2& at(int pos) const { return b[swz(pos)]; }
+};
+struct TileEx {  // the line's own column of the [pos][8] tile (in-place exchange)
+  double2* tile;
+  int t;
+  __device__ __forceinline__ double2& at(int pos) const { return tile[tile_at(pos, t)]; }
+};
+
+struct TileColIn {
+  const double2* tile;
+  int t, nvalid;
+  __device__ __forceinline__ double2 load(int pos, int) const {
+    return pos < nvalid ? tile[tile_at(pos, t)] : make_double2(0.0, 0.0);
+  }
+};
+struct TileColOut {
+  double2* tile;
+  int t;
+  __device__ __forceinline__ void store(int pos, int, double2 v) const { tile[tile_at(pos, t)] = v; }
+};
+struct RowIn {  // global line with position stride sp (1 for rows), zero beyond nvalid
+  const double2* p;
+  int64_t sp;
+  int nvalid;
+  bool ok;
+  __device__ __forceinline__ double2 load(int pos, int) const {
+    return (ok && pos < nvalid) ? __ldg(p + pos * sp) : make_double2(0.0, 0.0);
+  }
+};
+struct RowOut {
+  double2* p;
+  int64_t sp;
+  int nvalid;
+  bool ok;
+  double scale;
+  __device__ __forceinline__ void store(int pos, int, double2 v) const {
+    if (ok && pos < nvalid) p[pos * sp] = (scale == 1.0) ? v : cscale(v, scale);
+  }
+};
+struct RegsOut {  // keep the last stage's outputs in the caller's registers
+  double2* v;
+  __device__ __forceinline__ void store(int, int e, double2 x) const { v[e] = x; }
+};
+struct RegsIn {
+  const double2* v;
+  __device__ __forceinline__ double2 load(int, int e) const { return v[e]; }
+};
+
+}  // namespace fusg

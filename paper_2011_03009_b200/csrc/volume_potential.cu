@@ -20,7 +20,7 @@
 #include <cstdio>
 #include <vector>
 
-#include "fft_static.cuh"
+#include "fft_warp.cuh"
 #include "internal.hpp"
 
 namespace fusg {
@@ -107,9 +107,15 @@ struct RegMulAt {
   const double2* kv;
   __device__ __forceinline__ double2 load(int, int e) const { return cmul(v[e], kv[e]); }
 };
+// Kernel-spectrum octant addressing for pass C lines (i = ky, k = kx; position kz):
+// element = p + fold(kx) * s_kx + fold(ky) * s_ky + fold(kz) * s_kz.
 struct KOct {
   const double2* p;
-  int Hx, Hy, Px, Py, Pz;
+  int Px, Py, Pz;
+  int64_t s_kx, s_ky, s_kz;
+  __device__ __forceinline__ const double2* line(int ky, int kx) const {
+    return p + fold_index(kx, Px) * s_kx + fold_index(ky, Py) * s_ky;
+  }
 };
 
 // ---------------------------------------------------------------------------- kernels
@@ -136,13 +142,12 @@ __global__ void __launch_bounds__(512, 2) conv_pass(AxisPlan pl, LineGeom g, GLo
   const int i = tile * T + t;           // kx
   const bool ok = i < g.n_inner;
   const int ii = ok ? i : 0;
-  const double2* kline = ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px);
-  const int64_t sz = int64_t(ko.Hx) * ko.Hy;
+  const double2* kline = ko.line(ii, k);
   double2 kv[kMaxElems];
 #pragma unroll
   for (int e = 0; e < kMaxElems; ++e) {
     const int p = first_stage_pos(pl, jt, e);
-    kv[e] = (ok && p >= 0) ? __ldg(kline + int64_t(fold_index(p, ko.Pz)) * sz) : make_double2(0.0, 0.0);
+    kv[e] = (ok && p >= 0) ? __ldg(kline + fold_index(p, ko.Pz) * ko.s_kz) : make_double2(0.0, 0.0);
   }
   auto src = ld.at(ii, k, ok);
   auto dst = st.at(ii, k, ok);
@@ -268,7 +273,10 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_b
   const bool ok = i < g.n_inner;
   auto src = ld.at(ok ? i : 0, k, ok);
   auto dst = st.at(ok ? i : 0, k, ok);
-  fft_line_s<RL, T, INV>(sm, t, jt, tw, src, dst);
+  // twiddles staged in shared memory (first used after stage 1's barrier)
+  double2* tws = sm + RL::len() * T;
+  for (int m = threadIdx.x; m < RL::len(); m += SBounds<RL, T>::threads) tws[m] = __ldg(tw + m);
+  fft_line_s<RL, T, INV>(sm, t, jt, tws, src, dst);
 }
 
 // K^ read straight from global memory at the multiply (no register prefetch).
@@ -287,7 +295,7 @@ struct RegMulGlobalAt {
 // MINB: min resident blocks (register cap); KPREF: prefetch K^ into registers first.
 template <class RL, int T, int MINB, bool KPREF>
 __global__ void __launch_bounds__(SBounds<RL, T>::threads, MINB)
-    conv_pass_s(LineGeom g, GLoadF ld, GStoreF st, KOct ko, const double2* __restrict__ tw) {
+    conv_pass_s(LineGeom g, GLoadF ld, GStoreF st, KOct ko, const double2* tw) {
   extern __shared__ double2 sm[];
   const int tile = blockIdx.x % g.ntiles;
   const int k = blockIdx.x / g.ntiles;  // ky
@@ -295,8 +303,8 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, MINB)
   const int i = tile * T + t;           // kx
   const bool ok = i < g.n_inner;
   const int ii = ok ? i : 0;
-  const double2* kline = ko.p + int64_t(fold_index(k, ko.Py)) * ko.Hx + fold_index(ii, ko.Px);
-  const int64_t sz = int64_t(ko.Hx) * ko.Hy;
+  const double2* kline = ko.line(ii, k);
+  const int64_t sz = ko.s_kz;
   double2 kv[kMaxElems];
   if constexpr (KPREF) {
 #pragma unroll
@@ -308,6 +316,9 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, MINB)
   }
   auto src = ld.at(ii, k, ok);
   auto dst = st.at(ii, k, ok);
+  double2* tws = sm + RL::len() * T;
+  for (int m = threadIdx.x; m < RL::len(); m += SBounds<RL, T>::threads) tws[m] = __ldg(tw + m);
+  tw = tws;
   if constexpr (RL::at(0) == RL::at(RL::n - 1)) {
     RegIO mid;
     fft_line_s<RL, T, false>(sm, t, jt, tw, src, mid);
@@ -417,11 +428,143 @@ static const StaticEntry* find_static(int L, int kind) {
   return first;
 }
 
+// ---------------------------------------------------------------------------- warp engine
+// Warp-per-line kernels (fft_warp.cuh) for L <= 512: rows (x passes) are read and written
+// straight from global memory by their own lane group; columns (y, z passes) are staged as a
+// swizzled [pos][8] tile with one coalesced cooperative load and store (2 CTA barriers per
+// tile), the transforms in between use __syncwarp only.
+struct WArgs {
+  const double2* in;
+  int64_t in_si, in_sk, in_sp;
+  int in_nvalid;
+  double2* out;
+  int64_t out_si, out_sk, out_sp;
+  int out_nvalid;
+  double scale;
+  int n_inner, n_outer;
+  const double2* tw;
+  KOct ko;  // pass C only
+};
+
+constexpr int kWarpThreads = 256;  // 8 warps per CTA
+
+// Lines (i, k), i fastest: consecutive lane groups of a CTA take consecutive i, so column
+// lines (position stride sp, i contiguous) from one CTA share every 128-byte row through L1.
+template <class RL, int LANES, bool INV>
+__global__ void __launch_bounds__(kWarpThreads, 2) warp_line_pass(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  constexpr int LPC = kWarpThreads / LANES;  // lines per CTA
+  extern __shared__ double2 sm[];
+  const int g = threadIdx.x / LANES, lane = threadIdx.x % LANES;
+  const int64_t line = int64_t(blockIdx.x) * LPC + g;
+  const bool ok = line < int64_t(a.n_inner) * a.n_outer;
+  const int64_t li = ok ? line : 0;
+  const int64_t i = li % a.n_inner, k = li / a.n_inner;
+  PrivEx ex{sm + g * L};
+  RowIn src{a.in + i * a.in_si + k * a.in_sk, a.in_sp, a.in_nvalid, ok};
+  RowOut dst{a.out + i * a.out_si + k * a.out_sk, a.out_sp, a.out_nvalid, ok, a.scale};
+  double2 v[E];
+  warp_fft<RL, LANES, INV>(v, ex, lane, a.tw, src, dst);
+}
+
+// mirror-interleaved order 0, 1, P-1, 2, P-2, ...: lines ky and Py-ky (kx and Px-kx) read the
+// same folded K^ row and run close together, so the second read hits L2.
+__device__ __forceinline__ int interleave_index(int r, int P) {
+  if (r == 0) return 0;
+  const int m = (r + 1) >> 1;
+  return (r & 1) ? m : P - m;
+}
+
+// Pass C on rows of B [kx][ky][z] (z contiguous): forward z, * K^ (octant row [kx][ky][kz],
+// contiguous), inverse z; in place.  n_inner = Py, n_outer = Px.
+template <class RL, int LANES>
+__global__ void __launch_bounds__(kWarpThreads, 2) warp_row_conv(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  constexpr int LPC = kWarpThreads / LANES;
+  static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
+  extern __shared__ double2 sm[];
+  const int g = threadIdx.x / LANES, lane = threadIdx.x % LANES;
+  const int64_t line = int64_t(blockIdx.x) * LPC + g;
+  const bool ok = line < int64_t(a.n_inner) * a.n_outer;
+  const int64_t li = ok ? line : 0;
+  const int ky = interleave_index(int(li % a.n_inner), a.ko.Py);
+  const int kx = interleave_index(int(li / a.n_inner), a.ko.Px);
+  const double2* kline = a.ko.line(ky, kx);
+  PrivEx ex{sm + g * L};
+  RowIn src{a.in + ky * a.in_si + int64_t(kx) * a.in_sk, 1, a.in_nvalid, ok};
+  double2 v[E];
+  RegsOut mid{v};
+  warp_fft<RL, LANES, false>(v, ex, lane, a.tw, src, mid);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int pos = in_pos<RL, LANES, 0>(lane, e);
+    v[e] = cmul(v[e], __ldg(kline + fold_index(pos, L)));
+  }
+  RegsIn msrc{v};
+  RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, ok, a.scale};
+  warp_fft<RL, LANES, true>(v, ex, lane, a.tw, msrc, dst);
+}
+
+using WFn = void (*)(WArgs);
+struct WarpEntry {
+  int L, lanes;
+  WFn fwd, inv, conv;
+};
+#define FUSG_WARP(LN, ...)                                                                  \
+  WarpEntry {                                                                               \
+    Radices<__VA_ARGS__>::len(), LN, warp_line_pass<Radices<__VA_ARGS__>, LN, false>,       \
+        warp_line_pass<Radices<__VA_ARGS__>, LN, true>, warp_row_conv<Radices<__VA_ARGS__>, LN> \
+  }
+static const WarpEntry kWarpTab[] = {
+    FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
+    FUSG_WARP(32, 8, 4, 8),  // 256
+    FUSG_WARP(16, 8, 2, 8),  // 128 (cfg1)
+};
+
+enum WarpMode { kWRow = 0, kWCol = 1, kWConv = 2 };
+
+// FUSG_WARP=0 disables the warp engine.  Returns 1 launched, 0 not applicable, -1 error.
+static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a, cudaStream_t s) {
+  static const bool enabled = [] {
+    const char* e = getenv("FUSG_WARP");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!enabled) return 0;
+  const WarpEntry* we = nullptr;
+  for (const auto& e : kWarpTab)
+    if (e.L == L) we = &e;
+  if (!we) return 0;
+  static const int disable_mask = [] {  // FUSG_WARP_OFF bitmask: 1 rows, 2 columns, 4 conv
+    const char* e = getenv("FUSG_WARP_OFF");
+    return e ? atoi(e) : 0;
+  }();
+  if (disable_mask & (1 << mode)) return 0;
+  WFn fn = mode == kWConv ? we->conv : (inv ? we->inv : we->fwd);
+  if (mode == kWConv && inv) return 0;
+  const int lpc = kWarpThreads / we->lanes;
+  const size_t smem = size_t(lpc) * L * sizeof(double2);
+  const int64_t blocks = (int64_t(a.n_inner) * a.n_outer + lpc - 1) / lpc;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+    set_error(FUSG_CUDA, "warp pass: cannot configure shared memory");
+    return -1;
+  }
+  fn<<<unsigned(blocks), kWarpThreads, smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "warp fft pass");
+    return -1;
+  }
+  return 1;
+}
+
 template <class Fn, class... Args>
 static fusg_status launch_static(fusg_ctx* ctx, Fn fn, const StaticEntry& e, int n_inner, int n_outer,
                                  cudaStream_t s, Args... args) {
   LineGeom g{n_inner, n_outer, (n_inner + e.T - 1) / e.T};
-  const size_t smem = size_t(e.L) * e.T * sizeof(double2);
+  const size_t smem = size_t(e.L) * (e.T + 1) * sizeof(double2);  // tile + twiddles
   FUSG_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t blocks = int64_t(g.ntiles) * n_outer;
   fn<<<unsigned(blocks), e.threads, smem, s>>>(g, args...);
@@ -450,6 +593,14 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
   if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
     return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
   if constexpr (std::is_same<LD, GLoadF>::value && std::is_same<ST, GStoreF>::value) {
+    const bool rows = kind == kKindRow;
+    if ((rows && ld.g.sp == 1 && st.g.sp == 1) || (!rows && ld.g.si == 1 && st.g.si == 1)) {
+      const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
+                     st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
+      const int r = launch_warp(ctx, pl.L, rows ? kWRow : kWCol, INV, wa, s);
+      if (r < 0) return FUSG_CUDA;
+      if (r > 0) return FUSG_OK;
+    }
     if (const StaticEntry* e = find_static(pl.L, kind))
       return launch_static(ctx, INV ? e->inv : e->fwd, *e, n_inner, n_outer, s, ld, st, pl.tw);
   }
@@ -483,6 +634,13 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
                                cudaStream_t s) {
   if (size_t(pl.L) * sizeof(double2) > 200 * 1024)
     return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
+  if (ld.g.sp == 1 && st.g.sp == 1 && ko.s_kz == 1) {
+    const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
+                   st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, ko};
+    const int r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
+    if (r < 0) return FUSG_CUDA;
+    if (r > 0) return FUSG_OK;
+  }
   if (const StaticEntry* e = find_static(pl.L, kKindConv))
     return launch_static(ctx, e->conv, *e, n_inner, n_outer, s, ld, st, ko, pl.tw);
   switch (choose_tile(pl, n_inner)) {
@@ -530,7 +688,7 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Hx, Nz, l2, s2, s));
   // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant
   FoldF l3{K->bufB, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
-  GStoreF s3{GStore{K->koct, 1, Hx, int64_t(Hx) * Hy, Hz, 1.0}};
+  GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx][ky][kz]
   FUSG_TRY(launch_axis<false>(ctx, K->plan[2], Hx, Hy, l3, s3, s));
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return FUSG_OK;
@@ -545,31 +703,33 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
   fusg_ctx* ctx = K->ctx;
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
-  const int64_t PxNy = int64_t(Px) * Ny;
+  const int Hy = K->H[1], Hz = K->H[2];
+  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz, NyNx = int64_t(Ny) * Nx;
   const double total = double(Px) * double(Py) * double(Pz);
-  const int64_t PxPy = int64_t(Px) * Py;
+  // Layouts: f, u [z][y][x]; A [kx][z][y]; B [kx][ky][z]; octant [kx][ky][kz].  Every pass
+  // reads or writes whole rows or 8-line-wide column tiles; pass C (two transforms per
+  // element) runs on contiguous rows.
   mark(0);
-  // A: rows of f (stride Nx) -> rows of A (stride Px)
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{f, Nx, 0, 1, Nx}},
-                              GStoreF{GStore{K->bufA, Px, 0, 1, Px, 1.0}}, s, kKindRow));
+  // A: x rows of f (lines y, tiled; outer z) -> A, transposed so y is contiguous
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny, Nz, GLoadF{GLoad{f, Nx, NyNx, 1, Nx}},
+                              GStoreF{GStore{K->bufA, 1, Ny, NzNy, Px, 1.0}}, s, kKindRow));
   mark(1);
-  // B: y lines of A (Ny valid) -> y lines of B
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Px, Nz, GLoadF{GLoad{K->bufA, 1, PxNy, Px, Ny}},
-                              GStoreF{GStore{K->bufB, 1, PxPy, Px, Py, 1.0}}, s));
+  // B: y rows of A (lines z, tiled; outer kx) -> B, transposed so z is contiguous
+  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Nz, Px, GLoadF{GLoad{K->bufA, Ny, NzNy, 1, Ny}},
+                              GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
   mark(2);
-  // C: z lines of B: forward, * K^, inverse, keep Nz
-  FUSG_TRY(launch_conv(ctx, K->plan[2], Px, Py, GLoadF{GLoad{K->bufB, 1, Px, PxPy, Nz}},
-                       GStoreF{GStore{K->bufB, 1, Px, PxPy, Nz, 1.0}},
-                       KOct{K->koct, K->H[0], K->H[1], Px, Py, Pz}, s));
+  // C: z rows of B (lines ky; outer kx): forward, * K^, inverse, keep Nz; in place
+  FUSG_TRY(launch_conv(ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
+                       GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
+                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1}, s));
   mark(3);
-  // D: inverse y, keep Ny -> A
-  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Px, Nz,
-                             GLoadF{GLoad{K->bufB, 1, PxPy, Px, Py}},
-                             GStoreF{GStore{K->bufA, 1, PxNy, Px, Ny, 1.0}}, s));
+  // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of A, keep Ny
+  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Nz, Px, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
+                             GStoreF{GStore{K->bufA, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
   mark(4);
-  // E: inverse x, scale, crop -> u
-  FUSG_TRY(launch_axis<true>(ctx, K->plan[0], Ny * Nz, 1, GLoadF{GLoad{K->bufA, Px, 0, 1, Px}},
-                             GStoreF{GStore{u, Nx, 0, 1, Nx, scale / total}}, s, kKindRow));
+  // E: kx columns of A (lines y, tiled, contiguous; outer z) -> x rows of u, scale, crop
+  FUSG_TRY(launch_axis<true>(ctx, K->plan[0], Ny, Nz, GLoadF{GLoad{K->bufA, 1, Ny, NzNy, Px}},
+                             GStoreF{GStore{u, Nx, NyNx, 1, Nx, scale / total}}, s, kKindCol));
   mark(5);
   return FUSG_OK;
 }
