@@ -11,7 +11,9 @@
 namespace fusg {
 fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s);
 fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
-                          double kre, double kim, double amp, double2* out, cudaStream_t s);
+                          double kre, double kim, double amp, double2* out, cudaStream_t s,
+                          double dmax);
+double distance_bound(const double* src_host, int n_src, const double lo[3], const double hi[3]);
 fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
                             const fusg_grid& tgt, double2* out, cudaStream_t s);
 fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
@@ -19,7 +21,7 @@ fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t c
 fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s);
 fusg_status radiated_power_dev(fusg_ctx* ctx, const double* src_dev, int n_src, double x_disc,
                                double R, double kre, double kim, double amp, double rho0, double c0,
-                               int n_r, int n_theta, double* out_host, cudaStream_t s);
+                               int n_r, int n_theta, double* out_host, cudaStream_t s, double dmax);
 fusg_status check_monopole_flag(fusg_ctx* ctx, cudaStream_t s);
 }  // namespace fusg
 
@@ -34,12 +36,17 @@ bool same_grid(const fusg_grid& a, const fusg_grid& b) {  // src/cascade.cpp:15-
          a.dx == b.dx && a.lo[0] == b.lo[0] && a.lo[1] == b.lo[1] && a.lo[2] == b.lo[2];
 }
 
+// Kernel workspaces come from the context's stream-ordered pool; work on other streams
+// using this kernel must be complete before destruction (as with any GreenKernel owner).
 void free_kernel(fusg_kernel* K) {
   if (!K) return;
   cudaSetDevice(K->ctx->device);
-  cudaFree(K->bufA);
-  cudaFree(K->bufB);
-  cudaFree(K->koct);
+  cudaStream_t s = K->ctx->stream;
+  cudaFreeAsync(K->bufA, s);
+  cudaFreeAsync(K->bufB, s);
+  cudaFreeAsync(K->koct, s);
+  cudaFree(K->stage_f);
+  cudaFree(K->stage_u);
   for (auto* t : K->tw) cudaFree(t);
   delete K;
 }
@@ -81,6 +88,12 @@ fusg_status fusg_ctx_create(int32_t device, fusg_ctx** out) {
   FUSG_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   FUSG_CUDA_TRY(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
   FUSG_CUDA_TRY(cudaMalloc(&ctx->dev_flag, sizeof(int)));
+  {  // keep freed stream-ordered memory in the pool (kernels/cascade temporaries are reused)
+    cudaMemPool_t pool;
+    FUSG_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    FUSG_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  }
   FUSG_CUDA_TRY(cudaMemset(ctx->dev_flag, 0, sizeof(int)));
   *out = ctx.release();
   return FUSG_OK;
@@ -192,19 +205,17 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
   FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
   const size_t bytes = size_t(count_of(K->grid)) * 16;
   cudaStream_t s = K->ctx->stream;
-  double *f = nullptr, *u = nullptr;
-  FUSG_CUDA_TRY(cudaMallocAsync(&f, bytes, s));
-  FUSG_CUDA_TRY(cudaMallocAsync(&u, bytes, s));
-  FUSG_CUDA_TRY(cudaMemcpyAsync(f, f_host, bytes, cudaMemcpyHostToDevice, s));
-  fusg_status st;
-  {
-    std::lock_guard<std::mutex> lock(K->mu);
-    st = volume_potential_apply(K, reinterpret_cast<const double2*>(f), reinterpret_cast<double2*>(u),
-                                scale, s);
+  std::lock_guard<std::mutex> lock(K->mu);
+  if (!K->stage_f) {  // device staging for host-vector applies, allocated once per kernel
+    if (cudaMalloc(&K->stage_f, bytes) != cudaSuccess || cudaMalloc(&K->stage_u, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return set_error(FUSG_OOM, "kernel_apply_host: staging allocation failed");
+    }
+    K->bytes += 2 * bytes;
   }
-  if (st == FUSG_OK) FUSG_CUDA_TRY(cudaMemcpyAsync(u_host, u, bytes, cudaMemcpyDeviceToHost, s));
-  cudaFreeAsync(f, s);
-  cudaFreeAsync(u, s);
+  FUSG_CUDA_TRY(cudaMemcpyAsync(K->stage_f, f_host, bytes, cudaMemcpyHostToDevice, s));
+  fusg_status st = volume_potential_apply(K, K->stage_f, K->stage_u, scale, s);
+  if (st == FUSG_OK) FUSG_CUDA_TRY(cudaMemcpyAsync(u_host, K->stage_u, bytes, cudaMemcpyDeviceToHost, s));
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return st;
 }
@@ -241,8 +252,10 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
   double scale = 0.0;
   if (t.power != 0.0) {  // power_scale_factor (src/transducer.cpp:157-163)
     double pw = 0.0;
+    const double dlo[3] = {x_disc, -R, -R}, dhi[3] = {x_disc, R, R};
     st = radiated_power_dev(ctx, src, t.n_points, x_disc, R, k1.k_re, k1.k_im,
-                            1.0 * cap_area / double(t.n_points), med.rho0, med.c0, 384, 256, &pw, s);
+                            1.0 * cap_area / double(t.n_points), med.rho0, med.c0, 384, 256, &pw, s,
+                            distance_bound(t.points_host, t.n_points, dlo, dhi));
     if (st != FUSG_OK) return st;
     if (pw <= 0.0) return set_error(FUSG_RUNTIME, "power normalization: degenerate field, Pi(p) = 0");
     scale = std::sqrt(t.power / pw);
@@ -251,7 +264,8 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
   if (source_normalization) *source_normalization = norm;
   const double amp1 = scale * cap_area / double(t.n_points);
   st = monopole_grid(ctx, src, t.n_points, grid_of(1), k1.k_re, k1.k_im, amp1,
-                     reinterpret_cast<double2*>(out_dev[0]), s);
+                     reinterpret_cast<double2*>(out_dev[0]), s,
+                     distance_bound(t.points_host, t.n_points, grid_of(1).lo, grid_of(1).hi));
   if (st != FUSG_OK) return st;
   st = check_monopole_flag(ctx, s);
   if (st != FUSG_OK) return st;
@@ -293,7 +307,8 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
       }
       temps.push_back(tmp);
       if (m == 1 && d->recompute_p1_each_grid)
-        st = monopole_grid(ctx, src, t.n_points, grid, k1.k_re, k1.k_im, amp1, tmp, s);
+        st = monopole_grid(ctx, src, t.n_points, grid, k1.k_re, k1.k_im, amp1, tmp, s,
+                           distance_bound(t.points_host, t.n_points, grid.lo, grid.hi));
       else
         st = interpolate_dev(ctx, gm, pm, grid, tmp, s);
       if (st != FUSG_OK) break;
@@ -306,11 +321,12 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
     double2* f = nullptr;
     if (st == FUSG_OK) st = fusg_complex_wavenumber(&med, t.f0, i, &ki);
     if (st == FUSG_OK) {
-      tm.start();
       if (cudaMallocAsync(&f, size_t(count) * 16, s) != cudaSuccess) {
         cudaGetLastError();
         st = set_error(FUSG_OOM, "run_cascade: source allocation failed");
       } else {
+        cudaStreamSynchronize(s);  // keep first-touch pool growth out of the rhs timing
+        tm.start();
         st = rhs_dev(ctx, i, lower.data(), count, fusg_rhs_coefficient(&med, ki.omega, i), f, s);
         if (st == FUSG_OK) row.rhs_s = tm.stop();
       }

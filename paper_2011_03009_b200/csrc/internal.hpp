@@ -57,9 +57,11 @@ struct fusg_kernel {
   int H[3] = {0, 0, 0};  // octant extents P/2 + 1
   fusg::AxisPlan plan[3]{};
   double2* tw[3] = {nullptr, nullptr, nullptr};
-  double2* koct = nullptr;  // kernel spectrum octant [Hz][Hy][Hx]
-  double2* bufA = nullptr;  // [Nz][Ny][Px]
-  double2* bufB = nullptr;  // [Nz][Py][Px]
+  double2* koct = nullptr;  // kernel spectrum octant [kx][ky][kz]  (Hx x Hy x Hz)
+  double2* bufA = nullptr;  // [kx][z][y]  (Px x Nz x Ny)
+  double2* bufB = nullptr;  // [kx][ky][z]  (Px x Py x Nz)
+  double2* stage_f = nullptr;  // host-vector apply staging (lazily allocated)
+  double2* stage_u = nullptr;
   uint64_t bytes = 0;
   std::mutex mu;  // serialises applies sharing the workspace
 };

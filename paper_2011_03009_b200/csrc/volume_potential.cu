@@ -667,9 +667,12 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   const int Hx = K->H[0], Hy = K->H[1], Hz = K->H[2];
   const size_t nA = size_t(Px) * Ny * Nz, nB = size_t(Px) * Py * Nz;
   const size_t nK = size_t(Hx) * Hy * Hz;
-  if (cudaMalloc(&K->bufA, nA * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc(&K->bufB, nB * sizeof(double2)) != cudaSuccess ||
-      cudaMalloc(&K->koct, nK * sizeof(double2)) != cudaSuccess) {
+  // stream-ordered allocations: the context's pool keeps freed workspaces for the next kernel
+  // (a cascade builds one GreenKernel per harmonic)
+  cudaStream_t as = K->ctx->stream;
+  if (cudaMallocAsync(&K->bufA, nA * sizeof(double2), as) != cudaSuccess ||
+      cudaMallocAsync(&K->bufB, nB * sizeof(double2), as) != cudaSuccess ||
+      cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess) {
     cudaGetLastError();
     return set_error(FUSG_OOM, "GreenKernel: device allocation failed");
   }
