@@ -218,6 +218,36 @@ def run_reference(args, world, rank):
     return 0
 
 
+def nested_solve(ctx, reps=2):
+    """BASELINE metric part 2: wall time of the nested 5-harmonic recursion (run_cascade) on
+    config 4's geometry at the desk frequency 0.275 MHz (full size needs >= 4 GPUs: SURVEY.md
+    8(e)). Best of `reps` after one warm-up; per-stage rows come from CUDA events."""
+    import torch
+
+    from paper_2011_03009_b200 import fus
+    from tools import cascades
+
+    cfg = cascades.cfg4(fus, desk=True)
+    fus.run_cascade(cfg, ctx=ctx)
+    best, rows = None, None
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fus.run_cascade(cfg, ctx=ctx)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if best is None or dt < best:
+            best, rows = dt, r.timings
+    n2 = cfg.plan.for_harmonic(2).grid.count()
+    p1 = rows[0].p1_s
+    return {"config": "cfg4 geometry (bowl R 7.5 cm, l 15 cm, c 1540, rho 1050, beta 4.5, 1 MPa) at "
+                      "f0=0.275 MHz, 4096 points, nested n_w=6, 5 harmonics",
+            "solve_s": best,
+            "grids": [list(cfg.plan.for_harmonic(i).grid.dims) for i in range(2, 6)],
+            "rows": [{k: v for k, v in t.__dict__.items()} for t in rows],
+            "rayleigh_terms_per_s": n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None}
+
+
 # ------------------------------------------------------------------------- GPU arm
 def run_gpu(args, world, rank, local):
     import torch
@@ -299,6 +329,10 @@ def run_gpu(args, world, rank, local):
     ctx.synchronize()
     assert torch.equal(ud.cpu(), uh), "device and host-vector applies disagree"
 
+    solve = None
+    if rank == 0 and not args.no_cascade:
+        solve = nested_solve(ctx)
+
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
@@ -335,6 +369,7 @@ def run_gpu(args, world, rank, local):
             "gpu_launches": int(launches),
             "clocks": clocks,
             "cpu_baseline": cpu_baseline,
+            "nested_5_harmonic_solve": solve,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -347,6 +382,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fusg", choices=["fusg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cascade", action="store_true", help="skip the nested 5-harmonic solve")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:

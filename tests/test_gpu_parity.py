@@ -283,3 +283,32 @@ def test_launch_counter_counts_library_kernels(ctx):
     before = ctx.launch_count()
     K.apply(fus.random_vector(g.count(), 3))
     assert ctx.launch_count() - before == 5  # passes A..E
+
+
+def _reduced_cfg4(lib):
+    # BASELINE config 4 geometry (bowl R 7.5 cm, l 15 cm, c 1540, rho 1050, beta 4.5, 1 MPa
+    # surface pressure, nested plan d=10.2 mm, n_w=6, 5 harmonics) at f0 = 1.1 MHz / 8 with
+    # 256 points so the CPU oracle finishes in seconds (the reference's own tests scale f0 the
+    # same way, tests/acceptance.cpp:181).
+    med = lib.Medium("cfg4", 1050.0, 1540.0, 4.5, 0.0, 1.0)
+    t = lib.make_bowl("cfg4", 1.1e6 / 8, 0.15, 0.075, 0.0, 256)
+    k1 = lib.complex_wavenumber(med, t.f0, 1)
+    return med, t, k1
+
+
+def test_nested_5_harmonic_cascade_vs_oracle(ctx, orc):
+    med, t, k1 = _reduced_cfg4(fus)
+    medo, to, k1o = _reduced_cfg4(orc)
+    s = 2.0 * k1.k.real * 1.0e6  # surface pressure -> amplitude
+    t.power = fus.radiated_power(t, med, k1, s)
+    to.power = orc.radiated_power(to, medo, k1o, s)
+    assert t.power == pytest.approx(to.power, rel=1e-12)
+    cfg = fus.CascadeConfig(med, t, fus.plan_nested_meshes(t, med, 10.2e-3, 6, 5), 5)
+    cfgo = orc.CascadeConfig(medo, to, orc.plan_nested_meshes(to, medo, 10.2e-3, 6, 5), 5)
+    r = fus.run_cascade(cfg)
+    ro = orc.run_cascade(cfgo, workers=16)
+    assert r.source_normalization == pytest.approx(s, rel=1e-9)
+    for n in range(1, 6):
+        assert r.p(n).grid.dims == ro.p(n).grid.dims
+        assert rel_l2(r.p(n).values, ro.p(n).values) <= 1e-10, n
+    assert [row.harmonic for row in r.timings] == [2, 3, 4, 5]
