@@ -1,0 +1,241 @@
+// C++ drop-in check: the reference's own test cases (tests/test_*.cpp, tests/acceptance.cpp),
+// written against the `namespace fus` API exactly as a reference user would, linked against
+// libfus.so -> libfusg.so.  `test_fus_api host` runs the host-arithmetic cases (no GPU);
+// `test_fus_api all` adds the device cases.
+#include <Eigen/Dense>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+
+#include "fus/cascade.hpp"
+#include "fus/grid.hpp"
+#include "fus/medium.hpp"
+#include "fus/potential.hpp"
+#include "fus/transducer.hpp"
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                           \
+  do {                                                                        \
+    if (cond) {                                                               \
+      ++g_pass;                                                               \
+    } else {                                                                  \
+      ++g_fail;                                                               \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);             \
+    }                                                                         \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                              \
+  do {                                                                        \
+    bool caught_ = false;                                                     \
+    try {                                                                     \
+      (void)(expr);                                                           \
+    } catch (const T&) {                                                      \
+      caught_ = true;                                                         \
+    }                                                                         \
+    CHECK(caught_);                                                           \
+  } while (0)
+
+namespace {
+
+const fus::Medium kWater = fus::medium_preset("water");
+
+Eigen::VectorXcd random_vector(std::size_t n, unsigned seed) {  // tests/test_potential.cpp:14-20
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  Eigen::VectorXcd v(static_cast<Eigen::Index>(n));
+  for (auto& x : v) {
+    const double re = u(rng);
+    const double im = u(rng);
+    x = {re, im};
+  }
+  return v;
+}
+
+double max_abs(const Eigen::VectorXcd& v) { return v.cwiseAbs().maxCoeff(); }
+
+// direct quadrature (the reference's direct_potential_oracle, src/potential.cpp:203-238)
+Eigen::VectorXcd direct(const fus::Wavenumber& k, const fus::VoxelGrid& g, const Eigen::VectorXcd& f) {
+  const double vol = g.dx * g.dx * g.dx;
+  const std::complex<double> self = fus::self_weight(k, g.dx);
+  Eigen::VectorXcd out(static_cast<Eigen::Index>(g.count()));
+  for (int iz = 0; iz < g.dims.z(); ++iz)
+    for (int iy = 0; iy < g.dims.y(); ++iy)
+      for (int ix = 0; ix < g.dims.x(); ++ix) {
+        std::complex<double> acc = 0.0;
+        for (int jz = 0; jz < g.dims.z(); ++jz)
+          for (int jy = 0; jy < g.dims.y(); ++jy)
+            for (int jx = 0; jx < g.dims.x(); ++jx) {
+              const std::complex<double> fj = f[g.index(jx, jy, jz)];
+              if (ix == jx && iy == jy && iz == jz) {
+                acc += self * fj;
+              } else {
+                acc += vol * fus::green_function(g.center(ix, iy, iz), g.center(jx, jy, jz), k) * fj;
+              }
+            }
+        out[g.index(ix, iy, iz)] = acc;
+      }
+  return out;
+}
+
+void host_cases() {
+  // tests/test_grid.cpp:15-36
+  fus::DomainBox box{{0, 0, 0}, {10e-3, 7e-3, 5e-3}};
+  const fus::VoxelGrid g = fus::make_grid(box, 1e-3, 1);
+  CHECK(g.dims == Eigen::Vector3i(10, 7, 5));
+  CHECK(g.count() == 350);
+  CHECK(g.index(0, 1, 0) == 10 && g.index(0, 0, 1) == 70);
+  CHECK(g.box.contains(box, 1e-12));
+  CHECK_THROWS_AS(fus::make_grid(box, -1.0, 1), std::invalid_argument);
+  // golden: proj/test_output.txt:31
+  const fus::BowlTransducer h131 = fus::transducer_preset("H131", 100.0, 16);
+  const fus::MeshPlan plan = fus::plan_nested_meshes(h131, kWater, 10.2e-3, 6, 5);
+  CHECK(plan.reference.dims == Eigen::Vector3i(914, 737, 737));
+  CHECK(plan.for_harmonic(2).grid.dims == Eigen::Vector3i(366, 295, 295));
+  CHECK(std::fabs(plan.reduction_factor(2) - 15.586767385165057) < 1e-9);
+  CHECK_THROWS_AS(plan.for_harmonic(9), std::out_of_range);
+  CHECK(!plan.report().empty());
+  // tests/test_transducer.cpp:50-69 (count, on sphere)
+  for (int np : {1, 7, 128, 4096}) {
+    const auto pts = fus::distribute_points(35e-3, 16.5e-3, np);
+    CHECK(int(pts.size()) == np);
+    bool on = true;
+    for (const auto& p : pts)
+      on = on && std::fabs((p - Eigen::Vector3d(35e-3, 0, 0)).norm() - 35e-3) < 1e-13 * 35e-3;
+    CHECK(on);
+  }
+  // tests/test_medium.cpp
+  const fus::Medium liver = fus::medium_preset("liver");
+  const fus::Wavenumber k1 = fus::complex_wavenumber(liver, 1.1e6, 1);
+  const fus::Wavenumber k4 = fus::complex_wavenumber(liver, 1.1e6, 4);
+  CHECK(std::fabs(k4.k.real() - 4 * k1.k.real()) <= 1e-14 * k4.k.real());
+  CHECK(std::fabs(k4.k.imag() / k1.k.imag() - std::pow(4.0, liver.eta)) < 1e-12);
+  CHECK_THROWS_AS(fus::complex_wavenumber(liver, -1.0, 1), std::invalid_argument);
+  CHECK_THROWS_AS(fus::medium_preset("granite"), std::invalid_argument);
+  // tests/test_potential.cpp:40-46
+  CHECK(std::fabs(fus::equivalent_sphere_radius(1.0) - 0.6203504908994001) < 1e-12);
+}
+
+void device_cases() {
+  // tests/test_potential.cpp:75-92 and criterion 2
+  fus::DomainBox box{{0, 0, 0}, {20e-4, 18e-4, 16e-4}};
+  const fus::VoxelGrid grid = fus::make_grid(box, 1e-4, 2);
+  CHECK(grid.dims == Eigen::Vector3i(20, 18, 16));
+  const fus::Wavenumber k = fus::complex_wavenumber(kWater, 1.1e6, 2);
+  for (unsigned seed : {1234u, 2024u}) {
+    const Eigen::VectorXcd f = random_vector(grid.count(), seed);
+    const fus::GreenKernel kernel(grid, k);
+    const Eigen::VectorXcd u = kernel.apply(f);
+    const Eigen::VectorXcd ref = direct(k, grid, f);
+    CHECK(max_abs(u - ref) < 1e-12 * max_abs(ref));
+    const fus::GreenKernel padded(grid, k, true);
+    CHECK(max_abs(padded.apply(f) - ref) < 1e-12 * max_abs(ref));
+  }
+  CHECK_THROWS_AS(fus::GreenKernel(grid, k).apply(Eigen::VectorXcd(7)), std::invalid_argument);
+  // delta column, tests/test_potential.cpp:117-139
+  {
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {9e-4, 8e-4, 7e-4}}, 1e-4, 1);
+    const fus::Wavenumber k1 = fus::complex_wavenumber(kWater, 1.1e6, 1);
+    Eigen::VectorXcd delta = Eigen::VectorXcd::Zero(static_cast<Eigen::Index>(g.count()));
+    const std::size_t j = g.index(4, 3, 2);
+    delta[static_cast<Eigen::Index>(j)] = 1.0;
+    const Eigen::VectorXcd col = fus::GreenKernel(g, k1).apply(delta);
+    const double vol = g.dx * g.dx * g.dx;
+    bool ok = true;
+    for (int iz = 0; iz < g.dims.z(); ++iz)
+      for (int iy = 0; iy < g.dims.y(); ++iy)
+        for (int ix = 0; ix < g.dims.x(); ++ix) {
+          const std::size_t i = g.index(ix, iy, iz);
+          const std::complex<double> want =
+              i == j ? fus::self_weight(k1, g.dx)
+                     : vol * fus::green_function(g.center(ix, iy, iz), g.center(4, 3, 2), k1);
+          ok = ok && std::abs(col[static_cast<Eigen::Index>(i)] - want) < 1e-13 * std::abs(want) + 1e-20;
+        }
+    CHECK(ok);
+  }
+  // rhs coefficients, tests/test_cascade.cpp:33-63
+  {
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {2e-3, 2e-3, 2e-3}}, 1e-3, 1);
+    const double omega = 2 * M_PI * 1.1e6;
+    const std::complex<double> a(2.0, 1.0), b(0.5, -3.0);
+    std::vector<fus::HarmonicField> lower;
+    lower.push_back({g, Eigen::VectorXcd::Constant(static_cast<Eigen::Index>(g.count()), a),
+                     fus::complex_wavenumber(kWater, 1.1e6, 1)});
+    lower.push_back({g, Eigen::VectorXcd::Constant(static_cast<Eigen::Index>(g.count()), b),
+                     fus::complex_wavenumber(kWater, 1.1e6, 2)});
+    const double base = kWater.beta * omega * omega / (2 * kWater.rho0 * std::pow(kWater.c0, 4));
+    const Eigen::VectorXcd f3 = fus::rhs_source(3, lower, kWater, omega);
+    CHECK(std::abs(f3[0] - base * 9.0 * 2.0 * a * b) < 1e-10 * std::abs(f3[0]));
+    CHECK_THROWS_AS(fus::rhs_source(1, lower, kWater, omega), std::invalid_argument);
+  }
+  // interpolation exact on affine fields, tests/test_grid.cpp:90-122
+  {
+    const fus::VoxelGrid coarse = fus::make_grid({{0, 0, 0}, {8e-3, 8e-3, 8e-3}}, 1e-3, 1);
+    const fus::VoxelGrid fine = fus::make_grid({{1e-3, 1e-3, 1e-3}, {7e-3, 7e-3, 7e-3}}, 0.4e-3, 2);
+    auto affine = [](const Eigen::Vector3d& p) {
+      return std::complex<double>(2.0 + 100.0 * p.x() - 40.0 * p.y(), 7.0 * p.z());
+    };
+    fus::HarmonicField f{coarse, Eigen::VectorXcd(static_cast<Eigen::Index>(coarse.count())),
+                         fus::complex_wavenumber(kWater, 1.1e6, 1)};
+    for (int iz = 0; iz < coarse.dims.z(); ++iz)
+      for (int iy = 0; iy < coarse.dims.y(); ++iy)
+        for (int ix = 0; ix < coarse.dims.x(); ++ix)
+          f.values[static_cast<Eigen::Index>(coarse.index(ix, iy, iz))] = affine(coarse.center(ix, iy, iz));
+    const fus::HarmonicField gfield = fus::interpolate(f, fine);
+    double err = 0;
+    for (int iz = 0; iz < fine.dims.z(); ++iz)
+      for (int iy = 0; iy < fine.dims.y(); ++iy)
+        for (int ix = 0; ix < fine.dims.x(); ++ix)
+          err = std::max(err, std::abs(gfield.values[static_cast<Eigen::Index>(fine.index(ix, iy, iz))] -
+                                       affine(fine.center(ix, iy, iz))));
+    CHECK(err < 1e-12);
+  }
+  // power normalisation, tests/test_transducer.cpp:95-113
+  {
+    fus::BowlTransducer t = fus::transducer_preset("H131", 40.0, 512);
+    const fus::Wavenumber k1 = fus::complex_wavenumber(kWater, t.f0, 1);
+    const double s = fus::power_scale_factor(t, kWater, k1);
+    CHECK(std::fabs(fus::radiated_power(t, kWater, k1, s) - 40.0) < 1e-12 * 40.0);
+    t.power = 0.0;
+    CHECK(fus::power_scale_factor(t, kWater, k1) == 0.0);
+    CHECK_THROWS_AS(fus::unnormalized_field(t, {t.source_points[3]}, k1), std::invalid_argument);
+  }
+  // cascade structure, homogeneity and bitwise determinism, tests/test_cascade.cpp:65-106
+  {
+    auto tiny = [](double power) {
+      fus::CascadeConfig cfg;
+      cfg.medium = kWater;
+      cfg.transducer = fus::transducer_preset("H131", power, 128);
+      cfg.transducer.f0 = 0.25e6;
+      cfg.plan = fus::plan_nested_meshes(cfg.transducer, cfg.medium, 6e-3, 3, 3, 0.35);
+      cfg.n_harmonics = 3;
+      return cfg;
+    };
+    const fus::CascadeResult r1 = fus::run_cascade(tiny(10.0));
+    const fus::CascadeResult r4 = fus::run_cascade(tiny(40.0));
+    CHECK(r1.harmonics.size() == 3 && r1.timings.size() == 2);
+    CHECK(r1.timings[0].harmonic == 2 && r1.timings[1].harmonic == 3);
+    const double s[3] = {2.0, 4.0, 8.0};
+    for (int n = 1; n <= 3; ++n)
+      CHECK((r4.p(n).values - s[n - 1] * r1.p(n).values).norm() / r1.p(n).values.norm() < 1e-12);
+    const fus::CascadeResult again = fus::run_cascade(tiny(10.0));
+    CHECK(again.p(2).values == r1.p(2).values && again.p(3).values == r1.p(3).values);
+  }
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool all = argc > 1 && std::strcmp(argv[1], "all") == 0;
+  try {
+    host_cases();
+    if (all) device_cases();
+  } catch (const std::exception& e) {
+    std::printf("FAIL uncaught exception: %s\n", e.what());
+    ++g_fail;
+  }
+  std::printf("%s: %d passed, %d failed\n", g_fail ? "FAILED" : "OK", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -101,3 +101,15 @@ def test_rhs_coefficient_matches_reference_expression():
     for n in (2, 3, 5):
         want = w.beta * om * om * float(n) * float(n) / (2.0 * w.rho0 * math.pow(w.c0, 4))
         assert _lib.lib().fusg_rhs_coefficient(C.byref(w.c()), om, n) == want
+
+
+def test_cpp_dropin_api_host_cases():
+    """The reference's own host-side cases, compiled against the namespace fus headers
+    (include/fus/*.hpp) and linked to libfus.so -> libfusg.so."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "build", "test_fus_api")
+    assert os.path.exists(exe), "built by __graft_entry__.build() (make -C paper_2011_03009_b200/csrc)"
+    out = subprocess.run([exe, "host"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "OK:" in out.stdout

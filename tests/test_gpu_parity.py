@@ -312,3 +312,14 @@ def test_nested_5_harmonic_cascade_vs_oracle(ctx, orc):
         assert r.p(n).grid.dims == ro.p(n).grid.dims
         assert rel_l2(r.p(n).values, ro.p(n).values) <= 1e-10, n
     assert [row.harmonic for row in r.timings] == [2, 3, 4, 5]
+
+
+def test_cpp_dropin_api_all_cases(ctx):
+    """C++ namespace-fus drop-in: host + device cases (apply vs direct quadrature, delta
+    column, rhs, interpolation, power normalisation, cascade homogeneity/determinism)."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "test_fus_api")
+    out = subprocess.run([exe, "all"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
