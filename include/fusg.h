@@ -184,6 +184,37 @@ typedef struct fusg_cascade_desc {
 fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* desc, double* const* out_dev,
                              fusg_stage_timing* timings, double* source_normalization);
 
+/* ---------------------------------------------------------------- slab sharding
+ * rank r of G owns z-planes [z0, z0+nz) of f and u (ragged split: the first
+ * N mod G ranks take one extra plane) and spectral kx columns [x0, x0+nx) of the padded box.
+ * The apply transposes z-slab -> x-slab after the forward x pass and back before the inverse
+ * x pass (one all-to-all each way); the kernel spectrum is replicated. */
+fusg_status fusg_slab_range(int32_t n, int32_t nranks, int32_t rank, int32_t* begin, int32_t* count);
+/* Exchange plan of rank `rank` (arrays of nranks, complex128 element offsets/counts):
+ * a_off/a_cnt[q]: block of A_r [Px][nz_r][Ny] holding rank q's kx columns (sent to q in the
+ * forward transpose, received from q in the inverse one); r_off/r_cnt[p]: block of the staging
+ * buffer [p][nx_r][nz_p][Ny] received from p (forward) / sent to p (inverse). Host only. */
+fusg_status fusg_slab_exchange_plan(const fusg_grid* global_grid, int32_t nranks, int32_t rank,
+                                    int64_t* a_off, int64_t* a_cnt, int64_t* r_off, int64_t* r_cnt);
+/* NCCL transport: one process per GPU. Rank 0 creates the id; every rank attaches with it. */
+fusg_status fusg_nccl_unique_id(uint8_t id[128]);
+fusg_status fusg_ctx_attach_nccl(fusg_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+/* GreenKernel for rank `rank` of an nranks-way decomposition of the GLOBAL grid. */
+fusg_status fusg_kernel_create_slab(fusg_ctx* ctx, const fusg_grid* global_grid,
+                                    const fusg_wavenumber* k, int32_t pad_small_primes,
+                                    int32_t nranks, int32_t rank, fusg_kernel** out);
+fusg_status fusg_kernel_slab(const fusg_kernel* kernel, int32_t* z0, int32_t* nz, int32_t* x0,
+                             int32_t* nx);
+/* This rank's apply: f_dev/u_dev are its z-slab [nz][Ny][Nx]; collective over the context's
+ * NCCL communicator (all ranks call it). */
+fusg_status fusg_kernel_apply_slab(fusg_kernel* kernel, const double* f_dev, double* u_dev,
+                                   double scale, void* stream);
+/* Loopback transport: all ranks of one decomposition in this process on one device (same
+ * context), exchanging by device copies; same blocks and kernels as the NCCL path. */
+fusg_status fusg_kernel_apply_slab_loopback(fusg_kernel* const* ranks, int32_t nranks,
+                                            const double* const* f_dev, double* const* u_dev,
+                                            double scale);
+
 #ifdef __cplusplus
 }
 #endif

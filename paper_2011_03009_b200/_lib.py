@@ -95,6 +95,20 @@ SIGNATURES = {
     "fusg_interpolate": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.POINTER(Grid), _vp, _vp]),
     "fusg_run_cascade": (C.c_int, [_vp, C.POINTER(CascadeDesc), C.POINTER(_vp),
                                    C.POINTER(StageTiming), _dp]),
+    "fusg_slab_range": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_int32)]),
+    "fusg_slab_exchange_plan": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64)]),
+    "fusg_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "fusg_ctx_attach_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
+    "fusg_kernel_create_slab": (C.c_int, [_vp, C.POINTER(Grid), C.POINTER(Wave), C.c_int32, C.c_int32,
+                                          C.c_int32, C.POINTER(_vp)]),
+    "fusg_kernel_slab": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fusg_kernel_apply_slab": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp]),
+    "fusg_kernel_apply_slab_loopback": (C.c_int, [C.POINTER(_vp), C.c_int32, C.POINTER(_vp),
+                                                  C.POINTER(_vp), C.c_double]),
 }
 
 _lib = None

@@ -45,6 +45,8 @@ void free_kernel(fusg_kernel* K) {
   cudaFreeAsync(K->bufA, s);
   cudaFreeAsync(K->bufB, s);
   cudaFreeAsync(K->koct, s);
+  if (K->xbuf) cudaFreeAsync(K->xbuf, s);
+  if (K->rbuf) cudaFreeAsync(K->rbuf, s);
   cudaFree(K->stage_f);
   cudaFree(K->stage_u);
   for (auto* t : K->tw) cudaFree(t);
@@ -103,6 +105,7 @@ fusg_status fusg_ctx_destroy(fusg_ctx* ctx) {
   if (!ctx) return FUSG_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  destroy_nccl(ctx);
   cudaFree(ctx->dev_flag);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -136,7 +139,8 @@ fusg_status fusg_kernel_create(fusg_ctx* ctx, const fusg_grid* grid, const fusg_
   K->ctx = ctx;
   K->grid = *grid;
   K->k = *k;
-  st = volume_potential_build(K, make_double2(w0[0], w0[1]));
+  st = kernel_init_geometry(K, 1, 0);
+  if (st == FUSG_OK) st = volume_potential_build(K, make_double2(w0[0], w0[1]));
   if (st != FUSG_OK) {
     free_kernel(K);
     return st;

@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/fusg.h"
 #include "plan.hpp"
@@ -45,6 +46,8 @@ struct fusg_ctx {
   int num_sms = 148;
   int* dev_flag = nullptr;  // device error flag (monopole coincidence)
   std::atomic<uint64_t> launches{0};
+  void* nccl = nullptr;  // ncclComm_t of a sharded job (fusg_ctx_attach_nccl)
+  int nranks = 1, rank = 0;
   std::mutex mu;
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
 };
@@ -62,12 +65,28 @@ struct fusg_kernel {
   double2* bufB = nullptr;  // [kx][ky][z]  (Px x Py x Nz)
   double2* stage_f = nullptr;  // host-vector apply staging (lazily allocated)
   double2* stage_u = nullptr;
+  // slab decomposition (unsharded: G = 1, rank 0 owns everything)
+  int G = 1, rank = 0;
+  bool slab = false;   // created by fusg_kernel_create_slab: owns exchange buffers even at G = 1
+  int z0 = 0, nz = 0;  // this rank's z-planes of f/u
+  int x0 = 0, nx = 0;  // this rank's spectral kx columns
+  std::vector<int> zs, nzs, xs, nxs;  // all ranks' ranges (exchange offsets)
+  double2* xbuf = nullptr;  // x-slab X [nx][Nz][Ny] (G > 1; aliases bufA when G = 1)
+  double2* rbuf = nullptr;  // all-to-all staging [p][nx][nz_p][Ny] (G > 1)
+  std::vector<int64_t> aoff, acnt, roff, rcnt;  // exchange plan (fusg_slab_exchange_plan)
   uint64_t bytes = 0;
   std::mutex mu;  // serialises applies sharing the workspace
 };
 
 namespace fusg {
+// Padded sizes, FFT plans, twiddles and the slab decomposition (G ranks, this is `rank`).
+fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank);
+void slab_split(int n, int G, int r, int* begin, int* count);
 fusg_status volume_potential_build(fusg_kernel* K, double2 self);
+fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s);
+fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev = nullptr);
+fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t s);
+void destroy_nccl(fusg_ctx* ctx);
 // ev (optional): 6 events recorded before passes A..E and after E
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t st, cudaEvent_t* ev = nullptr);

@@ -109,12 +109,14 @@ struct RegMulAt {
 };
 // Kernel-spectrum octant addressing for pass C lines (i = ky, k = kx; position kz):
 // element = p + fold(kx) * s_kx + fold(ky) * s_ky + fold(kz) * s_kz.
+// kx is the local spectral column of an x-slab: global kx = kx + kx_off (0 unsharded).
 struct KOct {
   const double2* p;
   int Px, Py, Pz;
   int64_t s_kx, s_ky, s_kz;
+  int kx_off;
   __device__ __forceinline__ const double2* line(int ky, int kx) const {
-    return p + fold_index(kx, Px) * s_kx + fold_index(ky, Py) * s_ky;
+    return p + fold_index(kx + kx_off, Px) * s_kx + fold_index(ky, Py) * s_ky;
   }
 };
 
@@ -490,7 +492,9 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_conv(WArgs a) {
   const bool ok = line < int64_t(a.n_inner) * a.n_outer;
   const int64_t li = ok ? line : 0;
   const int ky = interleave_index(int(li % a.n_inner), a.ko.Py);
-  const int kx = interleave_index(int(li / a.n_inner), a.ko.Px);
+  // mirror-interleave kx only when this launch owns every column (unsharded)
+  const int kx = a.n_outer == a.ko.Px ? interleave_index(int(li / a.n_inner), a.ko.Px)
+                                      : int(li / a.n_inner);
   const double2* kline = a.ko.line(ky, kx);
   PrivEx ex{sm + g * L};
   RowIn src{a.in + ky * a.in_si + int64_t(kx) * a.in_sk, 1, a.in_nvalid, ok};
@@ -653,86 +657,151 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
 }
 
 // ---------------------------------------------------------------------------- build
-fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
-  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+void slab_split(int n, int G, int r, int* begin, int* count) {
+  const int base = n / G, extra = n % G;  // the first `extra` ranks take one more (ragged)
+  *count = base + (r < extra ? 1 : 0);
+  *begin = r * base + std::min(r, extra);
+}
+
+fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank) {
   for (int a = 0; a < 3; ++a) {
     K->P[a] = smooth_padded_size(K->grid.dims[a], false);
     K->H[a] = K->P[a] / 2 + 1;
     if (!make_plan_radices(K->P[a], K->plan[a]))
       return set_error(FUSG_INVALID_ARGUMENT, "no FFT plan for padded length");
+  }
+  if (G < 1 || rank < 0 || rank >= G) return set_error(FUSG_INVALID_ARGUMENT, "bad slab rank");
+  if (G > K->grid.dims[2] || G > K->P[0])
+    return set_error(FUSG_INVALID_ARGUMENT, "more ranks than z-planes or kx columns");
+  K->G = G;
+  K->rank = rank;
+  K->zs.resize(G);
+  K->nzs.resize(G);
+  K->xs.resize(G);
+  K->nxs.resize(G);
+  for (int r = 0; r < G; ++r) {
+    slab_split(K->grid.dims[2], G, r, &K->zs[r], &K->nzs[r]);
+    slab_split(K->P[0], G, r, &K->xs[r], &K->nxs[r]);
+  }
+  K->z0 = K->zs[rank];
+  K->nz = K->nzs[rank];
+  K->x0 = K->xs[rank];
+  K->nx = K->nxs[rank];
+  return FUSG_OK;
+}
+
+fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  for (int a = 0; a < 3; ++a) {
     FUSG_TRY(upload_twiddles(K->P[a], &K->tw[a]));
     K->plan[a].tw = K->tw[a];
   }
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
   const int Hx = K->H[0], Hy = K->H[1], Hz = K->H[2];
-  const size_t nA = size_t(Px) * Ny * Nz, nB = size_t(Px) * Py * Nz;
+  // rank-local apply buffers (unsharded: nz = Nz, nx = Px and X aliases A); the full octant
+  // is built on every rank (it depends only on the grid and k)
+  const size_t nA = size_t(Px) * Ny * K->nz, nB = size_t(K->nx) * Py * Nz;
   const size_t nK = size_t(Hx) * Hy * Hz;
+  const size_t nX = (K->G > 1 || K->slab) ? size_t(K->nx) * Nz * Ny : 0;
   // stream-ordered allocations: the context's pool keeps freed workspaces for the next kernel
   // (a cascade builds one GreenKernel per harmonic)
   cudaStream_t as = K->ctx->stream;
+  double2 *g1 = nullptr, *g2 = nullptr;  // build scratch: [oz][oy][kx] and [oz][ky][kx] half-ranges
   if (cudaMallocAsync(&K->bufA, nA * sizeof(double2), as) != cudaSuccess ||
       cudaMallocAsync(&K->bufB, nB * sizeof(double2), as) != cudaSuccess ||
-      cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess) {
+      cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess ||
+      (nX && cudaMallocAsync(&K->xbuf, nX * sizeof(double2), as) != cudaSuccess) ||
+      (nX && cudaMallocAsync(&K->rbuf, nX * sizeof(double2), as) != cudaSuccess) ||
+      cudaMallocAsync(&g1, size_t(Hx) * Ny * Nz * sizeof(double2), as) != cudaSuccess ||
+      cudaMallocAsync(&g2, size_t(Hx) * Hy * Nz * sizeof(double2), as) != cudaSuccess) {
     cudaGetLastError();
+    if (g1) cudaFreeAsync(g1, as);
+    if (g2) cudaFreeAsync(g2, as);
     return set_error(FUSG_OOM, "GreenKernel: device allocation failed");
   }
-  K->bytes = (nA + nB + nK) * sizeof(double2);
+  K->bytes = (nA + nB + nK + 2 * nX) * sizeof(double2);
 
   fusg_ctx* ctx = K->ctx;
   cudaStream_t s = ctx->stream;
   const double dx = K->grid.dx;
   // G1: generate K along x for offsets (oy, oz) >= 0, forward x, keep kx <= Px/2
   KGenF gen{Nx, Ny, Px, dx, dx * dx * dx, K->k.k_re, K->k.k_im, self};
-  GStoreF s1{GStore{K->bufA, Hx, 0, 1, Hx, 1.0}};
+  GStoreF s1{GStore{g1, Hx, 0, 1, Hx, 1.0}};
   FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, gen, s1, s));
   // G2: even extension along y, forward y, keep ky <= Py/2
-  FoldF l2{K->bufA, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
-  GStoreF s2{GStore{K->bufB, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
+  FoldF l2{g1, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
+  GStoreF s2{GStore{g2, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
   FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Hx, Nz, l2, s2, s));
   // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant
-  FoldF l3{K->bufB, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
+  FoldF l3{g2, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
   GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx][ky][kz]
   FUSG_TRY(launch_axis<false>(ctx, K->plan[2], Hx, Hy, l3, s3, s));
+  cudaFreeAsync(g1, s);
+  cudaFreeAsync(g2, s);
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return FUSG_OK;
 }
 
 // ---------------------------------------------------------------------------- apply
+// ---------------------------------------------------------------------------- apply phases
+// Rank r of G owns z-planes [z0, z0 + nz) of f/u and, in spectral space, columns
+// [x0, x0 + nx) of kx (unsharded: G = 1, nz = Nz, nx = Px, X == A).
+//   phase A : f_r [nz][Ny][Nx] -> A_r [Px][nz][Ny]            (pass A; slices of A_r by kx
+//             range are the all-to-all send blocks, contiguous)
+//   exchange: A_r -> X_r [nx][Nz][Ny]                          (transpose z-slab -> x-slab)
+//   phase BCD: X_r -> B_r [nx][Py][Nz] -> C in place -> X_r     (passes B, C, D)
+//   exchange: X_r -> A_r                                       (transpose back)
+//   phase E : A_r -> u_r                                       (pass E, scale/|P|, crop)
+fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1];
+  const int Px = K->P[0], nz = K->nz;
+  return launch_axis<false>(K->ctx, K->plan[0], Ny, nz,
+                            GLoadF{GLoad{f, Nx, int64_t(Ny) * Nx, 1, Nx}},
+                            GStoreF{GStore{K->bufA, 1, Ny, int64_t(nz) * Ny, Px, 1.0}}, s, kKindRow);
+}
+
+// passes B, C, D on the x-slab X [nx][Nz][Ny]; ev (optional) marks after B and after C
+fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev) {
+  const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
+  const int Hy = K->H[1], Hz = K->H[2];
+  const int nx = K->nx;
+  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  // B: y rows of X (lines z, tiled; outer kx) -> B, transposed so z is contiguous
+  FUSG_TRY(launch_axis<false>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{X, Ny, NzNy, 1, Ny}},
+                              GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
+  if (ev) cudaEventRecord(ev[0], s);
+  // C: z rows of B (lines ky; outer kx): forward, * K^, inverse, keep Nz; in place
+  FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
+                       GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
+                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0}, s));
+  if (ev) cudaEventRecord(ev[1], s);
+  // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of X, keep Ny
+  return launch_axis<true>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
+                           GStoreF{GStore{X, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol);
+}
+
+fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1];
+  const int Px = K->P[0], nz = K->nz;
+  const double total = double(K->P[0]) * double(K->P[1]) * double(K->P[2]);
+  return launch_axis<true>(K->ctx, K->plan[0], Ny, nz,
+                           GLoadF{GLoad{K->bufA, 1, Ny, int64_t(nz) * Ny, Px}},
+                           GStoreF{GStore{u, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
+}
+
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t s, cudaEvent_t* ev) {
+  if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: sharded kernel needs a slab apply");
   auto mark = [&](int i) {
     if (ev) cudaEventRecord(ev[i], s);
   };
-  fusg_ctx* ctx = K->ctx;
-  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
-  const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
-  const int Hy = K->H[1], Hz = K->H[2];
-  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz, NyNx = int64_t(Ny) * Nx;
-  const double total = double(Px) * double(Py) * double(Pz);
-  // Layouts: f, u [z][y][x]; A [kx][z][y]; B [kx][ky][z]; octant [kx][ky][kz].  Every pass
-  // reads or writes whole rows or 8-line-wide column tiles; pass C (two transforms per
-  // element) runs on contiguous rows.
   mark(0);
-  // A: x rows of f (lines y, tiled; outer z) -> A, transposed so y is contiguous
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny, Nz, GLoadF{GLoad{f, Nx, NyNx, 1, Nx}},
-                              GStoreF{GStore{K->bufA, 1, Ny, NzNy, Px, 1.0}}, s, kKindRow));
+  FUSG_TRY(apply_phase_A(K, f, s));
   mark(1);
-  // B: y rows of A (lines z, tiled; outer kx) -> B, transposed so z is contiguous
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Nz, Px, GLoadF{GLoad{K->bufA, Ny, NzNy, 1, Ny}},
-                              GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
-  mark(2);
-  // C: z rows of B (lines ky; outer kx): forward, * K^, inverse, keep Nz; in place
-  FUSG_TRY(launch_conv(ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
-                       GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
-                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1}, s));
-  mark(3);
-  // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of A, keep Ny
-  FUSG_TRY(launch_axis<true>(ctx, K->plan[1], Nz, Px, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
-                             GStoreF{GStore{K->bufA, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
+  FUSG_TRY(apply_phase_BCD(K, K->bufA, s, ev ? ev + 2 : nullptr));
   mark(4);
-  // E: kx columns of A (lines y, tiled, contiguous; outer z) -> x rows of u, scale, crop
-  FUSG_TRY(launch_axis<true>(ctx, K->plan[0], Ny, Nz, GLoadF{GLoad{K->bufA, 1, Ny, NzNy, Px}},
-                             GStoreF{GStore{u, Nx, NyNx, 1, Nx, scale / total}}, s, kKindCol));
+  FUSG_TRY(apply_phase_E(K, u, scale, s));
   mark(5);
   return FUSG_OK;
 }

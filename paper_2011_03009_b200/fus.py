@@ -564,3 +564,87 @@ def run_cascade(cfg: CascadeConfig, ctx: Optional[Context] = None) -> CascadeRes
         res.timings.append(StageTiming(r.harmonic, int(r.voxels), r.meshing_s, r.interpolation_s,
                                        r.kernel_s, r.potential_s, r.p1_s, r.rhs_s))
     return res
+
+
+# ------------------------------------------------------------------------ slab sharding
+def slab_range(n: int, nranks: int, rank: int):
+    """(begin, count) of rank's share of n (ragged: the first n % nranks ranks take one more)."""
+    b, c = C.c_int32(), C.c_int32()
+    check(lib().fusg_slab_range(int(n), int(nranks), int(rank), C.byref(b), C.byref(c)))
+    return b.value, c.value
+
+
+def slab_exchange_plan(grid: VoxelGrid, nranks: int, rank: int) -> dict:
+    """Per-peer element offsets/counts of the two slab transposes (include/fusg.h)."""
+    arrs = {k: np.zeros(nranks, np.int64) for k in ("a_off", "a_cnt", "r_off", "r_cnt")}
+    g = grid.c()
+    p = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+    check(lib().fusg_slab_exchange_plan(C.byref(g), int(nranks), int(rank), p(arrs["a_off"]),
+                                        p(arrs["a_cnt"]), p(arrs["r_off"]), p(arrs["r_cnt"])))
+    return arrs
+
+
+class SlabKernel:
+    """GreenKernel for rank `rank` of an nranks-way z-slab decomposition of the global grid."""
+
+    def __init__(self, grid: VoxelGrid, k: Wavenumber, nranks: int, rank: int,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or context()
+        self.grid, self.k, self.nranks, self.rank = grid, k, nranks, rank
+        h = C.c_void_p()
+        g, w = grid.c(), k.c()
+        check(lib().fusg_kernel_create_slab(self.ctx.handle, C.byref(g), C.byref(w), 0, int(nranks),
+                                            int(rank), C.byref(h)))
+        self.handle = h
+        v = [C.c_int32() for _ in range(4)]
+        check(lib().fusg_kernel_slab(h, *[C.byref(x) for x in v]))
+        self.z0, self.nz, self.x0, self.nx = (x.value for x in v)
+
+    def slab_count(self) -> int:
+        return self.nz * int(self.grid.dims[1]) * int(self.grid.dims[0])
+
+    def apply(self, f_slab, scale: float = 1.0):
+        """This rank's apply over NCCL (every rank calls it); f_slab: [nz][Ny][Nx] on device."""
+        u = torch.empty_like(f_slab)
+        _sync_torch_to(self.ctx)
+        check(lib().fusg_kernel_apply_slab(self.handle, f_slab.data_ptr(), u.data_ptr(), float(scale), None))
+        self.ctx.synchronize()
+        return u
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().fusg_kernel_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def attach_nccl(ctx: Context, nranks: int, rank: int, unique_id: bytes):
+    """Create this context's NCCL communicator (unique_id from nccl_unique_id() on rank 0)."""
+    buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+    check(lib().fusg_ctx_attach_nccl(ctx.handle, int(nranks), int(rank), buf))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().fusg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def apply_slab_loopback(grid: VoxelGrid, k: Wavenumber, f, nranks: int, scale: float = 1.0,
+                        ctx: Optional[Context] = None):
+    """Run an nranks-way slab decomposition of the apply in this process on one GPU (loopback
+    transport: the NCCL path's blocks and kernels with device copies); returns the global u."""
+    ctx = ctx or context()
+    fd = _on_device(f, ctx)
+    ks = [SlabKernel(grid, k, nranks, r, ctx) for r in range(nranks)]
+    plane = int(grid.dims[1]) * int(grid.dims[0])
+    fs = [fd[kk.z0 * plane:(kk.z0 + kk.nz) * plane].contiguous() for kk in ks]
+    us = [torch.empty_like(x) for x in fs]
+    hs = (C.c_void_p * nranks)(*[kk.handle.value for kk in ks])
+    fp = (C.c_void_p * nranks)(*[x.data_ptr() for x in fs])
+    up = (C.c_void_p * nranks)(*[x.data_ptr() for x in us])
+    _sync_torch_to(ctx)
+    check(lib().fusg_kernel_apply_slab_loopback(hs, int(nranks), fp, up, float(scale)))
+    return torch.cat(us)

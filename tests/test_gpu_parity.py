@@ -323,3 +323,33 @@ def test_cpp_dropin_api_all_cases(ctx):
     exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "build", "test_fus_api")
     out = subprocess.run([exe, "all"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("dims,G", [((37, 20, 19), 2), ((37, 20, 19), 3), ((64, 64, 64), 4),
+                                    ((16, 24, 9), 8), ((25, 30, 7), 7)])
+def test_slab_sharded_apply_loopback_is_bitwise_unsharded(ctx, dims, G):
+    # the sharded apply uses the same pass kernels and differs only in data
+    # movement, so every decomposition must reproduce the single-GPU apply bit for bit.
+    dx = 1e-4
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), 5)
+    want = fus.GreenKernel(g, k).apply(f)
+    got = fus.apply_slab_loopback(g, k, f, G)
+    assert torch.equal(got, want)
+
+
+def test_slab_apply_over_nccl_single_rank(ctx):
+    # The NCCL transport's full path (phase A, grouped send/recv, unpack, B-D, pack, send/recv,
+    # phase E) on a 1-rank communicator: every NCCL call runs (to self); bitwise = unsharded.
+    g = fus.make_grid([0, 0, 0], [37e-4, 20e-4, 19e-4], 1e-4, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), 11)
+    want = fus.GreenKernel(g, k).apply(f)
+    c = fus.Context(0)
+    fus.attach_nccl(c, 1, 0, fus.nccl_unique_id())
+    sk = fus.SlabKernel(g, k, 1, 0, c)
+    got = sk.apply(torch.from_numpy(f).cuda())
+    assert torch.equal(got, want)
+    # and the loopback transport with G = 1 takes the same exchange path
+    assert torch.equal(fus.apply_slab_loopback(g, k, f, 1, ctx=c), want)

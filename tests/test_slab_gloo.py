@@ -1,0 +1,90 @@
+"""N>1 path on CPU: the slab transposes of the sharded apply driven by the
+library's own exchange plan (fusg_slab_exchange_plan) over torch.distributed gloo, world_size 2
+and 3.  Each rank holds A_r = A[:, z-slab, :] of a global [Px][Nz][Ny] array; exchange 1 plus
+the unpack must give the x-slab A[x-slab, :, :]; exchange 2 after the pack must give A_r back.
+The NCCL path issues exactly these blocks (shard.cu)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2011_03009_b200 import fus
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, dims, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        g = fus.VoxelGrid(np.zeros(3), np.ones(3), 1e-4, dims, 2)
+        Px = fus.padded_dims(g)[0]
+        Nx, Ny, Nz = dims
+        rng = np.random.default_rng(7)
+        A = rng.standard_normal((Px, Nz, Ny)) + 1j * rng.standard_normal((Px, Nz, Ny))
+        z0, nz = fus.slab_range(Nz, world, rank)
+        x0, nx = fus.slab_range(Px, world, rank)
+        plan = fus.slab_exchange_plan(g, world, rank)
+        A_r = np.ascontiguousarray(A[:, z0:z0 + nz, :]).reshape(-1)
+        # exchange 1: send A_r blocks (a_off/a_cnt), receive staging blocks (r_off/r_cnt)
+        send = torch.from_numpy(A_r.view(np.float64).copy())
+        recv = torch.empty(2 * int(plan["r_cnt"].sum()), dtype=torch.float64)
+        assert list(plan["a_off"]) == list(np.concatenate([[0], np.cumsum(plan["a_cnt"])[:-1]]))
+        assert list(plan["r_off"]) == list(np.concatenate([[0], np.cumsum(plan["r_cnt"])[:-1]]))
+        dist.all_to_all_single(recv, send, [2 * int(c) for c in plan["r_cnt"]],
+                               [2 * int(c) for c in plan["a_cnt"]])
+        R = recv.numpy().view(np.complex128)
+        X = np.empty((nx, Nz, Ny), np.complex128)
+        for p in range(world):  # unpack (the 2D copies of shard.cu)
+            zp, nzp = fus.slab_range(Nz, world, p)
+            blk = R[plan["r_off"][p]:plan["r_off"][p] + plan["r_cnt"][p]].reshape(nx, nzp, Ny)
+            X[:, zp:zp + nzp, :] = blk
+        ok1 = np.array_equal(X, A[x0:x0 + nx])
+        # exchange 2: pack X by destination z-slab, receive into A_r's kx blocks
+        S = np.concatenate([np.ascontiguousarray(X[:, slice(*(lambda b, c: (b, b + c))(
+            *fus.slab_range(Nz, world, p))), :]).reshape(-1) for p in range(world)])
+        back = torch.empty(2 * int(plan["a_cnt"].sum()), dtype=torch.float64)
+        dist.all_to_all_single(back, torch.from_numpy(S.view(np.float64).copy()),
+                               [2 * int(c) for c in plan["a_cnt"]], [2 * int(c) for c in plan["r_cnt"]])
+        ok2 = np.array_equal(back.numpy().view(np.complex128), A_r)
+        q.put((rank, bool(ok1), bool(ok2)))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), None))
+
+
+@pytest.mark.parametrize("world,dims", [(2, (9, 7, 11)), (2, (16, 8, 8)), (3, (10, 5, 7))])
+def test_slab_exchange_plan_over_gloo(world, dims):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok1, ok2 in res:
+        assert ok1 is True and ok2 is True, (rank, ok1, ok2)
+
+
+def test_slab_ranges_cover_and_are_ragged():
+    for n in (1, 7, 64, 487):
+        for G in range(1, min(n, 9) + 1):
+            rs = [fus.slab_range(n, G, r) for r in range(G)]
+            assert rs[0][0] == 0 and sum(c for _, c in rs) == n
+            assert all(rs[i][0] + rs[i][1] == rs[i + 1][0] for i in range(G - 1))
+            assert max(c for _, c in rs) - min(c for _, c in rs) <= 1
+    with pytest.raises(ValueError):
+        fus.slab_range(4, 2, 2)
