@@ -11,8 +11,10 @@ separately.  Inputs and workspaces (0.27 + 1.6 GB) exceed the 126 MB L2, so no f
   python bench.py [--gpus N --steps K --warmup W]       # this framework (libfusg.so)
   python bench.py --impl reference ...                   # the CPU reference path (oracle port)
 
-N > 1 (torchrun): every rank applies its own independent cfg2 volume potential (independent
-harmonics/sources: weak scaling, no data-path collective); time = max over ranks.
+N > 1 (torchrun): the cfg2 apply is slab-sharded over the ranks (strong scaling): z-slabs of
+f/u, x-slabs of the spectrum, two NCCL all-to-all transposes over NVLink per apply
+(fusg_kernel_apply_slab); time = max over ranks of CUDA-event time.  --replicas runs
+independent per-rank applies instead (weak scaling).
 """
 import argparse
 import json
@@ -375,6 +377,109 @@ def run_gpu(args, world, rank, local):
     return 0
 
 
+def run_gpu_sharded(args, world, rank, local):
+    """N > 1: one cfg2 apply slab-sharded over all ranks (strong scaling). Rank r owns z-planes
+    of f/u and kx columns of the spectrum; the two transposes are NCCL grouped send/recv over
+    NVLink (fusg_kernel_apply_slab). Time = max over ranks of CUDA-event time."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2011_03009_b200 import _lib, fus
+
+    torch.cuda.set_device(local)
+    ctx = fus.context(local)
+    uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(fus.nccl_unique_id()), dtype=torch.uint8))
+    if world > 1:
+        dist.broadcast(uid, 0)
+    fus.attach_nccl(ctx, world, rank, bytes(uid.cpu().numpy().tobytes()))
+    g, k, f = cfg2_inputs()
+    N = g.count()
+    t0 = time.perf_counter()
+    K = fus.SlabKernel(g, k, world, rank, ctx)
+    build_s = time.perf_counter() - t0
+    plane = g.dims[0] * g.dims[1]
+    f_slab = np.ascontiguousarray(f[K.z0 * plane:(K.z0 + K.nz) * plane])
+    fd = torch.from_numpy(f_slab).to(f"cuda:{local}")
+    ud = torch.empty_like(fd)
+    L = _lib.lib()
+
+    def step():
+        _lib.check(L.fusg_kernel_apply_slab(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, None))
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    ctx.synchronize()
+    cs = torch.cuda.ExternalStream(ctx.stream_ptr)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier(world)
+    ctx.synchronize()
+    launches0 = ctx.launch_count()
+    ev0.record(cs)
+    for _ in range(args.steps):
+        step()
+    ev1.record(cs)
+    ev1.synchronize()
+    launches = ctx.launch_count() - launches0
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps, world, local)
+    barrier(world)
+    clocks = sampler.stop()
+    # end to end through the public API: pinned host slab -> device, sharded apply, -> host
+    fh = torch.from_numpy(f_slab).pin_memory()
+    uh = torch.empty_like(fh).pin_memory()
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        fd.copy_(fh, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        step()
+        ctx.synchronize()
+        uh.copy_(ud)
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, local)
+    # all-to-all volume: every rank sends all but its own block in each of the two transposes
+    plan = fus.slab_exchange_plan(g, world, rank)
+    sent = 2 * 16 * int(plan["a_cnt"].sum() - plan["a_cnt"][rank])
+    sent = max_over_ranks(float(sent), world, local)
+    per_pass, total_bytes = algorithmic_bytes(g.dims, K_padded(g))
+    hbm, hbm_kind = peaks()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD + "; z-slab sharded over ranks, NCCL all-to-all transposes",
+                       "grid": list(g.dims), "padded": list(K_padded(g)),
+                       "parallelism": f"slab{world}", "l2": "inputs+workspace > 126 MB L2; no flush"},
+            "roofline": {"bound": "hbm+nvlink", "kernel": "sharded apply (passes A-E + 2 all-to-all)",
+                         "achieved": total_bytes / world / (ms * 1e-3) / 1e9, "peak": hbm,
+                         "peak_kind": hbm_kind, "unit": "GB/s",
+                         "frac": total_bytes / world / (ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                         "nvlink_bytes_sent_per_gpu": sent,
+                         "nvlink_gbs_if_serialised": sent / (ms * 1e-3) / 1e9,
+                         "nvlink_peak_gbs": 770.0},
+            "kernel_build_s": build_s,
+            "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
+                    "d2h_bytes_per_step": 16 * N},
+            "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def K_padded(g):
+    from paper_2011_03009_b200 import fus
+
+    return fus.padded_dims(g)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -383,11 +488,16 @@ def main():
     ap.add_argument("--impl", default="fusg", choices=["fusg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cascade", action="store_true", help="skip the nested 5-harmonic solve")
+    ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N = 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent per-rank applies (weak scaling) instead of the sharded apply")
     args = ap.parse_args()
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
             return run_reference(args, world, rank)
+        if (world > 1 or args.sharded) and not args.replicas:
+            return run_gpu_sharded(args, world, rank, local)
         return run_gpu(args, world, rank, local)
     finally:
         if world > 1:
