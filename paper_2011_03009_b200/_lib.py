@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfusg.so")
+# FUSG_LIB: alternative build of the same library (kernel-variant experiments in tools/)
+LIB_PATH = os.environ.get("FUSG_LIB") or os.path.join(_HERE, "libfusg.so")
 
 FUSG_OK, FUSG_INVALID_ARGUMENT, FUSG_OUT_OF_RANGE, FUSG_RUNTIME, FUSG_CUDA, FUSG_NCCL, FUSG_OOM = range(7)
 

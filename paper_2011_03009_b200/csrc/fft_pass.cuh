@@ -24,6 +24,15 @@
 
 namespace fusg {
 
+// Shared tile [pos][T] with an XOR swizzle inside each row: element (pos, t) lives in slot
+// t ^ (pos mod T).  Column-side accesses (a warp = T lines x a few positions) stay permutations
+// of whole rows, and line-major accesses (a warp = one line x 32 positions, used to stage rows
+// coalesced) hit distinct banks.
+template <int T>
+__device__ __forceinline__ int tidx(int pos, int t) {
+  return pos * T + (t ^ (pos & (T - 1)));
+}
+
 // ------------------------------------------------------------------ stage
 // One Stockham stage of runtime radix R in {2,3,4,5,7,8}.  A thread owns up to
 // B = kMaxElems / R butterflies (j = jt + b * tpl); their values live in one fixed register
@@ -74,7 +83,7 @@ __device__ __forceinline__ void fft_stage(const AxisPlan& pl, int R, int Ns, dou
     v[e] = make_double2(0.0, 0.0);
     if (b < B && j < nb) {
       const int pos = j + r * nb;
-      v[e] = FIRST ? src.load(pos, e) : sm[pos * T + t];
+      v[e] = FIRST ? src.load(pos, e) : sm[tidx<T>(pos, t)];
     }
   }
   // everyone has read this stage's shared-memory inputs before anyone overwrites them
@@ -102,7 +111,7 @@ __device__ __forceinline__ void fft_stage(const AxisPlan& pl, int R, int Ns, dou
       const int k = j % Ns;
       const int p = (j - k) * R + k + r * Ns;  // (j / Ns) * Ns * R + k + r Ns
       if (LAST) dst.store(p, e, v[e]);
-      else sm[p * T + t] = v[e];
+      else sm[tidx<T>(p, t)] = v[e];
     }
   }
   if (!LAST) __syncthreads();  // outputs visible to the next stage (a smem-backed Dst syncs in the caller)
@@ -181,8 +190,8 @@ struct SmemIO {
   static constexpr bool kSmem = true;
   double2* sm;
   int t;
-  __device__ __forceinline__ double2 load(int pos, int) const { return sm[pos * T + t]; }
-  __device__ __forceinline__ void store(int pos, int, double2 v) const { sm[pos * T + t] = v; }
+  __device__ __forceinline__ double2 load(int pos, int) const { return sm[tidx<T>(pos, t)]; }
+  __device__ __forceinline__ void store(int pos, int, double2 v) const { sm[tidx<T>(pos, t)] = v; }
 };
 
 // Register endpoint: the last stage of one transform hands its outputs to the first stage

@@ -48,7 +48,7 @@ __device__ __forceinline__ void stage_s(double2* sm, int t, int jt, const double
     for (int r = 0; r < R; ++r) {
       const int pos = j + r * NB;
       double2 x = make_double2(0.0, 0.0);
-      if (ok) x = FIRST ? src.load(pos, b * R + r) : sm[pos * T + t];
+      if (ok) x = FIRST ? src.load(pos, b * R + r) : sm[tidx<T>(pos, t)];
       v[b * R + r] = x;
     }
   }
@@ -74,7 +74,7 @@ __device__ __forceinline__ void stage_s(double2* sm, int t, int jt, const double
       for (int r = 0; r < R; ++r) {
         const int p = base + r * NS;
         if constexpr (LAST) dst.store(p, b * R + r, v[b * R + r]);
-        else sm[p * T + t] = v[b * R + r];
+        else sm[tidx<T>(p, t)] = v[b * R + r];
       }
     }
   }

@@ -7,7 +7,8 @@
 // access patterns (lane-consecutive reads, stride-R writes) bank-conflict-free.
 //
 // Twiddles: one table load w^k per butterfly and stage; the powers w^{rk}, r < R, come from a
-// depth-3 multiply tree (<= 3 roundings), halving shared/L1 traffic versus loading all R-1.
+// depth-3 multiply tree (<= 3 roundings; FUSG_TWIDDLE_TREE=0 selects successive multiplication,
+// fewer live registers but measured slower), versus loading all R-1 from shared/L1.
 //
 // Stage s (radix R, NS = product of earlier radices, NB = L/R): butterfly j = lane + LANES*b,
 // slot e = b*R + r holds position j + r*NB on input and (j - j%NS)*R + j%NS + r*NS on output.
@@ -56,23 +57,34 @@ __device__ __forceinline__ int out_pos(int lane, int e) {
   return (j - k) * R + k + r * NS;
 }
 
+// Twiddle source: one L1/global table load w^k per butterfly and stage, powers from a multiply
+// tree.  (Keeping a persistent lane's twiddles in registers instead was measured slower: it
+// pushes pass C past 255 registers.)
+struct TwTable {
+  const double2* tw;
+  template <class RL, int LANES, int S, int R>
+  __device__ __forceinline__ void powers(int lane, int b, double2* p) const {
+    constexpr int NS = RL::ns(S);
+    constexpr int TWS = RL::len() / (NS * R);
+    const int k = (lane + LANES * b) % NS;
+    twiddle_powers<R>(__ldg(tw + k * TWS), p);
+  }
+};
+
 // Twiddle + butterflies of stage S on the register array v (input slots -> output slots).
-template <class RL, int LANES, bool INV, int S>
-__device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const double2* __restrict__ tw) {
+template <class RL, int LANES, bool INV, int S, class Tw>
+__device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const Tw& tw) {
   constexpr int R = RL::at(S);
   constexpr int NS = RL::ns(S);
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int B = E / R;
-  constexpr int TWS = L / (NS * R);
   static_assert(E % R == 0, "each lane must own whole butterflies");
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     if constexpr (NS > 1) {
-      const int j = lane + LANES * b;
-      const int k = j % NS;
       double2 p[8];
-      twiddle_powers<R>(__ldg(tw + k * TWS), p);
+      tw.template powers<RL, LANES, S, R>(lane, b, p);
 #pragma unroll
       for (int r = 1; r < R; ++r) v[b * R + r] = INV ? cmulc(v[b * R + r], p[r]) : cmul(v[b * R + r], p[r]);
     }
@@ -83,9 +95,8 @@ __device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const d
 // Full transform of the LANES-lane line owned by this lane group.
 //   src.load(pos, e) feeds stage 0; dst.store(pos, e, v) receives the last stage's outputs.
 //   ex.at(pos): this line's swizzled shared exchange slot for position pos.
-template <class RL, int LANES, bool INV, int S = 0, class Ex, class Src, class Dst>
-__device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const double2* __restrict__ tw,
-                                         Src& src, Dst& dst) {
+template <class RL, int LANES, bool INV, int S = 0, class Ex, class Tw, class Src, class Dst>
+__device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& tw, Src& src, Dst& dst) {
   constexpr int E = RL::len() / LANES;
   if constexpr (S == 0) {
 #pragma unroll
@@ -151,6 +162,23 @@ struct RowOut {
     if (ok && pos < nvalid) p[pos * sp] = (scale == 1.0) ? v : cscale(v, scale);
   }
 };
+struct StagedRowIn {  // a line staged (swizzled) in shared memory by cp.async, zero beyond nvalid
+  const double2* b;
+  int nvalid;
+  __device__ __forceinline__ double2 load(int pos, int) const {
+    return pos < nvalid ? b[swz(pos)] : make_double2(0.0, 0.0);
+  }
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const size_t ga = __cvta_generic_to_global(gmem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(ga) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 struct RegsOut {  // keep the last stage's outputs in the caller's registers
   double2* v;
   __device__ __forceinline__ void store(int, int e, double2 x) const { v[e] = x; }

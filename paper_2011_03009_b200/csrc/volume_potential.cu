@@ -99,7 +99,7 @@ struct SmemMulAt {
   const double2* sm;
   int t;
   const double2* kv;
-  __device__ __forceinline__ double2 load(int pos, int e) const { return cmul(sm[pos * T + t], kv[e]); }
+  __device__ __forceinline__ double2 load(int pos, int e) const { return cmul(sm[tidx<T>(pos, t)], kv[e]); }
 };
 struct RegMulAt {
   static constexpr bool kSmem = false;
@@ -264,21 +264,80 @@ struct SBounds {
   static constexpr int conv_min_blocks = threads >= 680 ? 1 : 680 / threads;
 };
 
-template <class RL, int T, bool INV>
+// Tile endpoints for the row side of transposing passes (staged through shared memory so the
+// global access is line-major: 32 consecutive positions of one row per warp instruction).
+template <int T>
+struct TileIn {
+  static constexpr bool kSmem = true;
+  const double2* sm;
+  int t, nvalid;
+  __device__ __forceinline__ double2 load(int pos, int) const {
+    return pos < nvalid ? sm[tidx<T>(pos, t)] : make_double2(0.0, 0.0);
+  }
+};
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const size_t ga = __cvta_generic_to_global(gmem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(ga), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// ROWIN: the input lines are contiguous rows (sp = 1): load the tile's valid rows line-major
+// with cp.async, then transform from shared memory.  ROWOUT: the output lines are contiguous
+// rows: the last stage writes the tile and the CTA stores it line-major.  Otherwise the first
+// (last) stage reads (writes) global memory directly, T adjacent lines = T*16 contiguous bytes.
+template <class RL, int T, bool INV, bool ROWIN, bool ROWOUT>
 __global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_blocks)
     axis_pass_s(LineGeom g, GLoadF ld, GStoreF st, const double2* __restrict__ tw) {
+  constexpr int NT = SBounds<RL, T>::threads;
   extern __shared__ double2 sm[];
   const int tile = blockIdx.x % g.ntiles;
   const int k = blockIdx.x / g.ntiles;
   const int t = threadIdx.x % T, jt = threadIdx.x / T;
   const int i = tile * T + t;
   const bool ok = i < g.n_inner;
-  auto src = ld.at(ok ? i : 0, k, ok);
-  auto dst = st.at(ok ? i : 0, k, ok);
+  const int lines_ok = min(T, g.n_inner - tile * T);
+  if constexpr (ROWIN) {
+    const int nin = ld.g.nvalid;
+    const double2* base = ld.g.p + int64_t(tile) * T * ld.g.si + k * ld.g.sk;
+#pragma unroll
+    for (int tt = 0; tt < T; ++tt)
+      for (int pos = threadIdx.x; pos < nin; pos += NT)
+        cp_async16_zfill(&sm[tidx<T>(pos, tt)], tt < lines_ok ? base + tt * ld.g.si + pos : ld.g.p,
+                         tt < lines_ok);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  auto gsrc = ld.at(ok ? i : 0, k, ok);
+  auto gdst = st.at(ok ? i : 0, k, ok);
+  TileIn<T> tsrc{sm, t, ld.g.nvalid};
+  SmemIO<T> tdst{sm, t};
+  auto& src = [&]() -> auto& {
+    if constexpr (ROWIN) return tsrc;
+    else return gsrc;
+  }();
+  auto& dst = [&]() -> auto& {
+    if constexpr (ROWOUT) return tdst;
+    else return gdst;
+  }();
   // twiddles staged in shared memory (first used after stage 1's barrier)
   double2* tws = sm + RL::len() * T;
-  for (int m = threadIdx.x; m < RL::len(); m += SBounds<RL, T>::threads) tws[m] = __ldg(tw + m);
+  for (int m = threadIdx.x; m < RL::len(); m += NT) tws[m] = __ldg(tw + m);
   fft_line_s<RL, T, INV>(sm, t, jt, tws, src, dst);
+  if constexpr (ROWOUT) {
+    __syncthreads();
+    const int nout = st.g.nvalid;
+    double2* base = st.g.p + int64_t(tile) * T * st.g.si + k * st.g.sk;
+    const double sc = st.g.scale;
+#pragma unroll
+    for (int tt = 0; tt < T; ++tt)
+      if (tt < lines_ok)
+        for (int pos = threadIdx.x; pos < nout; pos += NT) {
+          const double2 v = sm[tidx<T>(pos, tt)];
+          base[tt * st.g.si + pos] = (sc == 1.0) ? v : cscale(v, sc);
+        }
+  }
 }
 
 // K^ read straight from global memory at the multiply (no register prefetch).
@@ -350,20 +409,23 @@ using ConvFn = void (*)(LineGeom, GLoadF, GStoreF, KOct, const double2*);
 // axis kernels; conv is pass C.
 struct StaticEntry {
   int L, T, threads;
-  AxisFn fwd, inv;
+  AxisFn fwd, inv;   // plain (strided global on both sides)
   ConvFn conv;
+  AxisFn fwd_rowin, inv_rowout;  // transposing passes: row side staged line-major
 };
 
 #define FUSG_AX(TT, ...)                                                                   \
   StaticEntry {                                                                            \
     Radices<__VA_ARGS__>::len(), TT, Radices<__VA_ARGS__>::tpl() * TT,                     \
-        axis_pass_s<Radices<__VA_ARGS__>, TT, false>, axis_pass_s<Radices<__VA_ARGS__>, TT, true>, \
-        nullptr                                                                            \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, false, false, false>,                          \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, true, false, false>, nullptr,                  \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, false, true, false>,                           \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, true, false, true>                             \
   }
 #define FUSG_CV(TT, MINB, KPREF, ...)                                                      \
   StaticEntry {                                                                            \
     Radices<__VA_ARGS__>::len(), TT, Radices<__VA_ARGS__>::tpl() * TT, nullptr, nullptr,   \
-        conv_pass_s<Radices<__VA_ARGS__>, TT, MINB, KPREF>                                 \
+        conv_pass_s<Radices<__VA_ARGS__>, TT, MINB, KPREF>, nullptr, nullptr               \
   }
 
 static const StaticEntry kRowTab[] = {
@@ -449,11 +511,71 @@ struct WArgs {
 };
 
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
+#ifndef FUSG_WARP_MINB
+#define FUSG_WARP_MINB 2  // resident CTAs per SM the register budget is sized for
+#endif
+
+// Transposing passes on the warp engine.  A CTA owns 8 adjacent lines (i0..i0+7 at outer k); warp w
+// transforms line w using column w of a swizzled [pos][8] shared tile as its exchange buffer.
+//   row_to_col: input rows are contiguous (sp = 1): each warp loads its own row (512 B per warp
+//               instruction); the last stage writes the tile; after one barrier the CTA stores
+//               positions as 8 adjacent lines = 128 contiguous bytes (si = 1).
+//   col_to_row: the mirror: a cooperative 128-byte-row load of the tile, one barrier, then each
+//               warp transforms its column and stores its row contiguously.
+template <class RL, bool INV>
+__global__ void __launch_bounds__(kWarpThreads, 2) warp_row_to_col(WArgs a) {
+  constexpr int E = RL::len() / 32;
+  extern __shared__ double2 tile[];
+  const int ntiles = (a.n_inner + 7) / 8;
+  const int i0 = (blockIdx.x % ntiles) * 8;
+  const int k = blockIdx.x / ntiles;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lines_ok = min(8, a.n_inner - i0);
+  const bool ok = w < lines_ok;
+  RowIn src{a.in + int64_t(i0 + (ok ? w : 0)) * a.in_si + int64_t(k) * a.in_sk, 1, a.in_nvalid, ok};
+  TileEx ex{tile, w};
+  TileColOut dst{tile, w};
+  double2 v[E];
+  warp_fft<RL, 32, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
+  __syncthreads();
+  double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+  for (int e = threadIdx.x; e < a.out_nvalid * 8; e += kWarpThreads) {
+    const int pos = e >> 3, t = e & 7;
+    if (t < lines_ok) {
+      const double2 x = tile[tile_at(pos, t)];
+      base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+    }
+  }
+}
+
+template <class RL, bool INV>
+__global__ void __launch_bounds__(kWarpThreads, 2) warp_col_to_row(WArgs a) {
+  constexpr int E = RL::len() / 32;
+  extern __shared__ double2 tile[];
+  const int ntiles = (a.n_inner + 7) / 8;
+  const int i0 = (blockIdx.x % ntiles) * 8;
+  const int k = blockIdx.x / ntiles;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lines_ok = min(8, a.n_inner - i0);
+  const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
+  for (int e = threadIdx.x; e < a.in_nvalid * 8; e += kWarpThreads) {
+    const int pos = e >> 3, t = e & 7;
+    tile[tile_at(pos, t)] = t < lines_ok ? __ldg(base + t * a.in_si + pos * a.in_sp) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  const bool ok = w < lines_ok;
+  TileColIn src{tile, w, a.in_nvalid};
+  TileEx ex{tile, w};
+  RowOut dst{a.out + int64_t(i0 + (ok ? w : 0)) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok,
+             a.scale};
+  double2 v[E];
+  warp_fft<RL, 32, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
+}
 
 // Lines (i, k), i fastest: consecutive lane groups of a CTA take consecutive i, so column
 // lines (position stride sp, i contiguous) from one CTA share every 128-byte row through L1.
 template <class RL, int LANES, bool INV>
-__global__ void __launch_bounds__(kWarpThreads, 2) warp_line_pass(WArgs a) {
+__global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_line_pass(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int LPC = kWarpThreads / LANES;  // lines per CTA
@@ -467,7 +589,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_line_pass(WArgs a) {
   RowIn src{a.in + i * a.in_si + k * a.in_sk, a.in_sp, a.in_nvalid, ok};
   RowOut dst{a.out + i * a.out_si + k * a.out_sk, a.out_sp, a.out_nvalid, ok, a.scale};
   double2 v[E];
-  warp_fft<RL, LANES, INV>(v, ex, lane, a.tw, src, dst);
+  warp_fft<RL, LANES, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
 }
 
 // mirror-interleaved order 0, 1, P-1, 2, P-2, ...: lines ky and Py-ky (kx and Px-kx) read the
@@ -481,7 +603,7 @@ __device__ __forceinline__ int interleave_index(int r, int P) {
 // Pass C on rows of B [kx][ky][z] (z contiguous): forward z, * K^ (octant row [kx][ky][kz],
 // contiguous), inverse z; in place.  n_inner = Py, n_outer = Px.
 template <class RL, int LANES>
-__global__ void __launch_bounds__(kWarpThreads, 2) warp_row_conv(WArgs a) {
+__global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_row_conv(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int LPC = kWarpThreads / LANES;
@@ -500,7 +622,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_conv(WArgs a) {
   RowIn src{a.in + ky * a.in_si + int64_t(kx) * a.in_sk, 1, a.in_nvalid, ok};
   double2 v[E];
   RegsOut mid{v};
-  warp_fft<RL, LANES, false>(v, ex, lane, a.tw, src, mid);
+  warp_fft<RL, LANES, false>(v, ex, lane, TwTable{a.tw}, src, mid);
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int pos = in_pos<RL, LANES, 0>(lane, e);
@@ -508,18 +630,118 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_conv(WArgs a) {
   }
   RegsIn msrc{v};
   RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, ok, a.scale};
-  warp_fft<RL, LANES, true>(v, ex, lane, a.tw, msrc, dst);
+  warp_fft<RL, LANES, true>(v, ex, lane, TwTable{a.tw}, msrc, dst);
+}
+
+// Pass C, persistent and software-pipelined: every warp streams lines (stride = all warps of
+// the grid); while line i is transformed, line i+1's input row and K^ row are already being
+// copied into the warp's other shared buffers with cp.async, so neither HBM latency nor the
+// K^ fetch sits on the critical path.  Warp-private buffers; no CTA barriers.
+constexpr int kPPWarps = 4;  // warps per CTA (shared memory: 4 x (2 L + 2 K) x 16 B)
+
+template <int L>
+struct PPConvSmem {
+  static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;  // K^ row (L/2 + 1), padded to 32 B
+  static constexpr int PER_WARP = 2 * L + 2 * KROW;      // double2 elements
+  static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2);
+};
+
+template <class RL, int LANES>
+__global__ void __launch_bounds__(kPPWarps * 32, 1) warp_row_conv_pp(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  constexpr int HZ = L / 2 + 1;
+  using SM = PPConvSmem<L>;
+  static_assert(LANES == 32, "one line per warp");
+  static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
+  extern __shared__ double2 sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* base = sm + size_t(w) * SM::PER_WARP;
+  double2* buf[2] = {base, base + L};
+  double2* kbuf[2] = {base + 2 * L, base + 2 * L + SM::KROW};
+  const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t stride = int64_t(gridDim.x) * kPPWarps;
+  const bool mirror = a.n_outer == a.ko.Px;
+  auto coords = [&](int64_t line, int& ky, int& kx) {
+    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
+    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+  };
+  auto prefetch = [&](int64_t line, int b) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
+      const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
+      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(buf[b] + swz(pos), in + pos);
+      const double2* kl = a.ko.line(ky, kx);
+      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kbuf[b] + kz, kl + kz);
+    }
+    cp_async_commit();
+  };
+  const TwTable tw{a.tw};
+  int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
+  prefetch(line, 0);
+  for (int it = 0; line < nlines; line += stride, ++it) {
+    const int cur = it & 1;
+    prefetch(line + stride, cur ^ 1);
+    cp_async_wait1();
+    __syncwarp();  // this line's staged input and K^ row are visible to the whole warp
+    int ky, kx;
+    coords(line, ky, kx);
+    PrivEx ex{buf[cur]};
+    StagedRowIn src{buf[cur], a.in_nvalid};
+    double2 v[E];
+    RegsOut mid{v};
+    warp_fft<RL, LANES, false>(v, ex, lane, tw, src, mid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kbuf[cur][fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
+    RegsIn msrc{v};
+    RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
+    warp_fft<RL, LANES, true>(v, ex, lane, tw, msrc, dst);
+    __syncwarp();  // done with buf[cur]/kbuf[cur] before they are refilled
+  }
+  cp_async_wait0();
 }
 
 using WFn = void (*)(WArgs);
+
+template <class RL>
+constexpr bool whole_butterflies(int lanes) {
+  const int E = RL::len() / lanes;
+  if (RL::len() % lanes) return false;
+  for (int s = 0; s < RL::n; ++s)
+    if (E % RL::at(s)) return false;
+  return true;
+}
+template <class RL, int LN>
+constexpr WFn conv_pp_ptr() {
+  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32>;
+  else return nullptr;
+}
+
+template <class RL, int LN, bool INV>
+constexpr WFn transpose_ptr() {
+  if constexpr (LN == 32 && whole_butterflies<RL>(32)) {
+    if constexpr (INV) return warp_col_to_row<RL, true>;
+    else return warp_row_to_col<RL, false>;
+  } else {
+    return nullptr;
+  }
+}
+
 struct WarpEntry {
   int L, lanes;
   WFn fwd, inv, conv;
+  WFn row_to_col_fwd, col_to_row_inv;  // transposing passes (LANES = 32 only)
+  WFn conv_pp;      // persistent pipelined pass C (nullptr: not available)
+  size_t pp_smem;
 };
 #define FUSG_WARP(LN, ...)                                                                  \
   WarpEntry {                                                                               \
     Radices<__VA_ARGS__>::len(), LN, warp_line_pass<Radices<__VA_ARGS__>, LN, false>,       \
-        warp_line_pass<Radices<__VA_ARGS__>, LN, true>, warp_row_conv<Radices<__VA_ARGS__>, LN> \
+        warp_line_pass<Radices<__VA_ARGS__>, LN, true>, warp_row_conv<Radices<__VA_ARGS__>, LN>, \
+        transpose_ptr<Radices<__VA_ARGS__>, LN, false>(), transpose_ptr<Radices<__VA_ARGS__>, LN, true>(), \
+        conv_pp_ptr<Radices<__VA_ARGS__>, LN>(),                                                \
+        PPConvSmem<Radices<__VA_ARGS__>::len()>::BYTES                                           \
   }
 static const WarpEntry kWarpTab[] = {
     FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
@@ -527,7 +749,7 @@ static const WarpEntry kWarpTab[] = {
     FUSG_WARP(16, 8, 2, 8),  // 128 (cfg1)
 };
 
-enum WarpMode { kWRow = 0, kWCol = 1, kWConv = 2 };
+enum WarpMode { kWRow = 0, kWCol = 1, kWConv = 2, kWRowToCol = 3, kWColToRow = 4 };
 
 // FUSG_WARP=0 disables the warp engine.  Returns 1 launched, 0 not applicable, -1 error.
 static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a, cudaStream_t s) {
@@ -547,6 +769,50 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
   if (disable_mask & (1 << mode)) return 0;
   WFn fn = mode == kWConv ? we->conv : (inv ? we->inv : we->fwd);
   if (mode == kWConv && inv) return 0;
+  if (mode == kWRowToCol || mode == kWColToRow) {
+    fn = mode == kWRowToCol ? (inv ? nullptr : we->row_to_col_fwd) : (inv ? we->col_to_row_inv : nullptr);
+    if (!fn) return 0;
+    const size_t tsmem = size_t(L) * 8 * sizeof(double2);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem)) != cudaSuccess) {
+      set_error(FUSG_CUDA, "transposing warp pass: cannot configure shared memory");
+      return -1;
+    }
+    const int64_t tb = int64_t((a.n_inner + 7) / 8) * a.n_outer;
+    fn<<<unsigned(tb), kWarpThreads, tsmem, s>>>(a);
+    ctx->launches++;
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cuda_error(err, "transposing warp pass");
+      return -1;
+    }
+    return 1;
+  }
+  static const bool use_pp = [] {  // FUSG_CONV_PP=0 selects the one-line-per-warp pass C
+    const char* e = getenv("FUSG_CONV_PP");
+    return !(e && atoi(e) == 0);
+  }();
+  if (mode == kWConv && use_pp && we->conv_pp) {
+    if (cudaFuncSetAttribute(we->conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(we->pp_smem)) != cudaSuccess) {
+      set_error(FUSG_CUDA, "persistent pass C: cannot configure shared memory");
+      return -1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, we->conv_pp, kPPWarps * 32, we->pp_smem) !=
+            cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+    const int64_t lines = int64_t(a.n_inner) * a.n_outer;
+    const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
+    we->conv_pp<<<unsigned(grid), kPPWarps * 32, we->pp_smem, s>>>(a);
+    ctx->launches++;
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cuda_error(err, "persistent pass C");
+      return -1;
+    }
+    return 1;
+  }
   const int lpc = kWarpThreads / we->lanes;
   const size_t smem = size_t(lpc) * L * sizeof(double2);
   const int64_t blocks = (int64_t(a.n_inner) * a.n_outer + lpc - 1) / lpc;
@@ -598,6 +864,21 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
     return set_error(FUSG_INVALID_ARGUMENT, "padded axis length too large for one CTA");
   if constexpr (std::is_same<LD, GLoadF>::value && std::is_same<ST, GStoreF>::value) {
     const bool rows = kind == kKindRow;
+    // FUSG_WARP_TRANSPOSE bitmask: 1 row->col (forward A, B; default), 2 col->row (inverse D, E;
+    // measured slower than the row-staged CTA kernels: its cooperative load couples the warps)
+    static const int wt = [] {
+      const char* v = getenv("FUSG_WARP_TRANSPOSE");
+      return v ? atoi(v) : 1;
+    }();
+    const bool r2c = !INV && ld.g.sp == 1 && st.g.si == 1 && st.g.sp != 1 && (wt & 1);
+    const bool c2r = INV && ld.g.si == 1 && ld.g.sp != 1 && st.g.sp == 1 && (wt & 2);
+    if (r2c || c2r) {
+      const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
+                     st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
+      const int r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
+      if (r < 0) return FUSG_CUDA;
+      if (r > 0) return FUSG_OK;
+    }
     if ((rows && ld.g.sp == 1 && st.g.sp == 1) || (!rows && ld.g.si == 1 && st.g.si == 1)) {
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
@@ -605,8 +886,17 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
       if (r < 0) return FUSG_CUDA;
       if (r > 0) return FUSG_OK;
     }
-    if (const StaticEntry* e = find_static(pl.L, kind))
-      return launch_static(ctx, INV ? e->inv : e->fwd, *e, n_inner, n_outer, s, ld, st, pl.tw);
+    if (const StaticEntry* e = find_static(pl.L, kind)) {
+      // FUSG_STAGE_ROWS bitmask: 1 stage row loads (measured neutral), 2 stage row stores
+      static const int stage_rows = [] {
+        const char* v = getenv("FUSG_STAGE_ROWS");
+        return v ? atoi(v) : 2;
+      }();
+      AxisFn fn = INV ? e->inv : e->fwd;
+      if ((stage_rows & 1) && !INV && ld.g.sp == 1 && st.g.sp != 1) fn = e->fwd_rowin;
+      if ((stage_rows & 2) && INV && st.g.sp == 1 && ld.g.sp != 1) fn = e->inv_rowout;
+      return launch_static(ctx, fn, *e, n_inner, n_outer, s, ld, st, pl.tw);
+    }
   }
   switch (choose_tile(pl, n_inner)) {
     case 16: return launch_axis_t<INV, 16>(ctx, pl, n_inner, n_outer, ld, st, s);
