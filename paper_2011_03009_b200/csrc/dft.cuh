@@ -84,6 +84,42 @@ __device__ __forceinline__ void dft8(double2* a) {
   a[0] = x0; a[1] = x1; a[2] = x2; a[3] = x3; a[4] = x4; a[5] = x5; a[6] = x6; a[7] = x7;
 }
 
+// Pruned radix-8: inputs a[4..7] are zero (zero-padded upper half), so the first radix-2
+// level is a copy.
+template <bool INV>
+__device__ __forceinline__ void dft8_half_in(double2* a) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) a[r + 4] = a[r];
+  a[5] = w8<INV, 1>(a[5]);
+  a[6] = w8<INV, 2>(a[6]);
+  a[7] = w8<INV, 3>(a[7]);
+  dft4<INV>(a[0], a[1], a[2], a[3]);
+  dft4<INV>(a[4], a[5], a[6], a[7]);
+  const double2 x0 = a[0], x2 = a[1], x4 = a[2], x6 = a[3];
+  const double2 x1 = a[4], x3 = a[5], x5 = a[6], x7 = a[7];
+  a[0] = x0; a[1] = x1; a[2] = x2; a[3] = x3; a[4] = x4; a[5] = x5; a[6] = x6; a[7] = x7;
+}
+
+// Pruned radix-8: only X[0..3] are kept (cropped upper half); the last radix-4 level computes
+// just its first two outputs.
+template <bool INV>
+__device__ __forceinline__ void dft8_half_out(double2* a) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) dft2<INV>(a[r], a[r + 4]);
+  a[5] = w8<INV, 1>(a[5]);
+  a[6] = w8<INV, 2>(a[6]);
+  a[7] = w8<INV, 3>(a[7]);
+  // dft4 outputs 0 and 1 only: X[2q] (q = 0, 1) from the even half, X[2q+1] from the odd half
+  const double2 e0 = cadd(a[0], a[2]), e1 = csub(a[0], a[2]);
+  const double2 e2 = cadd(a[1], a[3]), e3 = rot90<INV>(csub(a[1], a[3]));
+  const double2 o0 = cadd(a[4], a[6]), o1 = csub(a[4], a[6]);
+  const double2 o2 = cadd(a[5], a[7]), o3 = rot90<INV>(csub(a[5], a[7]));
+  a[0] = cadd(e0, e2);
+  a[2] = cadd(e1, e3);
+  a[1] = cadd(o0, o2);
+  a[3] = cadd(o1, o3);
+}
+
 // multiply by w16^e (compile-time e)
 template <bool INV, int E>
 __device__ __forceinline__ double2 w16(double2 a) {

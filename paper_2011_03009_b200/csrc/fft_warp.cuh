@@ -72,7 +72,9 @@ struct TwTable {
 };
 
 // Twiddle + butterflies of stage S on the register array v (input slots -> output slots).
-template <class RL, int LANES, bool INV, int S, class Tw>
+// PRUNE bit 1: stage 0's inputs r >= R/2 are zero padding; bit 2: the last stage's outputs
+// r >= R/2 are cropped (radix-8 stages use the pruned butterflies).
+template <class RL, int LANES, bool INV, int S, int PRUNE, class Tw>
 __device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const Tw& tw) {
   constexpr int R = RL::at(S);
   constexpr int NS = RL::ns(S);
@@ -80,6 +82,8 @@ __device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const T
   constexpr int E = L / LANES;
   constexpr int B = E / R;
   static_assert(E % R == 0, "each lane must own whole butterflies");
+  // (recomputing the powers per butterfly even when k repeats keeps fewer registers live:
+  // sharing them across butterflies was measured slower in the register-bound pass C)
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     if constexpr (NS > 1) {
@@ -88,21 +92,28 @@ __device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const T
 #pragma unroll
       for (int r = 1; r < R; ++r) v[b * R + r] = INV ? cmulc(v[b * R + r], p[r]) : cmul(v[b * R + r], p[r]);
     }
-    dft<R, INV>(v + b * R);
+    if constexpr (R == 8 && S == 0 && (PRUNE & 1)) dft8_half_in<INV>(v + b * R);
+    else if constexpr (R == 8 && S == RL::n - 1 && (PRUNE & 2)) dft8_half_out<INV>(v + b * R);
+    else dft<R, INV>(v + b * R);
   }
 }
 
 // Full transform of the LANES-lane line owned by this lane group.
 //   src.load(pos, e) feeds stage 0; dst.store(pos, e, v) receives the last stage's outputs.
 //   ex.at(pos): this line's swizzled shared exchange slot for position pos.
-template <class RL, int LANES, bool INV, int S = 0, class Ex, class Tw, class Src, class Dst>
+template <class RL, int LANES, bool INV, int PRUNE = 0, int S = 0, class Ex, class Tw, class Src,
+          class Dst>
 __device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& tw, Src& src, Dst& dst) {
   constexpr int E = RL::len() / LANES;
+  constexpr int R0 = RL::at(0);
   if constexpr (S == 0) {
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = src.load(in_pos<RL, LANES, 0>(lane, e), e);
+    for (int e = 0; e < E; ++e) {
+      if ((PRUNE & 1) && R0 == 8 && (e % R0) >= R0 / 2) continue;  // zero padding: not loaded
+      v[e] = src.load(in_pos<RL, LANES, 0>(lane, e), e);
+    }
   }
-  warp_stage_compute<RL, LANES, INV, S>(v, lane, tw);
+  warp_stage_compute<RL, LANES, INV, S, PRUNE>(v, lane, tw);
   if constexpr (S + 1 < RL::n) {
     __syncwarp();  // all lanes finished reading the buffer (previous stage / caller)
 #pragma unroll
@@ -110,10 +121,14 @@ __device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& 
     __syncwarp();
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = ex.at(in_pos<RL, LANES, S + 1>(lane, e));
-    warp_fft<RL, LANES, INV, S + 1>(v, ex, lane, tw, src, dst);
+    warp_fft<RL, LANES, INV, PRUNE, S + 1>(v, ex, lane, tw, src, dst);
   } else {
+    constexpr int RL_ = RL::at(S);
 #pragma unroll
-    for (int e = 0; e < E; ++e) dst.store(out_pos<RL, LANES, S>(lane, e), e, v[e]);
+    for (int e = 0; e < E; ++e) {
+      if ((PRUNE & 2) && RL_ == 8 && (e % RL_) >= RL_ / 2) continue;  // cropped: never stored
+      dst.store(out_pos<RL, LANES, S>(lane, e), e, v[e]);
+    }
   }
 }
 

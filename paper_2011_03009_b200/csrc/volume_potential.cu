@@ -522,7 +522,7 @@ constexpr int kWarpThreads = 256;  // 8 warps per CTA
 //               positions as 8 adjacent lines = 128 contiguous bytes (si = 1).
 //   col_to_row: the mirror: a cooperative 128-byte-row load of the tile, one barrier, then each
 //               warp transforms its column and stores its row contiguously.
-template <class RL, bool INV>
+template <class RL, bool INV, bool PRUNED>
 __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_to_col(WArgs a) {
   constexpr int E = RL::len() / 32;
   extern __shared__ double2 tile[];
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_to_col(WArgs a) {
   TileEx ex{tile, w};
   TileColOut dst{tile, w};
   double2 v[E];
-  warp_fft<RL, 32, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
+  warp_fft<RL, 32, INV, PRUNED ? 1 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nvalid <= L/2
   __syncthreads();
   double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
   for (int e = threadIdx.x; e < a.out_nvalid * 8; e += kWarpThreads) {
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_to_col(WArgs a) {
   }
 }
 
-template <class RL, bool INV>
+template <class RL, bool INV, bool PRUNED>
 __global__ void __launch_bounds__(kWarpThreads, 2) warp_col_to_row(WArgs a) {
   constexpr int E = RL::len() / 32;
   extern __shared__ double2 tile[];
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_col_to_row(WArgs a) {
   RowOut dst{a.out + int64_t(i0 + (ok ? w : 0)) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok,
              a.scale};
   double2 v[E];
-  warp_fft<RL, 32, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
+  warp_fft<RL, 32, INV, PRUNED ? 2 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nout <= L/2
 }
 
 // Lines (i, k), i fastest: consecutive lane groups of a CTA take consecutive i, so column
@@ -646,7 +646,7 @@ struct PPConvSmem {
   static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2);
 };
 
-template <class RL, int LANES>
+template <class RL, int LANES, bool PRUNED>
 __global__ void __launch_bounds__(kPPWarps * 32, 1) warp_row_conv_pp(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
@@ -678,6 +678,9 @@ __global__ void __launch_bounds__(kPPWarps * 32, 1) warp_row_conv_pp(WArgs a) {
     cp_async_commit();
   };
   const TwTable tw{a.tw};
+  // PRUNED (host-selected when Nz <= L/2): zero-padded input and cropped output halves run the
+  // pruned first forward and last inverse radix-8 stages
+  constexpr int kPin = PRUNED ? 1 : 0, kPout = PRUNED ? 2 : 0;
   int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
   prefetch(line, 0);
   for (int it = 0; line < nlines; line += stride, ++it) {
@@ -691,12 +694,12 @@ __global__ void __launch_bounds__(kPPWarps * 32, 1) warp_row_conv_pp(WArgs a) {
     StagedRowIn src{buf[cur], a.in_nvalid};
     double2 v[E];
     RegsOut mid{v};
-    warp_fft<RL, LANES, false>(v, ex, lane, tw, src, mid);
+    warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, src, mid);
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kbuf[cur][fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     RegsIn msrc{v};
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
-    warp_fft<RL, LANES, true>(v, ex, lane, tw, msrc, dst);
+    warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, msrc, dst);
     __syncwarp();  // done with buf[cur]/kbuf[cur] before they are refilled
   }
   cp_async_wait0();
@@ -712,17 +715,17 @@ constexpr bool whole_butterflies(int lanes) {
     if (E % RL::at(s)) return false;
   return true;
 }
-template <class RL, int LN>
+template <class RL, int LN, bool PRUNED>
 constexpr WFn conv_pp_ptr() {
-  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32>;
+  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32, PRUNED>;
   else return nullptr;
 }
 
-template <class RL, int LN, bool INV>
+template <class RL, int LN, bool INV, bool PRUNED>
 constexpr WFn transpose_ptr() {
   if constexpr (LN == 32 && whole_butterflies<RL>(32)) {
-    if constexpr (INV) return warp_col_to_row<RL, true>;
-    else return warp_row_to_col<RL, false>;
+    if constexpr (INV) return warp_col_to_row<RL, true, PRUNED>;
+    else return warp_row_to_col<RL, false, PRUNED>;
   } else {
     return nullptr;
   }
@@ -731,16 +734,19 @@ constexpr WFn transpose_ptr() {
 struct WarpEntry {
   int L, lanes;
   WFn fwd, inv, conv;
-  WFn row_to_col_fwd, col_to_row_inv;  // transposing passes (LANES = 32 only)
-  WFn conv_pp;      // persistent pipelined pass C (nullptr: not available)
+  WFn row_to_col_fwd[2], col_to_row_inv[2];  // transposing passes (LANES = 32), [pruned]
+  WFn conv_pp[2];   // persistent pipelined pass C, [pruned] (nullptr: not available)
   size_t pp_smem;
 };
 #define FUSG_WARP(LN, ...)                                                                  \
   WarpEntry {                                                                               \
     Radices<__VA_ARGS__>::len(), LN, warp_line_pass<Radices<__VA_ARGS__>, LN, false>,       \
         warp_line_pass<Radices<__VA_ARGS__>, LN, true>, warp_row_conv<Radices<__VA_ARGS__>, LN>, \
-        transpose_ptr<Radices<__VA_ARGS__>, LN, false>(), transpose_ptr<Radices<__VA_ARGS__>, LN, true>(), \
-        conv_pp_ptr<Radices<__VA_ARGS__>, LN>(),                                                \
+        {transpose_ptr<Radices<__VA_ARGS__>, LN, false, false>(),                              \
+         transpose_ptr<Radices<__VA_ARGS__>, LN, false, true>()},                              \
+        {transpose_ptr<Radices<__VA_ARGS__>, LN, true, false>(),                               \
+         transpose_ptr<Radices<__VA_ARGS__>, LN, true, true>()},                               \
+        {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
         PPConvSmem<Radices<__VA_ARGS__>::len()>::BYTES                                           \
   }
 static const WarpEntry kWarpTab[] = {
@@ -770,7 +776,9 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
   WFn fn = mode == kWConv ? we->conv : (inv ? we->inv : we->fwd);
   if (mode == kWConv && inv) return 0;
   if (mode == kWRowToCol || mode == kWColToRow) {
-    fn = mode == kWRowToCol ? (inv ? nullptr : we->row_to_col_fwd) : (inv ? we->col_to_row_inv : nullptr);
+    // pruned radix-8 end stages when the zero padding / crop covers the upper half
+    const bool pr = mode == kWRowToCol ? 2 * a.in_nvalid <= L : 2 * a.out_nvalid <= L;
+    fn = mode == kWRowToCol ? (inv ? nullptr : we->row_to_col_fwd[pr]) : (inv ? we->col_to_row_inv[pr] : nullptr);
     if (!fn) return 0;
     const size_t tsmem = size_t(L) * 8 * sizeof(double2);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem)) != cudaSuccess) {
@@ -791,20 +799,21 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
     const char* e = getenv("FUSG_CONV_PP");
     return !(e && atoi(e) == 0);
   }();
-  if (mode == kWConv && use_pp && we->conv_pp) {
-    if (cudaFuncSetAttribute(we->conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(we->pp_smem)) != cudaSuccess) {
+  const WFn conv_pp = we->conv_pp[2 * a.in_nvalid <= L && 2 * a.out_nvalid <= L];
+  if (mode == kWConv && use_pp && conv_pp) {
+    if (cudaFuncSetAttribute(conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(we->pp_smem)) != cudaSuccess) {
       set_error(FUSG_CUDA, "persistent pass C: cannot configure shared memory");
       return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, we->conv_pp, kPPWarps * 32, we->pp_smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_pp, kPPWarps * 32, we->pp_smem) !=
             cudaSuccess || per_sm < 1) {
       cudaGetLastError();
       return 0;
     }
     const int64_t lines = int64_t(a.n_inner) * a.n_outer;
     const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
-    we->conv_pp<<<unsigned(grid), kPPWarps * 32, we->pp_smem, s>>>(a);
+    conv_pp<<<unsigned(grid), kPPWarps * 32, we->pp_smem, s>>>(a);
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
