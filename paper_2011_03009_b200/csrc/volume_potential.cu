@@ -638,6 +638,9 @@ __global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_row_conv(WA
 // copied into the warp's other shared buffers with cp.async, so neither HBM latency nor the
 // K^ fetch sits on the critical path.  Warp-private buffers; no CTA barriers.
 constexpr int kPPWarps = 4;  // warps per CTA (shared memory: 4 x (2 L + 2 K) x 16 B)
+#ifndef FUSG_PP_MINB
+#define FUSG_PP_MINB 1  // CTAs per SM the register budget targets (1: up to 255 registers)
+#endif
 
 template <int L>
 struct PPConvSmem {
@@ -647,7 +650,7 @@ struct PPConvSmem {
 };
 
 template <class RL, int LANES, bool PRUNED>
-__global__ void __launch_bounds__(kPPWarps * 32, 1) warp_row_conv_pp(WArgs a) {
+__global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int HZ = L / 2 + 1;
