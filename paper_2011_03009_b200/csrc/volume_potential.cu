@@ -659,9 +659,11 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
   static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
   extern __shared__ double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* base = sm + size_t(w) * SM::PER_WARP;
-  double2* buf[2] = {base, base + L};
-  double2* kbuf[2] = {base + 2 * L, base + 2 * L + SM::KROW};
+  // buffers addressed arithmetically from the shared base (a runtime-indexed pointer array
+  // would demote every access to generic LD/ST)
+  double2* const base = sm + size_t(w) * SM::PER_WARP;
+  auto buf = [&](int b) { return base + b * L; };
+  auto kbuf = [&](int b) { return base + 2 * L + b * SM::KROW; };
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -674,9 +676,9 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
       int ky, kx;
       coords(line, ky, kx);
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
-      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(buf[b] + swz(pos), in + pos);
+      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(buf(b) + swz(pos), in + pos);
       const double2* kl = a.ko.line(ky, kx);
-      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kbuf[b] + kz, kl + kz);
+      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kbuf(b) + kz, kl + kz);
     }
     cp_async_commit();
   };
@@ -693,13 +695,13 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
     __syncwarp();  // this line's staged input and K^ row are visible to the whole warp
     int ky, kx;
     coords(line, ky, kx);
-    PrivEx ex{buf[cur]};
-    StagedRowIn src{buf[cur], a.in_nvalid};
+    PrivEx ex{buf(cur)};
+    StagedRowIn src{buf(cur), a.in_nvalid};
     double2 v[E];
     RegsOut mid{v};
     warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, src, mid);
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kbuf[cur][fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
+    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kbuf(cur)[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     RegsIn msrc{v};
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
     warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, msrc, dst);
