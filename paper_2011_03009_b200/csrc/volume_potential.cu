@@ -634,18 +634,22 @@ __global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_row_conv(WA
 }
 
 // Pass C, persistent and software-pipelined: every warp streams lines (stride = all warps of
-// the grid); while line i is transformed, line i+1's input row and K^ row are already being
-// copied into the warp's other shared buffers with cp.async, so neither HBM latency nor the
-// K^ fetch sits on the critical path.  Warp-private buffers; no CTA barriers.
-constexpr int kPPWarps = 4;  // warps per CTA (shared memory: 4 x (2 L + 2 K) x 16 B)
+// the grid).  Per warp, shared memory holds an exchange buffer X (L), an input staging buffer S
+// (L/2 when PRUNED: the zero-padded half is never staged) and the K^ row.  S and the K^ row are
+// single-buffered: the next line's input is copied into S (cp.async) as soon as the first
+// forward stage has read it into registers, and the next K^ row right after the spectral
+// multiply, so both copies overlap the rest of the line's transform without a second buffer.
+// The small footprint (~16 KB per warp) lets 12 warps share an SM.  No CTA barriers.
+constexpr int kPPWarps = 4;  // warps per CTA
 #ifndef FUSG_PP_MINB
-#define FUSG_PP_MINB 1  // CTAs per SM the register budget targets (1: up to 255 registers)
+#define FUSG_PP_MINB 3  // CTAs per SM the register budget targets (3: <= 168 registers)
 #endif
 
-template <int L>
+template <int L, bool PRUNED>
 struct PPConvSmem {
   static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;  // K^ row (L/2 + 1), padded to 32 B
-  static constexpr int PER_WARP = 2 * L + 2 * KROW;      // double2 elements
+  static constexpr int STAGE = PRUNED ? L / 2 : L;      // staged input positions
+  static constexpr int PER_WARP = L + STAGE + KROW;      // double2 elements
   static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2);
 };
 
@@ -654,16 +658,17 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int HZ = L / 2 + 1;
-  using SM = PPConvSmem<L>;
+  constexpr int R0 = RL::at(0);
+  using SM = PPConvSmem<L, PRUNED>;
   static_assert(LANES == 32, "one line per warp");
   static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
   extern __shared__ double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // buffers addressed arithmetically from the shared base (a runtime-indexed pointer array
   // would demote every access to generic LD/ST)
-  double2* const base = sm + size_t(w) * SM::PER_WARP;
-  auto buf = [&](int b) { return base + b * L; };
-  auto kbuf = [&](int b) { return base + 2 * L + b * SM::KROW; };
+  double2* const xb = sm + size_t(w) * SM::PER_WARP;
+  double2* const sb = xb + L;
+  double2* const kb = sb + SM::STAGE;
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -671,14 +676,22 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
     ky = interleave_index(int(line % a.n_inner), a.ko.Py);
     kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
   };
-  auto prefetch = [&](int64_t line, int b) {
+  // staged position p lives at S[swz(p)] (PRUNED: p < L/2, so the swizzle stays inside S)
+  auto prefetch_in = [&](int64_t line) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
-      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(buf(b) + swz(pos), in + pos);
+      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(sb + swz(pos), in + pos);
+    }
+    cp_async_commit();
+  };
+  auto prefetch_k = [&](int64_t line) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
       const double2* kl = a.ko.line(ky, kx);
-      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kbuf(b) + kz, kl + kz);
+      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kb + kz, kl + kz);
     }
     cp_async_commit();
   };
@@ -686,26 +699,33 @@ __global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(
   // PRUNED (host-selected when Nz <= L/2): zero-padded input and cropped output halves run the
   // pruned first forward and last inverse radix-8 stages
   constexpr int kPin = PRUNED ? 1 : 0, kPout = PRUNED ? 2 : 0;
+  const PrivEx ex{xb};
   int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
-  prefetch(line, 0);
-  for (int it = 0; line < nlines; line += stride, ++it) {
-    const int cur = it & 1;
-    prefetch(line + stride, cur ^ 1);
-    cp_async_wait1();
+  prefetch_in(line);
+  prefetch_k(line);
+  for (; line < nlines; line += stride) {
+    cp_async_wait0();
     __syncwarp();  // this line's staged input and K^ row are visible to the whole warp
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if ((PRUNED && R0 == 8) && (e % R0) >= R0 / 2) continue;  // zero padding: not staged
+      const int pos = in_pos<RL, LANES, 0>(lane, e);
+      v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();  // S consumed: refill it with the next line while this one is transformed
+    prefetch_in(line + stride);
+    RegsIn vin{v};
+    RegsOut mid{v};
+    warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, vin, mid);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
+    __syncwarp();  // K^ row consumed
+    prefetch_k(line + stride);
     int ky, kx;
     coords(line, ky, kx);
-    PrivEx ex{buf(cur)};
-    StagedRowIn src{buf(cur), a.in_nvalid};
-    double2 v[E];
-    RegsOut mid{v};
-    warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, src, mid);
-#pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kbuf(cur)[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
-    RegsIn msrc{v};
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
-    warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, msrc, dst);
-    __syncwarp();  // done with buf[cur]/kbuf[cur] before they are refilled
+    warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, vin, dst);
   }
   cp_async_wait0();
 }
@@ -741,7 +761,7 @@ struct WarpEntry {
   WFn fwd, inv, conv;
   WFn row_to_col_fwd[2], col_to_row_inv[2];  // transposing passes (LANES = 32), [pruned]
   WFn conv_pp[2];   // persistent pipelined pass C, [pruned] (nullptr: not available)
-  size_t pp_smem;
+  size_t pp_smem[2];
 };
 #define FUSG_WARP(LN, ...)                                                                  \
   WarpEntry {                                                                               \
@@ -752,7 +772,8 @@ struct WarpEntry {
         {transpose_ptr<Radices<__VA_ARGS__>, LN, true, false>(),                               \
          transpose_ptr<Radices<__VA_ARGS__>, LN, true, true>()},                               \
         {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
-        PPConvSmem<Radices<__VA_ARGS__>::len()>::BYTES                                           \
+        {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
+         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES}                                   \
   }
 static const WarpEntry kWarpTab[] = {
     FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
@@ -804,21 +825,23 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
     const char* e = getenv("FUSG_CONV_PP");
     return !(e && atoi(e) == 0);
   }();
-  const WFn conv_pp = we->conv_pp[2 * a.in_nvalid <= L && 2 * a.out_nvalid <= L];
+  const int pruned = 2 * a.in_nvalid <= L && 2 * a.out_nvalid <= L;
+  const WFn conv_pp = we->conv_pp[pruned];
+  const size_t pp_smem = we->pp_smem[pruned];
   if (mode == kWConv && use_pp && conv_pp) {
-    if (cudaFuncSetAttribute(conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(we->pp_smem)) != cudaSuccess) {
+    if (cudaFuncSetAttribute(conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pp_smem)) != cudaSuccess) {
       set_error(FUSG_CUDA, "persistent pass C: cannot configure shared memory");
       return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_pp, kPPWarps * 32, we->pp_smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, conv_pp, kPPWarps * 32, pp_smem) !=
             cudaSuccess || per_sm < 1) {
       cudaGetLastError();
       return 0;
     }
     const int64_t lines = int64_t(a.n_inner) * a.n_outer;
     const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
-    conv_pp<<<unsigned(grid), kPPWarps * 32, we->pp_smem, s>>>(a);
+    conv_pp<<<unsigned(grid), kPPWarps * 32, pp_smem, s>>>(a);
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
