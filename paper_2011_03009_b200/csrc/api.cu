@@ -49,6 +49,8 @@ void free_kernel(fusg_kernel* K) {
   if (K->rbuf) cudaFreeAsync(K->rbuf, s);
   cudaFree(K->stage_f);
   cudaFree(K->stage_u);
+  for (cudaEvent_t e : K->chunk_ev) cudaEventDestroy(e);
+  if (K->copy_stream) cudaStreamDestroy(K->copy_stream);
   for (auto* t : K->tw) cudaFree(t);
   delete K;
 }
@@ -217,9 +219,55 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
     }
     K->bytes += 2 * bytes;
   }
-  FUSG_CUDA_TRY(cudaMemcpyAsync(K->stage_f, f_host, bytes, cudaMemcpyHostToDevice, s));
-  fusg_status st = volume_potential_apply(K, K->stage_f, K->stage_u, scale, s);
-  if (st == FUSG_OK) FUSG_CUDA_TRY(cudaMemcpyAsync(u_host, K->stage_u, bytes, cudaMemcpyDeviceToHost, s));
+  if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_host: sharded kernel needs a slab apply");
+  // z-chunk pipeline: chunk c is copied in on the copy stream while the compute stream runs
+  // passes A+B on chunk c-1; after pass C, passes D+E of chunk c overlap the copy-out of c-1.
+  const int Nz = K->grid.dims[2];
+  const size_t plane = bytes / size_t(Nz);
+  // FUSG_HOST_CHUNKS overrides the chunk count (any size); default 8 above 8 MB, else 1
+  const char* env_chunks = getenv("FUSG_HOST_CHUNKS");
+  const int nchunks = env_chunks ? std::min(std::max(1, atoi(env_chunks)), Nz)
+                                 : (bytes < (size_t(8) << 20) ? 1 : std::min(8, Nz));
+  if (!K->copy_stream) FUSG_CUDA_TRY(cudaStreamCreateWithFlags(&K->copy_stream, cudaStreamNonBlocking));
+  while (int(K->chunk_ev.size()) < 2 * nchunks + 1) {
+    cudaEvent_t e;
+    FUSG_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    K->chunk_ev.push_back(e);
+  }
+  cudaStream_t cs = K->copy_stream;
+  auto z_of = [&](int c) { return int(int64_t(Nz) * c / nchunks); };
+  auto* hf = reinterpret_cast<const char*>(f_host);
+  auto* hu = reinterpret_cast<char*>(u_host);
+  // the copy stream starts after the compute stream's earlier work (a previous apply's reads of
+  // the staging buffers)
+  FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[2 * nchunks], s));
+  FUSG_CUDA_TRY(cudaStreamWaitEvent(cs, K->chunk_ev[2 * nchunks], 0));
+  for (int c = 0; c < nchunks; ++c) {
+    const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
+    FUSG_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(K->stage_f) + z0 * plane, hf + z0 * plane,
+                                  nzc * plane, cudaMemcpyHostToDevice, cs));
+    FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[c], cs));
+  }
+  fusg_status st = FUSG_OK;
+  for (int c = 0; c < nchunks && st == FUSG_OK; ++c) {
+    const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
+    FUSG_CUDA_TRY(cudaStreamWaitEvent(s, K->chunk_ev[c], 0));
+    st = apply_chunk_AB(K, K->stage_f + int64_t(z0) * (plane / 16), z0, nzc, s);
+  }
+  if (st == FUSG_OK) st = apply_phase_C(K, s);
+  for (int c = 0; c < nchunks && st == FUSG_OK; ++c) {
+    const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
+    st = apply_chunk_DE(K, K->stage_u + int64_t(z0) * (plane / 16), z0, nzc, scale, s);
+    if (st != FUSG_OK) break;
+    FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[nchunks + c], s));
+    FUSG_CUDA_TRY(cudaStreamWaitEvent(cs, K->chunk_ev[nchunks + c], 0));
+    FUSG_CUDA_TRY(cudaMemcpyAsync(hu + z0 * plane, reinterpret_cast<char*>(K->stage_u) + z0 * plane,
+                                  nzc * plane, cudaMemcpyDeviceToHost, cs));
+  }
+  // the compute stream's later work must not overwrite the staging buffers under the copies
+  FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[2 * nchunks], cs));
+  FUSG_CUDA_TRY(cudaStreamWaitEvent(s, K->chunk_ev[2 * nchunks], 0));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(cs));
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return st;
 }

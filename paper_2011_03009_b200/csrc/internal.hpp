@@ -65,6 +65,8 @@ struct fusg_kernel {
   double2* bufB = nullptr;  // [kx][ky][z]  (Px x Py x Nz)
   double2* stage_f = nullptr;  // host-vector apply staging (lazily allocated)
   double2* stage_u = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-vector apply: chunked H2D / D2H beside the compute
+  std::vector<cudaEvent_t> chunk_ev;   // one per z-chunk: copied in, then computed out
   // slab decomposition (unsharded: G = 1, rank 0 owns everything)
   int G = 1, rank = 0;
   bool slab = false;   // created by fusg_kernel_create_slab: owns exchange buffers even at G = 1
@@ -86,6 +88,12 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self);
 fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s);
 fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev = nullptr);
 fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t s);
+// z-chunked unsharded apply (host-vector pipeline): planes [z0, z0 + nzc) of f (device pointer
+// to plane z0) through passes A and B; pass C on the whole box; planes [z0, z0 + nzc) through
+// passes D and E into u (device pointer to plane z0)
+fusg_status apply_chunk_AB(fusg_kernel* K, const double2* f_z0, int z0, int nzc, cudaStream_t s);
+fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s);
+fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s);
 void destroy_nccl(fusg_ctx* ctx);
 // ev (optional): 6 events recorded before passes A..E and after E
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,

@@ -1117,6 +1117,41 @@ fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t
                            GStoreF{GStore{u, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
 }
 
+// z-chunks of the unsharded apply.  Pass A and B lines never mix z-planes and neither do
+// passes D and E, so a chunk of planes runs through A+B as soon as its input has arrived and
+// through D+E as soon as pass C is done, while other chunks are still being copied.
+fusg_status apply_chunk_AB(fusg_kernel* K, const double2* f_z0, int z0, int nzc, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1];
+  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  double2* A = K->bufA + int64_t(z0) * Ny;
+  FUSG_TRY(launch_axis<false>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{f_z0, Nx, int64_t(Ny) * Nx, 1, Nx}},
+                              GStoreF{GStore{A, 1, Ny, NzNy, Px, 1.0}}, s, kKindRow));
+  return launch_axis<false>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{A, Ny, NzNy, 1, Ny}},
+                            GStoreF{GStore{K->bufB + z0, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow);
+}
+
+fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s) {
+  const int Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
+  const int64_t PyNz = int64_t(Py) * Nz;
+  return launch_conv(K->ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
+                     GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
+                     KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0}, s);
+}
+
+fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1];
+  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  const double total = double(K->P[0]) * double(K->P[1]) * double(K->P[2]);
+  double2* A = K->bufA + int64_t(z0) * Ny;
+  FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{K->bufB + z0, 1, PyNz, Nz, Py}},
+                             GStoreF{GStore{A, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
+  return launch_axis<true>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{A, 1, Ny, NzNy, Px}},
+                           GStoreF{GStore{u_z0, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
+}
+
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t s, cudaEvent_t* ev) {
   if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: sharded kernel needs a slab apply");
