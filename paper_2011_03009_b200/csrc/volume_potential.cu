@@ -432,8 +432,8 @@ static const StaticEntry kRowTab[] = {
     FUSG_AX(4, 8, 8, 8),        // 512  (cfg2)
     FUSG_AX(8, 8, 8, 8),
     FUSG_AX(16, 4, 8, 4),       // 128  (cfg1)
-    FUSG_AX(2, 8, 8, 3, 8),     // 1536 (cfg5)
-    FUSG_AX(4, 8, 8, 3, 8),
+    FUSG_AX(4, 8, 8, 3, 8),     // 1536 (cfg5): 64 B column segments (T = 2 measured 15% slower)
+    FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),  // 1050 (cfg3 x)
     FUSG_AX(2, 7, 4, 5, 7),     // 980  (cfg3 y, z)
     FUSG_AX(4, 5, 5, 5, 5),     // 625  (desk cfg4)
@@ -444,8 +444,8 @@ static const StaticEntry kColTab[] = {
     FUSG_AX(8, 8, 8, 8),
     FUSG_AX(4, 8, 8, 8),
     FUSG_AX(16, 4, 8, 4),
-    FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(4, 8, 8, 3, 8),
+    FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),
     FUSG_AX(2, 7, 4, 5, 7),
     FUSG_AX(4, 5, 5, 5, 5),
@@ -459,8 +459,8 @@ static const StaticEntry kConvTab[] = {
     FUSG_CV(8, 2, false, 8, 8, 8),
     FUSG_CV(4, 2, true, 8, 8, 8),
     FUSG_CV(16, 1, true, 4, 8, 4),
-    FUSG_CV(2, 1, true, 8, 8, 3, 8),
     FUSG_CV(4, 1, true, 8, 8, 3, 8),
+    FUSG_CV(2, 1, true, 8, 8, 3, 8),
     FUSG_CV(2, 1, true, 5, 7, 3, 2, 5),
     FUSG_CV(2, 1, true, 7, 4, 5, 7),
     FUSG_CV(4, 1, true, 5, 5, 5, 5),
