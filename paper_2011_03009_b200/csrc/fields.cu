@@ -99,13 +99,11 @@ __device__ __forceinline__ double attenuation(double t) {  // e^{-t}, t = Im k *
   }
 }
 
+// term from the squared distance d2
 template <int ATT>
-__device__ __forceinline__ void monopole_term(double x, double y, double z, double sx, double sy,
-                                              double sz, double k1, double kim,
-                                              const double2* __restrict__ tab, double2& acc,
-                                              bool& bad) {
-  const double ddx = x - sx, ddy = y - sy, ddz = z - sz;
-  const double d2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+__device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
+                                                 const double2* __restrict__ tab, double2& acc,
+                                                 bool& bad) {
   bad |= d2 < 1e-24;  // dist < 1e-12 (src/transducer.cpp:112)
   const double ir = rsqrt_refined(d2);
   const double d = d2 * ir;
@@ -123,6 +121,15 @@ __device__ __forceinline__ void monopole_term(double x, double y, double z, doub
   acc.y = fma(mc, sn, fma(ms, cs, acc.y));
 }
 
+template <int ATT>
+__device__ __forceinline__ void monopole_term(double x, double y, double z, double sx, double sy,
+                                              double sz, double k1, double kim,
+                                              const double2* __restrict__ tab, double2& acc,
+                                              bool& bad) {
+  const double ddx = x - sx, ddy = y - sy, ddz = z - sz;
+  monopole_term_d2<ATT>(fma(ddz, ddz, fma(ddy, ddy, ddx * ddx)), k1, kim, tab, acc, bad);
+}
+
 __device__ __forceinline__ void stage_sources(const double* src, int n_src, int base, double* sx,
                                               double* sy, double* sz) {
   for (int j = threadIdx.x; j < kSrcChunk && base + j < n_src; j += blockDim.x) {
@@ -132,6 +139,10 @@ __device__ __forceinline__ void stage_sources(const double* src, int n_src, int 
   }
 }
 
+// kVPT adjacent voxels of one x-row per thread: the (y, z) part of the squared distance is
+// shared, the source loads are amortised and the thread carries kVPT independent chains.
+constexpr int kVPT = 4;
+
 template <int ATT>
 __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __restrict__ src, int n_src,
                                                             GridDev g, double k1, double kim,
@@ -140,20 +151,25 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
   __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
   __shared__ double2 tab[kPhaseN];
   fill_phase_table(tab);  // visible after the first barrier of the source loop
-  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  const int row_threads = (g.dims[0] + kVPT - 1) / kVPT;
+  const int64_t count = int64_t(row_threads) * g.dims[1] * g.dims[2];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool active = idx < count;
-  double x = 0, y = 0, z = 0;
+  int ix0 = 0, nv = 0;
+  int64_t row = 0;
+  double x[kVPT], y = 0, z = 0;
   if (active) {
-    const int ix = int(idx % g.dims[0]);
-    const int64_t r = idx / g.dims[0];
-    const int iy = int(r % g.dims[1]);
-    const int iz = int(r / g.dims[1]);
-    x = centre(g.lo[0], ix, g.dx);
-    y = centre(g.lo[1], iy, g.dx);
-    z = centre(g.lo[2], iz, g.dx);
+    ix0 = int(idx % row_threads) * kVPT;
+    row = idx / row_threads;
+    nv = min(kVPT, g.dims[0] - ix0);
+    y = centre(g.lo[1], int(row % g.dims[1]), g.dx);
+    z = centre(g.lo[2], int(row / g.dims[1]), g.dx);
   }
-  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) x[v] = centre(g.lo[0], ix0 + min(v, max(nv - 1, 0)), g.dx);  // tail: repeat the last voxel
+  double2 acc[kVPT];
+#pragma unroll
+  for (int v = 0; v < kVPT; ++v) acc[v] = make_double2(0.0, 0.0);
   bool bad = false;
   for (int base = 0; base < n_src; base += kSrcChunk) {
     __syncthreads();
@@ -161,13 +177,25 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
     __syncthreads();
     if (active) {
       const int n = min(kSrcChunk, n_src - base);
-      #pragma unroll 4
-      for (int j = 0; j < n; ++j) monopole_term<ATT>(x, y, z, sx[j], sy[j], sz[j], k1, kim, tab, acc, bad);
+      #pragma unroll 2
+      for (int j = 0; j < n; ++j) {
+        const double ddy = y - sy[j], ddz = z - sz[j];
+        const double q = fma(ddz, ddz, ddy * ddy);
+        const double s0 = sx[j];
+#pragma unroll
+        for (int v = 0; v < kVPT; ++v) {
+          const double ddx = x[v] - s0;
+          monopole_term_d2<ATT>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad);
+        }
+      }
     }
   }
   if (active) {
     if (bad) atomicExch(flag, 1);
-    out[idx] = make_double2(amp * acc.x, amp * acc.y);
+    double2* o = out + row * g.dims[0] + ix0;
+#pragma unroll
+    for (int v = 0; v < kVPT; ++v)
+      if (v < nv) o[v] = make_double2(amp * acc[v].x, amp * acc[v].y);
   }
 }
 
@@ -399,7 +427,7 @@ static fusg_status check_flag(fusg_ctx* ctx, cudaStream_t s) {
 fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
                           double kre, double kim, double amp, double2* out, cudaStream_t s,
                           double dmax) {
-  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  const int64_t count = int64_t((g.dims[0] + kVPT - 1) / kVPT) * g.dims[1] * g.dims[2];
   const int threads = 256;
   FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel,
                     unsigned((count + threads - 1) / threads), threads, 0, s>>>(
