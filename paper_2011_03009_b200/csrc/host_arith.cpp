@@ -116,7 +116,8 @@ int32_t fusg_next_fast_size(int32_t n) {
 fusg_status fusg_padded_dims(const fusg_grid* g, int32_t pad_small_primes, int32_t out[3]) {
   for (int a = 0; a < 3; ++a) {
     if (g->dims[a] < 1) return set_error(FUSG_INVALID_ARGUMENT, "padded_dims: empty grid");
-    out[a] = fusg::smooth_padded_size(g->dims[a], pad_small_primes != 0);
+    out[a] = pad_small_primes ? fusg::smooth_padded_size(g->dims[a], true)
+                              : fusg::device_padded_size(g->dims[a], a);
   }
   return FUSG_OK;
 }

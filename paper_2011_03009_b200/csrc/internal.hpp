@@ -36,6 +36,7 @@ fusg_status cuda_error(cudaError_t e, const char* what);
   } while (0)
 
 int smooth_padded_size(int n, bool pad_small_primes);
+int device_padded_size(int n, int axis);  // the kernel's padded length on axis (z may prefer a warp length)
 bool make_plan_radices(int L, AxisPlan& pl);
 
 }  // namespace fusg

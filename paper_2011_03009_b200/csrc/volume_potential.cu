@@ -184,6 +184,23 @@ int smooth_padded_size(int n, bool pad_small_primes) {
   return p;
 }
 
+// Padded length the device uses on axis `axis`.  Any P >= 2N-1 is exact, and Pz only lives
+// inside pass C (which reads and writes the Nz valid values of each z-row) and the K^ octant, so
+// on z the smallest length the persistent warp pass C covers (256, 512, 768) is preferred when it
+// is within 1.35x of the smallest smooth size: e.g. Nz = 323 runs pass C at 768 instead of the
+// CTA-tiled kernel at 648.  FUSG_PZ_WARP=0 keeps the smallest smooth size.
+int device_padded_size(int n, int axis) {
+  const int p = smooth_padded_size(n, false);
+  static const bool pz_warp = [] {
+    const char* e = getenv("FUSG_PZ_WARP");
+    return !(e && atoi(e) == 0);
+  }();
+  if (axis != 2 || !pz_warp) return p;
+  for (int L : {256, 512, 768})
+    if (L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
+  return p;
+}
+
 bool make_plan_radices(int L, AxisPlan& pl) {
   int m = L, e2 = 0, e3 = 0, e5 = 0, e7 = 0;
   while (m % 2 == 0) { m /= 2; ++e2; }
@@ -647,6 +664,9 @@ constexpr int kPPWarps = 4;  // warps per CTA
 #ifndef FUSG_PP_MINB
 #define FUSG_PP_MINB 3  // CTAs per SM the register budget targets (3: <= 168 registers)
 #endif
+// L > 512: 24+ values per lane and ~25 KB of shared memory per warp allow 2 CTAs per SM
+template <int L>
+constexpr int pp_min_blocks() { return L <= 512 ? FUSG_PP_MINB : 2; }
 
 template <int L, bool PRUNED>
 struct PPConvSmem {
@@ -657,7 +677,7 @@ struct PPConvSmem {
 };
 
 template <class RL, int LANES, bool PRUNED>
-__global__ void __launch_bounds__(kPPWarps * 32, FUSG_PP_MINB) warp_row_conv_pp(WArgs a) {
+__global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) warp_row_conv_pp(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int HZ = L / 2 + 1;
@@ -780,6 +800,7 @@ struct WarpEntry {
   }
 static const WarpEntry kWarpTab[] = {
     FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
+    FUSG_WARP(32, 8, 4, 3, 8),  // 768 (pass C for Nz <= 384: the nested cascade grids)
     FUSG_WARP(32, 8, 4, 8),  // 256
     FUSG_WARP(16, 8, 2, 8),  // 128 (cfg1)
 };
@@ -995,7 +1016,7 @@ void slab_split(int n, int G, int r, int* begin, int* count) {
 
 fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank) {
   for (int a = 0; a < 3; ++a) {
-    K->P[a] = smooth_padded_size(K->grid.dims[a], false);
+    K->P[a] = device_padded_size(K->grid.dims[a], a);
     K->H[a] = K->P[a] / 2 + 1;
     if (!make_plan_radices(K->P[a], K->plan[a]))
       return set_error(FUSG_INVALID_ARGUMENT, "no FFT plan for padded length");
