@@ -186,7 +186,7 @@ int smooth_padded_size(int n, bool pad_small_primes) {
 
 // Padded length the device uses on axis `axis`.  Any P >= 2N-1 is exact, and Pz only lives
 // inside pass C (which reads and writes the Nz valid values of each z-row) and the K^ octant, so
-// on z the smallest length the persistent warp pass C covers (256, 512, 768) is preferred when it
+// on z the smallest length the persistent warp pass C covers (256, 512, 768, 1024) is preferred when it
 // is within 1.35x of the smallest smooth size: e.g. Nz = 323 runs pass C at 768 instead of the
 // CTA-tiled kernel at 648.  FUSG_PZ_WARP=0 keeps the smallest smooth size.
 int device_padded_size(int n, int axis) {
@@ -196,7 +196,7 @@ int device_padded_size(int n, int axis) {
     return !(e && atoi(e) == 0);
   }();
   if (axis != 2 || !pz_warp) return p;
-  for (int L : {256, 512, 768})
+  for (int L : {256, 512, 768, 1024})
     if (L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
   return p;
 }
@@ -449,6 +449,8 @@ static const StaticEntry kRowTab[] = {
     FUSG_AX(4, 8, 8, 8),        // 512  (cfg2)
     FUSG_AX(8, 8, 8, 8),
     FUSG_AX(16, 4, 8, 4),       // 128  (cfg1)
+    FUSG_AX(4, 8, 4, 3, 8),     // 768
+    FUSG_AX(8, 8, 4, 3, 8),
     FUSG_AX(4, 8, 8, 3, 8),     // 1536 (cfg5): 64 B column segments (T = 2 measured 15% slower)
     FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),  // 1050 (cfg3 x)
@@ -461,6 +463,8 @@ static const StaticEntry kColTab[] = {
     FUSG_AX(8, 8, 8, 8),
     FUSG_AX(4, 8, 8, 8),
     FUSG_AX(16, 4, 8, 4),
+    FUSG_AX(4, 8, 4, 3, 8),
+    FUSG_AX(8, 8, 4, 3, 8),
     FUSG_AX(4, 8, 8, 3, 8),
     FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),
@@ -798,9 +802,18 @@ struct WarpEntry {
         {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
          PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES}                                   \
   }
+// pass-C-only entry: the persistent pass C alone (the row/column kernels would spill at this E)
+#define FUSG_WARP_CONV_ONLY(LN, ...)                                                         \
+  WarpEntry {                                                                               \
+    Radices<__VA_ARGS__>::len(), LN, nullptr, nullptr, nullptr, {nullptr, nullptr}, {nullptr, nullptr}, \
+        {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
+        {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
+         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES}                                   \
+  }
 static const WarpEntry kWarpTab[] = {
     FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
     FUSG_WARP(32, 8, 4, 3, 8),  // 768 (pass C for Nz <= 384: the nested cascade grids)
+    FUSG_WARP_CONV_ONLY(32, 8, 4, 4, 8),  // 1024 (pass C for Nz <= 512: cfg3)
     FUSG_WARP(32, 8, 4, 8),  // 256
     FUSG_WARP(16, 8, 2, 8),  // 128 (cfg1)
 };
@@ -825,6 +838,7 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
   if (disable_mask & (1 << mode)) return 0;
   WFn fn = mode == kWConv ? we->conv : (inv ? we->inv : we->fwd);
   if (mode == kWConv && inv) return 0;
+  if (!we->fwd && mode != kWConv) return 0;  // pass-C-only entry
   if (mode == kWRowToCol || mode == kWColToRow) {
     // pruned radix-8 end stages when the zero padding / crop covers the upper half
     const bool pr = mode == kWRowToCol ? 2 * a.in_nvalid <= L : 2 * a.out_nvalid <= L;
@@ -874,6 +888,7 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
     }
     return 1;
   }
+  if (!fn) return 0;  // pass-C-only entry without an applicable persistent variant
   const int lpc = kWarpThreads / we->lanes;
   const size_t smem = size_t(lpc) * L * sizeof(double2);
   const int64_t blocks = (int64_t(a.n_inner) * a.n_outer + lpc - 1) / lpc;

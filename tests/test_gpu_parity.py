@@ -89,7 +89,9 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # (odd line count 9 x 5 exercises the half-filled last pair)
                                   (9, 7, 128), (5, 3, 256), (3, 2, 100), (6, 5, 129),
                                   # Nz = 300 / 341: Pz = 768 (warp pass C) instead of 600 / 686
-                                  (3, 2, 300), (2, 3, 341)])
+                                  (3, 2, 300), (2, 3, 341),
+                                  # Nz = 490: Pz = 1024 (warp pass C, pass-C-only entry)
+                                  (2, 2, 490)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
