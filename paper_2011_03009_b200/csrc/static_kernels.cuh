@@ -5,6 +5,7 @@
 #pragma once
 #include <cstddef>
 #include <cmath>
+#include <type_traits>
 
 #include "fft_warp.cuh"
 
@@ -140,9 +141,12 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // with cp.async, then transform from shared memory.  ROWOUT: the output lines are contiguous
 // rows: the last stage writes the tile and the CTA stores it line-major.  Otherwise the first
 // (last) stage reads (writes) global memory directly, T adjacent lines = T*16 contiguous bytes.
-template <class RL, int T, bool INV, bool ROWIN, bool ROWOUT>
+// LD is GLoadF for the apply passes, KGenF / FoldF for the kernel-spectrum build (ROWIN and
+// ROWOUT need GLoadF / GStoreF).
+template <class RL, int T, bool INV, bool ROWIN, bool ROWOUT, class LD = GLoadF>
 __global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_blocks)
-    axis_pass_s(LineGeom g, GLoadF ld, GStoreF st, const double2* __restrict__ tw) {
+    axis_pass_s(LineGeom g, LD ld, GStoreF st, const double2* __restrict__ tw) {
+  static_assert(!ROWIN || std::is_same<LD, GLoadF>::value, "row-staged input needs a plain load");
   constexpr int NT = SBounds<RL, T>::threads;
   extern __shared__ double2 sm[];
   const int tile = blockIdx.x % g.ntiles;
@@ -164,10 +168,9 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_b
   }
   auto gsrc = ld.at(ok ? i : 0, k, ok);
   auto gdst = st.at(ok ? i : 0, k, ok);
-  TileIn<T> tsrc{sm, t, ld.g.nvalid};
   SmemIO<T> tdst{sm, t};
-  auto& src = [&]() -> auto& {
-    if constexpr (ROWIN) return tsrc;
+  auto src = [&]() {
+    if constexpr (ROWIN) return TileIn<T>{sm, t, ld.g.nvalid};
     else return gsrc;
   }();
   auto& dst = [&]() -> auto& {
@@ -255,6 +258,8 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, MINB)
 }
 
 using AxisFn = void (*)(LineGeom, GLoadF, GStoreF, const double2*);
+using GenFn = void (*)(LineGeom, KGenF, GStoreF, const double2*);
+using FoldFn = void (*)(LineGeom, FoldF, GStoreF, const double2*);
 using ConvFn = void (*)(LineGeom, GLoadF, GStoreF, KOct, const double2*);
 
 // One table per pass kind; per length the first entry is the default, FUSG_{ROW,COL,CONV}_VAR
@@ -265,6 +270,8 @@ struct StaticEntry {
   AxisFn fwd, inv;   // plain (strided global on both sides)
   ConvFn conv;
   AxisFn fwd_rowin, inv_rowout;  // transposing passes: row side staged line-major
+  GenFn build_gen;                // kernel-spectrum build: generate K + forward (G1)
+  FoldFn build_fold;              // even extension + forward (G2, G3)
 };
 
 #define FUSG_AX(TT, ...)                                                                   \
@@ -273,12 +280,14 @@ struct StaticEntry {
         axis_pass_s<Radices<__VA_ARGS__>, TT, false, false, false>,                          \
         axis_pass_s<Radices<__VA_ARGS__>, TT, true, false, false>, nullptr,                  \
         axis_pass_s<Radices<__VA_ARGS__>, TT, false, true, false>,                           \
-        axis_pass_s<Radices<__VA_ARGS__>, TT, true, false, true>                             \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, true, false, true>,                            \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, false, false, false, KGenF>,                   \
+        axis_pass_s<Radices<__VA_ARGS__>, TT, false, false, false, FoldF>                    \
   }
 #define FUSG_CV(TT, MINB, KPREF, ...)                                                      \
   StaticEntry {                                                                            \
     Radices<__VA_ARGS__>::len(), TT, Radices<__VA_ARGS__>::tpl() * TT, nullptr, nullptr,   \
-        conv_pass_s<Radices<__VA_ARGS__>, TT, MINB, KPREF>, nullptr, nullptr               \
+        conv_pass_s<Radices<__VA_ARGS__>, TT, MINB, KPREF>, nullptr, nullptr, nullptr, nullptr \
   }
 
 enum StaticKind { kKindRow = 0, kKindCol = 1, kKindConv = 2 };

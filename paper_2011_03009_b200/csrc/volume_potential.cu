@@ -194,6 +194,7 @@ static const StaticEntry kRowTab[] = {
     FUSG_AX(16, 4, 8, 4),       // 128  (cfg1)
     FUSG_AX(4, 8, 4, 3, 8),     // 768
     FUSG_AX(8, 8, 4, 3, 8),
+    FUSG_AX(4, 8, 4, 4, 8),     // 1024 (pass C runs the warp kernel; build G3 and x/y here)
     FUSG_AX(4, 8, 8, 3, 8),     // 1536 (cfg5): 64 B column segments (T = 2 measured 15% slower)
     FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),  // 1050 (cfg3 x)
@@ -208,6 +209,7 @@ static const StaticEntry kColTab[] = {
     FUSG_AX(16, 4, 8, 4),
     FUSG_AX(4, 8, 4, 3, 8),
     FUSG_AX(8, 8, 4, 3, 8),
+    FUSG_AX(4, 8, 4, 4, 8),
     FUSG_AX(4, 8, 8, 3, 8),
     FUSG_AX(2, 8, 8, 3, 8),
     FUSG_AX(2, 5, 7, 3, 2, 5),
@@ -746,6 +748,17 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
       if ((stage_rows & 1) && !INV && ld.g.sp == 1 && st.g.sp != 1) fn = e->fwd_rowin;
       if ((stage_rows & 2) && INV && st.g.sp == 1 && ld.g.sp != 1) fn = e->inv_rowout;
       return launch_static(ctx, fn, *e, n_inner, n_outer, s, ld, st, pl.tw);
+    }
+  }
+  // kernel-spectrum build passes (generate / fold + forward) on compile-time plans
+  if constexpr (!INV && std::is_same<ST, GStoreF>::value &&
+                (std::is_same<LD, KGenF>::value || std::is_same<LD, FoldF>::value)) {
+    if (const StaticEntry* e = find_static(pl.L, kKindCol)) {
+      if constexpr (std::is_same<LD, KGenF>::value) {
+        if (e->build_gen) return launch_static(ctx, e->build_gen, *e, n_inner, n_outer, s, ld, st, pl.tw);
+      } else {
+        if (e->build_fold) return launch_static(ctx, e->build_fold, *e, n_inner, n_outer, s, ld, st, pl.tw);
+      }
     }
   }
   switch (choose_tile(pl, n_inner)) {
