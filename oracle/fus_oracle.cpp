@@ -233,6 +233,51 @@ int orc_direct_potential(const double* lo, const double* hi, double dx, const in
   return 0;
 }
 
+// direct_potential_oracle (src/potential.cpp:203-238) evaluated only at the output voxels idx[]:
+// the same per-pair formula, O(N) per output, no voxel guard.  Each output sums plane by
+// plane (plane partial sums in source order, then planes in order), so the result does not
+// depend on the thread count.  Used to check full-size applies at sampled voxels.
+int orc_direct_potential_at(const double* lo, const double* hi, double dx, const int* dims,
+                            double k_re, double k_im, const double* f, const std::int64_t* idx,
+                            std::int64_t n_idx, double* out) {
+  const Grid g = to_grid(lo, hi, dx, dims);
+  const cd k(k_re, k_im);
+  const double vol = dx * dx * dx;
+  double sw[2];
+  if (orc_self_weight(k_re, k_im, dx, sw)) return 1;
+  const cd self(sw[0], sw[1]);
+  const int nx = dims[0], ny = dims[1], nz = dims[2];
+  const cd* fc = reinterpret_cast<const cd*>(f);
+  cd* oc = reinterpret_cast<cd*>(out);
+  std::vector<cd> planes(nz);
+  for (std::int64_t q = 0; q < n_idx; ++q) {
+    const std::int64_t i = idx[q];
+    if (i < 0 || i >= std::int64_t(g.count())) return fail("direct_potential_at: voxel index out of range");
+    const int ix = int(i % nx), iy = int((i / nx) % ny), iz = int(i / (std::int64_t(nx) * ny));
+#pragma omp parallel for schedule(dynamic)
+    for (int jz = 0; jz < nz; ++jz) {
+      cd acc = 0.0;
+      for (int jy = 0; jy < ny; ++jy)
+        for (int jx = 0; jx < nx; ++jx) {
+          const cd fj = fc[g.index(jx, jy, jz)];
+          if (ix == jx && iy == jy && iz == jz) {
+            acc += self * fj;
+          } else {
+            const double r = dx * std::sqrt(double(ix - jx) * (ix - jx) + double(iy - jy) * (iy - jy) +
+                                            double(iz - jz) * (iz - jz));
+            const double mag = std::exp(-k.imag() * r) / (4.0 * M_PI * r);
+            acc += vol * std::polar(mag, k.real() * r) * fj;
+          }
+        }
+      planes[jz] = acc;
+    }
+    cd total = 0.0;
+    for (int jz = 0; jz < nz; ++jz) total += planes[jz];
+    oc[q] = total;
+  }
+  return 0;
+}
+
 // src/potential.cpp:161-201 evaluate_potential_at
 int orc_evaluate_potential_at(double k_re, double k_im, const double* lo, const double* hi,
                               double dx, const int* dims, const double* f, const double* pts,

@@ -52,6 +52,8 @@ def lib():
         L.orc_green.argtypes = [C.c_double, C.c_double, C.c_double, dp]
         L.orc_kernel_fill.argtypes = [ip, ip, C.c_double, C.c_double, C.c_double, dp]
         L.orc_direct_potential.argtypes = [dp, dp, C.c_double, ip, C.c_double, C.c_double, dp, dp]
+        L.orc_direct_potential_at.argtypes = [dp, dp, C.c_double, ip, C.c_double, C.c_double, dp,
+                                              C.POINTER(C.c_int64), C.c_int64, dp]
         L.orc_evaluate_potential_at.argtypes = [C.c_double, C.c_double, dp, dp, C.c_double, ip, dp,
                                                 dp, C.c_int64, dp]
         L.orc_distribute_points.argtypes = [C.c_double, C.c_double, C.c_int, dp]
@@ -287,6 +289,21 @@ def direct_potential_oracle(k: Wavenumber, grid: VoxelGrid, f: np.ndarray) -> np
     lo, hi, dx, dims = grid.args()
     _check(lib().orc_direct_potential(lo, hi, dx, dims, k.k.real, k.k.imag,
                                       _dp(f.view(np.float64)), _dp(out.view(np.float64))))
+    return out
+
+
+def direct_potential_at(k: Wavenumber, grid: VoxelGrid, f: np.ndarray, indices) -> np.ndarray:
+    """direct_potential_oracle (src/potential.cpp:203-238) at the voxels `indices` only (O(N)
+    per output): checks full-size applies at sampled voxels."""
+    if f.size != grid.count():
+        raise ValueError("direct_potential_at: field size mismatch")
+    f = np.ascontiguousarray(f, np.complex128)
+    idx = np.ascontiguousarray(indices, np.int64)
+    out = np.empty(idx.size, np.complex128)
+    lo, hi, dx, dims = grid.args()
+    _check(lib().orc_direct_potential_at(lo, hi, dx, dims, k.k.real, k.k.imag, _dp(f.view(np.float64)),
+                                         idx.ctypes.data_as(C.POINTER(C.c_int64)), idx.size,
+                                         _dp(out.view(np.float64))))
     return out
 
 

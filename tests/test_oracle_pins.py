@@ -421,3 +421,17 @@ def test_criterion1_golden_errors(orc):
     got = {nw: f"{e:.4g}" for nw, e in records}
     assert got == {4: "0.6437", 6: "0.2641", 8: "0.138", 10: "0.07983"}
     assert f"{slope:.4g}" == "-2.269"
+
+
+def test_direct_potential_at_matches_full_direct_oracle(orc):
+    # the sampled-voxel direct sum (used by the full-size GPU checks) is the same formula as
+    # direct_potential_oracle (src/potential.cpp:203-238) at every voxel
+    g = orc.make_grid([0, 0, 0], [9e-4, 8e-4, 7e-4], 1e-4, 1)
+    k = orc.complex_wavenumber(orc.medium_preset("water"), 1.1e6, 1)
+    f = orc.random_vector(g.count(), 3)
+    full = orc.direct_potential_oracle(k, g, f)
+    idx = np.arange(0, g.count(), 7)
+    at = orc.direct_potential_at(k, g, f, idx)
+    assert np.max(np.abs(at - full[idx])) <= 1e-14 * np.max(np.abs(full))
+    with pytest.raises(ValueError):
+        orc.direct_potential_at(k, g, f, [g.count()])
