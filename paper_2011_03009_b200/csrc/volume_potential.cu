@@ -372,6 +372,56 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_col_to_row(WArgs a) {
   warp_fft<RL, 32, INV, PRUNED ? 2 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nout <= L/2
 }
 
+// Passes D/E, persistent: one CTA of 8 warps per SM streams 8-line column tiles ([pos][8],
+// swizzled) with cp.async double buffering.  Tile i+1 is in flight while warp w transforms line
+// w of tile i in place (its column of the tile, __syncwarp only) and writes its output row
+// straight from registers (512 B per warp instruction).  Two CTA barriers per tile.
+template <class RL, bool PRUNED>
+__global__ void __launch_bounds__(kWarpThreads, 1) warp_col_to_row_pp(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / 32;
+  extern __shared__ double2 sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles_i = (a.n_inner + 7) / 8;
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto buf = [&](int b) { return sm + b * (L * 8); };
+  auto prefetch = [&](int64_t tix, int b) {
+    if (tix < ntiles) {
+      const int i0 = int(tix % ntiles_i) * 8;
+      const int k = int(tix / ntiles_i);
+      const int lines_ok = min(8, a.n_inner - i0);
+      const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
+      double2* t = buf(b);
+      for (int e = threadIdx.x; e < a.in_nvalid * 8; e += kWarpThreads) {
+        const int pos = e >> 3, tt = e & 7;
+        cp_async16_zfill(&t[tile_at(pos, tt)], tt < lines_ok ? base + tt * a.in_si + pos * a.in_sp : a.in,
+                         tt < lines_ok);
+      }
+    }
+    cp_async_commit();
+  };
+  int64_t tix = blockIdx.x;
+  prefetch(tix, 0);
+  for (int it = 0; tix < ntiles; tix += gridDim.x, ++it) {
+    const int b = it & 1;
+    __syncthreads();  // every warp is done with the other buffer (the previous tile)
+    prefetch(tix + gridDim.x, b ^ 1);
+    cp_async_wait1();
+    __syncthreads();  // this tile's copies (issued by all threads) have landed
+    const int i0 = int(tix % ntiles_i) * 8;
+    const int k = int(tix / ntiles_i);
+    const bool ok = w < min(8, a.n_inner - i0);
+    double2* const t = buf(b);
+    TileColIn src{t, w, a.in_nvalid};
+    TileEx ex{t, w};
+    RowOut dst{a.out + int64_t(i0 + (ok ? w : 0)) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok,
+               a.scale};
+    double2 v[E];
+    warp_fft<RL, 32, true, PRUNED ? 2 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nout <= L/2
+  }
+  cp_async_wait0();
+}
+
 // Lines (i, k), i fastest: consecutive lane groups of a CTA take consecutive i, so column
 // lines (position stride sp, i contiguous) from one CTA share every 128-byte row through L1.
 template <class RL, int LANES, bool INV>
@@ -544,6 +594,11 @@ constexpr bool whole_butterflies(int lanes) {
   return true;
 }
 template <class RL, int LN, bool PRUNED>
+constexpr WFn colrow_pp_ptr() {
+  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_col_to_row_pp<RL, PRUNED>;
+  else return nullptr;
+}
+template <class RL, int LN, bool PRUNED>
 constexpr WFn conv_pp_ptr() {
   if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32, PRUNED>;
   else return nullptr;
@@ -565,6 +620,7 @@ struct WarpEntry {
   WFn row_to_col_fwd[2], col_to_row_inv[2];  // transposing passes (LANES = 32), [pruned]
   WFn conv_pp[2];   // persistent pipelined pass C, [pruned] (nullptr: not available)
   size_t pp_smem[2];
+  WFn col_to_row_pp[2];  // persistent pipelined inverse column -> row (passes D, E), [pruned]
 };
 #define FUSG_WARP(LN, ...)                                                                  \
   WarpEntry {                                                                               \
@@ -576,7 +632,8 @@ struct WarpEntry {
          transpose_ptr<Radices<__VA_ARGS__>, LN, true, true>()},                               \
         {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
         {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
-         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES}                                   \
+         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES},                                  \
+        {colrow_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), colrow_pp_ptr<Radices<__VA_ARGS__>, LN, true>()} \
   }
 // pass-C-only entry: the persistent pass C alone (the row/column kernels would spill at this E)
 #define FUSG_WARP_CONV_ONLY(LN, ...)                                                         \
@@ -584,7 +641,8 @@ struct WarpEntry {
     Radices<__VA_ARGS__>::len(), LN, nullptr, nullptr, nullptr, {nullptr, nullptr}, {nullptr, nullptr}, \
         {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
         {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
-         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES}                                   \
+         PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES},                                  \
+        {nullptr, nullptr}                                                                       \
   }
 static const WarpEntry kWarpTab[] = {
     FUSG_WARP(32, 8, 8, 8),  // 512 (cfg2)
@@ -618,6 +676,33 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
   if (mode == kWRowToCol || mode == kWColToRow) {
     // pruned radix-8 end stages when the zero padding / crop covers the upper half
     const bool pr = mode == kWRowToCol ? 2 * a.in_nvalid <= L : 2 * a.out_nvalid <= L;
+    static const bool colrow_pp = [] {  // FUSG_COLROW_PP=0: one tile per CTA, no pipelining
+      const char* e = getenv("FUSG_COLROW_PP");
+      return !(e && atoi(e) == 0);
+    }();
+    if (mode == kWColToRow && inv && colrow_pp && we->col_to_row_pp[pr]) {
+      WFn pp = we->col_to_row_pp[pr];
+      const size_t psmem = size_t(L) * 8 * 2 * sizeof(double2);  // two tile buffers
+      if (cudaFuncSetAttribute(pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem)) != cudaSuccess) {
+        set_error(FUSG_CUDA, "persistent column->row pass: cannot configure shared memory");
+        return -1;
+      }
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp, kWarpThreads, psmem) == cudaSuccess &&
+          per_sm >= 1) {
+        const int64_t tiles = int64_t((a.n_inner + 7) / 8) * a.n_outer;
+        const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+        pp<<<unsigned(grid), kWarpThreads, psmem, s>>>(a);
+        ctx->launches++;
+        const cudaError_t err = cudaGetLastError();
+        if (err != cudaSuccess) {
+          cuda_error(err, "persistent column->row pass");
+          return -1;
+        }
+        return 1;
+      }
+      cudaGetLastError();
+    }
     fn = mode == kWRowToCol ? (inv ? nullptr : we->row_to_col_fwd[pr]) : (inv ? we->col_to_row_inv[pr] : nullptr);
     if (!fn) return 0;
     const size_t tsmem = size_t(L) * 8 * sizeof(double2);
@@ -723,7 +808,11 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
       return v ? atoi(v) : 1;
     }();
     const bool r2c = !INV && ld.g.sp == 1 && st.g.si == 1 && st.g.sp != 1 && (wt & 1);
-    const bool c2r = INV && ld.g.si == 1 && ld.g.sp != 1 && st.g.sp == 1 && (wt & 2);
+    static const bool colrow_pp = [] {
+      const char* v = getenv("FUSG_COLROW_PP");
+      return !(v && atoi(v) == 0);
+    }();
+    const bool c2r = INV && ld.g.si == 1 && ld.g.sp != 1 && st.g.sp == 1 && ((wt & 2) || colrow_pp);
     if (r2c || c2r) {
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
