@@ -214,6 +214,21 @@ fusg_status fusg_kernel_apply_slab(fusg_kernel* kernel, const double* f_dev, dou
 fusg_status fusg_kernel_apply_slab_loopback(fusg_kernel* const* ranks, int32_t nranks,
                                             const double* const* f_dev, double* const* u_dev,
                                             double scale);
+/* Fused peer-memory transposes (<= 8 ranks; padded x and y lengths 256, 512 or 768): the
+ * forward x pass stores every kx segment straight into the x-slab of the rank owning kx and the
+ * inverse y pass stores every z-row straight into the A slab of the rank owning z, over NVLink
+ * (CUDA IPC mappings). No exchange buffers or pack/unpack copies.
+ *  - ipc_handles: this rank's two 64-byte CUDA IPC handles (x-slab, A slab);
+ *  - attach_peers: `handles` = every rank's 128 bytes in rank order (gathered by the caller);
+ *  - apply_slab_p2p: this rank's apply; all ranks call it (two 1-int NCCL barriers per apply);
+ *  - apply_slab_loopback_p2p: the fused path for all ranks in this process on one device. */
+fusg_status fusg_kernel_slab_ipc_handles(const fusg_kernel* kernel, uint8_t out[128]);
+fusg_status fusg_kernel_slab_attach_peers(fusg_kernel* kernel, const uint8_t* handles);
+fusg_status fusg_kernel_apply_slab_p2p(fusg_kernel* kernel, const double* f_dev, double* u_dev,
+                                       double scale, void* stream);
+fusg_status fusg_kernel_apply_slab_loopback_p2p(fusg_kernel* const* ranks, int32_t nranks,
+                                                const double* const* f_dev, double* const* u_dev,
+                                                double scale);
 
 #ifdef __cplusplus
 }

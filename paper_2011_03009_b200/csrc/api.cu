@@ -42,10 +42,22 @@ void free_kernel(fusg_kernel* K) {
   if (!K) return;
   cudaSetDevice(K->ctx->device);
   cudaStream_t s = K->ctx->stream;
-  cudaFreeAsync(K->bufA, s);
+  for (size_t q = 0; q < K->peer_opened.size(); ++q)
+    if (K->peer_opened[q]) {
+      cudaIpcCloseMemHandle(K->peerX[q]);
+      cudaIpcCloseMemHandle(K->peerA[q]);
+    }
+  if (K->bar) cudaFree(K->bar);
+  if (K->ipc_bufs) {
+    cudaStreamSynchronize(s);
+    cudaFree(K->bufA);
+    if (K->xbuf) cudaFree(K->xbuf);
+  } else {
+    cudaFreeAsync(K->bufA, s);
+    if (K->xbuf) cudaFreeAsync(K->xbuf, s);
+  }
   cudaFreeAsync(K->bufB, s);
   cudaFreeAsync(K->koct, s);
-  if (K->xbuf) cudaFreeAsync(K->xbuf, s);
   if (K->rbuf) cudaFreeAsync(K->rbuf, s);
   cudaFree(K->stage_f);
   cudaFree(K->stage_u);

@@ -41,6 +41,34 @@ bool make_plan_radices(int L, AxisPlan& pl);
 
 }  // namespace fusg
 
+namespace fusg {
+// Destinations of a fused-transpose store (sharded apply): the element
+// (line i, outer k, position pos) of a pass goes to the rank q owning key = by_pos ? pos : i
+// (ranks own contiguous key ranges starting at begin[q]) at
+//   base[q] + off[q] + i * out_si + k * sk[q] + pos * out_sp.
+// n = 0: plain store to the pass's own output.  Pass A keys by kx (into the owners' x-slabs),
+// pass D by z (into the owners' A slabs); base[q] is the peer buffer (CUDA IPC mapping, or a
+// buffer of another in-process rank for the loopback).
+constexpr int kMaxPeers = 8;
+struct PeerMap {
+  int n = 0;
+  int by_pos = 0;
+  int begin[kMaxPeers] = {};
+  double2* base[kMaxPeers] = {};
+  int64_t off[kMaxPeers] = {};
+  int64_t sk[kMaxPeers] = {};
+#ifdef __CUDACC__
+  __host__ __device__ __forceinline__ int owner(int key) const {
+    int q = 0;
+#pragma unroll
+    for (int j = 1; j < kMaxPeers; ++j)
+      if (j < n && key >= begin[j]) q = j;
+    return q;
+  }
+#endif
+};
+}  // namespace fusg
+
 struct fusg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -77,6 +105,12 @@ struct fusg_kernel {
   double2* xbuf = nullptr;  // x-slab X [nx][Nz][Ny] (G > 1; aliases bufA when G = 1)
   double2* rbuf = nullptr;  // all-to-all staging [p][nx][nz_p][Ny] (G > 1)
   std::vector<int64_t> aoff, acnt, roff, rcnt;  // exchange plan (fusg_slab_exchange_plan)
+  // fused peer-memory transposes: xbuf and bufA are cudaMalloc'd (IPC-exportable) for slab
+  // kernels; peerX/peerA[q] = rank q's x-slab / A slab (own buffers for q == rank)
+  bool ipc_bufs = false;
+  std::vector<double2*> peerX, peerA;
+  std::vector<bool> peer_opened;  // IPC mappings to close on destroy
+  int* bar = nullptr;             // 1-int NCCL barrier buffer
   uint64_t bytes = 0;
   std::mutex mu;  // serialises applies sharing the workspace
 };
@@ -95,6 +129,11 @@ fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t
 fusg_status apply_chunk_AB(fusg_kernel* K, const double2* f_z0, int z0, int nzc, cudaStream_t s);
 fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s);
 fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s);
+// fused peer-memory transposes (shard.cu): pass A storing into the x-slabs owned by each kx,
+// passes B and C, pass D storing into the A slabs owned by each z
+fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap& pm, cudaStream_t s);
+fusg_status apply_phase_BC(fusg_kernel* K, double2* X, cudaStream_t s);
+fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t s);
 void destroy_nccl(fusg_ctx* ctx);
 // ev (optional): 6 events recorded before passes A..E and after E
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,

@@ -124,6 +124,33 @@ fusg_status create_slab(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenum
   return FUSG_OK;
 }
 
+// Peer maps of the fused transposes for rank K->rank, given every rank's x-slab / A buffer.
+//   pass A (key kx): element (y, z_local, kx) -> X_q[kx - x0_q][z0_r + z_local][y]
+//   pass D (key z):  element (z, kx_local, y) -> A_q[x0_r + kx_local][z - z0_q][y]
+void peer_maps(const fusg_kernel* K, double2* const* X, double2* const* A, PeerMap* pa, PeerMap* pd) {
+  const int64_t Ny = row(K), Nz = K->grid.dims[2];
+  const int G = K->G;
+  pa->n = pd->n = G;
+  pa->by_pos = 1;
+  pd->by_pos = 0;
+  for (int q = 0; q < G; ++q) {
+    pa->begin[q] = K->xs[q];
+    pa->base[q] = X[q];
+    pa->off[q] = int64_t(K->z0) * Ny - int64_t(K->xs[q]) * Nz * Ny;
+    pa->sk[q] = Ny;
+    pd->begin[q] = K->zs[q];
+    pd->base[q] = A[q];
+    pd->off[q] = int64_t(K->x0) * K->nzs[q] * Ny - int64_t(K->zs[q]) * Ny;
+    pd->sk[q] = int64_t(K->nzs[q]) * Ny;
+  }
+}
+
+fusg_status nccl_barrier(fusg_kernel* K, cudaStream_t s) {
+  if (K->G == 1) return FUSG_OK;
+  auto comm = static_cast<ncclComm_t>(K->ctx->nccl);
+  return nccl_check(ncclAllReduce(K->bar, K->bar, 1, ncclInt, ncclMax, comm, s), "ncclAllReduce (barrier)");
+}
+
 }  // namespace
 
 void destroy_nccl(fusg_ctx* ctx) {
@@ -252,6 +279,114 @@ fusg_status fusg_kernel_apply_slab_loopback(fusg_kernel* const* ranks, int32_t n
       if (a_cnt(ranks[r], q))
         FUSG_CUDA_TRY(cudaMemcpyAsync(ranks[r]->bufA + a_off(ranks[r], q), ranks[q]->rbuf + r_off(ranks[q], r),
                                       a_cnt(ranks[r], q) * kC, cudaMemcpyDeviceToDevice, s));
+  for (int r = 0; r < G; ++r) FUSG_TRY(apply_phase_E(ranks[r], reinterpret_cast<double2*>(u_dev[r]), scale, s));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return FUSG_OK;
+}
+
+// ---- fused peer-memory transposes (the transposes fused into passes A and D)
+fusg_status fusg_kernel_slab_ipc_handles(const fusg_kernel* K, uint8_t out[128]) {
+  if (!K || !out) return set_error(FUSG_INVALID_ARGUMENT, "slab_ipc_handles: null argument");
+  if (!K->ipc_bufs || !K->xbuf) return set_error(FUSG_INVALID_ARGUMENT, "slab_ipc_handles: not a slab kernel");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
+  cudaIpcMemHandle_t hx, ha;
+  FUSG_CUDA_TRY(cudaIpcGetMemHandle(&hx, K->xbuf));
+  FUSG_CUDA_TRY(cudaIpcGetMemHandle(&ha, K->bufA));
+  std::memcpy(out, &hx, 64);
+  std::memcpy(out + 64, &ha, 64);
+  return FUSG_OK;
+}
+
+fusg_status fusg_kernel_slab_attach_peers(fusg_kernel* K, const uint8_t* handles) {
+  if (!K || !handles) return set_error(FUSG_INVALID_ARGUMENT, "slab_attach_peers: null argument");
+  if (!K->ipc_bufs || !K->xbuf) return set_error(FUSG_INVALID_ARGUMENT, "slab_attach_peers: not a slab kernel");
+  if (K->G > kMaxPeers) return set_error(FUSG_INVALID_ARGUMENT, "slab_attach_peers: more than 8 ranks");
+  FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
+  std::lock_guard<std::mutex> lock(K->mu);
+  if (!K->peerX.empty()) return set_error(FUSG_INVALID_ARGUMENT, "slab_attach_peers: peers already attached");
+  K->peerX.assign(K->G, nullptr);
+  K->peerA.assign(K->G, nullptr);
+  K->peer_opened.assign(K->G, false);
+  for (int q = 0; q < K->G; ++q) {
+    if (q == K->rank) {
+      K->peerX[q] = K->xbuf;
+      K->peerA[q] = K->bufA;
+      continue;
+    }
+    cudaIpcMemHandle_t hx, ha;
+    std::memcpy(&hx, handles + 128 * q, 64);
+    std::memcpy(&ha, handles + 128 * q + 64, 64);
+    void *px = nullptr, *pa = nullptr;
+    FUSG_CUDA_TRY(cudaIpcOpenMemHandle(&px, hx, cudaIpcMemLazyEnablePeerAccess));
+    if (cudaIpcOpenMemHandle(&pa, ha, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaIpcCloseMemHandle(px);
+      return set_error(FUSG_CUDA, "slab_attach_peers: cannot map a peer A slab");
+    }
+    K->peerX[q] = static_cast<double2*>(px);
+    K->peerA[q] = static_cast<double2*>(pa);
+    K->peer_opened[q] = true;
+  }
+  if (!K->bar) {
+    FUSG_CUDA_TRY(cudaMalloc(&K->bar, sizeof(int)));
+    FUSG_CUDA_TRY(cudaMemset(K->bar, 0, sizeof(int)));
+  }
+  return FUSG_OK;
+}
+
+// One process per GPU, peers attached: pass A stores straight into the owners' x-slabs, a
+// stream barrier (1-int NCCL all-reduce), passes B, C, pass D stores straight into the owners'
+// A slabs, a barrier, pass E.  No exchange buffers, no pack/unpack copies.
+fusg_status fusg_kernel_apply_slab_p2p(fusg_kernel* K, const double* f_dev, double* u_dev, double scale,
+                                       void* stream) {
+  if (!K || !f_dev || !u_dev) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_slab_p2p: null argument");
+  fusg_ctx* ctx = K->ctx;
+  if (int(K->peerX.size()) != K->G)
+    return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_slab_p2p: peers not attached (fusg_kernel_slab_attach_peers)");
+  if (K->G > 1 && (!ctx->nccl || ctx->nranks != K->G || ctx->rank != K->rank))
+    return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_slab_p2p: context has no matching NCCL communicator");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  std::lock_guard<std::mutex> lock(K->mu);
+  cudaStream_t s = ctx->pick(stream);
+  PeerMap pa, pd;
+  peer_maps(K, K->peerX.data(), K->peerA.data(), &pa, &pd);
+  FUSG_TRY(apply_phase_A_peers(K, reinterpret_cast<const double2*>(f_dev), pa, s));
+  FUSG_TRY(nccl_barrier(K, s));
+  FUSG_TRY(apply_phase_BC(K, K->xbuf, s));
+  FUSG_TRY(apply_phase_D_peers(K, pd, s));
+  FUSG_TRY(nccl_barrier(K, s));
+  return apply_phase_E(K, reinterpret_cast<double2*>(u_dev), scale, s);
+}
+
+// The fused path for all G ranks in this process on one device (the peers are the other
+// in-process ranks' buffers; stream order stands in for the barriers).
+fusg_status fusg_kernel_apply_slab_loopback_p2p(fusg_kernel* const* ranks, int32_t nranks,
+                                                const double* const* f_dev, double* const* u_dev,
+                                                double scale) {
+  if (!ranks || nranks < 1 || !f_dev || !u_dev)
+    return set_error(FUSG_INVALID_ARGUMENT, "apply_slab_loopback_p2p: null argument");
+  if (nranks > kMaxPeers) return set_error(FUSG_INVALID_ARGUMENT, "apply_slab_loopback_p2p: more than 8 ranks");
+  for (int r = 0; r < nranks; ++r)
+    if (!ranks[r] || ranks[r]->G != nranks || ranks[r]->rank != r || ranks[r]->ctx != ranks[0]->ctx ||
+        !ranks[r]->ipc_bufs)
+      return set_error(FUSG_INVALID_ARGUMENT, "apply_slab_loopback_p2p: kernels must be ranks 0..G-1 of one decomposition on one context");
+  fusg_ctx* ctx = ranks[0]->ctx;
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const int G = nranks;
+  std::vector<double2*> X(G), A(G);
+  for (int q = 0; q < G; ++q) {
+    X[q] = ranks[q]->xbuf;
+    A[q] = ranks[q]->bufA;
+  }
+  std::vector<PeerMap> pa(G), pd(G);
+  for (int r = 0; r < G; ++r) peer_maps(ranks[r], X.data(), A.data(), &pa[r], &pd[r]);
+  for (int r = 0; r < G; ++r)
+    FUSG_TRY(apply_phase_A_peers(ranks[r], reinterpret_cast<const double2*>(f_dev[r]), pa[r], s));
+  for (int r = 0; r < G; ++r) {
+    FUSG_TRY(apply_phase_BC(ranks[r], ranks[r]->xbuf, s));
+    FUSG_TRY(apply_phase_D_peers(ranks[r], pd[r], s));
+  }
   for (int r = 0; r < G; ++r) FUSG_TRY(apply_phase_E(ranks[r], reinterpret_cast<double2*>(u_dev[r]), scale, s));
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return FUSG_OK;

@@ -307,7 +307,8 @@ struct WArgs {
   double scale;
   int n_inner, n_outer;
   const double2* tw;
-  KOct ko;  // pass C only
+  KOct ko;     // pass C only
+  PeerMap pm;  // fused peer-memory transpose stores (passes A and D of the sharded apply)
 };
 
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
@@ -338,13 +339,27 @@ __global__ void __launch_bounds__(kWarpThreads, 2) warp_row_to_col(WArgs a) {
   double2 v[E];
   warp_fft<RL, 32, INV, PRUNED ? 1 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nvalid <= L/2
   __syncthreads();
-  double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
-  for (int e = threadIdx.x; e < a.out_nvalid * 8; e += kWarpThreads) {
-    const int pos = e >> 3, t = e & 7;
-    if (t < lines_ok) {
-      const double2 x = tile[tile_at(pos, t)];
-      base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+  if (a.pm.n == 0) {
+    double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+    for (int e = threadIdx.x; e < a.out_nvalid * 8; e += kWarpThreads) {
+      const int pos = e >> 3, t = e & 7;
+      if (t < lines_ok) {
+        const double2 x = tile[tile_at(pos, t)];
+        base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+      }
     }
+  } else {
+    // fused transpose: the segment of position pos (kx) goes straight to the rank owning it
+    for (int e = threadIdx.x; e < a.out_nvalid * 8; e += kWarpThreads) {
+      const int pos = e >> 3, t = e & 7;
+      if (t < lines_ok) {
+        const int q = a.pm.owner(a.pm.by_pos ? pos : i0 + t);
+        const double2 x = tile[tile_at(pos, t)];
+        a.pm.base[q][a.pm.off[q] + int64_t(i0 + t) * a.out_si + int64_t(k) * a.pm.sk[q] + int64_t(pos) * a.out_sp] =
+            (a.scale == 1.0) ? x : cscale(x, a.scale);
+      }
+    }
+    __threadfence_system();  // remote stores performed before the barrier that follows the pass
   }
 }
 
@@ -414,12 +429,18 @@ __global__ void __launch_bounds__(kWarpThreads, 1) warp_col_to_row_pp(WArgs a) {
     double2* const t = buf(b);
     TileColIn src{t, w, a.in_nvalid};
     TileEx ex{t, w};
-    RowOut dst{a.out + int64_t(i0 + (ok ? w : 0)) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok,
-               a.scale};
+    const int line = i0 + (ok ? w : 0);
+    double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
+    if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
+      const int q = a.pm.owner(line);
+      orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
+    }
+    RowOut dst{orow, 1, a.out_nvalid, ok, a.scale};
     double2 v[E];
     warp_fft<RL, 32, true, PRUNED ? 2 : 0>(v, ex, lane, TwTable{a.tw}, src, dst);  // PRUNED: nout <= L/2
   }
   cp_async_wait0();
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
 
 // Lines (i, k), i fastest: consecutive lane groups of a CTA take consecutive i, so column
@@ -680,7 +701,8 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
       const char* e = getenv("FUSG_COLROW_PP");
       return !(e && atoi(e) == 0);
     }();
-    if (mode == kWColToRow && inv && colrow_pp && we->col_to_row_pp[pr]) {
+    if (a.pm.n && mode == kWColToRow && !we->col_to_row_pp[pr]) return 0;  // fused stores: pp kernel only
+    if (mode == kWColToRow && inv && (colrow_pp || a.pm.n) && we->col_to_row_pp[pr]) {
       WFn pp = we->col_to_row_pp[pr];
       const size_t psmem = size_t(L) * 8 * 2 * sizeof(double2);  // two tile buffers
       if (cudaFuncSetAttribute(pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(psmem)) != cudaSuccess) {
@@ -949,10 +971,16 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   // (a cascade builds one GreenKernel per harmonic)
   cudaStream_t as = K->ctx->stream;
   double2 *g1 = nullptr, *g2 = nullptr;  // build scratch: [oz][oy][kx] and [oz][ky][kx] half-ranges
-  if (cudaMallocAsync(&K->bufA, nA * sizeof(double2), as) != cudaSuccess ||
+  // slab kernels: the A and x-slab buffers are peer-store targets, exported with CUDA IPC,
+  // which needs cudaMalloc (not the stream-ordered pool)
+  K->ipc_bufs = K->slab;
+  auto alloc_ipc = [&](double2** p, size_t n) {
+    return K->ipc_bufs ? cudaMalloc(p, n * sizeof(double2)) : cudaMallocAsync(p, n * sizeof(double2), as);
+  };
+  if (alloc_ipc(&K->bufA, nA) != cudaSuccess ||
       cudaMallocAsync(&K->bufB, nB * sizeof(double2), as) != cudaSuccess ||
       cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess ||
-      (nX && cudaMallocAsync(&K->xbuf, nX * sizeof(double2), as) != cudaSuccess) ||
+      (nX && alloc_ipc(&K->xbuf, nX) != cudaSuccess) ||
       (nX && cudaMallocAsync(&K->rbuf, nX * sizeof(double2), as) != cudaSuccess) ||
       cudaMallocAsync(&g1, size_t(Hx) * Ny * Nz * sizeof(double2), as) != cudaSuccess ||
       cudaMallocAsync(&g2, size_t(Hx) * Hy * Nz * sizeof(double2), as) != cudaSuccess) {
@@ -1002,22 +1030,56 @@ fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s) {
                             GStoreF{GStore{K->bufA, 1, Ny, int64_t(nz) * Ny, Px, 1.0}}, s, kKindRow);
 }
 
-// passes B, C, D on the x-slab X [nx][Nz][Ny]; ev (optional) marks after B and after C
-fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev) {
+// passes B, C on the x-slab X [nx][Nz][Ny] into B (ev, optional: marks after B and after C)
+static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev) {
   const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
   const int Hy = K->H[1], Hz = K->H[2];
   const int nx = K->nx;
   const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
-  // B: y rows of X (lines z, tiled; outer kx) -> B, transposed so z is contiguous
   FUSG_TRY(launch_axis<false>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{X, Ny, NzNy, 1, Ny}},
                               GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
   if (ev) cudaEventRecord(ev[0], s);
-  // C: z rows of B (lines ky; outer kx): forward, * K^, inverse, keep Nz; in place
   FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
                        GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
                        KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0}, s));
   if (ev) cudaEventRecord(ev[1], s);
+  return FUSG_OK;
+}
+
+fusg_status apply_phase_BC(fusg_kernel* K, double2* X, cudaStream_t s) { return phase_BC(K, X, s, nullptr); }
+
+// Fused transposes of the sharded apply: pass A stores each kx segment into the x-slab of the
+// rank owning kx, pass D each z-row into the A slab of the rank owning z (PeerMap).  Both need
+// the transposing warp kernels (padded x / y lengths with a warp-engine entry).
+fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap& pm, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  WArgs a{f, Nx, int64_t(Ny) * Nx, 1, Nx, nullptr, 1, Ny, int64_t(Nz) * Ny, K->P[0], 1.0,
+          Ny, K->nz, K->plan[0].tw, KOct{}, pm};
+  const int r = launch_warp(K->ctx, K->P[0], kWRowToCol, false, a, s);
+  if (r < 0) return FUSG_CUDA;
+  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a warp-engine padded x length (256, 512, 768)");
+  return FUSG_OK;
+}
+
+fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t s) {
+  const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Py = K->P[1];
+  const int64_t PyNz = int64_t(Py) * Nz;
+  WArgs a{K->bufB, 1, PyNz, Nz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
+  const int r = launch_warp(K->ctx, Py, kWColToRow, true, a, s);
+  if (r < 0) return FUSG_CUDA;
+  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a warp-engine padded y length (256, 512, 768)");
+  return FUSG_OK;
+}
+
+// passes B, C, D on the x-slab X [nx][Nz][Ny]; ev (optional) marks after B and after C
+fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev) {
+  const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Py = K->P[1];
+  const int nx = K->nx;
+  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  FUSG_TRY(phase_BC(K, X, s, ev));
   // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of X, keep Ny
   return launch_axis<true>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
                            GStoreF{GStore{X, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol);

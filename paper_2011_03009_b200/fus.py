@@ -611,6 +611,29 @@ class SlabKernel:
         self.ctx.synchronize()
         return u
 
+    def ipc_handles(self) -> bytes:
+        """This rank's CUDA IPC handles (x-slab, A slab): 128 bytes to all-gather."""
+        buf = (C.c_uint8 * 128)()
+        check(lib().fusg_kernel_slab_ipc_handles(self.handle, buf))
+        return bytes(buf)
+
+    def attach_peers(self, handles: bytes):
+        """Map every rank's buffers (handles: all ranks' ipc_handles() concatenated in rank
+        order) for the fused peer-memory transposes."""
+        if len(handles) != 128 * self.nranks:
+            raise ValueError("attach_peers: need 128 bytes per rank")
+        buf = (C.c_uint8 * len(handles)).from_buffer_copy(handles)
+        check(lib().fusg_kernel_slab_attach_peers(self.handle, buf))
+
+    def apply_p2p(self, f_slab, scale: float = 1.0):
+        """This rank's apply with the transposes fused into passes A and D (peer stores over
+        NVLink); every rank calls it."""
+        u = torch.empty_like(f_slab)
+        _sync_torch_to(self.ctx)
+        check(lib().fusg_kernel_apply_slab_p2p(self.handle, f_slab.data_ptr(), u.data_ptr(), float(scale), None))
+        self.ctx.synchronize()
+        return u
+
     def __del__(self):
         try:
             if getattr(self, "handle", None):
@@ -633,9 +656,12 @@ def nccl_unique_id() -> bytes:
 
 
 def apply_slab_loopback(grid: VoxelGrid, k: Wavenumber, f, nranks: int, scale: float = 1.0,
-                        ctx: Optional[Context] = None):
-    """Run an nranks-way slab decomposition of the apply in this process on one GPU (loopback
-    transport: the NCCL path's blocks and kernels with device copies); returns the global u."""
+                        ctx: Optional[Context] = None, transport: str = "nccl"):
+    """Run an nranks-way slab decomposition of the apply in this process on one GPU and return
+    the global u.  transport "nccl": the NCCL path's blocks and kernels, with device copies;
+    "p2p": the fused peer-store transposes, with the other in-process ranks as peers."""
+    if transport not in ("nccl", "p2p"):
+        raise ValueError("apply_slab_loopback: transport is 'nccl' or 'p2p'")
     ctx = ctx or context()
     fd = _on_device(f, ctx)
     ks = [SlabKernel(grid, k, nranks, r, ctx) for r in range(nranks)]
@@ -646,5 +672,6 @@ def apply_slab_loopback(grid: VoxelGrid, k: Wavenumber, f, nranks: int, scale: f
     fp = (C.c_void_p * nranks)(*[x.data_ptr() for x in fs])
     up = (C.c_void_p * nranks)(*[x.data_ptr() for x in us])
     _sync_torch_to(ctx)
-    check(lib().fusg_kernel_apply_slab_loopback(hs, int(nranks), fp, up, float(scale)))
+    fn = lib().fusg_kernel_apply_slab_loopback_p2p if transport == "p2p" else lib().fusg_kernel_apply_slab_loopback
+    check(fn(hs, int(nranks), fp, up, float(scale)))
     return torch.cat(us)

@@ -363,6 +363,48 @@ def test_slab_sharded_apply_loopback_is_bitwise_unsharded(ctx, dims, G):
     assert torch.equal(got, want)
 
 
+@pytest.mark.parametrize("dims,G", [((128, 128, 19), 2), ((128, 126, 19), 3), ((256, 255, 9), 4),
+                                    ((128, 128, 40), 8), ((127, 128, 23), 7)])
+def test_slab_fused_peer_transposes_loopback_is_bitwise_unsharded(ctx, dims, G):
+    # The transposes fused into passes A and D (peer stores, no exchange buffers): every rank's
+    # pass A writes each kx segment into the owner's x-slab, pass D each z-row into the owner's
+    # A slab; ragged z and kx splits; must reproduce the single-GPU apply bit for bit.
+    dx = 1e-4
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    assert fus.padded_dims(g)[0] in (256, 512) and fus.padded_dims(g)[1] in (256, 512)
+    f = fus.random_vector(g.count(), 9)
+    want = fus.GreenKernel(g, k).apply(f, 0.5)
+    got = fus.apply_slab_loopback(g, k, f, G, 0.5, transport="p2p")
+    assert torch.equal(got, want)
+
+
+def test_slab_fused_transposes_need_warp_lengths(ctx):
+    g = fus.make_grid([0, 0, 0], [37e-4, 20e-4, 19e-4], 1e-4, 2)  # Px = 80: no transposing warp kernel
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    with pytest.raises(ValueError, match="warp-engine padded x length"):
+        fus.apply_slab_loopback(g, k, fus.random_vector(g.count(), 1), 2, transport="p2p")
+
+
+def test_slab_fused_p2p_over_nccl_single_rank_with_ipc_handles(ctx):
+    # The multi-process entry points on one rank: IPC handle export, peer attach (own buffers),
+    # the fused apply with its NCCL stream barriers; bitwise = unsharded.
+    g = fus.make_grid([0, 0, 0], [128e-4, 128e-4, 21e-4], 1e-4, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), 13)
+    want = fus.GreenKernel(g, k).apply(f)
+    c = fus.Context(0)
+    fus.attach_nccl(c, 1, 0, fus.nccl_unique_id())
+    sk = fus.SlabKernel(g, k, 1, 0, c)
+    with pytest.raises(ValueError, match="peers not attached"):
+        sk.apply_p2p(torch.from_numpy(f).cuda())
+    h = sk.ipc_handles()
+    assert len(h) == 128
+    sk.attach_peers(h)
+    for _ in range(2):
+        assert torch.equal(sk.apply_p2p(torch.from_numpy(f).cuda()), want)
+
+
 def test_slab_apply_over_nccl_single_rank(ctx):
     # The NCCL transport's full path (phase A, grouped send/recv, unpack, B-D, pack, send/recv,
     # phase E) on a 1-rank communicator: every NCCL call runs (to self); bitwise = unsharded.
