@@ -222,6 +222,15 @@ fusg_status fusg_kernel_apply_slab_loopback(fusg_kernel* const* ranks, int32_t n
  *  - attach_peers: `handles` = every rank's 128 bytes in rank order (gathered by the caller);
  *  - apply_slab_p2p: this rank's apply; all ranks call it (two 1-int NCCL barriers per apply);
  *  - apply_slab_loopback_p2p: the fused path for all ranks in this process on one device. */
+/* Peer-store plan of rank `rank` (arrays of nranks <= 8; host only), with owner(key) = the last
+ * q with begin[q] <= key:
+ *  pass A element (y, z_local, kx) of rank r goes to rank q = owner_a(kx), x-slab flat index
+ *    a_off[q] + y + z_local * a_sk[q] + kx * Nz * Ny;
+ *  pass D element (z, kx_local, y) goes to rank q = owner_d(z), A-slab flat index
+ *    d_off[q] + z * Ny + kx_local * d_sk[q] + y. */
+fusg_status fusg_slab_peer_plan(const fusg_grid* global_grid, int32_t nranks, int32_t rank, int64_t* a_begin,
+                                int64_t* a_off, int64_t* a_sk, int64_t* d_begin, int64_t* d_off,
+                                int64_t* d_sk);
 fusg_status fusg_kernel_slab_ipc_handles(const fusg_kernel* kernel, uint8_t out[128]);
 fusg_status fusg_kernel_slab_attach_peers(fusg_kernel* kernel, const uint8_t* handles);
 fusg_status fusg_kernel_apply_slab_p2p(fusg_kernel* kernel, const double* f_dev, double* u_dev,

@@ -110,6 +110,7 @@ SIGNATURES = {
     "fusg_kernel_apply_slab": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp]),
     "fusg_kernel_apply_slab_loopback": (C.c_int, [C.POINTER(_vp), C.c_int32, C.POINTER(_vp),
                                                   C.POINTER(_vp), C.c_double]),
+    "fusg_slab_peer_plan": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32] + [C.POINTER(C.c_int64)] * 6),
     "fusg_kernel_slab_ipc_handles": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
     "fusg_kernel_slab_attach_peers": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
     "fusg_kernel_apply_slab_p2p": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp]),

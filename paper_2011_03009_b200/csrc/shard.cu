@@ -124,24 +124,47 @@ fusg_status create_slab(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenum
   return FUSG_OK;
 }
 
-// Peer maps of the fused transposes for rank K->rank, given every rank's x-slab / A buffer.
-//   pass A (key kx): element (y, z_local, kx) -> X_q[kx - x0_q][z0_r + z_local][y]
-//   pass D (key z):  element (z, kx_local, y) -> A_q[x0_r + kx_local][z - z0_q][y]
+// Peer-store plan of the fused transposes for rank r (exported as fusg_slab_peer_plan):
+//   pass A (owner by kx): element (y, z_local, kx) -> X_q[kx - x0_q][z0_r + z_local][y]
+//     flat index a_off[q] + y + z_local * a_sk[q] + kx * Nz * Ny
+//   pass D (owner by z):  element (z, kx_local, y) -> A_q[x0_r + kx_local][z - z0_q][y]
+//     flat index d_off[q] + z * Ny + kx_local * d_sk[q] + y
+void peer_plan(const int dims[3], int Px, int G, int r, int64_t* a_begin, int64_t* a_off, int64_t* a_sk,
+               int64_t* d_begin, int64_t* d_off, int64_t* d_sk) {
+  const int64_t Ny = dims[1], Nz = dims[2];
+  int z0r, nzr, x0r, nxr;
+  slab_split(dims[2], G, r, &z0r, &nzr);
+  slab_split(Px, G, r, &x0r, &nxr);
+  for (int q = 0; q < G; ++q) {
+    int zq, nzq, xq, nxq;
+    slab_split(dims[2], G, q, &zq, &nzq);
+    slab_split(Px, G, q, &xq, &nxq);
+    a_begin[q] = xq;
+    a_off[q] = int64_t(z0r) * Ny - int64_t(xq) * Nz * Ny;
+    a_sk[q] = Ny;
+    d_begin[q] = zq;
+    d_off[q] = int64_t(x0r) * nzq * Ny - int64_t(zq) * Ny;
+    d_sk[q] = int64_t(nzq) * Ny;
+  }
+}
+
+// the plan plus every rank's x-slab / A buffer -> the kernels' peer maps
 void peer_maps(const fusg_kernel* K, double2* const* X, double2* const* A, PeerMap* pa, PeerMap* pd) {
-  const int64_t Ny = row(K), Nz = K->grid.dims[2];
   const int G = K->G;
+  int64_t ab[kMaxPeers], ao[kMaxPeers], as[kMaxPeers], db[kMaxPeers], dof[kMaxPeers], ds[kMaxPeers];
+  peer_plan(K->grid.dims, K->P[0], G, K->rank, ab, ao, as, db, dof, ds);
   pa->n = pd->n = G;
   pa->by_pos = 1;
   pd->by_pos = 0;
   for (int q = 0; q < G; ++q) {
-    pa->begin[q] = K->xs[q];
+    pa->begin[q] = int(ab[q]);
     pa->base[q] = X[q];
-    pa->off[q] = int64_t(K->z0) * Ny - int64_t(K->xs[q]) * Nz * Ny;
-    pa->sk[q] = Ny;
-    pd->begin[q] = K->zs[q];
+    pa->off[q] = ao[q];
+    pa->sk[q] = as[q];
+    pd->begin[q] = int(db[q]);
     pd->base[q] = A[q];
-    pd->off[q] = int64_t(K->x0) * K->nzs[q] * Ny - int64_t(K->zs[q]) * Ny;
-    pd->sk[q] = int64_t(K->nzs[q]) * Ny;
+    pd->off[q] = dof[q];
+    pd->sk[q] = ds[q];
   }
 }
 
@@ -183,6 +206,20 @@ fusg_status fusg_slab_exchange_plan(const fusg_grid* global_grid, int32_t nranks
   if (nranks > global_grid->dims[2] || nranks > P[0])
     return set_error(FUSG_INVALID_ARGUMENT, "more ranks than z-planes or kx columns");
   exchange_plan(global_grid->dims, P[0], nranks, rank, a_off, a_cnt, r_off, r_cnt);
+  return FUSG_OK;
+}
+
+fusg_status fusg_slab_peer_plan(const fusg_grid* global_grid, int32_t nranks, int32_t rank, int64_t* a_begin,
+                                int64_t* a_off, int64_t* a_sk, int64_t* d_begin, int64_t* d_off,
+                                int64_t* d_sk) {
+  if (!global_grid || nranks < 1 || nranks > kMaxPeers || rank < 0 || rank >= nranks || !a_begin || !a_off ||
+      !a_sk || !d_begin || !d_off || !d_sk)
+    return set_error(FUSG_INVALID_ARGUMENT, "slab_peer_plan: bad arguments");
+  int32_t P[3];
+  FUSG_TRY(fusg_padded_dims(global_grid, 0, P));
+  if (nranks > global_grid->dims[2] || nranks > P[0])
+    return set_error(FUSG_INVALID_ARGUMENT, "more ranks than z-planes or kx columns");
+  peer_plan(global_grid->dims, P[0], nranks, rank, a_begin, a_off, a_sk, d_begin, d_off, d_sk);
   return FUSG_OK;
 }
 

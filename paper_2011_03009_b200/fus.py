@@ -649,6 +649,16 @@ def attach_nccl(ctx: Context, nranks: int, rank: int, unique_id: bytes):
     check(lib().fusg_ctx_attach_nccl(ctx.handle, int(nranks), int(rank), buf))
 
 
+def slab_peer_plan(global_grid: VoxelGrid, nranks: int, rank: int) -> dict:
+    """Peer-store plan of the fused transposes (fusg_slab_peer_plan): per peer q, the first
+    owned key and the flat-index offset / outer stride of rank `rank`'s stores into q."""
+    arrs = {n: np.zeros(nranks, np.int64) for n in ("a_begin", "a_off", "a_sk", "d_begin", "d_off", "d_sk")}
+    g = global_grid.c()
+    ptrs = [a.ctypes.data_as(C.POINTER(C.c_int64)) for a in arrs.values()]
+    check(lib().fusg_slab_peer_plan(C.byref(g), int(nranks), int(rank), *ptrs))
+    return arrs
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     check(lib().fusg_nccl_unique_id(buf))

@@ -88,3 +88,76 @@ def test_slab_ranges_cover_and_are_ragged():
             assert max(c for _, c in rs) - min(c for _, c in rs) <= 1
     with pytest.raises(ValueError):
         fus.slab_range(4, 2, 2)
+
+
+def _peer_worker(rank, world, port, dims, q):
+    """The fused transposes' stores, emulated: every element of rank r's pass-A output (and of
+    its pass-D output) is sent to the owner named by fusg_slab_peer_plan together with its flat
+    index in the owner's buffer (gloo all-to-all); the owners scatter them and must hold exactly
+    their x-slab (resp. A slab)."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        g = fus.VoxelGrid(np.zeros(3), np.ones(3), 1.0, dims, 2)
+        Px = fus.padded_dims(g)[0]
+        Nx, Ny, Nz = dims
+        rng = np.random.default_rng(3)
+        S = rng.standard_normal((Px, Nz, Ny)) + 1j * rng.standard_normal((Px, Nz, Ny))  # [kx][z][y]
+        pl = fus.slab_peer_plan(g, world, rank)
+        z0, nz = fus.slab_range(Nz, world, rank)
+        x0, nx = fus.slab_range(Px, world, rank)
+
+        def owner(begin, key):
+            return np.searchsorted(begin, key, side="right") - 1
+
+        def scatter(dest_q, flat, vals, out_size):
+            order = np.argsort(dest_q, kind="stable")
+            dest_q, flat, vals = dest_q[order], flat[order], vals[order]
+            counts = [int(np.sum(dest_q == p)) for p in range(world)]
+            rc = torch.empty(world, dtype=torch.int64)
+            dist.all_to_all_single(rc, torch.tensor(counts, dtype=torch.int64))
+            rc = [int(c) for c in rc]
+            ri = torch.empty(sum(rc), dtype=torch.int64)
+            dist.all_to_all_single(ri, torch.from_numpy(flat), rc, counts)
+            rv = torch.empty(2 * sum(rc), dtype=torch.float64)
+            dist.all_to_all_single(rv, torch.from_numpy(vals.view(np.float64).copy()),
+                                   [2 * c for c in rc], [2 * c for c in counts])
+            out = np.full(out_size, np.nan + 0j)
+            out[ri.numpy()] = rv.numpy().view(np.complex128)
+            return out
+
+        # pass A: this rank's elements (kx, z_local, y) of S restricted to its z-slab
+        kx, zl, y = np.meshgrid(np.arange(Px), np.arange(nz), np.arange(Ny), indexing="ij")
+        kx, zl, y = kx.ravel(), zl.ravel(), y.ravel()
+        qa = owner(pl["a_begin"], kx)
+        flat = pl["a_off"][qa] + y + zl * pl["a_sk"][qa] + kx * Nz * Ny
+        X = scatter(qa, flat, S[kx, z0 + zl, y], nx * Nz * Ny).reshape(nx, Nz, Ny)
+        ok_a = np.array_equal(X, S[x0:x0 + nx])
+        # pass D: this rank's x-slab elements (z, kx_local, y) of T = S + 1 go to the z owners
+        T = S + 1.0
+        z, kl, y = np.meshgrid(np.arange(Nz), np.arange(nx), np.arange(Ny), indexing="ij")
+        z, kl, y = z.ravel(), kl.ravel(), y.ravel()
+        qd = owner(pl["d_begin"], z)
+        flat = pl["d_off"][qd] + z * Ny + kl * pl["d_sk"][qd] + y
+        A = scatter(qd, flat, T[x0 + kl, z, y], Px * nz * Ny).reshape(Px, nz, Ny)
+        ok_d = np.array_equal(A, T[:, z0:z0 + nz, :])
+        q.put((rank, bool(ok_a), bool(ok_d)))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), None))
+
+
+@pytest.mark.parametrize("world,dims", [(2, (9, 7, 11)), (3, (10, 5, 7)), (3, (16, 8, 9))])
+def test_slab_peer_plan_fused_stores_over_gloo(world, dims):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, dims, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, ok_a, ok_d in res:
+        assert ok_a is True and ok_d is True, (rank, ok_a, ok_d)
