@@ -402,14 +402,29 @@ def run_gpu_sharded(args, world, rank, local):
     t0 = time.perf_counter()
     K = fus.SlabKernel(g, k, world, rank, ctx)
     build_s = time.perf_counter() - t0
+    # fused peer-store transposes (default when the padded x/y lengths allow): gather every
+    # rank's CUDA IPC handles and map the peers' x-slab / A buffers
+    transport = args.transport
+    if transport == "p2p" and not (set(K_padded(g)[:2]) <= {256, 512, 768}):
+        transport = "nccl"
+    if transport == "p2p":
+        mine = torch.frombuffer(bytearray(K.ipc_handles()), dtype=torch.uint8).to(f"cuda:{local}")
+        allh = [torch.empty_like(mine) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allh, mine)
+        else:
+            allh = [mine]
+        K.attach_peers(b"".join(bytes(h.cpu().numpy().tobytes()) for h in allh))
     plane = g.dims[0] * g.dims[1]
     f_slab = np.ascontiguousarray(f[K.z0 * plane:(K.z0 + K.nz) * plane])
     fd = torch.from_numpy(f_slab).to(f"cuda:{local}")
     ud = torch.empty_like(fd)
     L = _lib.lib()
 
+    apply_fn = L.fusg_kernel_apply_slab_p2p if transport == "p2p" else L.fusg_kernel_apply_slab
+
     def step():
-        _lib.check(L.fusg_kernel_apply_slab(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, None))
+        _lib.check(apply_fn(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, None))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -456,10 +471,13 @@ def run_gpu_sharded(args, world, rank, local):
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD + "; z-slab sharded over ranks, NCCL all-to-all transposes",
+            "transport": transport,
+            "config": {"workload": WORKLOAD + ("; z-slab sharded over ranks, transposes fused into passes A/D as "
+                                               "NVLink peer stores" if transport == "p2p" else
+                                               "; z-slab sharded over ranks, NCCL all-to-all transposes"),
                        "grid": list(g.dims), "padded": list(K_padded(g)),
                        "parallelism": f"slab{world}", "l2": "inputs+workspace > 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm+nvlink", "kernel": "sharded apply (passes A-E + 2 all-to-all)",
+            "roofline": {"bound": "hbm+nvlink", "kernel": "sharded apply (passes A-E + 2 transposes)",
                          "achieved": total_bytes / world / (ms * 1e-3) / 1e9, "peak": hbm,
                          "peak_kind": hbm_kind, "unit": "GB/s",
                          "frac": total_bytes / world / (ms * 1e-3) / 1e9 / hbm, "traffic": None,
@@ -490,6 +508,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cascade", action="store_true", help="skip the nested 5-harmonic solve")
     ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N = 1")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="sharded apply: transposes fused into passes A/D as peer stores, or NCCL all-to-all")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: independent per-rank applies (weak scaling) instead of the sharded apply")
     args = ap.parse_args()
