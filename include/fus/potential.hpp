@@ -6,6 +6,7 @@
 #include <Eigen/Dense>
 #include <complex>
 #include <memory>
+#include <vector>
 
 #include "fus/grid.hpp"
 #include "fus/medium.hpp"
@@ -38,5 +39,11 @@ class GreenKernel {
   Wavenumber k_;
   std::shared_ptr<fusg_kernel> handle_;
 };
+
+// Off-grid potential (src/potential.cpp:161-201): sum over voxels of vol G(|x - c_j|) f_j
+// (self weight for |x - c_j| < 1e-9 dx, zero-f voxels skipped) at each point; on the GPU.
+Eigen::VectorXcd evaluate_potential_at(const Wavenumber& k, const VoxelGrid& grid,
+                                       const Eigen::VectorXcd& f,
+                                       const std::vector<Eigen::Vector3d>& points);
 
 }  // namespace fus

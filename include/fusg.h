@@ -153,6 +153,13 @@ fusg_status fusg_monopole_grid(fusg_ctx* ctx, const double* src_host, int32_t n_
 fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t n_src,
                                  const double* pts_dev, int64_t n_pts, double k_re, double k_im,
                                  double amp, double* out_dev, void* stream);
+/* evaluate_potential_at (src/potential.cpp:161-201): the volume potential of the device field
+ * f_dev on `grid` at n_pts arbitrary host points (n_pts x 3), O(N M): sum over voxels with
+ * f != 0 of vol G(r) f, self_weight f when r < 1e-9 dx. Deterministic (fixed-order partial
+ * sums); out_host receives n_pts complex128 values. */
+fusg_status fusg_evaluate_potential_at(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenumber* k,
+                                       const double* f_dev, const double* pts_host, int64_t n_pts,
+                                       double* out_host);
 /* radiated_power (src/transducer.cpp:134-155): deterministic fixed-order reduction. */
 fusg_status fusg_radiated_power(fusg_ctx* ctx, const double* src_host, int32_t n_src,
                                 double x_disc, double R, double k_re, double k_im, double amp,

@@ -121,6 +121,7 @@ fusg_status fusg_ctx_destroy(fusg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   destroy_nccl(ctx);
   cudaFree(ctx->dev_flag);
+  if (ctx->phase_tab) cudaFree(ctx->phase_tab);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return FUSG_OK;

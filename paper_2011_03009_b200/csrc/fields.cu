@@ -274,6 +274,106 @@ __global__ void __launch_bounds__(256) power_nodes_kernel(const double* __restri
   }
 }
 
+// ---------------------------------------------------------------------------- potential at points
+// evaluate_potential_at (src/potential.cpp:161-201): u(x_m) = sum over voxels j with f_j != 0 of
+// vol G(|x_m - c_j|) f_j, or self_weight(k, dx) f_j when |x_m - c_j| < 1e-9 dx.  O(N M) FP64: the
+// Rayleigh term (phase table, refined rsqrt) times a complex weight.  Grid: point blocks x voxel
+// chunk groups; a CTA stages kPotChunk consecutive voxels (whole or partial x-rows) in shared
+// memory, vs threads share a point and split the chunk (vs: a power of two, larger for few
+// points, so small point sets still fill the CTA), and each chunk group writes one
+// partial sum per point; potential_reduce_kernel adds the groups in order (deterministic).
+constexpr int kPotThreads = 256, kPotChunk = 1536;
+
+__global__ void phase_table_kernel(double2* tab) { fill_phase_table(tab); }
+
+template <int ATT>
+__global__ void __launch_bounds__(kPotThreads) potential_at_kernel(
+    GridDev g, const double2* __restrict__ f, const double* __restrict__ pts, int64_t n_pts, double k1,
+    double kim, double vol, double2 self, double coinc2, const double2* __restrict__ gtab,
+    double2* __restrict__ partial, int vs) {
+  __shared__ double2 fs[kPotChunk];  // vol * f of the staged voxels (self term: f, scaled back)
+  __shared__ double2 tab[kPhaseN];
+  __shared__ double2 red[kPotThreads];
+  for (int j = threadIdx.x; j < kPhaseN; j += kPotThreads) tab[j] = gtab[j];
+  const int pl = threadIdx.x / vs, sl = threadIdx.x % vs;
+  const int64_t pt = int64_t(blockIdx.x) * (kPotThreads / vs) + pl;
+  const bool active = pt < n_pts;
+  double x0 = 0, x1 = 0, x2 = 0;
+  if (active) {
+    x0 = pts[3 * pt];
+    x1 = pts[3 * pt + 1];
+    x2 = pts[3 * pt + 2];
+  }
+  const int Nx = g.dims[0], Ny = g.dims[1];
+  const int64_t count = int64_t(Nx) * Ny * g.dims[2];
+  const int64_t nchunks = (count + kPotChunk - 1) / kPotChunk;
+  const double inv_vol = 1.0 / vol;
+  double2 a4[4];
+  for (int c = 0; c < 4; ++c) a4[c] = make_double2(0.0, 0.0);
+  bool bad = false;
+  for (int64_t c = blockIdx.y; c < nchunks; c += gridDim.y) {
+    const int64_t v0 = c * kPotChunk, v1 = min(count, v0 + kPotChunk);
+    __syncthreads();  // previous chunk consumed (and, first time, the table staged)
+    for (int64_t v = v0 + threadIdx.x; v < v1; v += kPotThreads) {
+      const double2 x = f[v];
+      fs[v - v0] = make_double2(vol * x.x, vol * x.y);
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int64_t gi = v0; gi < v1;) {  // row segments of the chunk
+      const int64_t row = gi / Nx;
+      const int jx0 = int(gi - row * Nx);
+      const int64_t seg_end = min(v1, (row + 1) * Nx);
+      const double cy = centre(g.lo[1], int(row % Ny), g.dx) - x1;  // src/potential.cpp:181-183
+      const double cz = centre(g.lo[2], int(row / Ny), g.dx) - x2;
+      const double ryz2 = fma(cz, cz, cy * cy);
+      // branch-free term: a zero f_j adds an exact zero (the reference skips it, :186); a
+      // coincident voxel (r < 1e-9 dx, :189-190) takes the self weight instead of G
+      auto term = [&](int64_t q, double2& a) {
+        const double2 fj = fs[q - v0];  // vol * f_j
+        const double cx = centre(g.lo[0], jx0 + int(q - gi), g.dx) - x0;
+        const double d2 = fma(cx, cx, ryz2);
+        const bool co = d2 < coinc2;
+        double2 gk = make_double2(0.0, 0.0);
+        monopole_term_d2<ATT>(co ? 1.0 : d2, k1, kim, tab, gk, bad);  // e^{-Im k r} e^{i Re k r} / (4 pi r)
+        const double wx = co ? self.x * inv_vol : gk.x, wy = co ? self.y * inv_vol : gk.y;
+        a.x = fma(wx, fj.x, fma(-wy, fj.y, a.x));
+        a.y = fma(wx, fj.y, fma(wy, fj.x, a.y));
+      };
+      const int o = int(gi - v0);
+      int64_t q = gi + ((sl - o) % vs + vs) % vs;
+      for (; q + 3 * vs < seg_end; q += 4 * vs) {  // four independent chains
+        term(q, a4[0]);
+        term(q + vs, a4[1]);
+        term(q + 2 * vs, a4[2]);
+        term(q + 3 * vs, a4[3]);
+      }
+      for (; q < seg_end; q += vs) term(q, a4[0]);
+      gi = seg_end;
+    }
+  }
+  double2 acc = make_double2((a4[0].x + a4[1].x) + (a4[2].x + a4[3].x), (a4[0].y + a4[1].y) + (a4[2].y + a4[3].y));
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (active && sl == 0) {
+    double2 t = red[threadIdx.x];
+    for (int q = 1; q < vs; ++q) t = make_double2(t.x + red[threadIdx.x + q].x, t.y + red[threadIdx.x + q].y);
+    partial[int64_t(blockIdx.y) * n_pts + pt] = t;
+  }
+}
+
+__global__ void potential_reduce_kernel(const double2* __restrict__ partial, int groups, int64_t n_pts,
+                                        double2* __restrict__ out) {
+  for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < n_pts; p += int64_t(gridDim.x) * blockDim.x) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int y = 0; y < groups; ++y) {
+      const double2 v = partial[int64_t(y) * n_pts + p];
+      t = make_double2(t.x + v.x, t.y + v.y);
+    }
+    out[p] = t;
+  }
+}
+
 // Fixed-order reduction: ring j sums its n_theta nodes in order, times r_j; then rings in
 // order. One block; deterministic for any launch configuration.
 __global__ void power_reduce_kernel(const double* __restrict__ nodes, int n_r, int n_theta,
@@ -550,6 +650,73 @@ fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t 
   FUSG_LAUNCH_CHECK("monopole_points_kernel");
   cudaFreeAsync(src, s);
   return check_flag(ctx, s);
+}
+
+// evaluate_potential_at (src/potential.cpp:161-201)
+fusg_status fusg_evaluate_potential_at(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenumber* k,
+                                       const double* f_dev, const double* pts_host, int64_t n_pts,
+                                       double* out_host) {
+  if (!ctx || !grid || !k || (n_pts > 0 && (!f_dev || !pts_host || !out_host)))
+    return set_error(FUSG_INVALID_ARGUMENT, "evaluate_potential_at: null argument");
+  if (n_pts < 0) return set_error(FUSG_INVALID_ARGUMENT, "evaluate_potential_at: negative point count");
+  if (n_pts == 0) return FUSG_OK;
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  if (!ctx->phase_tab) {
+    FUSG_CUDA_TRY(cudaMalloc(&ctx->phase_tab, sizeof(double2) * kPhaseN));
+    phase_table_kernel<<<1, 256, 0, s>>>(ctx->phase_tab);
+    ctx->launches++;
+    FUSG_LAUNCH_CHECK("phase_table_kernel");
+  }
+  double sw[2];
+  FUSG_TRY(fusg_self_weight(k, grid->dx, sw));
+  const GridDev g = to_dev(*grid);
+  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  const int64_t nchunks = (count + kPotChunk - 1) / kPotChunk;
+  // threads per point: 4 for large point sets, up to the whole CTA for a handful of points
+  int vs = 4;
+  while (vs < kPotThreads && int64_t(kPotThreads / vs) > n_pts * 2) vs *= 2;
+  const int pb = kPotThreads / vs;
+  const int64_t pblocks = (n_pts + pb - 1) / pb;
+  // one full wave of resident CTAs (chunk groups loop over their chunks); one partial per
+  // (chunk group, point)
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, potential_at_kernel<2>, kPotThreads, 0);
+  per_sm = std::max(per_sm, 1);
+  const int64_t wave = int64_t(ctx->num_sms) * per_sm;
+  const int groups = int(std::max<int64_t>(1, std::min<int64_t>(nchunks, std::max<int64_t>(1, wave / pblocks))));
+  double *pts = nullptr;
+  double2 *partial = nullptr, *out = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&pts, sizeof(double) * 3 * n_pts, s));
+  FUSG_CUDA_TRY(cudaMallocAsync(&partial, sizeof(double2) * n_pts * groups, s));
+  FUSG_CUDA_TRY(cudaMallocAsync(&out, sizeof(double2) * n_pts, s));
+  FUSG_CUDA_TRY(cudaMemcpyAsync(pts, pts_host, sizeof(double) * 3 * n_pts, cudaMemcpyHostToDevice, s));
+  // distance bound: grid box vs the points' bounding box (attenuation polynomial eligibility)
+  double blo[3] = {grid->lo[0], grid->lo[1], grid->lo[2]}, bhi[3] = {grid->hi[0], grid->hi[1], grid->hi[2]};
+  for (int64_t i = 0; i < n_pts; ++i)
+    for (int a = 0; a < 3; ++a) {
+      blo[a] = std::min(blo[a], pts_host[3 * i + a]);
+      bhi[a] = std::max(bhi[a], pts_host[3 * i + a]);
+    }
+  double dd = 0.0;
+  for (int a = 0; a < 3; ++a) dd += (bhi[a] - blo[a]) * (bhi[a] - blo[a]);
+  const double coinc = 1e-9 * grid->dx;
+  FUSG_ATT_DISPATCH(att_mode(k->k_im, std::sqrt(dd) * (1.0 + 1e-12)), potential_at_kernel,
+                    dim3(unsigned(pblocks), unsigned(groups)), kPotThreads, 0,
+                    s>>>(g, reinterpret_cast<const double2*>(f_dev), pts, n_pts, phase_scale(k->k_re), k->k_im,
+                         grid->dx * grid->dx * grid->dx, make_double2(sw[0], sw[1]), coinc * coinc,
+                         ctx->phase_tab, partial, vs));
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("potential_at_kernel");
+  potential_reduce_kernel<<<grid_stride_blocks(ctx, n_pts, 256), 256, 0, s>>>(partial, groups, n_pts, out);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("potential_reduce_kernel");
+  FUSG_CUDA_TRY(cudaMemcpyAsync(out_host, out, sizeof(double2) * n_pts, cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(pts, s);
+  cudaFreeAsync(partial, s);
+  cudaFreeAsync(out, s);
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return FUSG_OK;
 }
 
 fusg_status fusg_radiated_power(fusg_ctx* ctx, const double* src_host, int32_t n_src, double x_disc,

@@ -305,6 +305,22 @@ Eigen::Vector3i GreenKernel::padded() const {
   return Eigen::Vector3i(p[0], p[1], p[2]);
 }
 
+Eigen::VectorXcd evaluate_potential_at(const Wavenumber& k, const VoxelGrid& grid, const Eigen::VectorXcd& f,
+                                       const std::vector<Eigen::Vector3d>& points) {
+  if (f.size() != Eigen::Index(grid.count()))
+    throw std::invalid_argument("evaluate_potential_at: field size mismatch");
+  const fusg_grid g = to_c(grid);
+  const fusg_wavenumber kc = to_c(k);
+  std::vector<double> pts(3 * points.size());
+  for (size_t i = 0; i < points.size(); ++i)
+    for (int a = 0; a < 3; ++a) pts[3 * i + a] = points[i][a];
+  const DevBuf fd = upload(f);
+  Eigen::VectorXcd out(static_cast<Eigen::Index>(points.size()));
+  check(fusg_evaluate_potential_at(ctx(), &g, &kc, fd.d(), pts.data(), int64_t(points.size()),
+                                   reinterpret_cast<double*>(out.data())));
+  return out;
+}
+
 // ------------------------------------------------------------------------------ transducer
 double BowlTransducer::cap_area() const {
   const double l = focal_length, R = outer_radius;

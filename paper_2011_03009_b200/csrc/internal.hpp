@@ -74,6 +74,7 @@ struct fusg_ctx {
   cudaStream_t stream = nullptr;
   int num_sms = 148;
   int* dev_flag = nullptr;  // device error flag (monopole coincidence)
+  double2* phase_tab = nullptr;  // e^{2 pi i j / 1024} / (4 pi), built on first use (fields.cu)
   std::atomic<uint64_t> launches{0};
   void* nccl = nullptr;  // ncclComm_t of a sharded job (fusg_ctx_attach_nccl)
   int nranks = 1, rank = 0;

@@ -141,6 +141,13 @@ __device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, b
 // with cp.async, then transform from shared memory.  ROWOUT: the output lines are contiguous
 // rows: the last stage writes the tile and the CTA stores it line-major.  Otherwise the first
 // (last) stage reads (writes) global memory directly, T adjacent lines = T*16 contiguous bytes.
+// compile-time choice between two endpoints (by reference)
+template <bool C, class A, class B>
+__device__ __forceinline__ auto& select_ref(A& a, B& b) {
+  if constexpr (C) return a;
+  else return b;
+}
+
 // LD is GLoadF for the apply passes, KGenF / FoldF for the kernel-spectrum build (ROWIN and
 // ROWOUT need GLoadF / GStoreF).
 template <class RL, int T, bool INV, bool ROWIN, bool ROWOUT, class LD = GLoadF>
@@ -173,10 +180,7 @@ __global__ void __launch_bounds__(SBounds<RL, T>::threads, SBounds<RL, T>::min_b
     if constexpr (ROWIN) return TileIn<T>{sm, t, ld.g.nvalid};
     else return gsrc;
   }();
-  auto& dst = [&]() -> auto& {
-    if constexpr (ROWOUT) return tdst;
-    else return gdst;
-  }();
+  auto& dst = select_ref<ROWOUT>(tdst, gdst);
   // twiddles staged in shared memory (first used after stage 1's barrier)
   double2* tws = sm + RL::len() * T;
   for (int m = threadIdx.x; m < RL::len(); m += NT) tws[m] = __ldg(tw + m);

@@ -219,6 +219,24 @@ def green_function(x, y, k: Wavenumber) -> complex:
     return complex(mag * math.cos(k.k.real * r), mag * math.sin(k.k.real * r))
 
 
+def evaluate_potential_at(k: Wavenumber, grid: VoxelGrid, f, points, ctx: Optional["Context"] = None) -> np.ndarray:
+    """src/potential.cpp:161-201: the volume potential of f (N complex128, host or device) at
+    arbitrary points (M x 3) as a host array of M complex128; on the device, O(N M)."""
+    n = grid.count()
+    size = f.numel() if torch is not None and isinstance(f, torch.Tensor) else np.size(f)
+    if size != n:
+        raise ValueError("evaluate_potential_at: field size mismatch")
+    ctx = ctx or context()
+    fd = _on_device(f, ctx)
+    pts = np.ascontiguousarray(np.asarray(points, float).reshape(-1, 3))
+    out = np.empty(len(pts), np.complex128)
+    g, w = grid.c(), k.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_evaluate_potential_at(ctx.handle, C.byref(g), C.byref(w), fd.data_ptr(),
+                                           pts.ctypes.data, len(pts), out.ctypes.data))
+    return out
+
+
 def next_fast_size(n: int) -> int:
     return int(lib().fusg_next_fast_size(int(n)))
 

@@ -155,6 +155,30 @@ void device_cases() {
         }
     CHECK(ok);
   }
+  // evaluate_potential_at agrees with apply at voxel centres, tests/test_potential.cpp:181-207
+  {
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {12e-4, 10e-4, 8e-4}}, 1e-4, 1);
+    const fus::Wavenumber k2 = fus::complex_wavenumber(kWater, 1.1e6, 2);
+    const Eigen::VectorXcd f = random_vector(g.count(), 99);
+    const Eigen::VectorXcd u = fus::GreenKernel(g, k2).apply(f);
+    std::vector<Eigen::Vector3d> pts;
+    std::vector<std::size_t> idx;
+    for (int iz = 0; iz < g.dims.z(); iz += 2)
+      for (int iy = 0; iy < g.dims.y(); iy += 3)
+        for (int ix = 0; ix < g.dims.x(); ix += 2) {
+          pts.push_back(g.center(ix, iy, iz));
+          idx.push_back(g.index(ix, iy, iz));
+        }
+    const Eigen::VectorXcd v = fus::evaluate_potential_at(k2, g, f, pts);
+    bool ok = true;
+    for (std::size_t i = 0; i < idx.size(); ++i)
+      ok = ok && std::abs(v[Eigen::Index(i)] - u[Eigen::Index(idx[i])]) < 1e-12 * u.cwiseAbs().maxCoeff();
+    CHECK(ok);
+    const Eigen::VectorXcd w =
+        fus::evaluate_potential_at(k2, g, f, {g.center(3, 2, 2) + Eigen::Vector3d(3e-5, 0, 0)});
+    CHECK(std::isfinite(std::abs(w[0])));
+    CHECK_THROWS_AS(fus::evaluate_potential_at(k2, g, Eigen::VectorXcd(3), pts), std::invalid_argument);
+  }
   // rhs coefficients, tests/test_cascade.cpp:33-63
   {
     const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {2e-3, 2e-3, 2e-3}}, 1e-3, 1);

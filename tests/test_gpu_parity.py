@@ -179,6 +179,46 @@ def test_host_apply_chunk_pipeline_is_bitwise_device_apply(ctx, monkeypatch, dim
         assert np.array_equal(K.apply_host(f, 0.5), want)
 
 
+# ------------------------------------------------------------------ off-grid potential (8(f) rank 1)
+@pytest.mark.parametrize("att", [True, False])
+def test_evaluate_potential_at_vs_oracle(ctx, orc, att):
+    # src/potential.cpp:161-201: on-grid points (self term), off-grid points, points outside the
+    # box, zero-f voxels (skipped); attenuating water or real k
+    g = fus.make_grid([0, 0, 0], [23e-4, 19e-4, 17e-4], 1e-4, 2)
+    go = orc.make_grid([0, 0, 0], [23e-4, 19e-4, 17e-4], 1e-4, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    if not att:
+        k = fus.Wavenumber(complex(k.k.real, 0.0), 2, k.omega)
+    ko = orc.Wavenumber(k.k, 2, k.omega)
+    f = fus.random_vector(g.count(), 21)
+    f[::7] = 0.0
+    rng = np.random.default_rng(5)
+    pts = [g.center(ix, iy, iz) for ix, iy, iz in ((0, 0, 0), (5, 7, 3), (22, 18, 16))]
+    pts += list(g.lo + rng.random((40, 3)) * (g.hi - g.lo))
+    pts += [g.hi + np.array([3e-3, -1e-3, 2e-3]), g.lo - np.array([1e-2, 0, 0])]
+    got = fus.evaluate_potential_at(k, g, f, pts)
+    ref = orc.evaluate_potential_at(ko, go, f, pts)
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+    # deterministic
+    assert np.array_equal(fus.evaluate_potential_at(k, g, torch.from_numpy(f).cuda(), pts), got)
+    with pytest.raises(ValueError):
+        fus.evaluate_potential_at(k, g, f[:5], pts)
+
+
+def test_evaluate_potential_at_agrees_with_apply_at_centres(ctx):
+    # tests/test_potential.cpp:181-207 (1e-12 of max |u|), on a 64^3 grid with 4096 points
+    g = fus.make_grid([0, 0, 0], [64e-4] * 3, 1e-4, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    f = fus.random_vector(g.count(), 99)
+    u = host(fus.GreenKernel(g, k).apply(f))
+    rng = np.random.default_rng(1)
+    ii = rng.integers(0, 64, (4096, 3))
+    pts = [g.center(*t) for t in ii]
+    v = fus.evaluate_potential_at(k, g, f, pts)
+    idx = [g.index(*t) for t in ii]
+    assert np.max(np.abs(v - u[idx])) < 1e-12 * np.max(np.abs(u))
+
+
 # ------------------------------------------------------------------ incident field
 def test_monopole_grid_and_points_vs_oracle(ctx, orc):
     t = fus.transducer_preset("H131", 100.0, 4096)
