@@ -335,6 +335,12 @@ def run_gpu(args, world, rank, local):
     solve = None
     if rank == 0 and not args.no_cascade:
         solve = nested_solve(ctx)
+    # evaluate_potential_at at the reference's use (on-axis nodes of a
+    # D2-grid field), with the CPU oracle on a bounded sample when the CPU leg runs
+    off_grid = None
+    if rank == 0 and world == 1 and not args.no_cascade:
+        from tools import potential_at_bench
+        off_grid = potential_at_bench.run(cpu_points=0 if args.no_cpu_baseline else 16)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -373,6 +379,7 @@ def run_gpu(args, world, rank, local):
             "clocks": clocks,
             "cpu_baseline": cpu_baseline,
             "nested_5_harmonic_solve": solve,
+            "evaluate_potential_at": off_grid,
         }
         print(json.dumps(line), flush=True)
     return 0
