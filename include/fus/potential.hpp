@@ -33,6 +33,8 @@ class GreenKernel {
   const VoxelGrid& grid() const { return grid_; }
   const Wavenumber& wavenumber() const { return k_; }
   Eigen::Vector3i padded() const;
+  // the device kernel (C-ABI handle) behind this GreenKernel
+  fusg_kernel* native() const { return handle_.get(); }
 
  private:
   VoxelGrid grid_;

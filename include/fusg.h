@@ -29,7 +29,8 @@ typedef enum fusg_status {
   FUSG_RUNTIME = 3,          /* std::runtime_error    */
   FUSG_CUDA = 4,             /* CUDA runtime failure  */
   FUSG_NCCL = 5,             /* NCCL failure          */
-  FUSG_OOM = 6               /* device allocation     */
+  FUSG_OOM = 6,              /* device allocation     */
+  FUSG_NOT_CONVERGED = 7     /* fus::ConvergenceError (GMRES; a std::runtime_error) */
 } fusg_status;
 
 /* VoxelGrid (include/fus/grid.hpp:30-50): covered box, spacing, voxel counts, harmonic. */
@@ -190,6 +191,43 @@ typedef struct fusg_cascade_desc {
 } fusg_cascade_desc;
 fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* desc, double* const* out_dev,
                              fusg_stage_timing* timings, double* source_normalization);
+
+/* ---------------------------------------------------------------- VIE mode
+ * SURVEY.md 8(f) rank 2 (src/vie.cpp). Fields are N complex128 device vectors on the kernel's
+ * grid; a medium map is N interleaved (c, beta) doubles (the raster order, x fastest). */
+/* MediumMap::wavenumber_contrast (src/vie.cpp:11-23): out = k_n(x)^2 - kbar_n^2 with
+ * k_n(x) = (n omega / c(x), Im kbar_n) where c != background c0, else 0. map_dev: device map. */
+fusg_status fusg_vie_contrast(fusg_ctx* ctx, const double* map_dev, int64_t count, const fusg_medium* background,
+                              double f0, int32_t n, double* out_dev, void* stream);
+/* vie_operator_apply (src/vie.cpp:133-139): out = p - V[contrast .* p]. */
+fusg_status fusg_vie_operator_apply(fusg_kernel* kernel, const double* contrast_dev, const double* p_dev,
+                                    double* out_dev, void* stream);
+/* gmres (src/vie.cpp:141-236) on device vectors with a caller operator: op(user, in, out)
+ * computes out = A in (device pointers, N complex128) and returns a status. x_dev receives the
+ * solution; the relative-residual history goes to history_host (up to history_capacity
+ * entries; history_len = full length). FUSG_NOT_CONVERGED past max_iter (history filled). */
+typedef fusg_status (*fusg_operator_fn)(void* user, const double* in_dev, double* out_dev);
+fusg_status fusg_gmres(fusg_ctx* ctx, fusg_operator_fn op, void* user, const double* rhs_dev, int64_t count,
+                       double tol, int32_t max_iter, int32_t restart, double* x_dev, double* history_host,
+                       int32_t history_capacity, int32_t* history_len, int32_t* iterations);
+/* solve_vie (src/vie.cpp:238-242): (I - V[contrast .]) x = rhs by restarted GMRES. */
+fusg_status fusg_solve_vie(fusg_kernel* kernel, const double* rhs_dev, const double* contrast_dev, double tol,
+                           int32_t max_iter, int32_t restart, double* x_dev, double* history_host,
+                           int32_t history_capacity, int32_t* history_len, int32_t* iterations);
+/* VieConfig (include/fus/vie.hpp:75-79). */
+typedef struct fusg_vie_config {
+  double tol;
+  int32_t max_iter, restart;
+} fusg_vie_config;
+/* run_cascade_inhomogeneous (src/vie.cpp:244-323): the master map (map_grid, map_host) is
+ * resampled onto every harmonic's grid; background supplies the wavenumbers and the source
+ * field. out_dev[n-1] receives p_n; timings[i-2] carries harmonic and voxels. */
+fusg_status fusg_run_cascade_inhomogeneous(fusg_ctx* ctx, const fusg_cascade_desc* desc, const fusg_grid* map_grid,
+                                           const double* map_host, const fusg_medium* background,
+                                           const fusg_vie_config* vie, double* const* out_dev,
+                                           fusg_stage_timing* timings, double* source_normalization);
+/* Device-to-device copy on the context stream, synchronous (for caller-supplied operators). */
+fusg_status fusg_device_copy(fusg_ctx* ctx, void* dst_dev, const void* src_dev, uint64_t bytes);
 
 /* ---------------------------------------------------------------- slab sharding
  * rank r of G owns z-planes [z0, z0+nz) of f and u (ragged split: the first

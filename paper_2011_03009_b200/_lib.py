@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # FUSG_LIB: alternative build of the same library (kernel-variant experiments in tools/)
 LIB_PATH = os.environ.get("FUSG_LIB") or os.path.join(_HERE, "libfusg.so")
 
-FUSG_OK, FUSG_INVALID_ARGUMENT, FUSG_OUT_OF_RANGE, FUSG_RUNTIME, FUSG_CUDA, FUSG_NCCL, FUSG_OOM = range(7)
+FUSG_OK, FUSG_INVALID_ARGUMENT, FUSG_OUT_OF_RANGE, FUSG_RUNTIME, FUSG_CUDA, FUSG_NCCL, FUSG_OOM, FUSG_NOT_CONVERGED = range(8)
 
 
 class FusgError(RuntimeError):
@@ -39,6 +39,13 @@ class Bowl(C.Structure):
     _fields_ = [("f0", C.c_double), ("focal_length", C.c_double), ("outer_radius", C.c_double),
                 ("power", C.c_double), ("n_points", C.c_int32),
                 ("points_host", C.POINTER(C.c_double))]
+
+
+OperatorFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class VieConfigC(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("restart", C.c_int32)]
 
 
 class StageTiming(C.Structure):
@@ -111,6 +118,16 @@ SIGNATURES = {
     "fusg_kernel_apply_slab": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp]),
     "fusg_kernel_apply_slab_loopback": (C.c_int, [C.POINTER(_vp), C.c_int32, C.POINTER(_vp),
                                                   C.POINTER(_vp), C.c_double]),
+    "fusg_vie_contrast": (C.c_int, [_vp, _vp, C.c_int64, C.POINTER(MediumC), C.c_double, C.c_int32, _vp, _vp]),
+    "fusg_vie_operator_apply": (C.c_int, [_vp, _vp, _vp, _vp, _vp]),
+    "fusg_gmres": (C.c_int, [_vp, OperatorFn, _vp, _vp, C.c_int64, C.c_double, C.c_int32, C.c_int32, _vp,
+                             C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fusg_solve_vie": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, _vp, C.POINTER(C.c_double),
+                                 C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fusg_run_cascade_inhomogeneous": (C.c_int, [_vp, C.POINTER(CascadeDesc), C.POINTER(Grid), _vp,
+                                                 C.POINTER(MediumC), C.POINTER(VieConfigC), C.POINTER(_vp),
+                                                 C.POINTER(StageTiming), C.POINTER(C.c_double)]),
+    "fusg_device_copy": (C.c_int, [_vp, _vp, _vp, C.c_uint64]),
     "fusg_slab_peer_plan": (C.c_int, [C.POINTER(Grid), C.c_int32, C.c_int32] + [C.POINTER(C.c_int64)] * 6),
     "fusg_kernel_slab_ipc_handles": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),
     "fusg_kernel_slab_attach_peers": (C.c_int, [_vp, C.POINTER(C.c_uint8)]),

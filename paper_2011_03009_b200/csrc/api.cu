@@ -8,22 +8,6 @@
 
 #include "internal.hpp"
 
-namespace fusg {
-fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s);
-fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
-                          double kre, double kim, double amp, double2* out, cudaStream_t s,
-                          double dmax);
-double distance_bound(const double* src_host, int n_src, const double lo[3], const double hi[3]);
-fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
-                            const fusg_grid& tgt, double2* out, cudaStream_t s);
-fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
-                    double2* out, cudaStream_t s);
-fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s);
-fusg_status radiated_power_dev(fusg_ctx* ctx, const double* src_dev, int n_src, double x_disc,
-                               double R, double kre, double kim, double amp, double rho0, double c0,
-                               int n_r, int n_theta, double* out_host, cudaStream_t s, double dmax);
-fusg_status check_monopole_flag(fusg_ctx* ctx, cudaStream_t s);
-}  // namespace fusg
 
 using namespace fusg;
 
@@ -90,6 +74,35 @@ struct EvTimer {
 };
 
 }  // namespace
+
+namespace fusg {
+// evaluate_source_field (src/transducer.cpp:198-206) into out on `grid`, sources already on
+// the device: power normalisation (power_scale_factor, :157-163) then the monopole sum, with
+// the coincidence check.  Returns k1, the normalisation (1 when power = 0) and the amplitude.
+fusg_status source_field_dev(fusg_ctx* ctx, const fusg_bowl& t, const fusg_medium& med, const double* src,
+                             const fusg_grid& grid, double2* out, fusg_wavenumber* k1, double* norm,
+                             double* amp1, cudaStream_t s) {
+  const double l = t.focal_length, R = t.outer_radius;
+  const double cap_area = 2.0 * M_PI * l * (l - std::sqrt(l * l - R * R));
+  const double x_disc = l - std::sqrt(l * l - R * R);
+  FUSG_TRY(fusg_complex_wavenumber(&med, t.f0, 1, k1));
+  double scale = 0.0;
+  if (t.power != 0.0) {
+    double pw = 0.0;
+    const double dlo[3] = {x_disc, -R, -R}, dhi[3] = {x_disc, R, R};
+    FUSG_TRY(radiated_power_dev(ctx, src, t.n_points, x_disc, R, k1->k_re, k1->k_im,
+                                1.0 * cap_area / double(t.n_points), med.rho0, med.c0, 384, 256, &pw, s,
+                                distance_bound(t.points_host, t.n_points, dlo, dhi)));
+    if (pw <= 0.0) return set_error(FUSG_RUNTIME, "power normalization: degenerate field, Pi(p) = 0");
+    scale = std::sqrt(t.power / pw);
+  }
+  *norm = scale > 0.0 ? scale : 1.0;
+  *amp1 = scale * cap_area / double(t.n_points);
+  FUSG_TRY(monopole_grid(ctx, src, t.n_points, grid, k1->k_re, k1->k_im, *amp1, out, s,
+                         distance_bound(t.points_host, t.n_points, grid.lo, grid.hi)));
+  return check_monopole_flag(ctx, s);
+}
+}  // namespace fusg
 
 extern "C" {
 
@@ -304,36 +317,16 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
   fusg_status st = upload_sources(t.points_host, t.n_points, &src, s);
   if (st != FUSG_OK) return st;
   std::unique_ptr<double, void (*)(double*)> src_guard(src, [](double* p) { cudaFree(p); });
-  const double l = t.focal_length, R = t.outer_radius;
-  const double cap_area = 2.0 * M_PI * l * (l - std::sqrt(l * l - R * R));
-  const double x_disc = l - std::sqrt(l * l - R * R);
 
   // p1 on the D_2 grid: evaluate_source_field (src/transducer.cpp:198-206)
   EvTimer tm(s);
   tm.start();
   fusg_wavenumber k1{};
-  st = fusg_complex_wavenumber(&med, t.f0, 1, &k1);
+  double norm = 1.0, amp1 = 0.0;
+  st = source_field_dev(ctx, t, med, src, grid_of(1), reinterpret_cast<double2*>(out_dev[0]), &k1, &norm,
+                        &amp1, s);
   if (st != FUSG_OK) return st;
-  double scale = 0.0;
-  if (t.power != 0.0) {  // power_scale_factor (src/transducer.cpp:157-163)
-    double pw = 0.0;
-    const double dlo[3] = {x_disc, -R, -R}, dhi[3] = {x_disc, R, R};
-    st = radiated_power_dev(ctx, src, t.n_points, x_disc, R, k1.k_re, k1.k_im,
-                            1.0 * cap_area / double(t.n_points), med.rho0, med.c0, 384, 256, &pw, s,
-                            distance_bound(t.points_host, t.n_points, dlo, dhi));
-    if (st != FUSG_OK) return st;
-    if (pw <= 0.0) return set_error(FUSG_RUNTIME, "power normalization: degenerate field, Pi(p) = 0");
-    scale = std::sqrt(t.power / pw);
-  }
-  const double norm = scale > 0.0 ? scale : 1.0;
   if (source_normalization) *source_normalization = norm;
-  const double amp1 = scale * cap_area / double(t.n_points);
-  st = monopole_grid(ctx, src, t.n_points, grid_of(1), k1.k_re, k1.k_im, amp1,
-                     reinterpret_cast<double2*>(out_dev[0]), s,
-                     distance_bound(t.points_host, t.n_points, grid_of(1).lo, grid_of(1).hi));
-  if (st != FUSG_OK) return st;
-  st = check_monopole_flag(ctx, s);
-  if (st != FUSG_OK) return st;
   const double p1_s = tm.stop();
   double peak = 0.0;
   st = max_abs_dev(ctx, reinterpret_cast<const double2*>(out_dev[0]), count_of(grid_of(1)), &peak, s);

@@ -20,10 +20,12 @@
 #include "fus/medium.hpp"
 #include "fus/potential.hpp"
 #include "fus/transducer.hpp"
+#include "fus/vie.hpp"
+#include "fus_api_detail.hpp"
 #include "fusg.h"
 
 namespace fus {
-namespace {
+namespace detail {
 
 void check(fusg_status st) {
   if (st == FUSG_OK) return;
@@ -48,19 +50,6 @@ fusg_ctx* ctx() {
   });
   return c;
 }
-
-// RAII device buffer
-struct DevBuf {
-  void* p = nullptr;
-  explicit DevBuf(size_t bytes) {
-    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
-  }
-  ~DevBuf() { cudaFree(p); }
-  DevBuf(DevBuf&& o) noexcept : p(o.p) { o.p = nullptr; }
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  double* d() const { return static_cast<double*>(p); }
-};
 
 DevBuf upload(const Eigen::VectorXcd& v) {
   DevBuf b(size_t(v.size()) * 16);
@@ -108,15 +97,8 @@ std::vector<double> flat_points(const std::vector<Eigen::Vector3d>& pts) {
   return f;
 }
 
-struct BowlC {
-  std::vector<double> pts;
-  fusg_bowl c{};
-  explicit BowlC(const BowlTransducer& t) : pts(flat_points(t.source_points)) {
-    c = {t.f0, t.focal_length, t.outer_radius, t.power, int32_t(t.source_points.size()), pts.data()};
-  }
-};
-
-}  // namespace
+}  // namespace detail
+using namespace detail;
 
 // ------------------------------------------------------------------------------ medium
 std::vector<std::string> Medium::validate() const {  // src/medium.cpp:11-23

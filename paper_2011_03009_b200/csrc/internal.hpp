@@ -140,3 +140,24 @@ void destroy_nccl(fusg_ctx* ctx);
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t st, cudaEvent_t* ev = nullptr);
 }  // namespace fusg
+
+namespace fusg {
+// device helpers of fields.cu / api.cu shared by the cascades (api.cu, vie.cu)
+fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s);
+fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
+                          double kre, double kim, double amp, double2* out, cudaStream_t s,
+                          double dmax);
+double distance_bound(const double* src_host, int n_src, const double lo[3], const double hi[3]);
+fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
+                            const fusg_grid& tgt, double2* out, cudaStream_t s);
+fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
+                    double2* out, cudaStream_t s);
+fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s);
+fusg_status radiated_power_dev(fusg_ctx* ctx, const double* src_dev, int n_src, double x_disc,
+                               double R, double kre, double kim, double amp, double rho0, double c0,
+                               int n_r, int n_theta, double* out_host, cudaStream_t s, double dmax);
+fusg_status check_monopole_flag(fusg_ctx* ctx, cudaStream_t s);
+fusg_status source_field_dev(fusg_ctx* ctx, const fusg_bowl& t, const fusg_medium& med, const double* src,
+                             const fusg_grid& grid, double2* out, fusg_wavenumber* k1, double* norm,
+                             double* amp1, cudaStream_t s);
+}  // namespace fusg

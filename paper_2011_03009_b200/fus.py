@@ -584,6 +584,197 @@ def run_cascade(cfg: CascadeConfig, ctx: Optional[Context] = None) -> CascadeRes
     return res
 
 
+# ------------------------------------------------------------------------ VIE mode
+# SURVEY.md 8(f) rank 2 (include/fus/vie.hpp, src/vie.cpp): heterogeneous media by a volume
+# integral equation solved with restarted GMRES, everything device resident.
+class ConvergenceError(RuntimeError):
+    """fus::ConvergenceError (include/fus/vie.hpp:60-65): carries the residual history."""
+
+    def __init__(self, what: str, residual_history):
+        super().__init__(what)
+        self.residual_history = list(residual_history)
+
+
+@dataclass
+class MediumMap:
+    """include/fus/vie.hpp:17-33: per-voxel sound speed and nonlinearity on a grid."""
+    grid: VoxelGrid
+    c: np.ndarray
+    beta: np.ndarray
+    background: Medium
+
+    def _packed(self, ctx) -> "torch.Tensor":  # (c, beta) interleaved, as one complex field
+        return _on_device(np.ascontiguousarray(self.c, float) + 1j * np.ascontiguousarray(self.beta, float), ctx)
+
+    def wavenumber_contrast(self, f0: float, n: int, ctx: Optional[Context] = None):
+        """src/vie.cpp:11-23 on the device; returns a CUDA tensor of N complex128."""
+        ctx = ctx or context()
+        m = self._packed(ctx)
+        out = torch.empty_like(m)
+        bg = self.background.c()
+        _sync_torch_to(ctx)
+        check(lib().fusg_vie_contrast(ctx.handle, m.data_ptr(), m.numel(), C.byref(bg), float(f0), int(n),
+                                      out.data_ptr(), None))
+        ctx.synchronize()
+        return out
+
+    def contrast_support(self, tol: float = 0.0) -> np.ndarray:
+        """src/vie.cpp:25-31"""
+        return np.nonzero((np.abs(self.c - self.background.c0) > tol) |
+                          (np.abs(self.beta - self.background.beta) > tol))[0]
+
+    def is_homogeneous(self) -> bool:
+        return self.contrast_support().size == 0
+
+    def resample(self, target: VoxelGrid, ctx: Optional[Context] = None) -> "MediumMap":
+        """src/vie.cpp:35-54: one trilinear pass over (c, beta) packed as a complex field."""
+        ctx = ctx or context()
+        r = interpolate(HarmonicField(self.grid, self._packed(ctx), None), target, ctx).values.cpu().numpy()
+        return MediumMap(target, r.real.copy(), r.imag.copy(), self.background)
+
+    def raster(self) -> np.ndarray:
+        """Interleaved (c, beta) doubles, x fastest (the C-ABI map layout)."""
+        out = np.empty(2 * self.c.size)
+        out[0::2], out[1::2] = self.c, self.beta
+        return out
+
+
+def homogeneous_map(grid: VoxelGrid, background: Medium) -> MediumMap:
+    """src/vie.cpp:56-63"""
+    n = grid.count()
+    return MediumMap(grid, np.full(n, background.c0), np.full(n, background.beta), background)
+
+
+def slab_map(grid: VoxelGrid, background: Medium, inclusion: Medium, x_center: float,
+             thickness: float) -> MediumMap:
+    """src/vie.cpp:65-81: the inclusion on voxels whose centre x lies in the closed slab."""
+    m = homogeneous_map(grid, background)
+    x0, x1 = x_center - thickness / 2.0, x_center + thickness / 2.0
+    xs = np.array([grid.center(ix, 0, 0)[0] for ix in range(grid.dims[0])])
+    inside = np.broadcast_to(((xs >= x0) & (xs <= x1))[None, None, :],
+                             (grid.dims[2], grid.dims[1], grid.dims[0])).reshape(-1)
+    m.c[inside] = inclusion.c0
+    m.beta[inside] = inclusion.beta
+    return m
+
+
+@dataclass
+class VieSolution:
+    field: "torch.Tensor"
+    residual_history: list
+    iterations: int = 0
+
+
+@dataclass
+class VieConfig:
+    tol: float = 1e-6
+    max_iter: int = 200
+    restart: int = 30
+
+
+def vie_operator_apply(fld, contrast, kernel: "GreenKernel"):
+    """src/vie.cpp:133-139: p - V_kbar[(k^2 - kbar^2) p]; returns a CUDA tensor."""
+    n = kernel._grid.count()
+    p, c = _on_device(fld, kernel.ctx), _on_device(contrast, kernel.ctx)
+    if p.numel() != n or c.numel() != n:
+        raise ValueError("vie_operator_apply: grid mismatch")
+    out = torch.empty_like(p)
+    _sync_torch_to(kernel.ctx)
+    check(lib().fusg_vie_operator_apply(kernel.handle, c.data_ptr(), p.data_ptr(), out.data_ptr(), None))
+    kernel.ctx.synchronize()
+    return out
+
+
+def _gmres_call(fn, args, n_hist):
+    hist = (C.c_double * n_hist)()
+    hl, it = C.c_int32(), C.c_int32()
+    st = fn(*args, hist, n_hist, C.byref(hl), C.byref(it))
+    h = [hist[i] for i in range(min(hl.value, n_hist))]
+    if st == _lib.FUSG_NOT_CONVERGED:
+        raise ConvergenceError(lib().fusg_last_error().decode(errors="replace"), h)
+    check(st)
+    return h, it.value
+
+
+def gmres(op, rhs, tol: float, max_iter: int, restart: int = 30, ctx: Optional[Context] = None) -> VieSolution:
+    """src/vie.cpp:141-236 on the device with a caller operator op(x) -> A x (CUDA tensors)."""
+    ctx = ctx or context()
+    b = _on_device(rhs, ctx)
+    x = torch.empty_like(b)
+    xin = torch.empty_like(b)
+    errors = []
+
+    def cb(_user, in_ptr, out_ptr):
+        try:
+            check(lib().fusg_device_copy(ctx.handle, xin.data_ptr(), in_ptr, 16 * b.numel()))
+            y = op(xin)
+            y = y.to(device=b.device, dtype=torch.complex128).contiguous()
+            torch.cuda.synchronize(b.device)
+            check(lib().fusg_device_copy(ctx.handle, out_ptr, y.data_ptr(), 16 * b.numel()))
+            return 0
+        except Exception as e:  # surfaced after the call
+            errors.append(e)
+            return _lib.FUSG_RUNTIME
+
+    fn = _lib.OperatorFn(cb)
+    _sync_torch_to(ctx)
+    try:
+        h, it = _gmres_call(lib().fusg_gmres, (ctx.handle, fn, None, b.data_ptr(), b.numel(), float(tol),
+                                               int(max_iter), int(restart), x.data_ptr()),
+                            int(max_iter) + int(max_iter) // max(1, int(restart)) + 4)
+    except Exception:
+        if errors:
+            raise errors[0]
+        raise
+    return VieSolution(x, h, it)
+
+
+def solve_vie(rhs, contrast, kernel: "GreenKernel", tol: float = 1e-6, max_iter: int = 200,
+              restart: int = 30) -> VieSolution:
+    """src/vie.cpp:238-242: (I - V[contrast .]) p = rhs by restarted GMRES, on the device."""
+    ctx = kernel.ctx
+    b, c = _on_device(rhs, ctx), _on_device(contrast, ctx)
+    if b.numel() != kernel._grid.count() or c.numel() != b.numel():
+        raise ValueError("solve_vie: grid mismatch")
+    x = torch.empty_like(b)
+    _sync_torch_to(ctx)
+    h, it = _gmres_call(lib().fusg_solve_vie, (kernel.handle, b.data_ptr(), c.data_ptr(), float(tol), int(max_iter),
+                                               int(restart), x.data_ptr()),
+                        int(max_iter) + int(max_iter) // max(1, int(restart)) + 4)
+    return VieSolution(x, h, it)
+
+
+def run_cascade_inhomogeneous(cfg: "CascadeConfig", master_map: MediumMap, vie: VieConfig = VieConfig(),
+                              ctx: Optional[Context] = None) -> "CascadeResult":
+    """src/vie.cpp:244-323, device resident (fusg_run_cascade_inhomogeneous)."""
+    ctx = ctx or context()
+    n = int(cfg.n_harmonics)
+    if n < 1:
+        raise ValueError("run_cascade_inhomogeneous: n_harmonics must be >= 1")
+    grids = [cfg.plan.for_harmonic(i).grid for i in range(2, max(n, 2) + 1)]
+    cg = (_lib.Grid * len(grids))(*[g.c() for g in grids])
+    dev = f"cuda:{ctx.device}"
+    outs = [torch.empty(grids[max(i - 1, 0)].count(), dtype=torch.complex128, device=dev) for i in range(n)]
+    ptrs = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    rows = (_lib.StageTiming * max(1, n - 1))()
+    norm = C.c_double()
+    desc = _lib.CascadeDesc(cfg.medium.c(), cfg.transducer.c(), cg, n, int(cfg.recompute_p1_each_grid),
+                            int(cfg.pad_small_primes))
+    mg, bg = master_map.grid.c(), master_map.background.c()
+    raster = np.ascontiguousarray(master_map.raster())
+    vc = _lib.VieConfigC(float(vie.tol), int(vie.max_iter), int(vie.restart))
+    _sync_torch_to(ctx)
+    check(lib().fusg_run_cascade_inhomogeneous(ctx.handle, C.byref(desc), C.byref(mg), raster.ctypes.data,
+                                               C.byref(bg), C.byref(vc), ptrs, rows, C.byref(norm)))
+    res = CascadeResult(source_normalization=norm.value)
+    for i in range(n):
+        k = complex_wavenumber(master_map.background, cfg.transducer.f0, i + 1)
+        res.harmonics.append(HarmonicField(grids[max(i - 1, 0)], outs[i], k))
+    for r in list(rows)[:n - 1]:
+        res.timings.append(StageTiming(r.harmonic, int(r.voxels), 0.0, 0.0, 0.0, 0.0, 0.0, 0.0))
+    return res
+
+
 # ------------------------------------------------------------------------ slab sharding
 def slab_range(n: int, nranks: int, rank: int):
     """(begin, count) of rank's share of n (ragged: the first n % nranks ranks take one more)."""

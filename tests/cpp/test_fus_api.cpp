@@ -16,6 +16,7 @@
 #include "fus/medium.hpp"
 #include "fus/potential.hpp"
 #include "fus/transducer.hpp"
+#include "fus/vie.hpp"
 
 static int g_fail = 0, g_pass = 0;
 #define CHECK(cond)                                                           \
@@ -178,6 +179,63 @@ void device_cases() {
         fus::evaluate_potential_at(k2, g, f, {g.center(3, 2, 2) + Eigen::Vector3d(3e-5, 0, 0)});
     CHECK(std::isfinite(std::abs(w[0])));
     CHECK_THROWS_AS(fus::evaluate_potential_at(k2, g, Eigen::VectorXcd(3), pts), std::invalid_argument);
+  }
+  // VIE mode, tests/test_vie.cpp:105-213 through the drop-in
+  {
+    const int n = 48;
+    std::mt19937 rng(7);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    std::vector<std::complex<double>> A(std::size_t(n) * n);  // dense, row-major
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) A[std::size_t(i) * n + j] = std::complex<double>(u(rng), u(rng)) * 0.1;
+    for (int i = 0; i < n; ++i) A[std::size_t(i) * n + i] += 3.0;
+    auto matvec = [](const std::vector<std::complex<double>>& M, int m, const Eigen::VectorXcd& x) {
+      Eigen::VectorXcd y = Eigen::VectorXcd::Zero(m);
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) y[i] += M[std::size_t(i) * m + j] * x[j];
+      return y;
+    };
+    const Eigen::VectorXcd b = random_vector(n, 9);
+    const fus::VieSolution sol =
+        fus::gmres([&](const Eigen::VectorXcd& x) { return matvec(A, n, x); }, b, 1e-12, 500, 20);
+    CHECK((matvec(A, n, sol.field) - b).norm() < 1e-11 * b.norm());
+    CHECK(!sol.residual_history.empty() && sol.residual_history.back() < 1e-12);
+    std::vector<std::complex<double>> S(64 * 64, 0.0);
+    for (int i = 0; i < 64; ++i) S[std::size_t(i) * 64 + (i + 1) % 64] = 1.0;
+    Eigen::VectorXcd e0 = Eigen::VectorXcd::Zero(64);
+    e0[0] = 1.0;
+    bool threw = false;
+    try {
+      fus::gmres([&](const Eigen::VectorXcd& x) { return matvec(S, 64, x); }, e0, 1e-14, 3, 3);
+    } catch (const fus::ConvergenceError& e) {
+      threw = !e.residual_history.empty();
+    }
+    CHECK(threw);
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {3e-3, 3e-3, 3e-3}}, 0.3e-3, 1);
+    const fus::Wavenumber k1 = fus::complex_wavenumber(kWater, 1.1e6, 1);
+    const Eigen::VectorXcd rhs = random_vector(g.count(), 11);
+    const fus::VieSolution z =
+        fus::solve_vie(rhs, Eigen::VectorXcd::Zero(Eigen::Index(g.count())), fus::GreenKernel(g, k1), 1e-10);
+    CHECK(max_abs(z.field - rhs) < 1e-10 * max_abs(rhs) && z.iterations <= 1);
+    fus::CascadeConfig cfg;
+    cfg.medium = kWater;
+    cfg.transducer = fus::transducer_preset("H131", 15.0, 128);
+    cfg.transducer.f0 = 0.25e6;
+    cfg.plan = fus::plan_nested_meshes(cfg.transducer, cfg.medium, 6e-3, 3, 3, 0.35);
+    cfg.n_harmonics = 3;
+    const fus::CascadeResult homo = fus::run_cascade(cfg);
+    fus::VieConfig vie;
+    vie.tol = 1e-8;
+    const fus::CascadeResult inhomo =
+        fus::run_cascade_inhomogeneous(cfg, fus::homogeneous_map(cfg.plan.for_harmonic(2).grid, kWater), vie);
+    for (int h = 1; h <= 3; ++h)
+      CHECK((inhomo.p(h).values - homo.p(h).values).norm() / homo.p(h).values.norm() < 1e-6);
+    const fus::MediumMap slab = fus::slab_map(cfg.plan.for_harmonic(2).grid, kWater,
+                                              fus::medium_preset("liver"), 20e-3, 4e-3);
+    CHECK(!slab.is_homogeneous());
+    const fus::CascadeResult ws = fus::run_cascade_inhomogeneous(cfg, slab);
+    const double rel = (ws.p(1).values - homo.p(1).values).norm() / homo.p(1).values.norm();
+    CHECK(rel > 1e-3 && rel < 0.5);
   }
   // rhs coefficients, tests/test_cascade.cpp:33-63
   {

@@ -16,6 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     text = open(os.path.join(ROOT, "include", "fusg.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    text = re.sub(r"typedef[^;]*;", "", text)  # types (incl. function-pointer typedefs) are not symbols
     return sorted(set(re.findall(r"\b(fusg_[a-z0-9_]+)\s*\(", text)))
 
 
