@@ -161,6 +161,13 @@ fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t 
 fusg_status fusg_evaluate_potential_at(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenumber* k,
                                        const double* f_dev, const double* pts_host, int64_t n_pts,
                                        double* out_host);
+/* shrink_domain_by_threshold (src/grid.cpp:114-139): index box [lo, hi] of the voxels with
+ * |f| >= max|f| 10^q0 (q0 >= 0: the maximum only); the DomainBox is lo + idx dx,
+ * lo + (hi + 1) dx. FUSG_INVALID_ARGUMENT for an identically zero field. */
+fusg_status fusg_field_threshold_box(fusg_ctx* ctx, const fusg_grid* grid, const double* f_dev, double q0,
+                                     int32_t lo_idx[3], int32_t hi_idx[3], double* max_abs_out);
+/* localisedness_map (src/analysis.cpp:80-90): q_dev[i] = log10(|f_i| / max|f|), -inf where f_i = 0. */
+fusg_status fusg_localisedness_map(fusg_ctx* ctx, const double* f_dev, int64_t count, double* q_dev);
 /* radiated_power (src/transducer.cpp:134-155): deterministic fixed-order reduction. */
 fusg_status fusg_radiated_power(fusg_ctx* ctx, const double* src_host, int32_t n_src,
                                 double x_disc, double R, double k_re, double k_im, double amp,

@@ -96,6 +96,9 @@ SIGNATURES = {
     "fusg_monopole_points": (C.c_int, [_vp, _dp, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double,
                                        C.c_double, _vp, _vp]),
     "fusg_evaluate_potential_at": (C.c_int, [_vp, C.POINTER(Grid), C.POINTER(Wave), _vp, _vp, C.c_int64, _vp]),
+    "fusg_field_threshold_box": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.c_double, C.POINTER(C.c_int32),
+                                           C.POINTER(C.c_int32), C.POINTER(C.c_double)]),
+    "fusg_localisedness_map": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "fusg_radiated_power": (C.c_int, [_vp, _dp, C.c_int32, C.c_double, C.c_double, C.c_double,
                                       C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32,
                                       C.c_int32, _dp]),

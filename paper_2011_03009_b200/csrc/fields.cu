@@ -9,6 +9,8 @@
 //    and gather kernels written with explicit round-to-nearest intrinsics, so they round
 //    exactly like the reference's non-FMA x86-64 build (bit-identical outputs).
 #include <algorithm>
+#include <climits>
+#include <math_constants.h>
 #include <cmath>
 #include <vector>
 
@@ -472,6 +474,55 @@ __global__ void max_abs_kernel(const double2* __restrict__ v, int64_t n, unsigne
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// shrink_domain_by_threshold (src/grid.cpp:114-139): index bounding box of |f| >= threshold;
+// block min/max reduction then one atomic per block (order independent: exact)
+__global__ void threshold_box_kernel(GridDev g, const double2* __restrict__ f, double thr, int* __restrict__ box) {
+  __shared__ int red[6][256];
+  int lo[3] = {INT_MAX, INT_MAX, INT_MAX}, hi[3] = {-1, -1, -1};
+  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+    if (hypot(f[i].x, f[i].y) >= thr) {
+      const int ix = int(i % g.dims[0]);
+      const int64_t r = i / g.dims[0];
+      const int ii[3] = {ix, int(r % g.dims[1]), int(r / g.dims[1])};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = min(lo[a], ii[a]);
+        hi[a] = max(hi[a], ii[a]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    red[a][threadIdx.x] = lo[a];
+    red[3 + a][threadIdx.x] = hi[a];
+  }
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        red[a][threadIdx.x] = min(red[a][threadIdx.x], red[a][threadIdx.x + w]);
+        red[3 + a][threadIdx.x] = max(red[3 + a][threadIdx.x], red[3 + a][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&box[a], red[a][0]);
+      atomicMax(&box[3 + a], red[3 + a][0]);
+    }
+}
+
+// localisedness_map (src/analysis.cpp:80-90): log10(|f| / max|f|), -inf for zero voxels
+__global__ void localisedness_kernel(const double2* __restrict__ f, int64_t n, double max_abs, double* __restrict__ q) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double a = hypot(f[i].x, f[i].y);
+    q[i] = a > 0.0 ? log10(a / max_abs) : -CUDART_INF;
+  }
+}
+
 // ---------------------------------------------------------------------------- launchers
 // Attenuation mode for a launch: 0 if Im k == 0; 1 if Im k * dmax <= kPolyAttMax (dmax bounds
 // every source-target distance); else 2.
@@ -715,6 +766,53 @@ fusg_status fusg_evaluate_potential_at(fusg_ctx* ctx, const fusg_grid* grid, con
   cudaFreeAsync(pts, s);
   cudaFreeAsync(partial, s);
   cudaFreeAsync(out, s);
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  return FUSG_OK;
+}
+
+fusg_status fusg_field_threshold_box(fusg_ctx* ctx, const fusg_grid* grid, const double* f_dev, double q0,
+                                     int32_t lo_idx[3], int32_t hi_idx[3], double* max_abs_out) {
+  if (!ctx || !grid || !f_dev || !lo_idx || !hi_idx)
+    return set_error(FUSG_INVALID_ARGUMENT, "threshold_box: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const GridDev g = to_dev(*grid);
+  const int64_t count = int64_t(g.dims[0]) * g.dims[1] * g.dims[2];
+  double m = 0.0;
+  FUSG_TRY(max_abs_dev(ctx, reinterpret_cast<const double2*>(f_dev), count, &m, s));
+  if (max_abs_out) *max_abs_out = m;
+  if (m <= 0.0) return set_error(FUSG_INVALID_ARGUMENT, "shrink_domain_by_threshold: field is identically zero");
+  const double thr = (q0 >= 0.0) ? m : m * std::pow(10.0, q0);  // q0 >= 0 keeps only the maximum
+  int* box = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&box, 6 * sizeof(int), s));
+  const int init[6] = {INT_MAX, INT_MAX, INT_MAX, -1, -1, -1};
+  FUSG_CUDA_TRY(cudaMemcpyAsync(box, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  threshold_box_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(g, reinterpret_cast<const double2*>(f_dev),
+                                                                            thr, box);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("threshold_box_kernel");
+  int h[6];
+  FUSG_CUDA_TRY(cudaMemcpyAsync(h, box, sizeof(h), cudaMemcpyDeviceToHost, s));
+  FUSG_CUDA_TRY(cudaFreeAsync(box, s));
+  FUSG_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int a = 0; a < 3; ++a) {
+    lo_idx[a] = h[a];
+    hi_idx[a] = h[3 + a];
+  }
+  return FUSG_OK;
+}
+
+fusg_status fusg_localisedness_map(fusg_ctx* ctx, const double* f_dev, int64_t count, double* q_dev) {
+  if (!ctx || (count > 0 && (!f_dev || !q_dev))) return set_error(FUSG_INVALID_ARGUMENT, "localisedness_map: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  double m = 0.0;
+  FUSG_TRY(max_abs_dev(ctx, reinterpret_cast<const double2*>(f_dev), count, &m, s));
+  if (m <= 0.0) return set_error(FUSG_INVALID_ARGUMENT, "localisedness_map: field is identically zero");
+  localisedness_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(reinterpret_cast<const double2*>(f_dev),
+                                                                           count, m, q_dev);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("localisedness_kernel");
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return FUSG_OK;
 }
