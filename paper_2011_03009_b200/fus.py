@@ -775,6 +775,213 @@ def run_cascade_inhomogeneous(cfg: "CascadeConfig", master_map: MediumMap, vie: 
     return res
 
 
+# ------------------------------------------------------------------------ analysis
+# SURVEY.md 8(f) rank 4 and the reference's studies (include/fus/analysis.hpp, src/analysis.cpp):
+# the O(N M) off-grid evaluations, sources, transfers and reductions run on the device; the
+# profile arithmetic (a few hundred nodes) is host numpy like the reference's.
+@dataclass
+class OnAxisProfile:
+    """include/fus/analysis.hpp:12-16"""
+    x: np.ndarray
+    p: np.ndarray
+    harmonic: int = 1
+
+
+@dataclass
+class ConvergenceRecord:
+    """include/fus/analysis.hpp:18-23"""
+    harmonic: int
+    control: str
+    value: float
+    error_percent: float
+
+
+@dataclass
+class QuadratureStudy:
+    records: List[ConvergenceRecord] = field(default_factory=list)
+    slope: float = 0.0
+
+
+def _axis_weights(lo: float, dx: float, n: int):  # src/analysis.cpp:13-23
+    q = (0.0 - lo) / dx - 0.5
+    j0 = int(math.floor(q))
+    j0 = 0 if j0 < 0 else j0
+    if j0 > n - 2:
+        j0 = max(0, n - 2)
+    t = q - j0
+    t = 0.0 if t < 0.0 else t
+    if t > 1.0:
+        t = 1.0 if n > 1 else 0.0
+    return j0, t
+
+
+def extract_on_axis(fld: HarmonicField) -> OnAxisProfile:
+    """src/analysis.cpp:49-68: the two straddling columns in y and z with linear weights."""
+    g = fld.grid
+    jy, ty = _axis_weights(g.lo[1], g.dx, g.dims[1])
+    jz, tz = _axis_weights(g.lo[2], g.dx, g.dims[2])
+    jy1, jz1 = min(jy + 1, g.dims[1] - 1), min(jz + 1, g.dims[2] - 1)
+    v = fld.values.reshape(g.dims[2], g.dims[1], g.dims[0]) if torch is not None and isinstance(
+        fld.values, torch.Tensor) else np.asarray(fld.values).reshape(g.dims[2], g.dims[1], g.dims[0])
+    rows = [v[jz, jy], v[jz, jy1], v[jz1, jy], v[jz1, jy1]]
+    rows = [r.cpu().numpy() if hasattr(r, "cpu") else np.asarray(r) for r in rows]
+    x = np.array([g.lo[0] + (ix + 0.5) * g.dx for ix in range(g.dims[0])])
+    p = ((1.0 - ty) * (1.0 - tz) * rows[0] + ty * (1.0 - tz) * rows[1] + (1.0 - ty) * tz * rows[2] +
+         ty * tz * rows[3])
+    h = fld.wavenumber.harmonic if fld.wavenumber is not None else 1
+    return OnAxisProfile(x, p, h)
+
+
+def resample_profile(prof: OnAxisProfile, nodes) -> np.ndarray:
+    """src/analysis.cpp:27-45 (linear, clamped at the ends)."""
+    px, pp = prof.x, prof.p
+    out = np.empty(len(nodes), np.complex128)
+    for i, xv in enumerate(nodes):
+        if xv <= px[0]:
+            out[i] = pp[0]
+        elif xv >= px[-1]:
+            out[i] = pp[-1]
+        else:
+            j = int((xv - px[0]) / (px[1] - px[0]))
+            while j + 1 < len(px) and px[j + 1] < xv:
+                j += 1
+            while j > 0 and px[j] > xv:
+                j -= 1
+            t = (xv - px[j]) / (px[j + 1] - px[j])
+            out[i] = (1.0 - t) * pp[j] + t * pp[j + 1]
+    return out
+
+
+def on_axis_error(p: OnAxisProfile, p_ref: OnAxisProfile, normalizer: OnAxisProfile) -> float:
+    """src/analysis.cpp:70-78: 100 ||p - p_ref|| / ||normalizer|| on the reference nodes."""
+    a = resample_profile(p, p_ref.x)
+    denom = float(np.linalg.norm(resample_profile(normalizer, p_ref.x)))
+    if denom == 0.0:
+        raise ValueError("on_axis_error: normalizer has zero norm")
+    return 100.0 * float(np.linalg.norm(a - p_ref.p)) / denom
+
+
+def localisedness_map(fld: HarmonicField, ctx: Optional[Context] = None):
+    """src/analysis.cpp:80-90 on the device; returns a CUDA float64 tensor."""
+    ctx = ctx or context()
+    v = _on_device(fld.values, ctx)
+    q = torch.empty(v.numel(), dtype=torch.float64, device=v.device)
+    _sync_torch_to(ctx)
+    check(lib().fusg_localisedness_map(ctx.handle, v.data_ptr(), v.numel(), q.data_ptr()))
+    return q
+
+
+def shrink_domain_by_threshold(fld: HarmonicField, q0: float, ctx: Optional[Context] = None):
+    """src/grid.cpp:114-139 on the device -> (lo, hi) of the tightest box holding
+    |f| >= max|f| 10^q0."""
+    ctx = ctx or context()
+    v = _on_device(fld.values, ctx)
+    g = fld.grid.c()
+    lo, hi, m = (C.c_int32 * 3)(), (C.c_int32 * 3)(), C.c_double()
+    _sync_torch_to(ctx)
+    check(lib().fusg_field_threshold_box(ctx.handle, C.byref(g), v.data_ptr(), float(q0), lo, hi, C.byref(m)))
+    gl = np.asarray(fld.grid.lo, float)
+    return gl + np.array(lo[:]) * fld.grid.dx, gl + (np.array(hi[:]) + 1) * fld.grid.dx
+
+
+def error_trend_diagnostic(p_i: OnAxisProfile, p1: OnAxisProfile, q0: float) -> float:
+    """src/analysis.cpp:243-246"""
+    return 10.0 * (np.linalg.norm(resample_profile(p_i, p1.x)) / np.linalg.norm(p1.p)) * math.sqrt(abs(q0))
+
+
+def _axis_nodes(x):
+    return np.stack([x, np.zeros_like(x), np.zeros_like(x)], 1)
+
+
+def quadrature_convergence_study(t: BowlTransducer, m: Medium, domain_lo, domain_hi, n_w_values, n_w_ref: int,
+                                 ctx: Optional[Context] = None) -> QuadratureStudy:
+    """src/analysis.cpp:92-162: p2 at each n_w evaluated at the n_w_ref solution's axis nodes
+    through the potential representation (the reference's criterion 1), on the device."""
+    ctx = ctx or context()
+    for nw in n_w_values:
+        if nw >= n_w_ref:
+            raise ValueError("quadrature_convergence_study: n_w_ref must exceed all n_w")
+    lambda1 = m.c0 / t.f0
+    k1, k2 = complex_wavenumber(m, t.f0, 1), complex_wavenumber(m, t.f0, 2)
+    scale = power_scale_factor(t, m, k1)
+
+    def source(nw):
+        grid = make_grid(domain_lo, domain_hi, lambda1 / (2.0 * nw), 2)
+        p1 = evaluate_first_harmonic(t, m, grid, scale, ctx)
+        return grid, rhs_source(2, [p1], m, k2.omega, ctx)
+
+    g, f = source(n_w_ref)
+    ref_x = np.array([g.lo[0] + (ix + 0.5) * g.dx for ix in range(g.dims[0])])
+    nodes = _axis_nodes(ref_x)
+    ref = OnAxisProfile(ref_x, -evaluate_potential_at(k2, g, f, nodes, ctx), 2)
+    study = QuadratureStudy()
+    sx = sy = sxx = sxy = 0.0
+    fitted = 0
+    for nw in n_w_values:
+        g, f = source(nw)
+        prof = OnAxisProfile(ref_x, -evaluate_potential_at(k2, g, f, nodes, ctx), 2)
+        err = on_axis_error(prof, ref, ref)
+        study.records.append(ConvergenceRecord(2, "n_w", float(nw), err))
+        if err > 0.0:
+            lx, ly = math.log(float(nw)), math.log(err)
+            sx, sy, sxx, sxy = sx + lx, sy + ly, sxx + lx * lx, sxy + lx * ly
+            fitted += 1
+    if fitted >= 2:
+        study.slope = (fitted * sxy - sx * sy) / (fitted * sxx - sx * sx)
+    return study
+
+
+def plan_full_domain(t: BowlTransducer, m: Medium, d: float, n_w: int, n_harmonics: int,
+                     width_scale: float = 1.0) -> "MeshPlan":
+    """src/analysis.cpp:164-174: every harmonic keeps the D_2 domain at its own resolution."""
+    plan = plan_nested_meshes(t, m, d, n_w, n_harmonics, width_scale)
+    d2lo, d2hi = np.array(plan.grids[0].domain_lo, float), np.array(plan.grids[0].domain_hi, float)
+    lambda1 = m.c0 / t.f0
+    for pg in plan.grids:
+        pg.domain_lo, pg.domain_hi = d2lo.copy(), d2hi.copy()
+        pg.grid = make_grid(d2lo, d2hi, lambda1 / (pg.harmonic * n_w), pg.harmonic, plan.focus)
+    return plan
+
+
+def domain_shrink_study(cfg: "CascadeConfig", reference: "CascadeResult", levels, q0_mode: bool,
+                        ctx: Optional[Context] = None) -> List[ConvergenceRecord]:
+    """src/analysis.cpp:176-241 on the device (transfers, sources, off-grid evaluation)."""
+    ctx = ctx or context()
+    medium, t, plan = cfg.medium, cfg.transducer, cfg.plan
+    lambda1 = medium.c0 / t.f0
+    focus = np.asarray(plan.focus, float)
+    p1_ref = extract_on_axis(reference.p(1))
+    records = []
+    for i in range(2, cfg.n_harmonics + 1):
+        pi_ref = extract_on_axis(reference.p(i))
+        full = plan.for_harmonic(i)
+        ki = complex_wavenumber(medium, t.f0, i)
+        integrand = None
+        if q0_mode:
+            lower = [reference.p(mm) if _same_grid(reference.p(mm).grid, full.grid)
+                     else interpolate(reference.p(mm), full.grid, ctx) for mm in range(1, i)]
+            integrand = HarmonicField(full.grid, rhs_source(i, lower, medium, ki.omega, ctx), ki)
+        for level in levels:
+            if q0_mode:
+                lo, hi = shrink_domain_by_threshold(integrand, level, ctx)
+            else:
+                L = focus[0] - full.domain_lo[0]
+                w = full.domain_hi[1]
+                lo = np.array([focus[0] - level * L, -level * w, -level * w])
+                hi = np.array([full.domain_hi[0], level * w, level * w])
+            grid = make_grid(lo, hi, lambda1 / (i * plan.n_w), i, focus)
+            lower = [interpolate(reference.p(mm), grid, ctx) for mm in range(1, i)]
+            f = rhs_source(i, lower, medium, ki.omega, ctx)
+            prof = OnAxisProfile(pi_ref.x, -evaluate_potential_at(ki, grid, f, _axis_nodes(pi_ref.x), ctx), i)
+            records.append(ConvergenceRecord(i, "Q0" if q0_mode else "fraction", float(level),
+                                             on_axis_error(prof, pi_ref, p1_ref)))
+    return records
+
+
+def _same_grid(a: VoxelGrid, b: VoxelGrid) -> bool:
+    return tuple(a.dims) == tuple(b.dims) and np.array_equal(np.asarray(a.lo), np.asarray(b.lo))
+
+
 # ------------------------------------------------------------------------ slab sharding
 def slab_range(n: int, nranks: int, rank: int):
     """(begin, count) of rank's share of n (ragged: the first n % nranks ranks take one more)."""
