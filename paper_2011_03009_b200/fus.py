@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass, field, replace
 from typing import List, Optional, Sequence
 
@@ -980,6 +981,98 @@ def domain_shrink_study(cfg: "CascadeConfig", reference: "CascadeResult", levels
 
 def _same_grid(a: VoxelGrid, b: VoxelGrid) -> bool:
     return tuple(a.dims) == tuple(b.dims) and np.array_equal(np.asarray(a.lo), np.asarray(b.lo))
+
+
+# ------------------------------------------------------------------------ file formats
+# include/fus/io.hpp contracts (src/io.cpp) and the medium-map rasters (include/fus/vie.hpp:42-46)
+def _num(v: float) -> str:  # the reference's std::setprecision(17) general notation
+    return format(float(v), ".17g")
+
+
+def parse_key_value_file(path: str) -> dict:
+    """'key = value' lines, '#' comments; RuntimeError with the line number when malformed."""
+    try:
+        lines = open(path).read().splitlines()
+    except OSError:
+        raise RuntimeError(f"cannot open config file '{path}'")
+    kv = {}
+    for n, line in enumerate(lines, 1):
+        t = line.strip(" \t\r")
+        if not t or t.startswith("#"):
+            continue
+        if "=" not in t:
+            raise RuntimeError(f"{path}:{n}: expected 'key = value'")
+        key, value = t.split("=", 1)
+        key = key.strip(" \t\r")
+        if not key:
+            raise RuntimeError(f"{path}:{n}: empty key")
+        kv[key] = value.strip(" \t\r")
+    return kv
+
+
+def require_string(kv: dict, key: str, context: str) -> str:
+    if key not in kv:
+        raise RuntimeError(f"{context}: missing required key '{key}'")
+    return kv[key]
+
+
+def require_double(kv: dict, key: str, context: str) -> float:
+    s = require_string(kv, key, context)
+    try:
+        return float(s)
+    except ValueError:
+        raise RuntimeError(f"{context}: key '{key}' is not a number: '{s}'")
+
+
+def write_on_axis_csv(path: str, x, p) -> None:
+    with open(path, "w") as out:
+        out.write("x_m,re_Pa,im_Pa,abs_Pa\n")
+        for xv, pv in zip(np.asarray(x, float), np.asarray(p, complex)):
+            out.write(f"{_num(xv)},{_num(pv.real)},{_num(pv.imag)},{_num(abs(pv))}\n")
+
+
+def write_field_dump(path: str, fld: HarmonicField) -> None:
+    v = fld.values.cpu().numpy() if hasattr(fld.values, "cpu") else np.asarray(fld.values)
+    np.ascontiguousarray(v, "<c16").tofile(path)
+    g, k = fld.grid, fld.wavenumber
+    with open(path + ".hdr", "w") as h:
+        h.write(f"nx = {g.dims[0]}\nny = {g.dims[1]}\nnz = {g.dims[2]}\ndx = {_num(g.dx)}\n"
+                f"origin_x = {_num(g.lo[0])}\norigin_y = {_num(g.lo[1])}\norigin_z = {_num(g.lo[2])}\n"
+                f"harmonic = {k.harmonic}\nk_re = {_num(k.k.real)}\nk_im = {_num(k.k.imag)}\n"
+                "layout = x_fastest_complex_f64_le\n")
+
+
+def write_csv(path: str, columns, rows) -> None:
+    with open(path, "w") as out:
+        out.write(",".join(columns) + "\n")
+        for row in rows:
+            out.write(",".join(_num(v) for v in row) + "\n")
+
+
+def load_medium_map(header_path: str, background: Medium) -> MediumMap:
+    kv = parse_key_value_file(header_path)
+    dims = tuple(int(require_double(kv, a, header_path)) for a in ("nx", "ny", "nz"))
+    dx = require_double(kv, "dx", header_path)
+    lo = np.array([require_double(kv, f"origin_{a}", header_path) for a in "xyz"])
+    raster = os.path.join(os.path.dirname(header_path), require_string(kv, "raster", header_path))
+    n = dims[0] * dims[1] * dims[2]
+    try:
+        data = np.fromfile(raster, "<f8")
+    except OSError:
+        raise RuntimeError(f"cannot open medium-map raster '{raster}'")
+    if data.size < 2 * n:
+        raise RuntimeError(f"medium-map raster '{raster}' is truncated")
+    g = VoxelGrid(lo, lo + np.array(dims) * dx, dx, dims, 1)
+    return MediumMap(g, data[0:2 * n:2].copy(), data[1:2 * n:2].copy(), background)
+
+
+def write_medium_map(header_path: str, raster_path: str, m: MediumMap) -> None:
+    g = m.grid
+    with open(header_path, "w") as h:
+        h.write(f"nx = {g.dims[0]}\nny = {g.dims[1]}\nnz = {g.dims[2]}\ndx = {_num(g.dx)}\n"
+                f"origin_x = {_num(g.lo[0])}\norigin_y = {_num(g.lo[1])}\norigin_z = {_num(g.lo[2])}\n"
+                f"raster = {os.path.basename(raster_path)}\n")
+    m.raster().astype("<f8").tofile(raster_path)
 
 
 # ------------------------------------------------------------------------ slab sharding

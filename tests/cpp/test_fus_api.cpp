@@ -17,6 +17,9 @@
 #include "fus/potential.hpp"
 #include "fus/transducer.hpp"
 #include "fus/vie.hpp"
+#include "fus/io.hpp"
+#include <fstream>
+#include <map>
 
 static int g_fail = 0, g_pass = 0;
 #define CHECK(cond)                                                           \
@@ -117,6 +120,85 @@ void host_cases() {
   CHECK_THROWS_AS(fus::medium_preset("granite"), std::invalid_argument);
   // tests/test_potential.cpp:40-46
   CHECK(std::fabs(fus::equivalent_sphere_radius(1.0) - 0.6203504908994001) < 1e-12);
+}
+
+// tests/test_io.cpp: parser, CSVs, field dump round trip; medium-map raster round trip
+void io_cases() {
+  {
+    std::ofstream("t_kv.txt") << "# comment\n\n  key1 = 7.5  \nkey2=text value\n";
+    const auto kv = fus::parse_key_value_file("t_kv.txt");
+    CHECK(kv.size() == 2);
+    CHECK(fus::require_double(kv, "key1", "test") == 7.5);
+    CHECK(fus::require_string(kv, "key2", "test") == "text value");
+    CHECK_THROWS_AS(fus::require_double(kv, "missing", "test"), std::runtime_error);
+    CHECK_THROWS_AS(fus::require_double(kv, "key2", "test"), std::runtime_error);
+    std::ofstream("t_bad.txt") << "ok = 1\nno equals sign here\n";
+    bool line2 = false;
+    try {
+      fus::parse_key_value_file("t_bad.txt");
+    } catch (const std::runtime_error& e) {
+      line2 = std::string(e.what()).find(":2") != std::string::npos;
+    }
+    CHECK(line2);
+    CHECK_THROWS_AS(fus::parse_key_value_file("no_such_file_anywhere.txt"), std::runtime_error);
+  }
+  {
+    Eigen::VectorXd x(2);
+    x[0] = 0.01;
+    x[1] = 0.02;
+    Eigen::VectorXcd p(2);
+    p[0] = std::complex<double>(3, 4);
+    p[1] = std::complex<double>(1, 0);
+    fus::write_on_axis_csv("t_axis.csv", x, p);
+    std::ifstream in("t_axis.csv");
+    std::string header, row1;
+    std::getline(in, header);
+    std::getline(in, row1);
+    CHECK(header == "x_m,re_Pa,im_Pa,abs_Pa");
+    CHECK(row1.substr(0, 5) == "0.01," && row1.find(",5") != std::string::npos);
+  }
+  {
+    fus::HarmonicField f;
+    f.grid = fus::make_grid({{0, 0, 0}, {3e-4, 2e-4, 2e-4}}, 1e-4, 2);
+    f.wavenumber = fus::complex_wavenumber(kWater, 1.1e6, 2);
+    f.values = random_vector(f.grid.count(), 3);
+    fus::write_field_dump("t_field.bin", f);
+    const auto hdr = fus::parse_key_value_file("t_field.bin.hdr");
+    CHECK(fus::require_double(hdr, "nx", "hdr") == f.grid.dims.x());
+    CHECK(fus::require_double(hdr, "dx", "hdr") == f.grid.dx);
+    CHECK(fus::require_double(hdr, "harmonic", "hdr") == 2);
+    CHECK(fus::require_double(hdr, "k_re", "hdr") == f.wavenumber.k.real());
+    CHECK(fus::require_string(hdr, "layout", "hdr") == "x_fastest_complex_f64_le");
+    Eigen::VectorXcd back(f.values.size());
+    std::ifstream in("t_field.bin", std::ios::binary);
+    in.read(reinterpret_cast<char*>(back.data()), std::streamsize(back.size() * 16));
+    CHECK(in.gcount() == std::streamsize(back.size() * 16));
+    bool same = true;
+    for (Eigen::Index i = 0; i < back.size(); ++i) same = same && back[i] == f.values[i];
+    CHECK(same);
+  }
+  {
+    fus::write_csv("t_gen.csv", {"a", "b"}, {{1, 2}, {3, 4.5}});
+    std::ifstream in("t_gen.csv");
+    std::string l0, l1, l2;
+    std::getline(in, l0);
+    std::getline(in, l1);
+    std::getline(in, l2);
+    CHECK(l0 == "a,b" && l1 == "1,2" && l2 == "3,4.5");
+  }
+  {
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {5e-3, 4e-3, 3e-3}}, 1e-3, 1);
+    const fus::MediumMap m = fus::slab_map(g, kWater, fus::medium_preset("liver"), 2e-3, 2e-3);
+    fus::write_medium_map("t_map.hdr", "t_map.bin", m);
+    const fus::MediumMap back = fus::load_medium_map("t_map.hdr", kWater);
+    CHECK(back.grid.dims == g.dims && back.grid.dx == g.dx);
+    bool same = back.c.size() == m.c.size();
+    for (Eigen::Index i = 0; same && i < m.c.size(); ++i) same = back.c[i] == m.c[i] && back.beta[i] == m.beta[i];
+    CHECK(same);
+  }
+  for (const char* f : {"t_kv.txt", "t_bad.txt", "t_axis.csv", "t_field.bin", "t_field.bin.hdr", "t_gen.csv",
+                        "t_map.hdr", "t_map.bin"})
+    std::remove(f);
 }
 
 void device_cases() {
@@ -313,6 +395,7 @@ int main(int argc, char** argv) {
   const bool all = argc > 1 && std::strcmp(argv[1], "all") == 0;
   try {
     host_cases();
+    io_cases();
     if (all) device_cases();
   } catch (const std::exception& e) {
     std::printf("FAIL uncaught exception: %s\n", e.what());
