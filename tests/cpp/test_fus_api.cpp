@@ -18,6 +18,7 @@
 #include "fus/transducer.hpp"
 #include "fus/vie.hpp"
 #include "fus/io.hpp"
+#include "fus/analysis.hpp"
 #include <fstream>
 #include <map>
 
@@ -318,6 +319,37 @@ void device_cases() {
     const fus::CascadeResult ws = fus::run_cascade_inhomogeneous(cfg, slab);
     const double rel = (ws.p(1).values - homo.p(1).values).norm() / homo.p(1).values.norm();
     CHECK(rel > 1e-3 && rel < 0.5);
+  }
+  // analysis through the drop-in: criterion 1's recorded errors and slope (proj/test_output.txt:20)
+  // and the domain-shrink full-size level (tests/test_analysis.cpp:116-131)
+  {
+    const fus::Medium liver = fus::medium_preset("liver");
+    const fus::BowlTransducer t = fus::transducer_preset("H131", 30.0, 128);
+    const double lam = liver.c0 / t.f0;
+    const Eigen::Vector3d focus = t.focus();
+    fus::DomainBox box;
+    box.lo = Eigen::Vector3d(focus.x() - 7.0 * lam, -1.5 * lam, -1.5 * lam);
+    box.hi = Eigen::Vector3d(focus.x() + 7.0 * lam, 1.5 * lam, 1.5 * lam);
+    const fus::QuadratureStudy st = fus::quadrature_convergence_study(t, liver, box, {4, 6, 8, 10}, 20);
+    auto g4 = [](double v) {
+      char b[32];
+      std::snprintf(b, sizeof(b), "%.4g", v);
+      return std::string(b);
+    };
+    CHECK(st.records.size() == 4 && g4(st.records[0].error_percent) == "0.6437" &&
+          g4(st.records[1].error_percent) == "0.2641" && g4(st.records[2].error_percent) == "0.138" &&
+          g4(st.records[3].error_percent) == "0.07983");
+    CHECK(g4(st.slope) == "-2.269");
+    fus::CascadeConfig cfg;
+    cfg.medium = kWater;
+    cfg.transducer = fus::transducer_preset("H131", 15.0, 128);
+    cfg.transducer.f0 = 0.25e6;
+    cfg.plan = fus::plan_full_domain(cfg.transducer, cfg.medium, 6e-3, 3, 2, 0.35);
+    cfg.n_harmonics = 2;
+    const fus::CascadeResult ref = fus::run_cascade(cfg);
+    const auto recs = fus::domain_shrink_study(cfg, ref, {1.0, 0.5}, false);
+    CHECK(recs.size() == 2 && recs[0].error_percent < 1e-6 && recs[1].error_percent > recs[0].error_percent &&
+          recs[1].control == "fraction");
   }
   // rhs coefficients, tests/test_cascade.cpp:33-63
   {
