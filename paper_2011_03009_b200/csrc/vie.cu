@@ -98,6 +98,35 @@ __global__ void __launch_bounds__(kRedThreads) dot_partial_kernel(const double2*
   if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
 }
 
+// MGS step fused: w -= (*s_prev) v_prev, then partial[b] = sum conj(v_next_i) w_i over the same
+// fixed slices as dot_partial_kernel (v_next == w gives |w|^2).  One pass over w instead of two.
+__global__ void __launch_bounds__(kRedThreads) axpy_dot_partial_kernel(double2* __restrict__ w,
+                                                                       const double2* __restrict__ v_prev,
+                                                                       const double2* __restrict__ s_prev,
+                                                                       const double2* v_next, int64_t n,
+                                                                       double2* __restrict__ partial) {
+  __shared__ double2 red[kRedThreads];
+  const double2 c = *s_prev;
+  double sr = 0.0, si = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * kRedThreads + threadIdx.x; i < n; i += int64_t(kRedBlocks) * kRedThreads) {
+    const double2 x = v_prev[i];
+    const double2 y = make_double2(w[i].x - (c.x * x.x - c.y * x.y), w[i].y - (c.x * x.y + c.y * x.x));
+    w[i] = y;
+    const double2 a = v_next == w ? y : v_next[i];
+    sr = fma(a.x, y.x, fma(a.y, y.y, sr));
+    si = fma(a.x, y.y, fma(-a.y, y.x, si));
+  }
+  red[threadIdx.x] = make_double2(sr, si);
+  __syncthreads();
+  for (int t = kRedThreads / 2; t > 0; t >>= 1) {
+    if (threadIdx.x < t)
+      red[threadIdx.x] = make_double2(red[threadIdx.x].x + red[threadIdx.x + t].x,
+                                      red[threadIdx.x].y + red[threadIdx.x + t].y);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
 __global__ void __launch_bounds__(kRedThreads) dot_final_kernel(const double2* __restrict__ partial,
                                                                 double2* __restrict__ result) {
   __shared__ double2 red[kRedThreads];
@@ -112,16 +141,6 @@ __global__ void __launch_bounds__(kRedThreads) dot_final_kernel(const double2* _
     __syncthreads();
   }
   if (threadIdx.x == 0) *result = red[0];
-}
-
-// w -= (*s) v, the coefficient read from device memory (Arnoldi, no host round trip)
-__global__ void axpy_dev_kernel(double2* __restrict__ w, const double2* __restrict__ v, const double2* __restrict__ s,
-                                int64_t n) {
-  const double2 c = *s;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    const double2 x = v[i];
-    w[i] = make_double2(w[i].x - (c.x * x.x - c.y * x.y), w[i].y - (c.x * x.y + c.y * x.x));
-  }
 }
 
 // x += y v (host coefficient)
@@ -235,12 +254,15 @@ fusg_status gmres_dev(fusg_ctx* ctx, const std::function<fusg_status(const doubl
     while (k < m && total < max_iter) {
       // Arnoldi with modified Gram-Schmidt, on the device
       FUSG_TRY(op(vec(k), w));
-      for (int j = 0; j <= k; ++j) {
-        FUSG_TRY(red.dot(vec(j), w, n, hcol + j));
-        axpy_dev_kernel<<<nb, 256, 0, s>>>(w, vec(j), hcol + j, n);
-        ctx->launches++;
+      // h_j = <v_j, w>; w -= h_j v_j, each axpy fused with the next dot (and the last with |w|^2)
+      FUSG_TRY(red.dot(vec(0), w, n, hcol));
+      for (int j = 1; j <= k + 1; ++j) {
+        axpy_dot_partial_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(w, vec(j - 1), hcol + j - 1,
+                                                                   j <= k ? vec(j) : w, n, partial);
+        dot_final_kernel<<<1, kRedThreads, 0, s>>>(partial, hcol + j);
+        ctx->launches += 2;
       }
-      FUSG_TRY(red.dot(w, w, n, hcol + k + 1));
+      FUSG_LAUNCH_CHECK("arnoldi kernels");
       FUSG_CUDA_TRY(cudaMemcpyAsync(col.data(), hcol, sizeof(double2) * (k + 2), cudaMemcpyDeviceToHost, s));
       FUSG_CUDA_TRY(cudaStreamSynchronize(s));
       for (int j = 0; j <= k; ++j) H(j, k) = cd(col[j].x, col[j].y);
