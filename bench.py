@@ -337,10 +337,16 @@ def run_gpu(args, world, rank, local):
         solve = nested_solve(ctx)
     # evaluate_potential_at at the reference's use (on-axis nodes of a
     # D2-grid field), with the CPU oracle on a bounded sample when the CPU leg runs
-    off_grid = None
+    off_grid = vie = acceptance = None
     if rank == 0 and world == 1 and not args.no_cascade:
-        from tools import potential_at_bench
+        from tools import acceptance_bench, potential_at_bench, vie_bench
         off_grid = potential_at_bench.run(cpu_points=0 if args.no_cpu_baseline else 16)
+        # a VIE solve at cfg2 size (liver slab), CPU oracle per iteration beside it
+        vie = vie_bench.run(cpu=not args.no_cpu_baseline)
+        # the reference's long acceptance workloads (recorded wall times in proj/test_output.txt)
+        acceptance_bench.criterion1()  # warm-up
+        acceptance = {"criterion_1": acceptance_bench.criterion1(), "criterion_6": acceptance_bench.criterion6(),
+                      "criterion_10_cascade": acceptance_bench.criterion10_cascade()}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -380,6 +386,8 @@ def run_gpu(args, world, rank, local):
             "cpu_baseline": cpu_baseline,
             "nested_5_harmonic_solve": solve,
             "evaluate_potential_at": off_grid,
+            "vie_solve": vie,
+            "acceptance": acceptance,
         }
         print(json.dumps(line), flush=True)
     return 0
