@@ -981,13 +981,22 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
       cudaMallocAsync(&K->bufB, nB * sizeof(double2), as) != cudaSuccess ||
       cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess ||
       (nX && alloc_ipc(&K->xbuf, nX) != cudaSuccess) ||
-      (nX && cudaMallocAsync(&K->rbuf, nX * sizeof(double2), as) != cudaSuccess) ||
-      cudaMallocAsync(&g1, size_t(Hx) * Ny * Nz * sizeof(double2), as) != cudaSuccess ||
-      cudaMallocAsync(&g2, size_t(Hx) * Hy * Nz * sizeof(double2), as) != cudaSuccess) {
+      (nX && cudaMallocAsync(&K->rbuf, nX * sizeof(double2), as) != cudaSuccess)) {
     cudaGetLastError();
-    if (g1) cudaFreeAsync(g1, as);
-    if (g2) cudaFreeAsync(g2, as);
     return set_error(FUSG_OOM, "GreenKernel: device allocation failed");
+  }
+  // build scratch: the apply workspaces are idle during the build, so G1/G2 live in bufA/bufB
+  // whenever they fit (always unsharded) -- the peak stays at the apply's own footprint, which
+  // is what lets a 1024^3 grid (2048^3 embedding) fit in one B200
+  const size_t n1 = size_t(Hx) * Ny * Nz, n2 = size_t(Hx) * Hy * Nz;
+  const bool g1_in_A = n1 <= nA, g2_in_B = n2 <= nB;
+  g1 = g1_in_A ? K->bufA : nullptr;
+  g2 = g2_in_B ? K->bufB : nullptr;
+  if ((!g1_in_A && cudaMallocAsync(&g1, n1 * sizeof(double2), as) != cudaSuccess) ||
+      (!g2_in_B && cudaMallocAsync(&g2, n2 * sizeof(double2), as) != cudaSuccess)) {
+    cudaGetLastError();
+    if (g1 && !g1_in_A) cudaFreeAsync(g1, as);
+    return set_error(FUSG_OOM, "GreenKernel: build scratch allocation failed");
   }
   K->bytes = (nA + nB + nK + 2 * nX) * sizeof(double2);
 
@@ -1006,8 +1015,8 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   FoldF l3{g2, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
   GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx][ky][kz]
   FUSG_TRY(launch_axis<false>(ctx, K->plan[2], Hx, Hy, l3, s3, s));
-  cudaFreeAsync(g1, s);
-  cudaFreeAsync(g2, s);
+  if (!g1_in_A) cudaFreeAsync(g1, s);
+  if (!g2_in_B) cudaFreeAsync(g2, s);
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return FUSG_OK;
 }
