@@ -98,12 +98,24 @@ __device__ __forceinline__ void warp_stage_compute(double2* v, int lane, const T
   }
 }
 
+// Exchange barriers of a line: one warp (__syncwarp) or a lane group of several warps (a named
+// barrier over exactly those warps' threads; ids 1..15, 0 is __syncthreads').
+struct WarpSync {
+  __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+template <int THREADS>
+struct GroupSync {
+  int id;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(THREADS) : "memory"); }
+};
+
 // Full transform of the LANES-lane line owned by this lane group.
 //   src.load(pos, e) feeds stage 0; dst.store(pos, e, v) receives the last stage's outputs.
 //   ex.at(pos): this line's swizzled shared exchange slot for position pos.
 template <class RL, int LANES, bool INV, int PRUNE = 0, int S = 0, class Ex, class Tw, class Src,
-          class Dst>
-__device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& tw, Src& src, Dst& dst) {
+          class Dst, class Sync = WarpSync>
+__device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& tw, Src& src, Dst& dst,
+                                         Sync sync = Sync{}) {
   constexpr int E = RL::len() / LANES;
   constexpr int R0 = RL::at(0);
   if constexpr (S == 0) {
@@ -115,13 +127,13 @@ __device__ __forceinline__ void warp_fft(double2* v, Ex ex, int lane, const Tw& 
   }
   warp_stage_compute<RL, LANES, INV, S, PRUNE>(v, lane, tw);
   if constexpr (S + 1 < RL::n) {
-    __syncwarp();  // all lanes finished reading the buffer (previous stage / caller)
+    sync();  // all lanes finished reading the buffer (previous stage / caller)
 #pragma unroll
     for (int e = 0; e < E; ++e) ex.at(out_pos<RL, LANES, S>(lane, e)) = v[e];
-    __syncwarp();
+    sync();
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = ex.at(in_pos<RL, LANES, S + 1>(lane, e));
-    warp_fft<RL, LANES, INV, PRUNE, S + 1>(v, ex, lane, tw, src, dst);
+    warp_fft<RL, LANES, INV, PRUNE, S + 1>(v, ex, lane, tw, src, dst, sync);
   } else {
     constexpr int RL_ = RL::at(S);
 #pragma unroll

@@ -614,6 +614,136 @@ constexpr bool whole_butterflies(int lanes) {
     if (E % RL::at(s)) return false;
   return true;
 }
+// Pass C for L > 1024 (1536, 2048): the persistent pipeline of warp_row_conv_pp with each line
+// owned by a group of two warps (64 lanes, 24 or 32 points per lane); the exchanges synchronise
+// the group with a named barrier.  GROUPS line groups per CTA (2 at 1536, 1 at 2048, for shared
+// memory).
+template <int L>
+constexpr int pp64_groups() { return L <= 1536 ? 2 : 1; }
+template <int L, bool PRUNED>
+struct PP64Smem {
+  static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;
+  static constexpr int STAGE = PRUNED ? L / 2 : L;
+  static constexpr int PER_GROUP = L + STAGE + KROW;
+  static constexpr size_t BYTES = size_t(pp64_groups<L>()) * PER_GROUP * sizeof(double2);
+};
+
+template <class RL, bool PRUNED>
+__global__ void __launch_bounds__(pp64_groups<RL::len()>() * 64, 3 - pp64_groups<RL::len()>())
+    warp_row_conv_pp64(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / 64;
+  constexpr int HZ = L / 2 + 1;
+  constexpr int R0 = RL::at(0);
+  constexpr int GROUPS = pp64_groups<L>();
+  using SM = PP64Smem<L, PRUNED>;
+  static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
+  extern __shared__ double2 sm[];
+  const int grp = threadIdx.x >> 6, lane = threadIdx.x & 63;
+  const GroupSync<64> sync{1 + grp};
+  double2* const xb = sm + size_t(grp) * SM::PER_GROUP;
+  double2* const sb = xb + L;
+  double2* const kb = sb + SM::STAGE;
+  const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t stride = int64_t(gridDim.x) * GROUPS;
+  const bool mirror = a.n_outer == a.ko.Px;
+  auto coords = [&](int64_t line, int& ky, int& kx) {
+    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
+    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+  };
+  auto prefetch_in = [&](int64_t line) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
+      const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
+      for (int pos = lane; pos < a.in_nvalid; pos += 64) cp_async16(sb + swz(pos), in + pos);
+    }
+    cp_async_commit();
+  };
+  auto prefetch_k = [&](int64_t line) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
+      const double2* kl = a.ko.line(ky, kx);
+      for (int kz = lane; kz < HZ; kz += 64) cp_async16(kb + kz, kl + kz);
+    }
+    cp_async_commit();
+  };
+  const TwTable tw{a.tw};
+  constexpr int kPin = PRUNED ? 1 : 0, kPout = PRUNED ? 2 : 0;
+  const PrivEx ex{xb};
+  int64_t line = int64_t(blockIdx.x) * GROUPS + grp;
+  prefetch_in(line);
+  prefetch_k(line);
+  for (; line < nlines; line += stride) {
+    cp_async_wait0();
+    sync();  // the group's staged input and K^ row have landed
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if ((PRUNED && R0 == 8) && (e % R0) >= R0 / 2) continue;
+      const int pos = in_pos<RL, 64, 0>(lane, e);
+      v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
+    }
+    sync();  // staging consumed by the whole group
+    prefetch_in(line + stride);
+    RegsIn vin{v};
+    RegsOut mid{v};
+    warp_fft<RL, 64, false, kPin>(v, ex, lane, tw, vin, mid, sync);
+#pragma unroll
+    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, 64, 0>(lane, e), L)]);
+    sync();  // K^ row consumed
+    prefetch_k(line + stride);
+    int ky, kx;
+    coords(line, ky, kx);
+    RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
+    warp_fft<RL, 64, true, kPout>(v, ex, lane, tw, vin, dst, sync);
+  }
+  cp_async_wait0();
+}
+
+// the long-line persistent pass C, or 0 when not applicable
+static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = getenv("FUSG_CONV_PP64");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on || 2 * a.in_nvalid > L || 2 * a.out_nvalid > L) return 0;  // pruned halves only
+  WFn fn = nullptr;
+  size_t smem = 0;
+  int groups = 1;
+  if (L == 1536) {
+    fn = warp_row_conv_pp64<Radices<8, 8, 3, 8>, true>;
+    smem = PP64Smem<1536, true>::BYTES;
+    groups = pp64_groups<1536>();
+  } else if (L == 2048) {
+    fn = warp_row_conv_pp64<Radices<8, 4, 8, 8>, true>;
+    smem = PP64Smem<2048, true>::BYTES;
+    groups = pp64_groups<2048>();
+  } else {
+    return 0;
+  }
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+    set_error(FUSG_CUDA, "long-line pass C: cannot configure shared memory");
+    return -1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, groups * 64, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t lines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t grid = std::min<int64_t>((lines + groups - 1) / groups, int64_t(per_sm) * ctx->num_sms);
+  fn<<<unsigned(grid), groups * 64, smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "long-line pass C");
+    return -1;
+  }
+  return 1;
+}
+
 template <class RL, int LN, bool PRUNED>
 constexpr WFn colrow_pp_ptr() {
   if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_col_to_row_pp<RL, PRUNED>;
@@ -905,7 +1035,8 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
   if (ld.g.sp == 1 && st.g.sp == 1 && ko.s_kz == 1) {
     const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                    st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, ko};
-    const int r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
+    int r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
+    if (r == 0) r = launch_conv64(ctx, pl.L, wa, s);
     if (r < 0) return FUSG_CUDA;
     if (r > 0) return FUSG_OK;
   }

@@ -91,7 +91,9 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # Nz = 300 / 341: Pz = 768 (warp pass C) instead of 600 / 686
                                   (3, 2, 300), (2, 3, 341),
                                   # Nz = 490: Pz = 1024 (warp pass C, pass-C-only entry)
-                                  (2, 2, 490)])
+                                  (2, 2, 490),
+                                  # Nz = 768 / 1024: Pz = 1536 / 2048 (two-warp-line pass C)
+                                  (3, 2, 768), (2, 3, 1024)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
