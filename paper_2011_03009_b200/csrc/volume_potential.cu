@@ -103,9 +103,9 @@ int device_padded_size(int n, int axis) {
     const char* e = getenv("FUSG_PAD_STATIC");
     return !(e && atoi(e) == 0);
   }();
-  static const bool pz_warp = [] {
+  static const int pz_warp = [] {  // FUSG_PZ_WARP: 0 off, else the largest preferred length
     const char* e = getenv("FUSG_PZ_WARP");
-    return !(e && atoi(e) == 0);
+    return e ? atoi(e) : 2048;
   }();
   int p = smooth;  // round up to a length with compile-time-planned kernels
   if (use_static)
@@ -115,8 +115,8 @@ int device_padded_size(int n, int axis) {
         break;
       }
   if (axis != 2 || !pz_warp) return p;
-  for (int L : {256, 512, 768, 1024})  // persistent warp pass C
-    if (L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
+  for (int L : {256, 512, 768, 1024, 1536, 2048})  // persistent pass C (warp / multi-warp lines)
+    if (L <= pz_warp && L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
   return p;
 }
 
@@ -615,9 +615,9 @@ constexpr bool whole_butterflies(int lanes) {
   return true;
 }
 // Pass C for L > 1024 (1536, 2048): the persistent pipeline of warp_row_conv_pp with each line
-// owned by a group of two warps (64 lanes, 24 or 32 points per lane); the exchanges synchronise
-// the group with a named barrier.  GROUPS line groups per CTA (2 at 1536, 1 at 2048, for shared
-// memory).
+// owned by a group of LANES = 64 or 128 lanes (two or four warps; 24 or 16 points per lane); the
+// exchanges synchronise the group with a named barrier.  GROUPS line groups per CTA (2 at 1536,
+// 1 at 2048, for shared memory).
 template <int L>
 constexpr int pp64_groups() { return L <= 1536 ? 2 : 1; }
 template <int L, bool PRUNED>
@@ -628,19 +628,19 @@ struct PP64Smem {
   static constexpr size_t BYTES = size_t(pp64_groups<L>()) * PER_GROUP * sizeof(double2);
 };
 
-template <class RL, bool PRUNED>
-__global__ void __launch_bounds__(pp64_groups<RL::len()>() * 64, 3 - pp64_groups<RL::len()>())
+template <class RL, int LANES, bool PRUNED>
+__global__ void __launch_bounds__(pp64_groups<RL::len()>() * LANES, LANES == 64 ? 3 - pp64_groups<RL::len()>() : 3)
     warp_row_conv_pp64(WArgs a) {
   constexpr int L = RL::len();
-  constexpr int E = L / 64;
+  constexpr int E = L / LANES;
   constexpr int HZ = L / 2 + 1;
   constexpr int R0 = RL::at(0);
   constexpr int GROUPS = pp64_groups<L>();
   using SM = PP64Smem<L, PRUNED>;
   static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
   extern __shared__ double2 sm[];
-  const int grp = threadIdx.x >> 6, lane = threadIdx.x & 63;
-  const GroupSync<64> sync{1 + grp};
+  const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
+  const GroupSync<LANES> sync{1 + grp};
   double2* const xb = sm + size_t(grp) * SM::PER_GROUP;
   double2* const sb = xb + L;
   double2* const kb = sb + SM::STAGE;
@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(pp64_groups<RL::len()>() * 64, 3 - pp64_groups
       int ky, kx;
       coords(line, ky, kx);
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
-      for (int pos = lane; pos < a.in_nvalid; pos += 64) cp_async16(sb + swz(pos), in + pos);
+      for (int pos = lane; pos < a.in_nvalid; pos += LANES) cp_async16(sb + swz(pos), in + pos);
     }
     cp_async_commit();
   };
@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(pp64_groups<RL::len()>() * 64, 3 - pp64_groups
       int ky, kx;
       coords(line, ky, kx);
       const double2* kl = a.ko.line(ky, kx);
-      for (int kz = lane; kz < HZ; kz += 64) cp_async16(kb + kz, kl + kz);
+      for (int kz = lane; kz < HZ; kz += LANES) cp_async16(kb + kz, kl + kz);
     }
     cp_async_commit();
   };
@@ -682,22 +682,22 @@ __global__ void __launch_bounds__(pp64_groups<RL::len()>() * 64, 3 - pp64_groups
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if ((PRUNED && R0 == 8) && (e % R0) >= R0 / 2) continue;
-      const int pos = in_pos<RL, 64, 0>(lane, e);
+      const int pos = in_pos<RL, LANES, 0>(lane, e);
       v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
     }
     sync();  // staging consumed by the whole group
     prefetch_in(line + stride);
     RegsIn vin{v};
     RegsOut mid{v};
-    warp_fft<RL, 64, false, kPin>(v, ex, lane, tw, vin, mid, sync);
+    warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, vin, mid, sync);
 #pragma unroll
-    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, 64, 0>(lane, e), L)]);
+    for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     sync();  // K^ row consumed
     prefetch_k(line + stride);
     int ky, kx;
     coords(line, ky, kx);
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
-    warp_fft<RL, 64, true, kPout>(v, ex, lane, tw, vin, dst, sync);
+    warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, vin, dst, sync);
   }
   cp_async_wait0();
 }
@@ -709,15 +709,21 @@ static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
     return !(e && atoi(e) == 0);
   }();
   if (!on || 2 * a.in_nvalid > L || 2 * a.out_nvalid > L) return 0;  // pruned halves only
+  static const int lanes2048 = [] {  // FUSG_PP2048_LANES: 64 or 128 lanes per 2048-point line
+    const char* e = getenv("FUSG_PP2048_LANES");
+    return e && atoi(e) == 64 ? 64 : 128;
+  }();
   WFn fn = nullptr;
   size_t smem = 0;
-  int groups = 1;
+  int groups = 1, lanes = 64;
   if (L == 1536) {
-    fn = warp_row_conv_pp64<Radices<8, 8, 3, 8>, true>;
+    fn = warp_row_conv_pp64<Radices<8, 8, 3, 8>, 64, true>;
     smem = PP64Smem<1536, true>::BYTES;
     groups = pp64_groups<1536>();
   } else if (L == 2048) {
-    fn = warp_row_conv_pp64<Radices<8, 4, 8, 8>, true>;
+    lanes = lanes2048;
+    fn = lanes == 64 ? warp_row_conv_pp64<Radices<8, 4, 8, 8>, 64, true>
+                     : warp_row_conv_pp64<Radices<8, 4, 8, 8>, 128, true>;
     smem = PP64Smem<2048, true>::BYTES;
     groups = pp64_groups<2048>();
   } else {
@@ -728,13 +734,13 @@ static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
     return -1;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, groups * 64, smem) != cudaSuccess || per_sm < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, groups * lanes, smem) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     return 0;
   }
   const int64_t lines = int64_t(a.n_inner) * a.n_outer;
   const int64_t grid = std::min<int64_t>((lines + groups - 1) / groups, int64_t(per_sm) * ctx->num_sms);
-  fn<<<unsigned(grid), groups * 64, smem, s>>>(a);
+  fn<<<unsigned(grid), groups * lanes, smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
