@@ -13,6 +13,7 @@
 // so its spectrum is even too: only the octant [0,Px/2]x[0,Py/2]x[0,Pz/2] is built and
 // stored, and pass C folds its index.  The octant is built by the same pass machinery with
 // the kernel values generated in registers (no padded tensor is ever materialised).
+#include <string>
 #include <cmath>
 #include <algorithm>
 #include <cstdlib>
@@ -614,29 +615,27 @@ constexpr bool whole_butterflies(int lanes) {
     if (E % RL::at(s)) return false;
   return true;
 }
-// Pass C for L > 1024 (1536, 2048): the persistent pipeline of warp_row_conv_pp with each line
-// owned by a group of LANES = 64 or 128 lanes (two or four warps; 24 or 16 points per lane); the
-// exchanges synchronise the group with a named barrier.  GROUPS line groups per CTA (2 at 1536,
-// 1 at 2048, for shared memory).
-template <int L>
-constexpr int pp64_groups() { return L <= 1536 ? 2 : 1; }
-template <int L, bool PRUNED>
+// Pass C on multi-warp lines: the persistent pipeline of warp_row_conv_pp with each line owned
+// by a group of LANES = 64..256 lanes (2..8 warps); the exchanges synchronise the group with a
+// named barrier.  GROUPS line groups per CTA, MINB CTAs per SM for the register budget.  Long
+// lines (1536, 2048) need it for registers; short ones (512, 1024) use it to put more warps on
+// each line in flight (latency hiding at the same shared-memory footprint).
+template <int L, bool PRUNED, int GROUPS>
 struct PP64Smem {
   static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;
   static constexpr int STAGE = PRUNED ? L / 2 : L;
   static constexpr int PER_GROUP = L + STAGE + KROW;
-  static constexpr size_t BYTES = size_t(pp64_groups<L>()) * PER_GROUP * sizeof(double2);
+  static constexpr size_t BYTES = size_t(GROUPS) * PER_GROUP * sizeof(double2);
 };
 
-template <class RL, int LANES, bool PRUNED>
-__global__ void __launch_bounds__(pp64_groups<RL::len()>() * LANES, LANES == 64 ? 3 - pp64_groups<RL::len()>() : 3)
-    warp_row_conv_pp64(WArgs a) {
+template <class RL, int LANES, int GROUPS, int MINB, bool PRUNED>
+__global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
   constexpr int HZ = L / 2 + 1;
   constexpr int R0 = RL::at(0);
-  constexpr int GROUPS = pp64_groups<L>();
-  using SM = PP64Smem<L, PRUNED>;
+  using SM = PP64Smem<L, PRUNED, GROUPS>;
+  static_assert(GROUPS < 16, "named barrier ids 1..15");
   static_assert(RL::at(0) == RL::at(RL::n - 1), "register hand-off needs equal first/last radix");
   extern __shared__ double2 sm[];
   const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
@@ -702,33 +701,47 @@ __global__ void __launch_bounds__(pp64_groups<RL::len()>() * LANES, LANES == 64 
   cp_async_wait0();
 }
 
-// the long-line persistent pass C, or 0 when not applicable
+struct PPMVariant {
+  int L, lanes, groups;
+  WFn fn;
+  size_t smem;
+};
+#define FUSG_PPM(LANES, GROUPS, MINB, ...)                                                  \
+  PPMVariant {                                                                              \
+    Radices<__VA_ARGS__>::len(), LANES, GROUPS, warp_row_conv_pp64<Radices<__VA_ARGS__>, LANES, GROUPS, MINB, true>, \
+        PP64Smem<Radices<__VA_ARGS__>::len(), true, GROUPS>::BYTES                          \
+  }
+// Variants per length, selected by FUSG_PPM_<L> (index; -1 = none: 512/1024 then run the
+// one-warp pp kernel).  The first entry of each length is the default.
+static const PPMVariant kPPM[] = {
+    FUSG_PPM(64, 2, 1, 8, 8, 3, 8),   // 1536: 24 points per lane
+    FUSG_PPM(128, 1, 3, 8, 4, 8, 8),  // 2048: 16 per lane (64 lanes: 118 ms at 1024^3; 256: 93; this: 81)
+    FUSG_PPM(64, 1, 6, 8, 4, 4, 8),   // 1024: 16 per lane (one warp: 14.4 ms at 512^3; 128 lanes: 10.6; this: 9.4)
+    // 512 and 768 stay on one-warp lines: 64-lane variants measured 1.05-1.08 ms against 0.89
+    // (cfg2 pass C) and 5.7 ms against 4.0 (384^3, 12 points per lane on radices 4,4,3,4,4)
+};
+#undef FUSG_PPM
+
+// the multi-warp-line persistent pass C, or 0 when not applicable
 static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
   static const bool on = [] {
     const char* e = getenv("FUSG_CONV_PP64");
     return !(e && atoi(e) == 0);
   }();
   if (!on || 2 * a.in_nvalid > L || 2 * a.out_nvalid > L) return 0;  // pruned halves only
-  static const int lanes2048 = [] {  // FUSG_PP2048_LANES: 64 or 128 lanes per 2048-point line
-    const char* e = getenv("FUSG_PP2048_LANES");
-    return e && atoi(e) == 64 ? 64 : 128;
-  }();
-  WFn fn = nullptr;
-  size_t smem = 0;
-  int groups = 1, lanes = 64;
-  if (L == 1536) {
-    fn = warp_row_conv_pp64<Radices<8, 8, 3, 8>, 64, true>;
-    smem = PP64Smem<1536, true>::BYTES;
-    groups = pp64_groups<1536>();
-  } else if (L == 2048) {
-    lanes = lanes2048;
-    fn = lanes == 64 ? warp_row_conv_pp64<Radices<8, 4, 8, 8>, 64, true>
-                     : warp_row_conv_pp64<Radices<8, 4, 8, 8>, 128, true>;
-    smem = PP64Smem<2048, true>::BYTES;
-    groups = pp64_groups<2048>();
-  } else {
-    return 0;
-  }
+  const std::string var_name = "FUSG_PPM_" + std::to_string(L);
+  const char* ve = getenv(var_name.c_str());
+  const int def = 0;
+  const int want = ve ? atoi(ve) : def;
+  if (want < 0) return 0;
+  const PPMVariant* v = nullptr;
+  int seen = 0;
+  for (const auto& c : kPPM)
+    if (c.L == L && seen++ == want) v = &c;
+  if (!v) return 0;
+  const WFn fn = v->fn;
+  const size_t smem = v->smem;
+  const int groups = v->groups, lanes = v->lanes;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
     set_error(FUSG_CUDA, "long-line pass C: cannot configure shared memory");
     return -1;
@@ -1041,8 +1054,8 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
   if (ld.g.sp == 1 && st.g.sp == 1 && ko.s_kz == 1) {
     const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                    st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, ko};
-    int r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
-    if (r == 0) r = launch_conv64(ctx, pl.L, wa, s);
+    int r = launch_conv64(ctx, pl.L, wa, s);
+    if (r == 0) r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
     if (r < 0) return FUSG_CUDA;
     if (r > 0) return FUSG_OK;
   }

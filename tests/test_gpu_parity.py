@@ -88,12 +88,14 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # Pz = 256 / 512 with pruned halves: the two-stage pass C
                                   # (odd line count 9 x 5 exercises the half-filled last pair)
                                   (9, 7, 128), (5, 3, 256), (3, 2, 100), (6, 5, 129),
-                                  # Nz = 300 / 341: Pz = 768 (warp pass C) instead of 600 / 686
+                                  # Nz = 300 / 341: Pz = 768 (multi-warp pass C) instead of 600 / 686
                                   (3, 2, 300), (2, 3, 341),
-                                  # Nz = 490: Pz = 1024 (warp pass C, pass-C-only entry)
+                                  # Nz = 490: Pz = 1024 (two-warp-line pass C)
                                   (2, 2, 490),
-                                  # Nz = 768 / 1024: Pz = 1536 / 2048 (two-warp-line pass C)
-                                  (3, 2, 768), (2, 3, 1024)])
+                                  # Nz = 768 / 1024: Pz = 1536 / 2048 (two- / four-warp lines)
+                                  (3, 2, 768), (2, 3, 1024),
+                                  # Nz = 600 / 900: Pz = 1536 / 2048 preferred over 1200 / 1800
+                                  (2, 2, 600), (2, 1, 900)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
