@@ -701,6 +701,224 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
   cp_async_wait0();
 }
 
+// Transposing passes on multi-warp lines (L = 1024..2048, where a one-warp line spills and an
+// 8-line [pos][8] tile no longer fits): persistent CTAs of T lines x LANES lanes.  Each line has
+// a private swizzled exchange buffer X (stride L + 8/T: the skew makes the cooperative tile
+// reads / stores below bank-conflict-free); stages synchronise the line's warps with a named
+// barrier.
+//   mw_row_to_col (A, B): every line group stages its own next input row by cp.async while the
+//     current one is transformed; the last stage lands in X and, after one CTA barrier, the CTA
+//     stores position-major segments of T adjacent lines (T x 16 B contiguous).
+//   mw_col_to_row (D, E): the CTA stages the next [pos][T] column tile (swizzled) by cp.async
+//     while each group transforms its column of the current one and stores its output row from
+//     registers.
+template <int T>
+__device__ __forceinline__ int mtile_at(int pos, int t) { return pos * T + (t ^ ((pos / (8 / T)) & (T - 1))); }
+
+template <int L, int T>
+struct MWSmem {
+  static constexpr int XSTRIDE = L + 8 / T;
+  static constexpr size_t R2C_BYTES = (size_t(T) * XSTRIDE + size_t(T) * (L / 2)) * sizeof(double2);
+  static constexpr size_t C2R_BYTES = (size_t(T) * XSTRIDE + size_t(T) * L) * sizeof(double2);
+};
+
+template <class RL, int LANES, int T, int MINB>
+__global__ void __launch_bounds__(T * LANES, MINB) mw_row_to_col(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  constexpr int R0 = RL::at(0);
+  using SM = MWSmem<L, T>;
+  static_assert(T == 2 || T == 4 || T == 8, "tile lines");
+  extern __shared__ double2 sm[];
+  const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
+  const GroupSync<LANES> sync{1 + grp};
+  double2* const xb = sm + grp * SM::XSTRIDE;
+  double2* const sb = sm + T * SM::XSTRIDE + grp * (L / 2);  // staged input row (pruned: < L/2)
+  const int ntiles_i = (a.n_inner + T - 1) / T;
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto prefetch = [&](int64_t tix) {
+    if (tix < ntiles) {
+      const int i = int(tix % ntiles_i) * T + grp;
+      const int k = int(tix / ntiles_i);
+      if (i < a.n_inner) {
+        const double2* in = a.in + int64_t(i) * a.in_si + int64_t(k) * a.in_sk;
+        for (int pos = lane; pos < a.in_nvalid; pos += LANES) cp_async16(sb + swz(pos), in + pos);
+      }
+    }
+    cp_async_commit();
+  };
+  const TwTable tw{a.tw};
+  const PrivEx ex{xb};
+  int64_t tix = blockIdx.x;
+  prefetch(tix);
+  for (; tix < ntiles; tix += gridDim.x) {
+    const int i0 = int(tix % ntiles_i) * T;
+    const int k = int(tix / ntiles_i);
+    const int lines_ok = min(T, a.n_inner - i0);
+    cp_async_wait0();
+    sync();  // the group's own staged row has landed
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (R0 == 8 && (e % R0) >= R0 / 2) continue;  // zero padding: not staged
+      const int pos = in_pos<RL, LANES, 0>(lane, e);
+      v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
+    }
+    sync();  // staging consumed by the group: refill it with the next tile's row
+    prefetch(tix + gridDim.x);
+    RegsIn vin{v};
+    RegsOut vout{v};
+    warp_fft<RL, LANES, false, 1>(v, ex, lane, tw, vin, vout, sync);
+    sync();  // every lane of the group is done reading X (last exchange)
+#pragma unroll
+    for (int e = 0; e < E; ++e) ex.at(out_pos<RL, LANES, RL::n - 1>(lane, e)) = v[e];
+    __syncthreads();  // all T lines are in X
+    double2* const base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+    for (int e = threadIdx.x; e < a.out_nvalid * T; e += T * LANES) {
+      const int pos = e / T, t = e % T;
+      if (t < lines_ok) {
+        const double2 x = sm[t * SM::XSTRIDE + swz(pos)];
+        base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+      }
+    }
+    __syncthreads();  // X read out before the next tile's first exchange
+  }
+  cp_async_wait0();
+}
+
+template <class RL, int LANES, int T, int MINB>
+__global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
+  constexpr int L = RL::len();
+  constexpr int E = L / LANES;
+  using SM = MWSmem<L, T>;
+  static_assert(T == 2 || T == 4 || T == 8, "tile lines");
+  extern __shared__ double2 sm[];
+  const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
+  const GroupSync<LANES> sync{1 + grp};
+  double2* const tile = sm + T * SM::XSTRIDE;
+  const int ntiles_i = (a.n_inner + T - 1) / T;
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto prefetch = [&](int64_t tix) {
+    if (tix < ntiles) {
+      const int i0 = int(tix % ntiles_i) * T;
+      const int k = int(tix / ntiles_i);
+      const int lines_ok = min(T, a.n_inner - i0);
+      const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
+      for (int e = threadIdx.x; e < a.in_nvalid * T; e += T * LANES) {
+        const int pos = e / T, t = e % T;
+        cp_async16_zfill(&tile[mtile_at<T>(pos, t)], t < lines_ok ? base + t * a.in_si + pos * a.in_sp : a.in,
+                         t < lines_ok);
+      }
+    }
+    cp_async_commit();
+  };
+  const TwTable tw{a.tw};
+  const PrivEx ex{sm + grp * SM::XSTRIDE};
+  int64_t tix = blockIdx.x;
+  prefetch(tix);
+  for (; tix < ntiles; tix += gridDim.x) {
+    const int i0 = int(tix % ntiles_i) * T;
+    const int k = int(tix / ntiles_i);
+    const bool ok = grp < min(T, a.n_inner - i0);
+    cp_async_wait0();
+    __syncthreads();  // this tile's copies (issued by all threads) have landed
+    double2 v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int pos = in_pos<RL, LANES, 0>(lane, e);
+      v[e] = pos < a.in_nvalid ? tile[mtile_at<T>(pos, grp)] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // tile consumed by every group
+    prefetch(tix + gridDim.x);
+    const int line = i0 + (ok ? grp : 0);
+    RegsIn vin{v};
+    RowOut dst{a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok, a.scale};
+    warp_fft<RL, LANES, true, 2>(v, ex, lane, tw, vin, dst, sync);  // cropped output half
+  }
+  cp_async_wait0();
+}
+
+struct MWVariant {
+  int L;
+  bool r2c, def;
+  int lanes, T;
+  WFn fn;
+  size_t smem;
+};
+#define FUSG_MW_R2C(DEF, LANES, T, MINB, ...)                                               \
+  MWVariant {                                                                               \
+    Radices<__VA_ARGS__>::len(), true, DEF, LANES, T, mw_row_to_col<Radices<__VA_ARGS__>, LANES, T, MINB>, \
+        MWSmem<Radices<__VA_ARGS__>::len(), T>::R2C_BYTES                                   \
+  }
+#define FUSG_MW_C2R(DEF, LANES, T, MINB, ...)                                               \
+  MWVariant {                                                                               \
+    Radices<__VA_ARGS__>::len(), false, DEF, LANES, T, mw_col_to_row<Radices<__VA_ARGS__>, LANES, T, MINB>, \
+        MWSmem<Radices<__VA_ARGS__>::len(), T>::C2R_BYTES                                   \
+  }
+// Variants per (length, direction); FUSG_MW_<L>_R2C / _C2R = index among them (-1: static
+// kernels), else the one marked default.  Measured (tools/pass_times.py, ms for A B D E):
+//   1536 (768^3): static 8.8 17.4 17.8 8.5 -> 6.7 12.7 11.0 6.3 (apply 86.1 -> 70.4 ms);
+//                 T = 2 tiles: 12.5 14.0 10.8 11.6
+//   1024 (512^3): static 1.95 3.75 3.93 2.03 -> r2c 1.96 3.76 (kept static), c2r 3.33 1.88
+//   2048 (1024^3): static 19.5 38.5 38.7 19.6 -> 29.6 52.0 34.8 29.6 with T = 2 (32-byte
+//                 segments at a 16 MB position stride in pass E): kept static
+static const MWVariant kMW[] = {
+    FUSG_MW_R2C(true, 64, 4, 1, 8, 8, 3, 8),  // 1536: 24 points per lane
+    FUSG_MW_R2C(false, 64, 2, 2, 8, 8, 3, 8),
+    FUSG_MW_C2R(true, 64, 4, 1, 8, 8, 3, 8),
+    FUSG_MW_C2R(false, 64, 2, 1, 8, 8, 3, 8),
+    FUSG_MW_R2C(false, 64, 4, 1, 8, 4, 4, 8),  // 1024: 16 points per lane
+    FUSG_MW_R2C(false, 128, 4, 1, 8, 4, 4, 8),
+    FUSG_MW_C2R(true, 64, 4, 1, 8, 4, 4, 8),
+    FUSG_MW_C2R(false, 128, 4, 1, 8, 4, 4, 8),
+    FUSG_MW_R2C(false, 128, 2, 1, 8, 4, 8, 8),  // 2048: 16 points per lane
+    FUSG_MW_C2R(false, 128, 2, 1, 8, 4, 8, 8),
+};
+#undef FUSG_MW_R2C
+#undef FUSG_MW_C2R
+
+// Transposing pass on multi-warp lines: 1 launched, 0 not applicable, -1 error.  Pruned halves
+// only (zero-padded input of row_to_col, cropped output of col_to_row), as in every apply.
+static int launch_mw(fusg_ctx* ctx, int L, bool r2c, const WArgs& a, cudaStream_t s) {
+  if (a.pm.n) return 0;
+  if (r2c ? 2 * a.in_nvalid > L : 2 * a.out_nvalid > L) return 0;
+  const std::string var_name = "FUSG_MW_" + std::to_string(L) + (r2c ? "_R2C" : "_C2R");
+  const char* ve = getenv(var_name.c_str());
+  const int want = ve ? atoi(ve) : -2;
+  if (want == -1) return 0;
+  const MWVariant* v = nullptr;
+  int seen = 0;
+  for (const auto& c : kMW)
+    if (c.L == L && c.r2c == r2c) {
+      if (want >= 0 ? seen == want : c.def) {
+        v = &c;
+        break;
+      }
+      ++seen;
+    }
+  if (!v) return 0;
+  if (cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v->smem)) != cudaSuccess) {
+    set_error(FUSG_CUDA, "multi-warp transposing pass: cannot configure shared memory");
+    return -1;
+  }
+  const int threads = v->T * v->lanes;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v->fn, threads, v->smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t tiles = int64_t((a.n_inner + v->T - 1) / v->T) * a.n_outer;
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+  v->fn<<<unsigned(grid), threads, v->smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "multi-warp transposing pass");
+    return -1;
+  }
+  return 1;
+}
+
 struct PPMVariant {
   int L, lanes, groups;
   WFn fn;
@@ -987,7 +1205,8 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
     if (r2c || c2r) {
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
-      const int r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
+      int r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
+      if (r == 0) r = launch_mw(ctx, pl.L, r2c, wa, s);
       if (r < 0) return FUSG_CUDA;
       if (r > 0) return FUSG_OK;
     }

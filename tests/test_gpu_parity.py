@@ -95,7 +95,11 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # Nz = 768 / 1024: Pz = 1536 / 2048 (two- / four-warp lines)
                                   (3, 2, 768), (2, 3, 1024),
                                   # Nz = 600 / 900: Pz = 1536 / 2048 preferred over 1200 / 1800
-                                  (2, 2, 600), (2, 1, 900)])
+                                  (2, 2, 600), (2, 1, 900),
+                                  # Nx / Ny = 512, 768, 1024: Px / Py = 1024, 1536, 2048 (multi-
+                                  # warp-line transposing passes; ragged T-line tiles)
+                                  (512, 5, 3), (3, 512, 4), (768, 3, 2), (2, 768, 3),
+                                  (1024, 2, 2), (2, 1024, 2)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
