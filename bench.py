@@ -420,7 +420,7 @@ def run_gpu_sharded(args, world, rank, local):
     # fused peer-store transposes (default when the padded x/y lengths allow): gather every
     # rank's CUDA IPC handles and map the peers' x-slab / A buffers
     transport = args.transport
-    if transport == "p2p" and not (set(K_padded(g)[:2]) <= {256, 512, 768}):
+    if transport == "p2p" and not (set(K_padded(g)[:2]) <= {256, 512, 768, 1024, 1536, 2048}):
         transport = "nccl"
     if transport == "p2p":
         mine = torch.frombuffer(bytearray(K.ipc_handles()), dtype=torch.uint8).to(f"cuda:{local}")

@@ -712,6 +712,19 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
 //   mw_col_to_row (D, E): the CTA stages the next [pos][T] column tile (swizzled) by cp.async
 //     while each group transforms its column of the current one and stores its output row from
 //     registers.
+// the line's exchange barrier: __syncwarp for one-warp lines, a named barrier (id 1 + group)
+// over the group's warps otherwise
+template <int LANES>
+struct LineSync {
+  using type = GroupSync<LANES>;
+  static __device__ __forceinline__ type make(int grp) { return type{1 + grp}; }
+};
+template <>
+struct LineSync<32> {
+  using type = WarpSync;
+  static __device__ __forceinline__ type make(int) { return type{}; }
+};
+
 template <int T>
 __device__ __forceinline__ int mtile_at(int pos, int t) { return pos * T + (t ^ ((pos / (8 / T)) & (T - 1))); }
 
@@ -731,7 +744,7 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_row_to_col(WArgs a) {
   static_assert(T == 2 || T == 4 || T == 8, "tile lines");
   extern __shared__ double2 sm[];
   const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
-  const GroupSync<LANES> sync{1 + grp};
+  const typename LineSync<LANES>::type sync = LineSync<LANES>::make(grp);
   double2* const xb = sm + grp * SM::XSTRIDE;
   double2* const sb = sm + T * SM::XSTRIDE + grp * (L / 2);  // staged input row (pruned: < L/2)
   const int ntiles_i = (a.n_inner + T - 1) / T;
@@ -778,12 +791,19 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_row_to_col(WArgs a) {
       const int pos = e / T, t = e % T;
       if (t < lines_ok) {
         const double2 x = sm[t * SM::XSTRIDE + swz(pos)];
-        base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+        const double2 y = (a.scale == 1.0) ? x : cscale(x, a.scale);
+        if (a.pm.n == 0) {
+          base[t * a.out_si + pos * a.out_sp] = y;
+        } else {  // fused transpose: the segment goes straight to the rank owning it
+          const int q = a.pm.owner(a.pm.by_pos ? pos : i0 + t);
+          a.pm.base[q][a.pm.off[q] + int64_t(i0 + t) * a.out_si + int64_t(k) * a.pm.sk[q] + int64_t(pos) * a.out_sp] = y;
+        }
       }
     }
     __syncthreads();  // X read out before the next tile's first exchange
   }
   cp_async_wait0();
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
 
 template <class RL, int LANES, int T, int MINB>
@@ -794,7 +814,7 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
   static_assert(T == 2 || T == 4 || T == 8, "tile lines");
   extern __shared__ double2 sm[];
   const int grp = threadIdx.x / LANES, lane = threadIdx.x % LANES;
-  const GroupSync<LANES> sync{1 + grp};
+  const typename LineSync<LANES>::type sync = LineSync<LANES>::make(grp);
   double2* const tile = sm + T * SM::XSTRIDE;
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
@@ -832,10 +852,16 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
     prefetch(tix + gridDim.x);
     const int line = i0 + (ok ? grp : 0);
     RegsIn vin{v};
-    RowOut dst{a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk, 1, a.out_nvalid, ok, a.scale};
+    double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
+    if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
+      const int q = a.pm.owner(line);
+      orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
+    }
+    RowOut dst{orow, 1, a.out_nvalid, ok, a.scale};
     warp_fft<RL, LANES, true, 2>(v, ex, lane, tw, vin, dst, sync);  // cropped output half
   }
   cp_async_wait0();
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
 
 struct MWVariant {
@@ -860,6 +886,9 @@ struct MWVariant {
 //   1536 (768^3): static 8.8 17.4 17.8 8.5 -> 6.7 12.7 11.0 6.3 (apply 86.1 -> 70.4 ms);
 //                 T = 2 tiles: 12.5 14.0 10.8 11.6
 //   1024 (512^3): static 1.95 3.75 3.93 2.03 -> r2c 1.96 3.76 (kept static), c2r 3.33 1.88
+//   512 (cfg2): pp warp kernels 0.156 0.297 0.344 0.178 -> c2r on 4-line tiles (3 CTAs, 12
+//                 warps per SM) 0.295 0.166 (apply 1.861 -> 1.800 ms); 8-line tiles 0.348 0.180;
+//                 4 CTAs at 128 registers 0.301 0.172; 2-line tiles 0.349+; r2c 0.18 0.34 (kept warp)
 //   2048 (1024^3): static 19.5 38.5 38.7 19.6 -> 29.6 52.0 34.8 29.6 with T = 2 (32-byte
 //                 segments at a 16 MB position stride in pass E): kept static
 static const MWVariant kMW[] = {
@@ -871,6 +900,10 @@ static const MWVariant kMW[] = {
     FUSG_MW_R2C(false, 128, 4, 1, 8, 4, 4, 8),
     FUSG_MW_C2R(true, 64, 4, 1, 8, 4, 4, 8),
     FUSG_MW_C2R(false, 128, 4, 1, 8, 4, 4, 8),
+    FUSG_MW_R2C(false, 32, 4, 3, 8, 8, 8),  // 512: one-warp lines, 4- / 8-line tiles
+    FUSG_MW_R2C(false, 32, 8, 1, 8, 8, 8),
+    FUSG_MW_C2R(true, 32, 4, 3, 8, 8, 8),
+    FUSG_MW_C2R(false, 32, 8, 1, 8, 8, 8),
     FUSG_MW_R2C(false, 128, 2, 1, 8, 4, 8, 8),  // 2048: 16 points per lane
     FUSG_MW_C2R(false, 128, 2, 1, 8, 4, 8, 8),
 };
@@ -880,22 +913,24 @@ static const MWVariant kMW[] = {
 // Transposing pass on multi-warp lines: 1 launched, 0 not applicable, -1 error.  Pruned halves
 // only (zero-padded input of row_to_col, cropped output of col_to_row), as in every apply.
 static int launch_mw(fusg_ctx* ctx, int L, bool r2c, const WArgs& a, cudaStream_t s) {
-  if (a.pm.n) return 0;
   if (r2c ? 2 * a.in_nvalid > L : 2 * a.out_nvalid > L) return 0;
   const std::string var_name = "FUSG_MW_" + std::to_string(L) + (r2c ? "_R2C" : "_C2R");
   const char* ve = getenv(var_name.c_str());
   const int want = ve ? atoi(ve) : -2;
   if (want == -1) return 0;
   const MWVariant* v = nullptr;
+  const MWVariant* first = nullptr;
   int seen = 0;
   for (const auto& c : kMW)
     if (c.L == L && c.r2c == r2c) {
+      if (!first) first = &c;
       if (want >= 0 ? seen == want : c.def) {
         v = &c;
         break;
       }
       ++seen;
     }
+  if (!v && a.pm.n && want < 0) v = first;  // fused peer stores need a transposing kernel
   if (!v) return 0;
   if (cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v->smem)) != cudaSuccess) {
     set_error(FUSG_CUDA, "multi-warp transposing pass: cannot configure shared memory");
@@ -1205,8 +1240,8 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
     if (r2c || c2r) {
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
-      int r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
-      if (r == 0) r = launch_mw(ctx, pl.L, r2c, wa, s);
+      int r = launch_mw(ctx, pl.L, r2c, wa, s);
+      if (r == 0) r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
       if (r < 0) return FUSG_CUDA;
       if (r > 0) return FUSG_OK;
     }
@@ -1434,9 +1469,10 @@ fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap&
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   WArgs a{f, Nx, int64_t(Ny) * Nx, 1, Nx, nullptr, 1, Ny, int64_t(Nz) * Ny, K->P[0], 1.0,
           Ny, K->nz, K->plan[0].tw, KOct{}, pm};
-  const int r = launch_warp(K->ctx, K->P[0], kWRowToCol, false, a, s);
+  int r = launch_mw(K->ctx, K->P[0], true, a, s);
+  if (r == 0) r = launch_warp(K->ctx, K->P[0], kWRowToCol, false, a, s);
   if (r < 0) return FUSG_CUDA;
-  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a warp-engine padded x length (256, 512, 768)");
+  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a padded x length of 256, 512, 768, 1024 or 1536");
   return FUSG_OK;
 }
 
@@ -1445,9 +1481,10 @@ fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t 
   const int Py = K->P[1];
   const int64_t PyNz = int64_t(Py) * Nz;
   WArgs a{K->bufB, 1, PyNz, Nz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
-  const int r = launch_warp(K->ctx, Py, kWColToRow, true, a, s);
+  int r = launch_mw(K->ctx, Py, false, a, s);
+  if (r == 0) r = launch_warp(K->ctx, Py, kWColToRow, true, a, s);
   if (r < 0) return FUSG_CUDA;
-  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a warp-engine padded y length (256, 512, 768)");
+  if (r == 0) return set_error(FUSG_INVALID_ARGUMENT, "fused transposes need a padded y length of 256, 512, 768, 1024 or 1536");
   return FUSG_OK;
 }
 

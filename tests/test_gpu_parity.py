@@ -412,7 +412,9 @@ def test_slab_sharded_apply_loopback_is_bitwise_unsharded(ctx, dims, G):
 
 
 @pytest.mark.parametrize("dims,G", [((128, 128, 19), 2), ((128, 126, 19), 3), ((256, 255, 9), 4),
-                                    ((128, 128, 40), 8), ((127, 128, 23), 7)])
+                                    ((128, 128, 40), 8), ((127, 128, 23), 7),
+                                    # Px = 1536 / Py = 1024: the multi-warp-line transposing kernels
+                                    ((768, 512, 5), 3)])
 def test_slab_fused_peer_transposes_loopback_is_bitwise_unsharded(ctx, dims, G):
     # The transposes fused into passes A and D (peer stores, no exchange buffers): every rank's
     # pass A writes each kx segment into the owner's x-slab, pass D each z-row into the owner's
@@ -420,7 +422,7 @@ def test_slab_fused_peer_transposes_loopback_is_bitwise_unsharded(ctx, dims, G):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
     k = fus.complex_wavenumber(water(), 1.1e6, 2)
-    assert fus.padded_dims(g)[0] in (256, 512) and fus.padded_dims(g)[1] in (256, 512)
+    assert fus.padded_dims(g)[0] in (256, 512, 1536) and fus.padded_dims(g)[1] in (256, 512, 1024)
     f = fus.random_vector(g.count(), 9)
     want = fus.GreenKernel(g, k).apply(f, 0.5)
     got = fus.apply_slab_loopback(g, k, f, G, 0.5, transport="p2p")
@@ -430,7 +432,7 @@ def test_slab_fused_peer_transposes_loopback_is_bitwise_unsharded(ctx, dims, G):
 def test_slab_fused_transposes_need_warp_lengths(ctx):
     g = fus.make_grid([0, 0, 0], [37e-4, 20e-4, 19e-4], 1e-4, 2)  # Px = 80: no transposing warp kernel
     k = fus.complex_wavenumber(water(), 1.1e6, 2)
-    with pytest.raises(ValueError, match="warp-engine padded x length"):
+    with pytest.raises(ValueError, match="fused transposes need a padded x length"):
         fus.apply_slab_loopback(g, k, fus.random_vector(g.count(), 1), 2, transport="p2p")
 
 
