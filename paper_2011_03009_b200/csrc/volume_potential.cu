@@ -525,10 +525,14 @@ struct PPConvSmem {
   static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;  // K^ row (L/2 + 1), padded to 32 B
   static constexpr int STAGE = PRUNED ? L / 2 : L;      // staged input positions
   static constexpr int PER_WARP = L + STAGE + KROW;      // double2 elements
-  static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2);
+  // + two mbarriers per warp (bulk staging: input row, K^ row)
+  static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2) + kPPWarps * 2 * sizeof(uint64_t);
 };
 
-template <class RL, int LANES, bool PRUNED>
+// BULK: the input row and the K^ row are staged by one lane's 1-D bulk copy (TMA) into linear
+// buffers, completion tracked by the warp's two mbarriers; else by per-lane cp.async into a
+// swizzled S (measured: the LDGSTS path costs 2.4x its ideal shared wavefronts).
+template <class RL, int LANES, bool PRUNED, bool BULK>
 __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) warp_row_conv_pp(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
@@ -544,6 +548,16 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
   double2* const xb = sm + size_t(w) * SM::PER_WARP;
   double2* const sb = xb + L;
   double2* const kb = sb + SM::STAGE;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(kPPWarps) * SM::PER_WARP) + 2 * w;
+  if constexpr (BULK) {
+    if (lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+  }
+  unsigned ph_in = 0, ph_k = 0;
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -557,18 +571,26 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
       int ky, kx;
       coords(line, ky, kx);
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
-      for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(sb + swz(pos), in + pos);
+      if constexpr (BULK) {
+        if (lane == 0) bulk_stage(sb, in, unsigned(a.in_nvalid) * sizeof(double2), bars);
+      } else {
+        for (int pos = lane; pos < a.in_nvalid; pos += 32) cp_async16(sb + swz(pos), in + pos);
+      }
     }
-    cp_async_commit();
+    if constexpr (!BULK) cp_async_commit();
   };
   auto prefetch_k = [&](int64_t line) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
       const double2* kl = a.ko.line(ky, kx);
-      for (int kz = lane; kz < HZ; kz += 32) cp_async16(kb + kz, kl + kz);
+      if constexpr (BULK) {
+        if (lane == 0) bulk_stage(kb, kl, HZ * sizeof(double2), bars + 1);
+      } else {
+        for (int kz = lane; kz < HZ; kz += 32) cp_async16(kb + kz, kl + kz);
+      }
     }
-    cp_async_commit();
+    if constexpr (!BULK) cp_async_commit();
   };
   const TwTable tw{a.tw};
   // PRUNED (host-selected when Nz <= L/2): zero-padded input and cropped output halves run the
@@ -579,20 +601,29 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
   prefetch_in(line);
   prefetch_k(line);
   for (; line < nlines; line += stride) {
-    cp_async_wait0();
-    __syncwarp();  // this line's staged input and K^ row are visible to the whole warp
+    if constexpr (BULK) {
+      mbar_wait(bars, ph_in);  // this line's staged input has landed
+      ph_in ^= 1;
+    } else {
+      cp_async_wait0();
+      __syncwarp();  // this line's staged input and K^ row are visible to the whole warp
+    }
     double2 v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if ((PRUNED && R0 == 8) && (e % R0) >= R0 / 2) continue;  // zero padding: not staged
       const int pos = in_pos<RL, LANES, 0>(lane, e);
-      v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
+      v[e] = pos < a.in_nvalid ? sb[BULK ? pos : swz(pos)] : make_double2(0.0, 0.0);
     }
     __syncwarp();  // S consumed: refill it with the next line while this one is transformed
     prefetch_in(line + stride);
     RegsIn vin{v};
     RegsOut mid{v};
     warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, vin, mid);
+    if constexpr (BULK) {
+      mbar_wait(bars + 1, ph_k);  // this line's K^ row has landed
+      ph_k ^= 1;
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     __syncwarp();  // K^ row consumed
@@ -602,7 +633,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
     warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, vin, dst);
   }
-  cp_async_wait0();
+  if constexpr (!BULK) cp_async_wait0();
 }
 
 using WFn = void (*)(WArgs);
@@ -625,10 +656,10 @@ struct PP64Smem {
   static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;
   static constexpr int STAGE = PRUNED ? L / 2 : L;
   static constexpr int PER_GROUP = L + STAGE + KROW;
-  static constexpr size_t BYTES = size_t(GROUPS) * PER_GROUP * sizeof(double2);
+  static constexpr size_t BYTES = size_t(GROUPS) * PER_GROUP * sizeof(double2) + GROUPS * 2 * sizeof(uint64_t);
 };
 
-template <class RL, int LANES, int GROUPS, int MINB, bool PRUNED>
+template <class RL, int LANES, int GROUPS, int MINB, bool PRUNED, bool BULK>
 __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs a) {
   constexpr int L = RL::len();
   constexpr int E = L / LANES;
@@ -643,6 +674,16 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
   double2* const xb = sm + size_t(grp) * SM::PER_GROUP;
   double2* const sb = xb + L;
   double2* const kb = sb + SM::STAGE;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(GROUPS) * SM::PER_GROUP) + 2 * grp;
+  if constexpr (BULK) {
+    if (lane == 0) {
+      mbar_init(bars, 1);
+      mbar_init(bars + 1, 1);
+      mbar_init_fence();
+    }
+    sync();
+  }
+  unsigned ph_in = 0, ph_k = 0;
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = int64_t(gridDim.x) * GROUPS;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -655,18 +696,26 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
       int ky, kx;
       coords(line, ky, kx);
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
-      for (int pos = lane; pos < a.in_nvalid; pos += LANES) cp_async16(sb + swz(pos), in + pos);
+      if constexpr (BULK) {
+        if (lane == 0) bulk_stage(sb, in, unsigned(a.in_nvalid) * sizeof(double2), bars);
+      } else {
+        for (int pos = lane; pos < a.in_nvalid; pos += LANES) cp_async16(sb + swz(pos), in + pos);
+      }
     }
-    cp_async_commit();
+    if constexpr (!BULK) cp_async_commit();
   };
   auto prefetch_k = [&](int64_t line) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
       const double2* kl = a.ko.line(ky, kx);
-      for (int kz = lane; kz < HZ; kz += LANES) cp_async16(kb + kz, kl + kz);
+      if constexpr (BULK) {
+        if (lane == 0) bulk_stage(kb, kl, HZ * sizeof(double2), bars + 1);
+      } else {
+        for (int kz = lane; kz < HZ; kz += LANES) cp_async16(kb + kz, kl + kz);
+      }
     }
-    cp_async_commit();
+    if constexpr (!BULK) cp_async_commit();
   };
   const TwTable tw{a.tw};
   constexpr int kPin = PRUNED ? 1 : 0, kPout = PRUNED ? 2 : 0;
@@ -675,20 +724,29 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
   prefetch_in(line);
   prefetch_k(line);
   for (; line < nlines; line += stride) {
-    cp_async_wait0();
-    sync();  // the group's staged input and K^ row have landed
+    if constexpr (BULK) {
+      mbar_wait(bars, ph_in);  // the group's staged input has landed
+      ph_in ^= 1;
+    } else {
+      cp_async_wait0();
+      sync();  // the group's staged input and K^ row have landed
+    }
     double2 v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if ((PRUNED && R0 == 8) && (e % R0) >= R0 / 2) continue;
       const int pos = in_pos<RL, LANES, 0>(lane, e);
-      v[e] = pos < a.in_nvalid ? sb[swz(pos)] : make_double2(0.0, 0.0);
+      v[e] = pos < a.in_nvalid ? sb[BULK ? pos : swz(pos)] : make_double2(0.0, 0.0);
     }
     sync();  // staging consumed by the whole group
     prefetch_in(line + stride);
     RegsIn vin{v};
     RegsOut mid{v};
     warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, vin, mid, sync);
+    if constexpr (BULK) {
+      mbar_wait(bars + 1, ph_k);  // the group's K^ row has landed
+      ph_k ^= 1;
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     sync();  // K^ row consumed
@@ -698,7 +756,7 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
     warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, vin, dst, sync);
   }
-  cp_async_wait0();
+  if constexpr (!BULK) cp_async_wait0();
 }
 
 // Transposing passes on multi-warp lines (L = 1024..2048, where a one-warp line spills and an
@@ -954,14 +1012,25 @@ static int launch_mw(fusg_ctx* ctx, int L, bool r2c, const WArgs& a, cudaStream_
   return 1;
 }
 
+// FUSG_BULK=0: pass C stages its rows with per-lane cp.async instead of 1-D bulk copies
+static int bulk_staging() {
+  static const int on = [] {
+    const char* e = getenv("FUSG_BULK");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 struct PPMVariant {
   int L, lanes, groups;
-  WFn fn;
+  WFn fn[2];  // [bulk staging]
   size_t smem;
 };
 #define FUSG_PPM(LANES, GROUPS, MINB, ...)                                                  \
   PPMVariant {                                                                              \
-    Radices<__VA_ARGS__>::len(), LANES, GROUPS, warp_row_conv_pp64<Radices<__VA_ARGS__>, LANES, GROUPS, MINB, true>, \
+    Radices<__VA_ARGS__>::len(), LANES, GROUPS,                                             \
+        {warp_row_conv_pp64<Radices<__VA_ARGS__>, LANES, GROUPS, MINB, true, false>,         \
+         warp_row_conv_pp64<Radices<__VA_ARGS__>, LANES, GROUPS, MINB, true, true>},         \
         PP64Smem<Radices<__VA_ARGS__>::len(), true, GROUPS>::BYTES                          \
   }
 // Variants per length, selected by FUSG_PPM_<L> (index; -1 = none: 512/1024 then run the
@@ -981,7 +1050,7 @@ static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
     const char* e = getenv("FUSG_CONV_PP64");
     return !(e && atoi(e) == 0);
   }();
-  if (!on || 2 * a.in_nvalid > L || 2 * a.out_nvalid > L) return 0;  // pruned halves only
+  if (!on || 2 * a.in_nvalid > L || 2 * a.out_nvalid > L || a.in_nvalid < 1) return 0;  // pruned halves only
   const std::string var_name = "FUSG_PPM_" + std::to_string(L);
   const char* ve = getenv(var_name.c_str());
   const int def = 0;
@@ -992,7 +1061,7 @@ static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
   for (const auto& c : kPPM)
     if (c.L == L && seen++ == want) v = &c;
   if (!v) return 0;
-  const WFn fn = v->fn;
+  const WFn fn = v->fn[bulk_staging()];
   const size_t smem = v->smem;
   const int groups = v->groups, lanes = v->lanes;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
@@ -1021,9 +1090,9 @@ constexpr WFn colrow_pp_ptr() {
   if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_col_to_row_pp<RL, PRUNED>;
   else return nullptr;
 }
-template <class RL, int LN, bool PRUNED>
+template <class RL, int LN, bool PRUNED, bool BULK>
 constexpr WFn conv_pp_ptr() {
-  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32, PRUNED>;
+  if constexpr (LN == 32 && whole_butterflies<RL>(32)) return warp_row_conv_pp<RL, 32, PRUNED, BULK>;
   else return nullptr;
 }
 
@@ -1041,7 +1110,7 @@ struct WarpEntry {
   int L, lanes;
   WFn fwd, inv, conv;
   WFn row_to_col_fwd[2], col_to_row_inv[2];  // transposing passes (LANES = 32), [pruned]
-  WFn conv_pp[2];   // persistent pipelined pass C, [pruned] (nullptr: not available)
+  WFn conv_pp[2][2];  // persistent pipelined pass C, [pruned][bulk staging] (nullptr: not available)
   size_t pp_smem[2];
   WFn col_to_row_pp[2];  // persistent pipelined inverse column -> row (passes D, E), [pruned]
 };
@@ -1053,7 +1122,8 @@ struct WarpEntry {
          transpose_ptr<Radices<__VA_ARGS__>, LN, false, true>()},                              \
         {transpose_ptr<Radices<__VA_ARGS__>, LN, true, false>(),                               \
          transpose_ptr<Radices<__VA_ARGS__>, LN, true, true>()},                               \
-        {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
+        {{conv_pp_ptr<Radices<__VA_ARGS__>, LN, false, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, false, true>()}, \
+         {conv_pp_ptr<Radices<__VA_ARGS__>, LN, true, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true, true>()}}, \
         {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
          PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES},                                  \
         {colrow_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), colrow_pp_ptr<Radices<__VA_ARGS__>, LN, true>()} \
@@ -1062,7 +1132,8 @@ struct WarpEntry {
 #define FUSG_WARP_CONV_ONLY(LN, ...)                                                         \
   WarpEntry {                                                                               \
     Radices<__VA_ARGS__>::len(), LN, nullptr, nullptr, nullptr, {nullptr, nullptr}, {nullptr, nullptr}, \
-        {conv_pp_ptr<Radices<__VA_ARGS__>, LN, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true>()}, \
+        {{conv_pp_ptr<Radices<__VA_ARGS__>, LN, false, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, false, true>()}, \
+         {conv_pp_ptr<Radices<__VA_ARGS__>, LN, true, false>(), conv_pp_ptr<Radices<__VA_ARGS__>, LN, true, true>()}}, \
         {PPConvSmem<Radices<__VA_ARGS__>::len(), false>::BYTES,                                  \
          PPConvSmem<Radices<__VA_ARGS__>::len(), true>::BYTES},                                  \
         {nullptr, nullptr}                                                                       \
@@ -1149,7 +1220,7 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
     return !(e && atoi(e) == 0);
   }();
   const int pruned = 2 * a.in_nvalid <= L && 2 * a.out_nvalid <= L;
-  const WFn conv_pp = we->conv_pp[pruned];
+  const WFn conv_pp = a.in_nvalid >= 1 ? we->conv_pp[pruned][bulk_staging()] : nullptr;
   const size_t pp_smem = we->pp_smem[pruned];
   if (mode == kWConv && use_pp && conv_pp) {
     if (cudaFuncSetAttribute(conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pp_smem)) != cudaSuccess) {
