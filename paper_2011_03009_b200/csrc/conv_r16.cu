@@ -1,0 +1,224 @@
+// Pass C of the apply at padded z length 512 as a 16 x 16 x 2 transform per warp (see below).
+#include <utility>
+#include <cstdlib>
+#include <algorithm>
+
+#include "warp_args.cuh"
+
+namespace fusg {
+
+// Pass C at L = 512, pruned (Nz <= 256 in and out), as 512 = 16 x 16 x 2 on one warp:
+//   stage A  radix 16 in registers over n1 (n = 32 n1 + n2, lane = n2), twiddle W512^(n2 k1);
+//   exchange through shared memory (registers k1 -> registers n2hi, n2 = 2 n2hi + n2lo);
+//   stage B  radix 16 in registers over n2hi, then the last radix 2 over n2lo ACROSS the lane
+//            pair (lane, lane ^ 16) with one half-exchange of 8 values by warp shuffle.
+// Against the radix-8 Stockham kernel (two shared exchanges per transform) this moves half the
+// bytes through the L1/shared data pipe per line (one shared exchange + half a shuffle
+// exchange), the unit that kernel saturates.  The inverse transform is the adjoint, so the
+// spectrum stays in the half-exchanged layout for the K^ multiply and the inverse radix 2
+// starts in-lane.  Layout after the forward transform: lane = 16 b + k1 holds, in slot i,
+// X[k1 + 16 (i + 8 b)] and, in slot i + 8, X[k1 + 16 (i + 8 b) + 256].
+// Exchange buffer: row k1 (32 entries), column n2 ^ (k1 & 7): both access patterns are
+// bank-conflict-free (8 lanes of each 128-byte phase hit 8 distinct 16-byte bank groups).
+struct R16Tw {  // W512^(n2 k) for k = 1..15 from four exact table powers (<= 3 products)
+  const double2* t;  // [w1, w2, w4, w8][lane] in shared memory, shared by the CTA's warps
+  int lane;
+  template <bool CONJ>
+  __device__ __forceinline__ void apply(double2* v) const {
+    auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+    const double2 w1 = t[lane], w2 = t[32 + lane], w4 = t[64 + lane];
+    const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+    v[1] = m(v[1], w1);
+    v[2] = m(v[2], w2);
+    v[3] = m(v[3], w3);
+    v[4] = m(v[4], w4);
+    v[5] = m(v[5], w5);
+    v[6] = m(v[6], w6);
+    v[7] = m(v[7], w7);
+    const double2 w8 = t[96 + lane];
+    v[8] = m(v[8], w8);
+    v[9] = m(v[9], cmul(w8, w1));
+    v[10] = m(v[10], cmul(w8, w2));
+    v[11] = m(v[11], cmul(w8, w3));
+    v[12] = m(v[12], cmul(w8, w4));
+    v[13] = m(v[13], cmul(w8, w5));
+    v[14] = m(v[14], cmul(w8, w6));
+    v[15] = m(v[15], cmul(w8, w7));
+  }
+};
+
+__device__ __forceinline__ double2 shfl_xor_d2(double2 x, int m) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, x.x, m), __shfl_xor_sync(0xffffffffu, x.y, m));
+}
+__device__ __forceinline__ double2 sel_d2(bool p, double2 a, double2 b) { return p ? a : b; }
+
+// radix 2 over n2lo with twiddle W32^(q1 n2lo), q1 = i + 8 b (forward), and its adjoint
+template <int I>
+__device__ __forceinline__ void r16_fwd_r2(double2* v, bool b) {
+  const double2 send = sel_d2(b, v[I], v[I + 8]);  // lane b keeps q1 in [8b, 8b + 8)
+  const double2 recv = shfl_xor_d2(send, 16);
+  const double2 z0 = sel_d2(b, recv, v[I]);
+  const double2 z1 = sel_d2(b, v[I + 8], recv);
+  double2 t = w32<false, I>(z1);
+  t = sel_d2(b, rot90<false>(t), t);  // W32^8 = -i
+  v[I] = cadd(z0, t);
+  v[I + 8] = csub(z0, t);
+}
+template <int I>
+__device__ __forceinline__ void r16_inv_r2(double2* v, bool b) {
+  const double2 z0 = cadd(v[I], v[I + 8]);
+  double2 z1 = w32<true, I>(csub(v[I], v[I + 8]));
+  z1 = sel_d2(b, rot90<true>(z1), z1);
+  const double2 send = sel_d2(b, z0, z1);  // lane b collects Z_b[q1] for every q1
+  const double2 recv = shfl_xor_d2(send, 16);
+  v[I] = sel_d2(b, recv, z0);
+  v[I + 8] = sel_d2(b, z1, recv);
+}
+template <bool INV, int... Is>
+__device__ __forceinline__ void r16_r2_all(double2* v, bool b, std::integer_sequence<int, Is...>) {
+  if constexpr (INV) (r16_inv_r2<Is>(v, b), ...);
+  else (r16_fwd_r2<Is>(v, b), ...);
+}
+
+__device__ __forceinline__ int r16_ex(int row, int col) { return row * 32 + (col ^ (row & 7)); }
+
+// per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
+constexpr size_t kR16SmemBytes = PPConvSmem<512, true>::BYTES + 4 * 32 * sizeof(double2);
+
+template <int MINB>
+__global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a) {
+  constexpr int L = 512;
+  constexpr int HZ = L / 2 + 1;
+  using SM = PPConvSmem<L, true>;
+  extern __shared__ double2 sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* const xb = sm + size_t(w) * SM::PER_WARP;
+  double2* const sb = xb + L;
+  double2* const kb = sb + SM::STAGE;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(kPPWarps) * SM::PER_WARP) + 2 * w;
+  if (lane == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+  unsigned ph_in = 0, ph_k = 0;
+  const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t stride = int64_t(gridDim.x) * kPPWarps;
+  const bool mirror = a.n_outer == a.ko.Px;
+  auto coords = [&](int64_t line, int& ky, int& kx) {
+    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
+    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+  };
+  auto prefetch_in = [&](int64_t line) {
+    if (line < nlines && lane == 0) {
+      int ky, kx;
+      coords(line, ky, kx);
+      bulk_stage(sb, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(a.in_nvalid) * sizeof(double2), bars);
+    }
+  };
+  auto prefetch_k = [&](int64_t line) {
+    if (line < nlines && lane == 0) {
+      int ky, kx;
+      coords(line, ky, kx);
+      bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
+    }
+  };
+  double2* const tws = sm + size_t(kPPWarps) * SM::PER_WARP + 4;  // after the 8 mbarriers (64 B)
+  if (w == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane << j) & (L - 1)));
+  }
+  __syncthreads();
+  const R16Tw tw{tws, lane};
+  const bool b = lane >= 16;
+  const int k1 = lane & 15;
+  const auto I8 = std::make_integer_sequence<int, 8>{};
+  int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
+  prefetch_in(line);
+  prefetch_k(line);
+  for (; line < nlines; line += stride) {
+    mbar_wait(bars, ph_in);
+    ph_in ^= 1;
+    double2 v[16];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int pos = lane + 32 * e;
+      v[e] = pos < a.in_nvalid ? sb[pos] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();  // S consumed: refill it with the next line while this one is transformed
+    prefetch_in(line + stride);
+    // forward stage A (upper half zero) and its twiddle
+    dft16_half_in<false>(v);
+    tw.apply<false>(v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xb[r16_ex(k, lane)] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 16; ++h) v[h] = xb[r16_ex(k1, 2 * h + int(b))];
+    // forward stage B and the cross-lane radix 2
+    dft16<false>(v);
+    r16_r2_all<false>(v, b, I8);
+    mbar_wait(bars + 1, ph_k);
+    ph_k ^= 1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
+      v[i] = cmul(v[i], kb[p]);
+      v[i + 8] = cmul(v[i + 8], kb[256 - p]);
+    }
+    __syncwarp();  // K^ row consumed
+    prefetch_k(line + stride);
+    // inverse: radix 2 (in-lane) + half-exchange back, stage B, exchange, twiddle, stage A
+    r16_r2_all<true>(v, b, I8);
+    dft16<true>(v);
+#pragma unroll
+    for (int h = 0; h < 16; ++h) xb[r16_ex(k1, 2 * h + int(b))] = v[h];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xb[r16_ex(k, lane)];
+    tw.apply<true>(v);
+    dft16_half_out<true>(v);
+    int ky, kx;
+    coords(line, ky, kx);
+    double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int pos = lane + 32 * e;
+      if (pos < a.out_nvalid) out[pos] = (a.scale == 1.0) ? v[e] : cscale(v[e], a.scale);
+    }
+    __syncwarp();  // every lane has read the exchange buffer before the next line writes it
+  }
+}
+
+
+int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
+  static const bool on = [] {  // FUSG_CONV_R16=0 selects the radix-8 Stockham pass C at 512
+    const char* e = getenv("FUSG_CONV_R16");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on || 2 * a.in_nvalid > 512 || 2 * a.out_nvalid > 512 || a.in_nvalid < 1) return 0;
+  const auto fn = warp_row_conv_r16<FUSG_PP_MINB>;
+  const size_t smem = kR16SmemBytes;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+    set_error(FUSG_CUDA, "pass C (16x16x2): cannot configure shared memory");
+    return -1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPPWarps * 32, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  const int64_t lines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
+  fn<<<unsigned(grid), kPPWarps * 32, smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "pass C (16x16x2)");
+    return -1;
+  }
+  return 1;
+}
+
+}  // namespace fusg

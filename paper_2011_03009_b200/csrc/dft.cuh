@@ -169,6 +169,81 @@ __device__ __forceinline__ void dft16(double2* a) {
     for (int q2 = 0; q2 < 4; ++q2) a[q1 + 4 * q2] = t[4 * q1 + q2];
 }
 
+// Pruned radix-16: inputs a[8..15] are zero (zero-padded upper half), so each inner DFT4
+// sees two inputs.
+template <bool INV>
+__device__ __forceinline__ void dft16_half_in(double2* a) {
+#pragma unroll
+  for (int r2 = 0; r2 < 4; ++r2) {
+    const double2 x0 = a[r2], x1 = a[r2 + 4], x1r = rot90<INV>(x1);
+    a[r2] = cadd(x0, x1);
+    a[r2 + 4] = cadd(x0, x1r);
+    a[r2 + 8] = csub(x0, x1);
+    a[r2 + 12] = csub(x0, x1r);
+  }
+  a[5] = w16<INV, 1>(a[5]);
+  a[9] = w16<INV, 2>(a[9]);
+  a[13] = w16<INV, 3>(a[13]);
+  a[6] = w16<INV, 2>(a[6]);
+  a[10] = w16<INV, 4>(a[10]);
+  a[14] = w16<INV, 6>(a[14]);
+  a[7] = w16<INV, 3>(a[7]);
+  a[11] = w16<INV, 6>(a[11]);
+  a[15] = w16<INV, 9>(a[15]);
+#pragma unroll
+  for (int q1 = 0; q1 < 4; ++q1) dft4<INV>(a[4 * q1], a[4 * q1 + 1], a[4 * q1 + 2], a[4 * q1 + 3]);
+  double2 t[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t[i] = a[i];
+#pragma unroll
+  for (int q1 = 0; q1 < 4; ++q1)
+#pragma unroll
+    for (int q2 = 0; q2 < 4; ++q2) a[q1 + 4 * q2] = t[4 * q1 + q2];
+}
+
+// Pruned radix-16: only X[0..7] are kept (cropped upper half) in a[0..7].
+template <bool INV>
+__device__ __forceinline__ void dft16_half_out(double2* a) {
+#pragma unroll
+  for (int r2 = 0; r2 < 4; ++r2) dft4<INV>(a[r2], a[r2 + 4], a[r2 + 8], a[r2 + 12]);
+  a[5] = w16<INV, 1>(a[5]);
+  a[9] = w16<INV, 2>(a[9]);
+  a[13] = w16<INV, 3>(a[13]);
+  a[6] = w16<INV, 2>(a[6]);
+  a[10] = w16<INV, 4>(a[10]);
+  a[14] = w16<INV, 6>(a[14]);
+  a[7] = w16<INV, 3>(a[7]);
+  a[11] = w16<INV, 6>(a[11]);
+  a[15] = w16<INV, 9>(a[15]);
+  // outer DFT4 over a[4 q1 .. 4 q1 + 3], outputs q2 = 0, 1 only: X[q1 + 4 q2]
+  double2 x[8];
+#pragma unroll
+  for (int q1 = 0; q1 < 4; ++q1) {
+    const double2 t0 = cadd(a[4 * q1], a[4 * q1 + 2]), t1 = csub(a[4 * q1], a[4 * q1 + 2]);
+    const double2 t2 = cadd(a[4 * q1 + 1], a[4 * q1 + 3]), t3 = rot90<INV>(csub(a[4 * q1 + 1], a[4 * q1 + 3]));
+    x[q1] = cadd(t0, t2);
+    x[q1 + 4] = cadd(t1, t3);
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = x[i];
+}
+
+// multiply by w32^e, w32 = exp(-+2 pi i / 32), e in 0..7 (compile-time)
+template <bool INV, int E>
+__device__ __forceinline__ double2 w32(double2 a) {
+  static_assert(E >= 0 && E < 8, "w32: e in 0..7");
+  if constexpr ((E & 1) == 0) {
+    return w16<INV, E / 2>(a);
+  } else {
+    // cos, sin of 2 pi e / 32 for odd e
+    constexpr double cs[4] = {0.98078528040323044912618, 0.83146961230254523707879, 0.55557023301960222474283,
+                              0.19509032201612826784828};
+    constexpr double cq = cs[E / 2], sq = cs[3 - E / 2];
+    constexpr double si = INV ? sq : -sq;  // w = (cq, -+sq)
+    return make_double2(cq * a.x - si * a.y, cq * a.y + si * a.x);
+  }
+}
+
 template <bool INV>
 __device__ __forceinline__ void dft3(double2* a) {
   const double2 t1 = cadd(a[1], a[2]);

@@ -20,9 +20,11 @@
 #include <type_traits>
 #include <cstdio>
 #include <vector>
+#include <utility>
 
 #include "internal.hpp"
 #include "static_kernels.cuh"
+#include "warp_args.cuh"
 
 namespace fusg {
 
@@ -298,19 +300,7 @@ static const std::vector<int>& static_lengths(bool conv) {
 // straight from global memory by their own lane group; columns (y, z passes) are staged as a
 // swizzled [pos][8] tile with one coalesced cooperative load and store (2 CTA barriers per
 // tile), the transforms in between use __syncwarp only.
-struct WArgs {
-  const double2* in;
-  int64_t in_si, in_sk, in_sp;
-  int in_nvalid;
-  double2* out;
-  int64_t out_si, out_sk, out_sp;
-  int out_nvalid;
-  double scale;
-  int n_inner, n_outer;
-  const double2* tw;
-  KOct ko;     // pass C only
-  PeerMap pm;  // fused peer-memory transpose stores (passes A and D of the sharded apply)
-};
+
 
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
 #ifndef FUSG_WARP_MINB
@@ -464,13 +454,6 @@ __global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_line_pass(W
   warp_fft<RL, LANES, INV>(v, ex, lane, TwTable{a.tw}, src, dst);
 }
 
-// mirror-interleaved order 0, 1, P-1, 2, P-2, ...: lines ky and Py-ky (kx and Px-kx) read the
-// same folded K^ row and run close together, so the second read hits L2.
-__device__ __forceinline__ int interleave_index(int r, int P) {
-  if (r == 0) return 0;
-  const int m = (r + 1) >> 1;
-  return (r & 1) ? m : P - m;
-}
 
 // Pass C on rows of B [kx][ky][z] (z contiguous): forward z, * K^ (octant row [kx][ky][kz],
 // contiguous), inverse z; in place.  n_inner = Py, n_outer = Px.
@@ -512,22 +495,7 @@ __global__ void __launch_bounds__(kWarpThreads, FUSG_WARP_MINB) warp_row_conv(WA
 // forward stage has read it into registers, and the next K^ row right after the spectral
 // multiply, so both copies overlap the rest of the line's transform without a second buffer.
 // The small footprint (~16 KB per warp) lets 12 warps share an SM.  No CTA barriers.
-constexpr int kPPWarps = 4;  // warps per CTA
-#ifndef FUSG_PP_MINB
-#define FUSG_PP_MINB 3  // CTAs per SM the register budget targets (3: <= 168 registers)
-#endif
-// L > 512: 24+ values per lane and ~25 KB of shared memory per warp allow 2 CTAs per SM
-template <int L>
-constexpr int pp_min_blocks() { return L <= 512 ? FUSG_PP_MINB : 2; }
 
-template <int L, bool PRUNED>
-struct PPConvSmem {
-  static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;  // K^ row (L/2 + 1), padded to 32 B
-  static constexpr int STAGE = PRUNED ? L / 2 : L;      // staged input positions
-  static constexpr int PER_WARP = L + STAGE + KROW;      // double2 elements
-  // + two mbarriers per warp (bulk staging: input row, K^ row)
-  static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2) + kPPWarps * 2 * sizeof(uint64_t);
-};
 
 // BULK: the input row and the K^ row are staged by one lane's 1-D bulk copy (TMA) into linear
 // buffers, completion tracked by the warp's two mbarriers; else by per-lane cp.async into a
@@ -1222,6 +1190,10 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
   const int pruned = 2 * a.in_nvalid <= L && 2 * a.out_nvalid <= L;
   const WFn conv_pp = a.in_nvalid >= 1 ? we->conv_pp[pruned][bulk_staging()] : nullptr;
   const size_t pp_smem = we->pp_smem[pruned];
+  if (mode == kWConv && use_pp && L == 512 && bulk_staging()) {  // 16 x 16 x 2 pass C (conv_r16.cu)
+    const int r = launch_conv_r16(ctx, a, s);
+    if (r != 0) return r;
+  }
   if (mode == kWConv && use_pp && conv_pp) {
     if (cudaFuncSetAttribute(conv_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pp_smem)) != cudaSuccess) {
       set_error(FUSG_CUDA, "persistent pass C: cannot configure shared memory");

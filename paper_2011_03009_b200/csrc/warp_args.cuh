@@ -1,0 +1,52 @@
+// Arguments and shared-memory geometry of the warp-engine passes (volume_potential.cu) and the
+// 16x16x2 pass C (conv_r16.cu).
+#pragma once
+#include "internal.hpp"
+#include "static_kernels.cuh"
+#include "fft_warp.cuh"
+
+namespace fusg {
+
+struct WArgs {
+  const double2* in;
+  int64_t in_si, in_sk, in_sp;
+  int in_nvalid;
+  double2* out;
+  int64_t out_si, out_sk, out_sp;
+  int out_nvalid;
+  double scale;
+  int n_inner, n_outer;
+  const double2* tw;
+  KOct ko;     // pass C only
+  PeerMap pm;  // fused peer-memory transpose stores (passes A and D of the sharded apply)
+};
+
+// mirror-interleaved order 0, 1, P-1, 2, P-2, ...: lines ky and Py-ky (kx and Px-kx) read the
+// same folded K^ row and run close together, so the second read hits L2.
+__device__ __forceinline__ int interleave_index(int r, int P) {
+  if (r == 0) return 0;
+  const int m = (r + 1) >> 1;
+  return (r & 1) ? m : P - m;
+}
+
+constexpr int kPPWarps = 4;  // warps per CTA
+#ifndef FUSG_PP_MINB
+#define FUSG_PP_MINB 3  // CTAs per SM the register budget targets (3: <= 168 registers)
+#endif
+// L > 512: 24+ values per lane and ~25 KB of shared memory per warp allow 2 CTAs per SM
+template <int L>
+constexpr int pp_min_blocks() { return L <= 512 ? FUSG_PP_MINB : 2; }
+
+template <int L, bool PRUNED>
+struct PPConvSmem {
+  static constexpr int KROW = ((L / 2 + 1) + 1) & ~1;  // K^ row (L/2 + 1), padded to 32 B
+  static constexpr int STAGE = PRUNED ? L / 2 : L;      // staged input positions
+  static constexpr int PER_WARP = L + STAGE + KROW;      // double2 elements
+  // + two mbarriers per warp (bulk staging: input row, K^ row)
+  static constexpr size_t BYTES = size_t(kPPWarps) * PER_WARP * sizeof(double2) + kPPWarps * 2 * sizeof(uint64_t);
+};
+
+// pass C at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16.cu)
+int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
+
+}  // namespace fusg

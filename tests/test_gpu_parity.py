@@ -87,7 +87,7 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   (16, 16, 16), (25, 30, 7), (64, 3, 40),
                                   # Pz = 256 / 512 with pruned halves: the two-stage pass C
                                   # (odd line count 9 x 5 exercises the half-filled last pair)
-                                  (9, 7, 128), (5, 3, 256), (3, 2, 100), (6, 5, 129),
+                                  (9, 7, 128), (5, 3, 256), (3, 2, 100), (6, 5, 129), (4, 3, 200),
                                   # Nz = 300 / 341: Pz = 768 (multi-warp pass C) instead of 600 / 686
                                   (3, 2, 300), (2, 3, 341),
                                   # Nz = 490: Pz = 1024 (two-warp-line pass C)
