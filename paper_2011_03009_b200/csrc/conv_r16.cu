@@ -20,12 +20,21 @@ namespace fusg {
 // X[k1 + 16 (i + 8 b)] and, in slot i + 8, X[k1 + 16 (i + 8 b) + 256].
 // Exchange buffer: row k1 (32 entries), column n2 ^ (k1 & 7): both access patterns are
 // bank-conflict-free (8 lanes of each 128-byte phase hit 8 distinct 16-byte bank groups).
-struct R16Tw {  // W512^(n2 k) for k = 1..15 from four exact table powers (<= 3 products)
-  const double2* t;  // [w1, w2, w4, w8][lane] in shared memory, shared by the CTA's warps
+// TAB = false: from four exact table powers [w1, w2, w4, w8][lane] (<= 3 products);
+// TAB = true: all fifteen from an exact [k][lane] table (more shared loads, fewer FP64 ops).
+// Either table lives in shared memory, shared by the CTA's warps.
+template <bool TAB>
+struct R16Tw {  // W512^(n2 k) for k = 1..15
+  const double2* t;
   int lane;
   template <bool CONJ>
   __device__ __forceinline__ void apply(double2* v) const {
     auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+    if constexpr (TAB) {
+#pragma unroll
+      for (int k = 1; k < 16; ++k) v[k] = m(v[k], t[32 * k + lane]);
+      return;
+    }
     const double2 w1 = t[lane], w2 = t[32 + lane], w4 = t[64 + lane];
     const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
     v[1] = m(v[1], w1);
@@ -83,9 +92,10 @@ __device__ __forceinline__ void r16_r2_all(double2* v, bool b, std::integer_sequ
 __device__ __forceinline__ int r16_ex(int row, int col) { return row * 32 + (col ^ (row & 7)); }
 
 // per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
-constexpr size_t kR16SmemBytes = PPConvSmem<512, true>::BYTES + 4 * 32 * sizeof(double2);
+template <bool TAB>
+constexpr size_t r16_smem_bytes() { return PPConvSmem<512, true>::BYTES + (TAB ? 16 : 4) * 32 * sizeof(double2); }
 
-template <int MINB>
+template <int MINB, bool TAB>
 __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a) {
   constexpr int L = 512;
   constexpr int HZ = L / 2 + 1;
@@ -106,9 +116,11 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
-  auto coords = [&](int64_t line, int& ky, int& kx) {
-    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
-    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+  auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
+    const unsigned l = unsigned(line), ni = unsigned(a.n_inner);
+    const unsigned q = l / ni;
+    ky = interleave_index(int(l - q * ni), a.ko.Py);
+    kx = mirror ? interleave_index(int(q), a.ko.Px) : int(q);
   };
   auto prefetch_in = [&](int64_t line) {
     if (line < nlines && lane == 0) {
@@ -126,11 +138,15 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
   };
   double2* const tws = sm + size_t(kPPWarps) * SM::PER_WARP + 4;  // after the 8 mbarriers (64 B)
   if (w == 0) {
+    if constexpr (TAB) {
+      for (int j = 0; j < 16; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane * j) & (L - 1)));
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane << j) & (L - 1)));
+      for (int j = 0; j < 4; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane << j) & (L - 1)));
+    }
   }
   __syncthreads();
-  const R16Tw tw{tws, lane};
+  const R16Tw<TAB> tw{tws, lane};
   const bool b = lane >= 16;
   const int k1 = lane & 15;
   const auto I8 = std::make_integer_sequence<int, 8>{};
@@ -198,8 +214,14 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     return !(e && atoi(e) == 0);
   }();
   if (!on || 2 * a.in_nvalid > 512 || 2 * a.out_nvalid > 512 || a.in_nvalid < 1) return 0;
-  const auto fn = warp_row_conv_r16<FUSG_PP_MINB>;
-  const size_t smem = kR16SmemBytes;
+  static const int tab = [] {  // FUSG_R16_TAB=1: all fifteen twiddles from the shared table
+    const char* e = getenv("FUSG_R16_TAB");
+    return e ? atoi(e) : 0;
+  }();
+  const int64_t nl = int64_t(a.n_inner) * a.n_outer;
+  if (nl >= (int64_t(1) << 31)) return 0;
+  const auto fn = tab ? warp_row_conv_r16<FUSG_PP_MINB, true> : warp_row_conv_r16<FUSG_PP_MINB, false>;
+  const size_t smem = tab ? r16_smem_bytes<true>() : r16_smem_bytes<false>();
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
     set_error(FUSG_CUDA, "pass C (16x16x2): cannot configure shared memory");
     return -1;
