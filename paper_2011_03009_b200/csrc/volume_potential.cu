@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(kWarpThreads, 1) warp_col_to_row_pp(WArgs a) {
   auto buf = [&](int b) { return sm + b * (L * 8); };
   auto prefetch = [&](int64_t tix, int b) {
     if (tix < ntiles) {
-      const int i0 = int(tix % ntiles_i) * 8;
-      const int k = int(tix / ntiles_i);
+      const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * 8;
+      const int k = int(unsigned(tix) / unsigned(ntiles_i));
       const int lines_ok = min(8, a.n_inner - i0);
       const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
       double2* t = buf(b);
@@ -414,8 +414,8 @@ __global__ void __launch_bounds__(kWarpThreads, 1) warp_col_to_row_pp(WArgs a) {
     prefetch(tix + gridDim.x, b ^ 1);
     cp_async_wait1();
     __syncthreads();  // this tile's copies (issued by all threads) have landed
-    const int i0 = int(tix % ntiles_i) * 8;
-    const int k = int(tix / ntiles_i);
+    const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * 8;
+    const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const bool ok = w < min(8, a.n_inner - i0);
     double2* const t = buf(b);
     TileColIn src{t, w, a.in_nvalid};
@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {
-    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
-    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+    ky = interleave_index(int(unsigned(line) % unsigned(a.n_inner)), a.ko.Py);
+    kx = mirror ? interleave_index(int(unsigned(line) / unsigned(a.n_inner)), a.ko.Px) : int(unsigned(line) / unsigned(a.n_inner));
   };
   // staged position p lives at S[swz(p)] (PRUNED: p < L/2, so the swizzle stays inside S)
   auto prefetch_in = [&](int64_t line) {
@@ -656,8 +656,8 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
   const int64_t stride = int64_t(gridDim.x) * GROUPS;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {
-    ky = interleave_index(int(line % a.n_inner), a.ko.Py);
-    kx = mirror ? interleave_index(int(line / a.n_inner), a.ko.Px) : int(line / a.n_inner);
+    ky = interleave_index(int(unsigned(line) % unsigned(a.n_inner)), a.ko.Py);
+    kx = mirror ? interleave_index(int(unsigned(line) / unsigned(a.n_inner)), a.ko.Px) : int(unsigned(line) / unsigned(a.n_inner));
   };
   auto prefetch_in = [&](int64_t line) {
     if (line < nlines) {
@@ -777,8 +777,8 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_row_to_col(WArgs a) {
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix) {
     if (tix < ntiles) {
-      const int i = int(tix % ntiles_i) * T + grp;
-      const int k = int(tix / ntiles_i);
+      const int i = int(unsigned(tix) % unsigned(ntiles_i)) * T + grp;
+      const int k = int(unsigned(tix) / unsigned(ntiles_i));
       if (i < a.n_inner) {
         const double2* in = a.in + int64_t(i) * a.in_si + int64_t(k) * a.in_sk;
         for (int pos = lane; pos < a.in_nvalid; pos += LANES) cp_async16(sb + swz(pos), in + pos);
@@ -791,8 +791,8 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_row_to_col(WArgs a) {
   int64_t tix = blockIdx.x;
   prefetch(tix);
   for (; tix < ntiles; tix += gridDim.x) {
-    const int i0 = int(tix % ntiles_i) * T;
-    const int k = int(tix / ntiles_i);
+    const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+    const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
     cp_async_wait0();
     sync();  // the group's own staged row has landed
@@ -846,8 +846,8 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix) {
     if (tix < ntiles) {
-      const int i0 = int(tix % ntiles_i) * T;
-      const int k = int(tix / ntiles_i);
+      const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+      const int k = int(unsigned(tix) / unsigned(ntiles_i));
       const int lines_ok = min(T, a.n_inner - i0);
       const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
       for (int e = threadIdx.x; e < a.in_nvalid * T; e += T * LANES) {
@@ -863,8 +863,8 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
   int64_t tix = blockIdx.x;
   prefetch(tix);
   for (; tix < ntiles; tix += gridDim.x) {
-    const int i0 = int(tix % ntiles_i) * T;
-    const int k = int(tix / ntiles_i);
+    const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+    const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const bool ok = grp < min(T, a.n_inner - i0);
     cp_async_wait0();
     __syncthreads();  // this tile's copies (issued by all threads) have landed
