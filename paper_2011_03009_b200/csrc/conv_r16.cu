@@ -23,6 +23,27 @@ namespace fusg {
 // TAB = false: from four exact table powers [w1, w2, w4, w8][lane] (<= 3 products);
 // TAB = true: all fifteen from an exact [k][lane] table (more shared loads, fewer FP64 ops).
 // Either table lives in shared memory, shared by the CTA's warps.
+template <bool CONJ>
+__device__ __forceinline__ void r16_twiddle(double2* v, double2 w1, double2 w2, double2 w4, double2 w8) {
+  auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+  const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+  v[1] = m(v[1], w1);
+  v[2] = m(v[2], w2);
+  v[3] = m(v[3], w3);
+  v[4] = m(v[4], w4);
+  v[5] = m(v[5], w5);
+  v[6] = m(v[6], w6);
+  v[7] = m(v[7], w7);
+  v[8] = m(v[8], w8);
+  v[9] = m(v[9], cmul(w8, w1));
+  v[10] = m(v[10], cmul(w8, w2));
+  v[11] = m(v[11], cmul(w8, w3));
+  v[12] = m(v[12], cmul(w8, w4));
+  v[13] = m(v[13], cmul(w8, w5));
+  v[14] = m(v[14], cmul(w8, w6));
+  v[15] = m(v[15], cmul(w8, w7));
+}
+
 template <bool TAB>
 struct R16Tw {  // W512^(n2 k) for k = 1..15
   const double2* t;
@@ -35,24 +56,7 @@ struct R16Tw {  // W512^(n2 k) for k = 1..15
       for (int k = 1; k < 16; ++k) v[k] = m(v[k], t[32 * k + lane]);
       return;
     }
-    const double2 w1 = t[lane], w2 = t[32 + lane], w4 = t[64 + lane];
-    const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
-    v[1] = m(v[1], w1);
-    v[2] = m(v[2], w2);
-    v[3] = m(v[3], w3);
-    v[4] = m(v[4], w4);
-    v[5] = m(v[5], w5);
-    v[6] = m(v[6], w6);
-    v[7] = m(v[7], w7);
-    const double2 w8 = t[96 + lane];
-    v[8] = m(v[8], w8);
-    v[9] = m(v[9], cmul(w8, w1));
-    v[10] = m(v[10], cmul(w8, w2));
-    v[11] = m(v[11], cmul(w8, w3));
-    v[12] = m(v[12], cmul(w8, w4));
-    v[13] = m(v[13], cmul(w8, w5));
-    v[14] = m(v[14], cmul(w8, w6));
-    v[15] = m(v[15], cmul(w8, w7));
+    r16_twiddle<CONJ>(v, t[lane], t[32 + lane], t[64 + lane], t[96 + lane]);
   }
 };
 
@@ -238,6 +242,203 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     cuda_error(err, "pass C (16x16x2)");
+    return -1;
+  }
+  return 1;
+}
+
+// ---------------------------------------------------------------------------- transposing passes
+// Passes A/B (forward, zero-padded upper input half) and D/E (inverse, cropped upper output
+// half) at L = 512 on the same 16 x 16 x 2 warp transform.
+
+// A/B: a CTA owns 8 adjacent rows (i0..i0+7 at outer k), warp w transforms row w read straight
+// from global memory (512 B per warp instruction), exchanges in place in column w of the
+// swizzled [pos][8] tile, leaves its spectrum there, and after one CTA barrier the CTA stores
+// positions as 8 adjacent lines (128 contiguous bytes).
+constexpr size_t kR16TileBytes = size_t(512) * 8 * sizeof(double2);
+
+__global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
+  constexpr int L = 512;
+  extern __shared__ double2 tile[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned ntiles = unsigned(a.n_inner + 7) / 8u;
+  const unsigned kq = blockIdx.x / ntiles;
+  const int i0 = int(blockIdx.x - kq * ntiles) * 8;
+  const int k = int(kq);
+  const int lines_ok = min(8, a.n_inner - i0);
+  const bool ok = w < lines_ok;
+  const double2* in = a.in + int64_t(i0 + (ok ? w : 0)) * a.in_si + int64_t(k) * a.in_sk;
+  double2 v[16];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int pos = lane + 32 * e;
+    v[e] = (ok && pos < a.in_nvalid) ? __ldg(in + pos) : make_double2(0.0, 0.0);
+  }
+  dft16_half_in<false>(v);
+  {  // one exact table power per lane, the others by squaring (one FFT per warp)
+    const double2 w1 = __ldg(a.tw + lane), w2 = cmul(w1, w1), w4 = cmul(w2, w2);
+    r16_twiddle<false>(v, w1, w2, w4, cmul(w4, w4));
+  }
+  const bool b = lane >= 16;
+  const int k1 = lane & 15;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) tile[tile_at(r16_ex(q, lane), w)] = v[q];
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 16; ++h) v[h] = tile[tile_at(r16_ex(k1, 2 * h + int(b)), w)];
+  dft16<false>(v);
+  r16_r2_all<false>(v, b, std::make_integer_sequence<int, 8>{});
+  __syncwarp();  // every lane has read its exchange slots
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int p = k1 + 16 * (i + 8 * int(b));
+    tile[tile_at(p, w)] = v[i];
+    tile[tile_at(p + 256, w)] = v[i + 8];
+  }
+  __syncthreads();
+  if (a.pm.n == 0) {
+    double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+    for (int e = threadIdx.x; e < a.out_nvalid * 8; e += 256) {
+      const int pos = e >> 3, t = e & 7;
+      if (t < lines_ok) {
+        const double2 x = tile[tile_at(pos, t)];
+        base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+      }
+    }
+  } else {  // fused transpose: the segment of position pos (kx) goes straight to the rank owning it
+    for (int e = threadIdx.x; e < a.out_nvalid * 8; e += 256) {
+      const int pos = e >> 3, t = e & 7;
+      if (t < lines_ok) {
+        const int q = a.pm.owner(a.pm.by_pos ? pos : i0 + t);
+        const double2 x = tile[tile_at(pos, t)];
+        a.pm.base[q][a.pm.off[q] + int64_t(i0 + t) * a.out_si + int64_t(k) * a.pm.sk[q] + int64_t(pos) * a.out_sp] =
+            (a.scale == 1.0) ? x : cscale(x, a.scale);
+      }
+    }
+    __threadfence_system();  // remote stores performed before the barrier that follows the pass
+  }
+}
+
+// D/E, persistent: CTAs of 4 warps stream 4-line column tiles [pos][4] (swizzled, cp.async,
+// the next tile in flight while the current one is transformed); warp g reads column g in the
+// transform's spectral layout, runs the inverse 16 x 16 x 2 transform with a private exchange
+// buffer and stores its cropped output row from registers (512 B per warp instruction).
+constexpr int kR16CT = 4;
+constexpr size_t kR16C2RBytes = (size_t(kR16CT) * 512 + size_t(512) * kR16CT + 4 * 32) * sizeof(double2);
+
+template <int MINB>
+__global__ void __launch_bounds__(kR16CT * 32, MINB) col_to_row_r16(WArgs a) {
+  constexpr int L = 512, T = kR16CT;
+  extern __shared__ double2 sm[];
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* const xb = sm + g * L;
+  double2* const tile = sm + T * L;
+  double2* const tws = tile + L * T;
+  if (g == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane << j) & (L - 1)));
+  }
+  const unsigned ntiles_i = unsigned(a.n_inner + T - 1) / unsigned(T);
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto prefetch = [&](int64_t tix) {
+    if (tix < ntiles) {
+      const unsigned kq = unsigned(tix) / ntiles_i;
+      const int i0 = int(unsigned(tix) - kq * ntiles_i) * T;
+      const int lines_ok = min(T, a.n_inner - i0);
+      const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(kq) * a.in_sk;
+      for (int e = threadIdx.x; e < a.in_nvalid * T; e += T * 32) {
+        const int pos = e / T, t = e % T;
+        cp_async16_zfill(&tile[mtile_at<T>(pos, t)], t < lines_ok ? base + t * a.in_si + pos * a.in_sp : a.in,
+                         t < lines_ok);
+      }
+    }
+    cp_async_commit();
+  };
+  const R16Tw<false> tw{tws, lane};
+  const bool b = lane >= 16;
+  const int k1 = lane & 15;
+  int64_t tix = blockIdx.x;
+  prefetch(tix);
+  for (; tix < ntiles; tix += gridDim.x) {
+    const unsigned kq = unsigned(tix) / ntiles_i;
+    const int i0 = int(unsigned(tix) - kq * ntiles_i) * T;
+    const bool ok = g < min(T, a.n_inner - i0);
+    cp_async_wait0();
+    __syncthreads();  // this tile's copies (issued by all threads) have landed
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = k1 + 16 * (i + 8 * int(b));
+      v[i] = p < a.in_nvalid ? tile[mtile_at<T>(p, g)] : make_double2(0.0, 0.0);
+      v[i + 8] = p + 256 < a.in_nvalid ? tile[mtile_at<T>(p + 256, g)] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // tile consumed by every warp
+    prefetch(tix + gridDim.x);
+    r16_r2_all<true>(v, b, std::make_integer_sequence<int, 8>{});
+    dft16<true>(v);
+#pragma unroll
+    for (int h = 0; h < 16; ++h) xb[r16_ex(k1, 2 * h + int(b))] = v[h];
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = xb[r16_ex(q, lane)];
+    tw.apply<true>(v);
+    dft16_half_out<true>(v);
+    const int line = i0 + (ok ? g : 0);
+    double2* orow = a.out + int64_t(line) * a.out_si + int64_t(kq) * a.out_sk;
+    if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
+      const int q = a.pm.owner(line);
+      orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(kq) * a.pm.sk[q]);
+    }
+    if (ok) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int pos = lane + 32 * e;
+        if (pos < a.out_nvalid) orow[pos] = (a.scale == 1.0) ? v[e] : cscale(v[e], a.scale);
+      }
+    }
+    __syncwarp();  // exchange buffer read out before the next tile's writes
+  }
+  cp_async_wait0();
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
+}
+
+int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s) {
+  static const int mask = [] {  // FUSG_R16_T bitmask: 1 passes A/B, 2 passes D/E (default both)
+    const char* e = getenv("FUSG_R16_T");
+    return e ? atoi(e) : 3;
+  }();
+  if (!(mask & (r2c ? 1 : 2))) return 0;
+  if (r2c ? (2 * a.in_nvalid > 512 || a.in_sp != 1) : (2 * a.out_nvalid > 512 || a.out_sp != 1)) return 0;
+  const int64_t tiles8 = int64_t((a.n_inner + 7) / 8) * a.n_outer;
+  if (tiles8 >= (int64_t(1) << 31)) return 0;
+  cudaError_t err;
+  if (r2c) {
+    const auto fn = warp_row_to_col_r16;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR16TileBytes)) != cudaSuccess) {
+      set_error(FUSG_CUDA, "transposing pass (16x16x2): cannot configure shared memory");
+      return -1;
+    }
+    fn<<<unsigned(tiles8), 256, kR16TileBytes, s>>>(a);
+  } else {
+    const auto fn = col_to_row_r16<3>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR16C2RBytes)) != cudaSuccess) {
+      set_error(FUSG_CUDA, "transposing pass (16x16x2): cannot configure shared memory");
+      return -1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kR16CT * 32, kR16C2RBytes) != cudaSuccess ||
+        per_sm < 1) {
+      cudaGetLastError();
+      return 0;
+    }
+    const int64_t tiles = int64_t((a.n_inner + kR16CT - 1) / kR16CT) * a.n_outer;
+    const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+    fn<<<unsigned(grid), kR16CT * 32, kR16C2RBytes, s>>>(a);
+  }
+  ctx->launches++;
+  err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "transposing pass (16x16x2)");
     return -1;
   }
   return 1;

@@ -48,5 +48,11 @@ struct PPConvSmem {
 
 // pass C at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16.cu)
 int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
+// passes A/B (r2c) or D/E at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error
+int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s);
+
+// swizzled [pos][T] column tile of the multi-line transposing passes (T = 2, 4, 8)
+template <int T>
+__device__ __forceinline__ int mtile_at(int pos, int t) { return pos * T + (t ^ ((pos / (8 / T)) & (T - 1))); }
 
 }  // namespace fusg

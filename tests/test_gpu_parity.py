@@ -99,7 +99,9 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # Nx / Ny = 512, 768, 1024: Px / Py = 1024, 1536, 2048 (multi-
                                   # warp-line transposing passes; ragged T-line tiles)
                                   (512, 5, 3), (3, 512, 4), (768, 3, 2), (2, 768, 3),
-                                  (1024, 2, 2), (2, 1024, 2)])
+                                  (1024, 2, 2), (2, 1024, 2),
+                                  # Nx / Ny in (128, 256]: Px / Py = 512 (16x16x2 transposing passes)
+                                  (200, 3, 2), (3, 230, 4), (256, 7, 3)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
