@@ -32,6 +32,7 @@ void free_kernel(fusg_kernel* K) {
       cudaIpcCloseMemHandle(K->peerA[q]);
     }
   if (K->bar) cudaFree(K->bar);
+  if (K->absync) cudaFree(K->absync);
   if (K->ipc_bufs) {
     cudaStreamSynchronize(s);
     cudaFree(K->bufA);

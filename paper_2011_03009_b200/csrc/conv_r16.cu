@@ -257,22 +257,53 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
 // positions as 8 adjacent lines (128 contiguous bytes).
 constexpr size_t kR16TileBytes = size_t(512) * 8 * sizeof(double2);
 
-__global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
-  constexpr int L = 512;
-  extern __shared__ double2 tile[];
+// L2 eviction-priority hints for the fused A+B pass: the streamed input f and output B are
+// evict-first so they do not push the ring out of L2; ring stores are evict-last.
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_nc_hint(const double2* p, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void l2_discard(const void* p) {  // drop a dead 128-byte line, no write-back
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// Input / output access modes of r2c_tile: plain (__ldg, st), fused-pass reads of f (evict-first)
+// and of the ring (ld.global.cg: written by other CTAs of the launch), stores to the ring
+// (evict-last) and to B (evict-first).
+enum R2CMode { kR2CPlain = 0, kR2CFusedA = 1, kR2CFusedB = 2 };
+
+// One 8-row tile (rows i0..i0+7 at outer k) of a row -> column pass; CG: read the input rows
+// through L2 only (ld.global.cg: rows another CTA of the same launch wrote).
+// (in_base, out_base, n_inner override a's for the fused A+B kernel.)
+template <int MODE>
+__device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base, double2* out_base, int n_inner,
+                                         int i0, int k, double2* tile) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned ntiles = unsigned(a.n_inner + 7) / 8u;
-  const unsigned kq = blockIdx.x / ntiles;
-  const int i0 = int(blockIdx.x - kq * ntiles) * 8;
-  const int k = int(kq);
-  const int lines_ok = min(8, a.n_inner - i0);
+  const int lines_ok = min(8, n_inner - i0);
   const bool ok = w < lines_ok;
-  const double2* in = a.in + int64_t(i0 + (ok ? w : 0)) * a.in_si + int64_t(k) * a.in_sk;
+  const double2* in = in_base + int64_t(i0 + (ok ? w : 0)) * a.in_si + int64_t(k) * a.in_sk;
   double2 v[16];
+  const uint64_t pol_first = MODE != kR2CPlain ? l2_policy_first() : 0;
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int pos = lane + 32 * e;
-    v[e] = (ok && pos < a.in_nvalid) ? __ldg(in + pos) : make_double2(0.0, 0.0);
+    v[e] = make_double2(0.0, 0.0);
+    if (ok && pos < a.in_nvalid)
+      v[e] = MODE == kR2CFusedB ? __ldcg(in + pos) : MODE == kR2CFusedA ? ld_nc_hint(in + pos, pol_first) : __ldg(in + pos);
   }
   dft16_half_in<false>(v);
   {  // one exact table power per lane, the others by squaring (one FFT per warp)
@@ -297,12 +328,15 @@ __global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
   }
   __syncthreads();
   if (a.pm.n == 0) {
-    double2* base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+    double2* base = out_base + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+    const uint64_t pol = MODE == kR2CFusedA ? l2_policy_last() : pol_first;
     for (int e = threadIdx.x; e < a.out_nvalid * 8; e += 256) {
       const int pos = e >> 3, t = e & 7;
       if (t < lines_ok) {
         const double2 x = tile[tile_at(pos, t)];
-        base[t * a.out_si + pos * a.out_sp] = (a.scale == 1.0) ? x : cscale(x, a.scale);
+        const double2 y = (a.scale == 1.0) ? x : cscale(x, a.scale);
+        if constexpr (MODE == kR2CPlain) base[t * a.out_si + pos * a.out_sp] = y;
+        else st_hint(base + t * a.out_si + pos * a.out_sp, y, pol);
       }
     }
   } else {  // fused transpose: the segment of position pos (kx) goes straight to the rank owning it
@@ -316,6 +350,138 @@ __global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
       }
     }
     __threadfence_system();  // remote stores performed before the barrier that follows the pass
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
+  extern __shared__ double2 tile[];
+  const unsigned ntiles = unsigned(a.n_inner + 7) / 8u;
+  const unsigned kq = blockIdx.x / ntiles;
+  r2c_tile<kR2CPlain>(a, a.in, a.out, a.n_inner, int(blockIdx.x - kq * ntiles) * 8, int(kq), tile);
+}
+
+// Passes A and B fused through an L2-resident ring of z-slabs (8 planes each).  Pass A of slab
+// s writes its [kx][8][y] block into ring slot s % R; pass B of slab s reads it back (through
+// L2) as soon as every pass-A tile of the slab is done.  The ring replaces the full [kx][z][y]
+// intermediate, whose HBM write and read-back were a third of the A + B traffic.
+// Persistent CTAs take work items from a global ticket in the order A(0), A(1), B(0), A(2),
+// B(1), ..., B(S-1); B(s) waits for A(s) to finish and A(s) (s >= R) for B(s - R), both
+// dispatched earlier, so the waits cannot deadlock.
+
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Work item t of the fused A+B order A(0) | [A(p), B(p-1)], p = 1..S-1 | B(S-1): kind, slab s,
+// index r within the slab's items, and the counter / count it waits for (none: dep = nullptr).
+struct ABItem {
+  bool isA;
+  int s, r;
+  const int* dep;
+  int need;
+};
+__device__ __forceinline__ ABItem ab_item(const ABFused& f, int t) {
+  const int nyt = (f.a.n_inner + 7) / 8, nkx = f.b.n_outer, S = f.slabs;
+  const int last_nz = f.nz - 8 * (S - 1);
+  const int na_full = nyt * 8, na_last = nyt * last_nz;
+  ABItem it;
+  const int a0 = S == 1 ? na_last : na_full;
+  if (t < a0) {
+    it.isA = true, it.s = 0, it.r = t;
+  } else {
+    const int rem = t - a0;
+    const int full = na_full + nkx;  // groups p = 1..S-2: A(p) (full slab) then B(p-1)
+    const int nfull = S >= 2 ? S - 2 : 0;
+    if (rem < nfull * full) {
+      const int p = 1 + rem / full, r = rem - (p - 1) * full;
+      if (r < na_full) it.isA = true, it.s = p, it.r = r;
+      else it.isA = false, it.s = p - 1, it.r = r - na_full;
+    } else {
+      int r = rem - nfull * full;
+      if (S >= 2 && r < na_last) {  // A(S-1), the ragged last slab
+        it.isA = true, it.s = S - 1, it.r = r;
+      } else {
+        if (S >= 2) r -= na_last;
+        if (S >= 2 && r < nkx) it.isA = false, it.s = S - 2, it.r = r;
+        else it.isA = false, it.s = S - 1, it.r = S >= 2 ? r - nkx : r;
+      }
+    }
+  }
+  if (it.isA) {  // the ring slot must have been read out by B(s - R)
+    it.dep = it.s >= f.ring ? f.sync + 1 + S + (it.s - f.ring) : nullptr;
+    it.need = nkx;
+  } else {  // every pass-A tile of the slab must be in the ring
+    it.dep = f.sync + 1 + it.s;
+    it.need = it.s == S - 1 ? na_last : na_full;
+  }
+  return it;
+}
+
+// Persistent CTAs take items round-robin (CTA c: c, c + G, ...), all co-resident.  The
+// smallest unfinished item's dependencies all have smaller indices, so some CTA can always
+// progress.  Thread 0 prefetches the counter the CTA's next item depends on while the current
+// one is computed; completions are published by thread 0 after a CTA barrier (fence + add).
+__global__ void __launch_bounds__(256, 2) ab_fused_r16(ABFused f) {
+  extern __shared__ double2 tile[];
+  const int nyt = (f.a.n_inner + 7) / 8;
+  const int last_nz = f.nz - 8 * (f.slabs - 1);
+  const int total = nyt * f.nz + f.b.n_outer * f.slabs;
+  int* const doneA = f.sync + 1;
+  int* const doneB = f.sync + 1 + f.slabs;
+  int seen = 0;  // thread 0: prefetched value of the current item's dependency counter
+  if (threadIdx.x == 0 && int(blockIdx.x) < total) {
+    const ABItem it = ab_item(f, blockIdx.x);
+    seen = it.dep ? ld_relaxed(it.dep) : 0;
+  }
+  for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    const ABItem it = ab_item(f, t);
+    if (threadIdx.x == 0) {
+      if (it.dep && seen < it.need)
+        while (ld_acquire(it.dep) < it.need) __nanosleep(32);
+      else if (it.dep && !(f.mode & 1))
+        __threadfence();  // acquire side of the prefetched observation
+      const int tn = t + int(gridDim.x);
+      if (tn < total) {  // prefetch the next item's dependency
+        const ABItem nx = ab_item(f, tn);
+        seen = nx.dep ? ld_relaxed(nx.dep) : 0;
+      }
+    }
+    __syncthreads();
+    double2* const slot = const_cast<double2*>(f.b.in) + int64_t(it.s % f.ring) * f.slot;
+    if (it.isA) {
+      const int zz = it.r / nyt, yt = it.r - zz * nyt;
+      // k = z indexes f; in the slot it is z - 8 s
+      r2c_tile<kR2CFusedA>(f.a, f.a.in, slot - int64_t(8 * it.s) * f.a.out_sk, f.a.n_inner, yt * 8,
+                           8 * it.s + zz, tile);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (!(f.mode & 2)) __threadfence();
+        atomicAdd(doneA + it.s, 1);
+      }
+    } else {
+      const int nzs = it.s == f.slabs - 1 ? last_nz : 8;
+      r2c_tile<kR2CFusedB>(f.b, slot, f.b.out + 8 * it.s, nzs, 0, it.r, tile);  // z offset 8 s in B
+      // the block [kx = r][zz < nzs][y] is dead (read only by this item): drop its L2 lines
+      // without write-back
+      const char* blk = reinterpret_cast<const char*>(slot + int64_t(it.r) * f.b.in_sk);
+      const int lines = int((int64_t(nzs) * f.b.in_si * int64_t(sizeof(double2)) + 127) / 128);
+      if (!(f.mode & 4))
+        for (int l = threadIdx.x; l < lines; l += 256) l2_discard(blk + 128 * l);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (!(f.mode & 2)) __threadfence();  // discards (weak writes) ordered before the slot is released to A(s + R)
+        atomicAdd(doneB + it.s, 1);
+      }
+    }
   }
 }
 
@@ -439,6 +605,45 @@ int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s
   err = cudaGetLastError();
   if (err != cudaSuccess) {
     cuda_error(err, "transposing pass (16x16x2)");
+    return -1;
+  }
+  return 1;
+}
+
+int launch_ab_fused_r16(fusg_ctx* ctx, const ABFused& f, cudaStream_t s) {
+  // FUSG_AB_FUSED=1 opts in.  Measured on cfg2: DRAM traffic of A+B drops from 2.3 to 1.33 GB
+  // (the ring stays in L2, its dead lines discarded), but the launch takes 0.52-0.58 ms against
+  // 0.434 ms for the two separate launches, so it is off by default.
+  static const bool on = [] {
+    const char* e = getenv("FUSG_AB_FUSED");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return 0;
+  const auto fn = ab_fused_r16;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR16TileBytes)) != cudaSuccess) {
+    set_error(FUSG_CUDA, "fused passes A+B: cannot configure shared memory");
+    return -1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kR16TileBytes) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (cudaMemsetAsync(f.sync, 0, sizeof(int) * (1 + 2 * size_t(f.slabs)), s) != cudaSuccess) {  // counters
+    cuda_error(cudaGetLastError(), "fused passes A+B: reset");
+    return -1;
+  }
+  static const int mode = [] {
+    const char* e = getenv("FUSG_ABF_MODE");
+    return e ? atoi(e) : 0;
+  }();
+  ABFused g = f;
+  g.mode = mode;
+  fn<<<unsigned(per_sm * ctx->num_sms), 256, kR16TileBytes, s>>>(g);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "fused passes A+B");
     return -1;
   }
   return 1;

@@ -112,6 +112,7 @@ struct fusg_kernel {
   std::vector<double2*> peerX, peerA;
   std::vector<bool> peer_opened;  // IPC mappings to close on destroy
   int* bar = nullptr;             // 1-int NCCL barrier buffer
+  int* absync = nullptr;          // fused A+B pass: ticket and per-slab completion counters
   uint64_t bytes = 0;
   std::mutex mu;  // serialises applies sharing the workspace
 };

@@ -1588,6 +1588,34 @@ fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, doubl
                            GStoreF{GStore{u_z0, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
 }
 
+// Passes A and B as one launch through an L2-resident ring (conv_r16.cu): unsharded applies
+// with Px = Py = 512 and pruned x / y halves (the 16 x 16 x 2 kernels), ring slot <= 24 MB.
+// The ring lives in the head of bufA, which pass D overwrites afterwards.  1 done, 0 n/a.
+static int try_ab_fused(fusg_kernel* K, const double2* f, cudaStream_t s) {
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1];
+  if (K->G != 1 || K->slab || Px != 512 || Py != 512 || 2 * Nx > Px || 2 * Ny > Py) return 0;
+  constexpr int kRing = 3;
+  const int64_t slot = int64_t(Px) * 8 * Ny;
+  if (slot * int64_t(sizeof(double2)) > (int64_t(24) << 20) || kRing * slot > int64_t(Px) * Nz * Ny) return 0;
+  const int slabs = (Nz + 7) / 8;
+  if (!K->absync && cudaMalloc(&K->absync, sizeof(int) * (1 + 2 * 4096)) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (slabs > 4096) return 0;
+  const int64_t PyNz = int64_t(Py) * Nz;
+  ABFused fa;
+  fa.a = WArgs{f, Nx, int64_t(Ny) * Nx, 1, Nx, K->bufA, 1, Ny, 8 * int64_t(Ny), Px, 1.0, Ny, Nz, K->plan[0].tw, KOct{}};
+  fa.b = WArgs{K->bufA, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB, 1, PyNz, Nz, Py, 1.0, 8, Px, K->plan[1].tw, KOct{}};
+  fa.nz = Nz;
+  fa.slabs = slabs;
+  fa.ring = kRing;
+  fa.slot = slot;
+  fa.sync = K->absync;
+  return launch_ab_fused_r16(K->ctx, fa, s);
+}
+
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t s, cudaEvent_t* ev) {
   if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: sharded kernel needs a slab apply");
@@ -1595,6 +1623,22 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
     if (ev) cudaEventRecord(ev[i], s);
   };
   mark(0);
+  const int fused = try_ab_fused(K, f, s);
+  if (fused < 0) return FUSG_CUDA;
+  if (fused) {  // A+B in one launch (both marks after it), then C, D, E
+    const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+    const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(K->P[1]) * Nz;
+    mark(1);
+    mark(2);
+    FUSG_TRY(apply_phase_C(K, s));
+    mark(3);
+    FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], Nz, K->P[0], GLoadF{GLoad{K->bufB, 1, PyNz, Nz, K->P[1]}},
+                               GStoreF{GStore{K->bufA, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
+    mark(4);
+    FUSG_TRY(apply_phase_E(K, u, scale, s));
+    mark(5);
+    return FUSG_OK;
+  }
   FUSG_TRY(apply_phase_A(K, f, s));
   mark(1);
   FUSG_TRY(apply_phase_BCD(K, K->bufA, s, ev ? ev + 2 : nullptr));

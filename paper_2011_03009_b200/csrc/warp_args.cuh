@@ -48,6 +48,17 @@ struct PPConvSmem {
 
 // pass C at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16.cu)
 int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
+// Passes A and B fused through an L2-resident ring of 8-plane z-slabs (conv_r16.cu)
+struct ABFused {
+  WArgs a;          // pass A: f rows -> ring (out = ring base; out_sk = Ny: z within the slab)
+  WArgs b;          // pass B: ring -> B (in = ring base, out = bufB)
+  int nz, slabs, ring;
+  int64_t slot;     // elements per ring slot (Px * 8 * Ny)
+  int* sync;        // [0] unused, [1 .. slabs] A tiles done, [1 + slabs ..] B tiles done
+  int mode = 0;     // FUSG_ABF_MODE experiment bits
+};
+int launch_ab_fused_r16(fusg_ctx* ctx, const ABFused& f, cudaStream_t s);
+
 // passes A/B (r2c) or D/E at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error
 int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s);
 

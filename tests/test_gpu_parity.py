@@ -101,7 +101,10 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   (512, 5, 3), (3, 512, 4), (768, 3, 2), (2, 768, 3),
                                   (1024, 2, 2), (2, 1024, 2),
                                   # Nx / Ny in (128, 256]: Px / Py = 512 (16x16x2 transposing passes)
-                                  (200, 3, 2), (3, 230, 4), (256, 7, 3)])
+                                  (200, 3, 2), (3, 230, 4), (256, 7, 3),
+                                  # Px = Py = 512: passes A+B fused through the z-slab ring
+                                  # (slabs of 8 planes, ragged last slab, single slab)
+                                  (200, 150, 13), (130, 129, 37), (256, 256, 3)])
 def test_apply_ragged_sizes_vs_oracle(ctx, orc, dims):
     dx = 1e-4
     g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
