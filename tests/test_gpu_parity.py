@@ -474,3 +474,38 @@ def test_slab_apply_over_nccl_single_rank(ctx):
     assert torch.equal(got, want)
     # and the loopback transport with G = 1 takes the same exchange path
     assert torch.equal(fus.apply_slab_loopback(g, k, f, 1, ctx=c), want)
+
+
+_AB_FUSED_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2011_03009_b200 import fus
+w = fus.medium_preset("water")
+out = []
+for dims in [(200, 150, 13), (130, 129, 37), (256, 256, 3), (256, 256, 256)]:
+    g = fus.make_grid([0, 0, 0], [d * 1e-4 for d in dims], 1e-4, 2)
+    k = fus.complex_wavenumber(w, 1.1e6, 2)
+    f = fus.random_vector(g.count(), 17)
+    out.append(fus.GreenKernel(g, k).apply(f).cpu().numpy())
+np.savez(sys.argv[2], *out)
+"""
+
+
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_ab_fused_ring_path_is_bitwise_two_pass(tmp_path, fused):
+    # Passes A+B through the L2-resident z-slab ring (FUSG_AB_FUSED=1, opt-in) run the same
+    # 16x16x2 tiles as the two separate launches: results must agree bit for bit.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for v in ("0", fused):
+        p = tmp_path / f"u{v}.npz"
+        env = dict(os.environ, FUSG_AB_FUSED=v)
+        r = subprocess.run([sys.executable, "-c", _AB_FUSED_CHILD, root, str(p)], env=env,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[v] = np.load(p)
+    for key in res["0"].files:
+        assert np.array_equal(res["0"][key], res[fused][key])
