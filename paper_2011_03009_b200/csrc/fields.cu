@@ -18,7 +18,7 @@
 
 namespace fusg {
 
-constexpr int kSrcChunk = 1024;
+constexpr int kSrcChunk = 512;  // 12 KB of staged sources (+ 32 KB phase table: static smem)
 
 struct GridDev {
   double lo[3];
@@ -48,18 +48,18 @@ __device__ __forceinline__ double centre(double lo, int i, double dx) {
 //
 // Phase: u = d Re k N / (2 pi) turns-of-table; j = rint(u) (magic-number rounding, whose low
 // word is the table index mod N), v = u - j exactly, so e^{i Re k d} = T[j] e^{2 pi i v / N}
-// with |2 pi v / N| <= pi / N = 3.1e-3: sin to degree 5 (error < 1e-21) and cos to degree 4
-// (< 2e-18).  T[j] = e^{2 pi i j / N} / (4 pi) lives in shared memory.  The rounding of u
+// with |2 pi v / N| <= pi / N = 1.5e-3: sin to degree 3 (error < 1e-16 relative) and cos to
+// degree 4 (< 1e-19).  T[j] = e^{2 pi i j / N} / (4 pi) lives in shared memory.  The rounding of u
 // carries the same absolute phase error as any double evaluation of Re k * d (~1e-16 |k d|).
 // 1/d: rsqrt.approx (rel. error < 2^-22) refined by one third-order step (error ~ e^3 < 2^-64).
-// Together ~33 FP64 instructions per term against ~47 (+36 constant moves) for sincospi.
+// Together ~31 FP64 instructions per term against ~47 (+36 constant moves) for sincospi.
 constexpr double kInv4Pi = 0.0795774715459476678844;  // 1 / (4 pi)
 constexpr double kPolyAttMax = 0.03;
-constexpr int kPhaseBits = 10;
+constexpr int kPhaseBits = 11;
 constexpr int kPhaseN = 1 << kPhaseBits;
 constexpr double kTwoPi = 6.283185307179586476925;
 constexpr double kPhC = kTwoPi / kPhaseN;  // radians per table step
-constexpr double kS1 = kPhC, kS3 = -kPhC * kPhC * kPhC / 6.0, kS5 = kPhC * kPhC * kPhC * kPhC * kPhC / 120.0;
+constexpr double kS1 = kPhC, kS3 = -kPhC * kPhC * kPhC / 6.0;
 constexpr double kC2 = -kPhC * kPhC / 2.0, kC4 = kPhC * kPhC * kPhC * kPhC / 24.0;
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 
@@ -106,7 +106,9 @@ template <int ATT>
 __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
                                                  const double2* __restrict__ tab, double2& acc,
                                                  bool& bad) {
-  bad |= d2 < 1e-24;  // dist < 1e-12 (src/transducer.cpp:112)
+  // dist < 1e-12 (src/transducer.cpp:112), i.e. d2 < 1e-24: for d2 >= +0 the IEEE order is the
+  // integer order of the bit patterns, so the test runs on the integer pipe, exactly
+  bad |= __double_as_longlong(d2) < 0x3AF357C299A88EA7LL;
   const double ir = rsqrt_refined(d2);
   const double d = d2 * ir;
   const double u = d * k1;
@@ -114,7 +116,7 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
   const int j = __double2loint(t) & (kPhaseN - 1);
   const double v = u - (t - kRoundMagic);
   const double v2 = v * v;
-  const double sn = v * fma(v2, fma(v2, kS5, kS3), kS1);
+  const double sn = v * fma(v2, kS3, kS1);
   const double cs = fma(v2, fma(v2, kC4, kC2), 1.0);
   const double2 w = tab[j];
   const double mag = ATT == 0 ? ir : ir * attenuation<ATT>(kim * d);
@@ -284,7 +286,7 @@ __global__ void __launch_bounds__(256) power_nodes_kernel(const double* __restri
 // memory, vs threads share a point and split the chunk (vs: a power of two, larger for few
 // points, so small point sets still fill the CTA), and each chunk group writes one
 // partial sum per point; potential_reduce_kernel adds the groups in order (deterministic).
-constexpr int kPotThreads = 256, kPotChunk = 1536;
+constexpr int kPotThreads = 256, kPotChunk = 768;  // 12 KB staged + 32 KB phase table + 4 KB: static smem
 
 __global__ void phase_table_kernel(double2* tab) { fill_phase_table(tab); }
 
