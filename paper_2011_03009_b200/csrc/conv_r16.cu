@@ -291,7 +291,7 @@ enum R2CMode { kR2CPlain = 0, kR2CFusedA = 1, kR2CFusedB = 2 };
 // (in_base, out_base, n_inner override a's for the fused A+B kernel.)
 template <int MODE>
 __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base, double2* out_base, int n_inner,
-                                         int i0, int k, double2* tile) {
+                                         int i0, int k, double2* tile, bool hints = true) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lines_ok = min(8, n_inner - i0);
   const bool ok = w < lines_ok;
@@ -303,7 +303,8 @@ __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base,
     const int pos = lane + 32 * e;
     v[e] = make_double2(0.0, 0.0);
     if (ok && pos < a.in_nvalid)
-      v[e] = MODE == kR2CFusedB ? __ldcg(in + pos) : MODE == kR2CFusedA ? ld_nc_hint(in + pos, pol_first) : __ldg(in + pos);
+      v[e] = MODE == kR2CFusedB ? __ldcg(in + pos)
+             : (MODE == kR2CFusedA && hints) ? ld_nc_hint(in + pos, pol_first) : __ldg(in + pos);
   }
   dft16_half_in<false>(v);
   {  // one exact table power per lane, the others by squaring (one FFT per warp)
@@ -335,7 +336,7 @@ __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base,
       if (t < lines_ok) {
         const double2 x = tile[tile_at(pos, t)];
         const double2 y = (a.scale == 1.0) ? x : cscale(x, a.scale);
-        if constexpr (MODE == kR2CPlain) base[t * a.out_si + pos * a.out_sp] = y;
+        if (MODE == kR2CPlain || !hints) base[t * a.out_si + pos * a.out_sp] = y;
         else st_hint(base + t * a.out_si + pos * a.out_sp, y, pol);
       }
     }
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(256, 2) ab_fused_r16(ABFused f) {
       const int zz = it.r / nyt, yt = it.r - zz * nyt;
       // k = z indexes f; in the slot it is z - 8 s
       r2c_tile<kR2CFusedA>(f.a, f.a.in, slot - int64_t(8 * it.s) * f.a.out_sk, f.a.n_inner, yt * 8,
-                           8 * it.s + zz, tile);
+                           8 * it.s + zz, tile, !(f.mode & 8));
       __syncthreads();
       if (threadIdx.x == 0) {
         if (!(f.mode & 2)) __threadfence();
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(256, 2) ab_fused_r16(ABFused f) {
       }
     } else {
       const int nzs = it.s == f.slabs - 1 ? last_nz : 8;
-      r2c_tile<kR2CFusedB>(f.b, slot, f.b.out + 8 * it.s, nzs, 0, it.r, tile);  // z offset 8 s in B
+      r2c_tile<kR2CFusedB>(f.b, slot, f.b.out + 8 * it.s, nzs, 0, it.r, tile, !(f.mode & 8));  // z offset 8 s in B
       // the block [kx = r][zz < nzs][y] is dead (read only by this item): drop its L2 lines
       // without write-back
       const char* blk = reinterpret_cast<const char*>(slot + int64_t(it.r) * f.b.in_sk);
