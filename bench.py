@@ -248,7 +248,12 @@ def nested_solve(ctx, reps=2):
             "solve_s": best,
             "grids": [list(cfg.plan.for_harmonic(i).grid.dims) for i in range(2, 6)],
             "rows": [{k: v for k, v in t.__dict__.items()} for t in rows],
-            "rayleigh_terms_per_s": n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None}
+            "rayleigh_terms_per_s": n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None,
+            # FP64 pipe fraction of the Rayleigh sum: 23 FP64 instructions per term (SASS of
+            # monopole_grid_kernel<0>'s inner loop: 276 per 12 terms) against the pipe's
+            # 64 lanes/clk/SM x 148 SMs x 1.965 GHz
+            "rayleigh_fp64_pipe_frac": (n2 * len(cfg.transducer.source_points) / p1 * 23.0
+                                        / (64 * 148 * 1.965e9)) if p1 > 0 else None}
 
 
 # ------------------------------------------------------------------------- GPU arm
@@ -264,6 +269,12 @@ def run_gpu(args, world, rank, local):
     t0 = time.perf_counter()
     K = fus.GreenKernel(g, k, ctx=ctx)
     build_s = time.perf_counter() - t0
+    # the same build again: the first one also pays the context's first allocations and module
+    # loads; this is the "Evaluate G_k" cost of every further kernel (e.g. each cascade harmonic)
+    t0 = time.perf_counter()
+    K2 = fus.GreenKernel(g, k, ctx=ctx)
+    build_warm_s = time.perf_counter() - t0
+    del K2
     P = K.padded
     fd = torch.from_numpy(f).to(f"cuda:{local}")
     ud = torch.empty_like(fd)
@@ -378,7 +389,7 @@ def run_gpu(args, world, rank, local):
                                "achieved_gbs": total_bytes / (ms * 1e-3) / 1e9,
                                "frac": total_bytes / (ms * 1e-3) / 1e9 / hbm},
             "passes_ms": dict(zip(names, pass_ms)),
-            "kernel_build_s": build_s,
+            "kernel_build_s": build_s, "kernel_build_warm_s": build_warm_s,
             "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
             "gpu_launches": int(launches),
