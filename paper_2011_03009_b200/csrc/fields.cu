@@ -74,6 +74,19 @@ __device__ __forceinline__ void fill_phase_table(double2* tab) {
   }
 }
 
+// ATT 3 tables (monopole_grid_kernel): rows e^{2 pi i j / N} e^{-alpha j} / (4 pi) and the
+// coarse factors eh[m] = e^{-alpha N m}, m < n_eh (the host bounds Re k d / (2 pi) N by N n_eh).
+constexpr int kEhMax = 512;
+__device__ __forceinline__ void fill_att_tables(double2* tab, double* eh, double alpha, int n_eh) {
+  for (int j = threadIdx.x; j < kPhaseN; j += blockDim.x) {
+    double sn, cs;
+    sincospi(2.0 * j / kPhaseN, &sn, &cs);
+    const double a = exp(-alpha * j) * kInv4Pi;
+    tab[j] = make_double2(cs * a, sn * a);
+  }
+  for (int m = threadIdx.x; m < n_eh; m += blockDim.x) eh[m] = exp(-alpha * double(kPhaseN) * m);
+}
+
 __device__ __forceinline__ double rsqrt_refined(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -105,7 +118,7 @@ __device__ __forceinline__ double attenuation(double t) {  // e^{-t}, t = Im k *
 template <int ATT>
 __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
                                                  const double2* __restrict__ tab, double2& acc,
-                                                 bool& bad) {
+                                                 bool& bad, const double* __restrict__ eh = nullptr) {
   // dist < 1e-12 (src/transducer.cpp:112), i.e. d2 < 1e-24: for d2 >= +0 the IEEE order is the
   // integer order of the bit patterns, so the test runs on the integer pipe, exactly
   bad |= __double_as_longlong(d2) < 0x3AF357C299A88EA7LL;
@@ -119,7 +132,15 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
   const double sn = v * fma(v2, kS3, kS1);
   const double cs = fma(v2, fma(v2, kC4, kC2), 1.0);
   const double2 w = tab[j];
-  const double mag = ATT == 0 ? ir : ir * attenuation<ATT>(kim * d);
+  double mag;
+  if constexpr (ATT == 3) {
+    // tabulated attenuation: kim carries alpha = Im k / k1, the table rows already hold
+    // e^{-alpha (j mod N)}, eh[m] = e^{-alpha N m}, and e^{-alpha v} = 1 - alpha v to
+    // (alpha v)^2 / 2 < 1e-18
+    mag = ir * eh[__double2loint(t) >> kPhaseBits] * fma(-kim, v, 1.0);
+  } else {
+    mag = ATT == 0 ? ir : ir * attenuation<ATT>(kim * d);
+  }
   const double mc = mag * w.x, ms = mag * w.y;
   acc.x = fma(mc, cs, fma(-ms, sn, acc.x));
   acc.y = fma(mc, sn, fma(ms, cs, acc.y));
@@ -151,10 +172,13 @@ template <int ATT>
 __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __restrict__ src, int n_src,
                                                             GridDev g, double k1, double kim,
                                                             double amp, double2* __restrict__ out,
-                                                            int* flag) {
+                                                            int* flag, int n_eh = 0) {
   __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
   __shared__ double2 tab[kPhaseN];
-  fill_phase_table(tab);  // visible after the first barrier of the source loop
+  __shared__ double eh[ATT == 3 ? kEhMax : 1];
+  // visible after the first barrier of the source loop
+  if constexpr (ATT == 3) fill_att_tables(tab, eh, kim, n_eh);
+  else fill_phase_table(tab);
   const int row_threads = (g.dims[0] + kVPT - 1) / kVPT;
   const int64_t count = int64_t(row_threads) * g.dims[1] * g.dims[2];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -189,7 +213,7 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
 #pragma unroll
         for (int v = 0; v < kVPT; ++v) {
           const double ddx = x[v] - s0;
-          monopole_term_d2<ATT>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad);
+          monopole_term_d2<ATT>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh);
         }
       }
     }
@@ -582,9 +606,23 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
                           double dmax) {
   const int64_t count = int64_t((g.dims[0] + kVPT - 1) / kVPT) * g.dims[1] * g.dims[2];
   const int threads = 256;
-  FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel,
-                    unsigned((count + threads - 1) / threads), threads, 0, s>>>(
-                        src_dev, n_src, to_dev(g), phase_scale(kre), kim, amp, out, ctx->dev_flag));
+  const unsigned blocks = unsigned((count + threads - 1) / threads);
+  const double k1 = phase_scale(kre);
+  // attenuating media: tabulated attenuation (ATT 3) when every Re k d / (2 pi) N fits the
+  // coarse table (FUSG_ATT_TABLE=0 keeps the polynomial / exp() modes)
+  static const bool att_table = [] {
+    const char* e = getenv("FUSG_ATT_TABLE");
+    return !(e && atoi(e) == 0);
+  }();
+  const double umax = dmax * k1;
+  const int n_eh = dmax >= 0.0 ? int(umax / kPhaseN) + 2 : kEhMax + 1;
+  if (att_table && kim > 0.0 && k1 > 0.0 && n_eh <= kEhMax && umax < 1e9) {
+    monopole_grid_kernel<3><<<blocks, threads, 0, s>>>(src_dev, n_src, to_dev(g), k1, kim / k1, amp, out,
+                                                       ctx->dev_flag, n_eh);
+  } else {
+    FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel, blocks, threads, 0, s>>>(
+                          src_dev, n_src, to_dev(g), k1, kim, amp, out, ctx->dev_flag));
+  }
   ctx->launches++;
   FUSG_LAUNCH_CHECK("monopole_grid_kernel");
   return FUSG_OK;
