@@ -115,16 +115,20 @@ __device__ __forceinline__ double attenuation(double t) {  // e^{-t}, t = Im k *
 }
 
 // term from the squared distance d2
-template <int ATT>
+// SC (scaled coordinates, monopole_grid_kernel): coordinates arrive pre-multiplied by k1, so d2
+// is already in table turns squared, u = d, the magnitude 1/d carries a factor 1/k1 the caller
+// restores once per voxel, and the coincidence bound is (k1 1e-12)^2 (bits in tiny_bits).
+template <int ATT, bool SC = false>
 __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
                                                  const double2* __restrict__ tab, double2& acc,
-                                                 bool& bad, const double* __restrict__ eh = nullptr) {
+                                                 bool& bad, const double* __restrict__ eh = nullptr,
+                                                 long long tiny_bits = 0x3AF357C299A88EA7LL) {
   // dist < 1e-12 (src/transducer.cpp:112), i.e. d2 < 1e-24: for d2 >= +0 the IEEE order is the
   // integer order of the bit patterns, so the test runs on the integer pipe, exactly
-  bad |= __double_as_longlong(d2) < 0x3AF357C299A88EA7LL;
+  bad |= __double_as_longlong(d2) < tiny_bits;
   const double ir = rsqrt_refined(d2);
   const double d = d2 * ir;
-  const double u = d * k1;
+  const double u = SC ? d : d * k1;
   const double t = u + kRoundMagic;
   const int j = __double2loint(t) & (kPhaseN - 1);
   const double v = u - (t - kRoundMagic);
@@ -156,11 +160,11 @@ __device__ __forceinline__ void monopole_term(double x, double y, double z, doub
 }
 
 __device__ __forceinline__ void stage_sources(const double* src, int n_src, int base, double* sx,
-                                              double* sy, double* sz) {
+                                              double* sy, double* sz, double scale = 1.0) {
   for (int j = threadIdx.x; j < kSrcChunk && base + j < n_src; j += blockDim.x) {
-    sx[j] = src[3 * (base + j)];
-    sy[j] = src[3 * (base + j) + 1];
-    sz[j] = src[3 * (base + j) + 2];
+    sx[j] = scale * src[3 * (base + j)];
+    sy[j] = scale * src[3 * (base + j) + 1];
+    sz[j] = scale * src[3 * (base + j) + 2];
   }
 }
 
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
                                                             GridDev g, double k1, double kim,
                                                             double amp, double2* __restrict__ out,
                                                             int* flag, int n_eh = 0) {
+  // coordinates scaled by k1 (distances in table turns, SC terms); kim arrives as Im k / k1
   __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
   __shared__ double2 tab[kPhaseN];
   __shared__ double eh[ATT == 3 ? kEhMax : 1];
@@ -190,18 +195,19 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
     ix0 = int(idx % row_threads) * kVPT;
     row = idx / row_threads;
     nv = min(kVPT, g.dims[0] - ix0);
-    y = centre(g.lo[1], int(row % g.dims[1]), g.dx);
-    z = centre(g.lo[2], int(row / g.dims[1]), g.dx);
+    y = k1 * centre(g.lo[1], int(row % g.dims[1]), g.dx);
+    z = k1 * centre(g.lo[2], int(row / g.dims[1]), g.dx);
   }
 #pragma unroll
-  for (int v = 0; v < kVPT; ++v) x[v] = centre(g.lo[0], ix0 + min(v, max(nv - 1, 0)), g.dx);  // tail: repeat the last voxel
+  for (int v = 0; v < kVPT; ++v) x[v] = k1 * centre(g.lo[0], ix0 + min(v, max(nv - 1, 0)), g.dx);  // tail: repeat the last voxel
+  const long long tiny_bits = __double_as_longlong(k1 * 1e-12 * (k1 * 1e-12));
   double2 acc[kVPT];
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) acc[v] = make_double2(0.0, 0.0);
   bool bad = false;
   for (int base = 0; base < n_src; base += kSrcChunk) {
     __syncthreads();
-    stage_sources(src, n_src, base, sx, sy, sz);
+    stage_sources(src, n_src, base, sx, sy, sz, k1);
     __syncthreads();
     if (active) {
       const int n = min(kSrcChunk, n_src - base);
@@ -213,7 +219,7 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
 #pragma unroll
         for (int v = 0; v < kVPT; ++v) {
           const double ddx = x[v] - s0;
-          monopole_term_d2<ATT>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh);
+          monopole_term_d2<ATT, true>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh, tiny_bits);
         }
       }
     }
@@ -221,9 +227,10 @@ __global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __rest
   if (active) {
     if (bad) atomicExch(flag, 1);
     double2* o = out + row * g.dims[0] + ix0;
+    const double a = amp * k1;  // the terms' 1/d is in table turns: 1/d = k1 / d'
 #pragma unroll
     for (int v = 0; v < kVPT; ++v)
-      if (v < nv) o[v] = make_double2(amp * acc[v].x, amp * acc[v].y);
+      if (v < nv) o[v] = make_double2(a * acc[v].x, a * acc[v].y);
   }
 }
 
@@ -608,6 +615,8 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   const int threads = 256;
   const unsigned blocks = unsigned((count + threads - 1) / threads);
   const double k1 = phase_scale(kre);
+  if (!(k1 > 0.0))  // the grid kernel measures distances in phase-table turns (Re k > 0)
+    return set_error(FUSG_INVALID_ARGUMENT, "monopole_grid: Re k must be positive");
   // attenuating media: tabulated attenuation (ATT 3) when every Re k d / (2 pi) N fits the
   // coarse table (FUSG_ATT_TABLE=0 keeps the polynomial / exp() modes)
   static const bool att_table = [] {
@@ -621,7 +630,7 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
                                                        ctx->dev_flag, n_eh);
   } else {
     FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel, blocks, threads, 0, s>>>(
-                          src_dev, n_src, to_dev(g), k1, kim, amp, out, ctx->dev_flag));
+                          src_dev, n_src, to_dev(g), k1, kim / k1, amp, out, ctx->dev_flag));
   }
   ctx->launches++;
   FUSG_LAUNCH_CHECK("monopole_grid_kernel");
