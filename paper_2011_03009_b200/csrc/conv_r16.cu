@@ -289,9 +289,17 @@ enum R2CMode { kR2CPlain = 0, kR2CFusedA = 1, kR2CFusedB = 2 };
 // One 8-row tile (rows i0..i0+7 at outer k) of a row -> column pass; CG: read the input rows
 // through L2 only (ld.global.cg: rows another CTA of the same launch wrote).
 // (in_base, out_base, n_inner override a's for the fused A+B kernel.)
-template <int MODE>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// stage (optional): the tile's input rows already staged in shared memory, row w at
+// stage + w * a.in_si; after_load() runs once every warp has its row in registers (after a CTA
+// barrier), so the caller may refill the stage while the tile is transformed.
+template <int MODE, class Hook = NoHook>
 __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base, double2* out_base, int n_inner,
-                                         int i0, int k, double2* tile, bool hints = true) {
+                                         int i0, int k, double2* tile, bool hints = true,
+                                         const double2* stage = nullptr, Hook after_load = Hook{}) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lines_ok = min(8, n_inner - i0);
   const bool ok = w < lines_ok;
@@ -302,9 +310,16 @@ __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base,
   for (int e = 0; e < 8; ++e) {
     const int pos = lane + 32 * e;
     v[e] = make_double2(0.0, 0.0);
-    if (ok && pos < a.in_nvalid)
-      v[e] = MODE == kR2CFusedB ? __ldcg(in + pos)
-             : (MODE == kR2CFusedA && hints) ? ld_nc_hint(in + pos, pol_first) : __ldg(in + pos);
+    if (ok && pos < a.in_nvalid) {
+      if (stage) v[e] = stage[w * a.in_si + pos];
+      else
+        v[e] = MODE == kR2CFusedB ? __ldcg(in + pos)
+               : (MODE == kR2CFusedA && hints) ? ld_nc_hint(in + pos, pol_first) : __ldg(in + pos);
+    }
+  }
+  if (stage) {
+    __syncthreads();  // every warp has its row: the stage may be refilled
+    after_load();
   }
   dft16_half_in<false>(v);
   {  // one exact table power per lane, the others by squaring (one FFT per warp)
@@ -331,6 +346,7 @@ __device__ __forceinline__ void r2c_tile(const WArgs& a, const double2* in_base,
   if (a.pm.n == 0) {
     double2* base = out_base + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
     const uint64_t pol = MODE == kR2CFusedA ? l2_policy_last() : pol_first;
+#pragma unroll 4
     for (int e = threadIdx.x; e < a.out_nvalid * 8; e += 256) {
       const int pos = e >> 3, t = e & 7;
       if (t < lines_ok) {
@@ -395,6 +411,18 @@ __device__ __forceinline__ ABItem ab_item(const ABFused& f, int t) {
   const int last_nz = f.nz - 8 * (S - 1);
   const int na_full = nyt * 8, na_last = nyt * last_nz;
   ABItem it;
+  if (f.mode & 16) {  // experiment: every A item, then every B item (ring = one slot per slab)
+    const int na = nyt * f.nz;
+    if (t < na) {
+      it.isA = true, it.s = t / na_full, it.r = t - it.s * na_full, it.dep = nullptr, it.need = 0;
+    } else {
+      const int u = t - na;
+      it.isA = false, it.s = u / nkx, it.r = u - it.s * nkx;
+      it.dep = f.sync + 1 + it.s;
+      it.need = it.s == S - 1 ? na_last : na_full;
+    }
+    return it;
+  }
   const int a0 = S == 1 ? na_last : na_full;
   if (t < a0) {
     it.isA = true, it.s = 0, it.r = t;
@@ -429,60 +457,123 @@ __device__ __forceinline__ ABItem ab_item(const ABFused& f, int t) {
 
 // Persistent CTAs take items round-robin (CTA c: c, c + G, ...), all co-resident.  The
 // smallest unfinished item's dependencies all have smaller indices, so some CTA can always
-// progress.  Thread 0 prefetches the counter the CTA's next item depends on while the current
-// one is computed; completions are published by thread 0 after a CTA barrier (fence + add).
+// progress.  Each item's input is one contiguous block (8 rows of f, or the ring block
+// [kx][zz][y] of one kx), copied into a 32 KB shared stage by one 1-D bulk copy (TMA); the next
+// item's copy is issued as soon as the current rows are in registers (if its dependency is
+// already met, else at its start).  Completions are published by thread 0 after a CTA barrier
+// (fence + add).
+constexpr int kABStage = 8 * 256;  // staged input elements (8 rows of <= 256)
+constexpr size_t kABFusedBytes = kR16TileBytes + kABStage * sizeof(double2) + 16;
+
 __global__ void __launch_bounds__(256, 2) ab_fused_r16(ABFused f) {
-  extern __shared__ double2 tile[];
+  extern __shared__ double2 sm[];
+  double2* const tile = sm;
+  double2* const stage = sm + 512 * 8;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(stage + kABStage);
   const int nyt = (f.a.n_inner + 7) / 8;
   const int last_nz = f.nz - 8 * (f.slabs - 1);
   const int total = nyt * f.nz + f.b.n_outer * f.slabs;
   int* const doneA = f.sync + 1;
   int* const doneB = f.sync + 1 + f.slabs;
-  int seen = 0;  // thread 0: prefetched value of the current item's dependency counter
-  if (threadIdx.x == 0 && int(blockIdx.x) < total) {
-    const ABItem it = ab_item(f, blockIdx.x);
-    seen = it.dep ? ld_relaxed(it.dep) : 0;
+  auto slot_of = [&](int s) { return const_cast<double2*>(f.b.in) + int64_t(s % f.ring) * f.slot; };
+  // thread 0: issue the bulk copy of item it's input block
+  auto issue = [&](const ABItem& it) {
+    const double2* src;
+    unsigned bytes;
+    if (it.isA) {
+      const int zz = it.r / nyt, y0 = (it.r - zz * nyt) * 8;
+      src = f.a.in + int64_t(y0) * f.a.in_si + int64_t(8 * it.s + zz) * f.a.in_sk;
+      bytes = unsigned(min(8, f.a.n_inner - y0) * f.a.in_si * sizeof(double2));
+    } else {
+      const int nzs = it.s == f.slabs - 1 ? last_nz : 8;
+      src = slot_of(it.s) + int64_t(it.r) * f.b.in_sk;
+      bytes = unsigned(nzs * f.b.in_si * sizeof(double2));
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // ring rows written by generic stores
+    }
+    bulk_stage(stage, src, bytes, bar);
+  };
+  // thread 0: is item it's input dependency met (B: its slab's pass-A tiles all done)?
+  auto input_ready = [&](const ABItem& it, bool wait) {
+    if (it.isA) return true;
+    if (wait) {
+      while (ld_acquire(doneA + it.s) < it.need) __nanosleep(32);
+      return true;
+    }
+    if (ld_relaxed(doneA + it.s) < it.need) return false;
+    __threadfence();  // acquire side of the observation
+    return true;
+  };
+  bool pre = false;     // thread 0: the current item's input copy is already in flight
+  int* pub = nullptr;   // thread 0: counter of the finished item not yet published
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init_fence();
+    if (int(blockIdx.x) < total) {
+      const ABItem it = ab_item(f, blockIdx.x);
+      pre = input_ready(it, false);
+      if (pre) issue(it);
+    }
   }
+  __syncthreads();
+  unsigned phase = 0;
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     const ABItem it = ab_item(f, t);
     if (threadIdx.x == 0) {
-      if (it.dep && seen < it.need)
-        while (ld_acquire(it.dep) < it.need) __nanosleep(32);
-      else if (it.dep && !(f.mode & 1))
-        __threadfence();  // acquire side of the prefetched observation
-      const int tn = t + int(gridDim.x);
-      if (tn < total) {  // prefetch the next item's dependency
-        const ABItem nx = ab_item(f, tn);
-        seen = nx.dep ? ld_relaxed(nx.dep) : 0;
+      if (pub && (!pre || (it.isA && it.dep))) {  // about to block: publish first (no self-wait)
+        if (!(f.mode & 2)) __threadfence();
+        atomicAdd(pub, 1);
+        pub = nullptr;
       }
+      if (!pre) {
+        input_ready(it, true);
+        issue(it);
+      }
+      if (it.isA && it.dep)  // the ring slot must have been read out by B(s - R)
+        while (ld_acquire(it.dep) < it.need) __nanosleep(32);
     }
-    __syncthreads();
-    double2* const slot = const_cast<double2*>(f.b.in) + int64_t(it.s % f.ring) * f.slot;
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    double2* const slot = slot_of(it.s);
+    const int nzs = it.s == f.slabs - 1 ? last_nz : 8;
+    auto refill = [&]() {  // after the CTA barrier in r2c_tile: the stage is free
+      if (threadIdx.x == 0) {
+        if (pub) {  // the previous item's stores were all issued before this barrier
+          if (!(f.mode & 2)) __threadfence();
+          atomicAdd(pub, 1);
+          pub = nullptr;
+        }
+        pre = false;
+        const int tn = t + int(gridDim.x);
+        if (tn < total) {
+          const ABItem nx = ab_item(f, tn);
+          pre = input_ready(nx, false);
+          if (pre) issue(nx);
+        }
+      }
+      if (!it.isA && !(f.mode & 4)) {
+        // the ring block [kx = r][zz < nzs][y] is dead (this item's rows are in registers): drop
+        // its L2 lines without write-back
+        const char* blk = reinterpret_cast<const char*>(slot + int64_t(it.r) * f.b.in_sk);
+        const int lines = int((int64_t(nzs) * f.b.in_si * int64_t(sizeof(double2)) + 127) / 128);
+        for (int l = threadIdx.x; l < lines; l += 256) l2_discard(blk + 128 * l);
+      }
+    };
     if (it.isA) {
       const int zz = it.r / nyt, yt = it.r - zz * nyt;
       // k = z indexes f; in the slot it is z - 8 s
       r2c_tile<kR2CFusedA>(f.a, f.a.in, slot - int64_t(8 * it.s) * f.a.out_sk, f.a.n_inner, yt * 8,
-                           8 * it.s + zz, tile, !(f.mode & 8));
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (!(f.mode & 2)) __threadfence();
-        atomicAdd(doneA + it.s, 1);
-      }
+                           8 * it.s + zz, tile, !(f.mode & 8), stage, refill);
     } else {
-      const int nzs = it.s == f.slabs - 1 ? last_nz : 8;
-      r2c_tile<kR2CFusedB>(f.b, slot, f.b.out + 8 * it.s, nzs, 0, it.r, tile, !(f.mode & 8));  // z offset 8 s in B
-      // the block [kx = r][zz < nzs][y] is dead (read only by this item): drop its L2 lines
-      // without write-back
-      const char* blk = reinterpret_cast<const char*>(slot + int64_t(it.r) * f.b.in_sk);
-      const int lines = int((int64_t(nzs) * f.b.in_si * int64_t(sizeof(double2)) + 127) / 128);
-      if (!(f.mode & 4))
-        for (int l = threadIdx.x; l < lines; l += 256) l2_discard(blk + 128 * l);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (!(f.mode & 2)) __threadfence();  // discards (weak writes) ordered before the slot is released to A(s + R)
-        atomicAdd(doneB + it.s, 1);
-      }
+      r2c_tile<kR2CFusedB>(f.b, slot, f.b.out + 8 * it.s, nzs, 0, it.r, tile, !(f.mode & 8), stage, refill);
     }
+    // publication is deferred to the next item's refill barrier (or the end); the tile is
+    // reused by the next item only after its own exchange barriers
+    if (threadIdx.x == 0) pub = it.isA ? doneA + it.s : doneB + it.s;  // B: also its discards
+    __syncthreads();  // the tile's cooperative reads are done before the next item writes it
+  }
+  if (threadIdx.x == 0 && pub) {
+    if (!(f.mode & 2)) __threadfence();
+    atomicAdd(pub, 1);
   }
 }
 
@@ -613,20 +704,23 @@ int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s
 
 int launch_ab_fused_r16(fusg_ctx* ctx, const ABFused& f, cudaStream_t s) {
   // FUSG_AB_FUSED=1 opts in.  Measured on cfg2: DRAM traffic of A+B drops from 2.3 to 1.33 GB
-  // (the ring stays in L2, its dead lines discarded), but the launch takes 0.52-0.58 ms against
-  // 0.434 ms for the two separate launches, so it is off by default.
+  // (the ring stays in L2, its dead lines discarded), but the launch takes 0.63 ms against
+  // 0.434 ms for the two separate launches, so it is off by default.  The persistent item loop
+  // itself is the cost: with every A item before every B item and the whole bufA as the ring
+  // (FUSG_ABF_MODE=16, DRAM traffic as unfused) it also takes 0.63 ms; ncu shows CTA-barrier
+  // and FP64-dependency stalls at 16 warps per SM where the one-shot launches overlap CTAs.
   static const bool on = [] {
     const char* e = getenv("FUSG_AB_FUSED");
     return e && atoi(e) != 0;
   }();
   if (!on) return 0;
   const auto fn = ab_fused_r16;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR16TileBytes)) != cudaSuccess) {
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kABFusedBytes)) != cudaSuccess) {
     set_error(FUSG_CUDA, "fused passes A+B: cannot configure shared memory");
     return -1;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kR16TileBytes) != cudaSuccess || per_sm < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kABFusedBytes) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     return 0;
   }
@@ -640,7 +734,11 @@ int launch_ab_fused_r16(fusg_ctx* ctx, const ABFused& f, cudaStream_t s) {
   }();
   ABFused g = f;
   g.mode = mode;
-  fn<<<unsigned(per_sm * ctx->num_sms), 256, kR16TileBytes, s>>>(g);
+  if (mode & 16) {  // experiment (Nz a multiple of 8): the whole bufA as the ring
+    if (int64_t(g.slabs) * 8 != g.nz) return 0;
+    g.ring = g.slabs;
+  }
+  fn<<<unsigned(per_sm * ctx->num_sms), 256, kABFusedBytes, s>>>(g);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
