@@ -236,7 +236,14 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     return 0;
   }
   const int64_t lines = int64_t(a.n_inner) * a.n_outer;
-  const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
+  // FUSG_R16_WAVES: CTAs per resident slot (1 = fully persistent).  8 measured best on cfg2
+  // (0.730 -> 0.687 ms): CTAs retiring and relaunching through the block scheduler keep the
+  // SMs' warps out of phase better than one long-lived CTA per slot.
+  static const int waves = [] {
+    const char* e = getenv("FUSG_R16_WAVES");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms * waves);
   fn<<<unsigned(grid), kPPWarps * 32, smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
@@ -690,7 +697,11 @@ int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s
       return 0;
     }
     const int64_t tiles = int64_t((a.n_inner + kR16CT - 1) / kR16CT) * a.n_outer;
-    const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+    static const int waves = [] {  // FUSG_R16_C2R_WAVES: CTAs per SM slot (1 = persistent)
+      const char* e = getenv("FUSG_R16_C2R_WAVES");
+      return e ? std::max(1, atoi(e)) : 1;
+    }();
+    const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * waves);
     fn<<<unsigned(grid), kR16CT * 32, kR16C2RBytes, s>>>(a);
   }
   ctx->launches++;

@@ -117,6 +117,15 @@ int device_padded_size(int n, int axis) {
         if (L <= smooth * 1.35) p = L;
         break;
       }
+  static const int pxy_warp = [] {  // FUSG_PXY_WARP: prefer warp-engine lengths on x / y too
+    const char* e = getenv("FUSG_PXY_WARP");
+    return e ? atoi(e) : 0;
+  }();
+  if (axis != 2 && pxy_warp) {
+    for (int L : {256, 512, 768, 1024, 1536})
+      if (L <= pxy_warp && L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
+    return p;
+  }
   if (axis != 2 || !pz_warp) return p;
   for (int L : {256, 512, 768, 1024, 1536, 2048})  // persistent pass C (warp / multi-warp lines)
     if (L <= pz_warp && L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
@@ -888,6 +897,17 @@ __global__ void __launch_bounds__(T * LANES, MINB) mw_col_to_row(WArgs a) {
   if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
 
+// FUSG_PP_WAVES: CTAs per resident slot of the persistent warp kernels of the other lengths
+// (pass C, multi-warp lines, D/E col->row); 1 = fully persistent.  8: 768^3 apply 73.5 -> 71.8
+// ms, 323^3 6.17 -> 6.12 ms (the block scheduler's relaunches desynchronise the warps).
+static int pp_waves() {
+  static const int w = [] {
+    const char* e = getenv("FUSG_PP_WAVES");
+    return e ? std::max(1, atoi(e)) : 8;
+  }();
+  return w;
+}
+
 struct MWVariant {
   int L;
   bool r2c, def;
@@ -967,7 +987,7 @@ static int launch_mw(fusg_ctx* ctx, int L, bool r2c, const WArgs& a, cudaStream_
     return 0;
   }
   const int64_t tiles = int64_t((a.n_inner + v->T - 1) / v->T) * a.n_outer;
-  const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * pp_waves());
   v->fn<<<unsigned(grid), threads, v->smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
@@ -977,6 +997,7 @@ static int launch_mw(fusg_ctx* ctx, int L, bool r2c, const WArgs& a, cudaStream_
   }
   return 1;
 }
+
 
 // FUSG_BULK=0: pass C stages its rows with per-lane cp.async instead of 1-D bulk copies
 static int bulk_staging() {
@@ -1040,7 +1061,7 @@ static int launch_conv64(fusg_ctx* ctx, int L, const WArgs& a, cudaStream_t s) {
     return 0;
   }
   const int64_t lines = int64_t(a.n_inner) * a.n_outer;
-  const int64_t grid = std::min<int64_t>((lines + groups - 1) / groups, int64_t(per_sm) * ctx->num_sms);
+  const int64_t grid = std::min<int64_t>((lines + groups - 1) / groups, int64_t(per_sm) * ctx->num_sms * pp_waves());
   fn<<<unsigned(grid), groups * lanes, smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
@@ -1152,7 +1173,7 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
       if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pp, kWarpThreads, psmem) == cudaSuccess &&
           per_sm >= 1) {
         const int64_t tiles = int64_t((a.n_inner + 7) / 8) * a.n_outer;
-        const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms);
+        const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * pp_waves());
         pp<<<unsigned(grid), kWarpThreads, psmem, s>>>(a);
         ctx->launches++;
         const cudaError_t err = cudaGetLastError();
@@ -1204,7 +1225,7 @@ static int launch_warp(fusg_ctx* ctx, int L, int mode, bool inv, const WArgs& a,
       return 0;
     }
     const int64_t lines = int64_t(a.n_inner) * a.n_outer;
-    const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms);
+    const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms * pp_waves());
     conv_pp<<<unsigned(grid), kPPWarps * 32, pp_smem, s>>>(a);
     ctx->launches++;
     const cudaError_t err = cudaGetLastError();
