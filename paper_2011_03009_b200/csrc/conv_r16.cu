@@ -97,10 +97,13 @@ __device__ __forceinline__ int r16_ex(int row, int col) { return row * 32 + (col
 
 // per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
 template <bool TAB>
-constexpr size_t r16_smem_bytes() { return PPConvSmem<512, true>::BYTES + (TAB ? 16 : 4) * 32 * sizeof(double2); }
+constexpr size_t r16_smem_bytes(int nw) {
+  return size_t(nw) * PPConvSmem<512, true>::PER_WARP * sizeof(double2) + nw * 2 * sizeof(uint64_t) +
+         (TAB ? 16 : 4) * 32 * sizeof(double2);
+}
 
-template <int MINB, bool TAB>
-__global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a) {
+template <int NW, int MINB, bool TAB>
+__global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   constexpr int L = 512;
   constexpr int HZ = L / 2 + 1;
   using SM = PPConvSmem<L, true>;
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
   double2* const xb = sm + size_t(w) * SM::PER_WARP;
   double2* const sb = xb + L;
   double2* const kb = sb + SM::STAGE;
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(kPPWarps) * SM::PER_WARP) + 2 * w;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(NW) * SM::PER_WARP) + 2 * w;
   if (lane == 0) {
     mbar_init(bars, 1);
     mbar_init(bars + 1, 1);
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
   __syncwarp();
   unsigned ph_in = 0, ph_k = 0;
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
-  const int64_t stride = int64_t(gridDim.x) * kPPWarps;
+  const int64_t stride = int64_t(gridDim.x) * NW;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
     const unsigned l = unsigned(line), ni = unsigned(a.n_inner);
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
       bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
     }
   };
-  double2* const tws = sm + size_t(kPPWarps) * SM::PER_WARP + 4;  // after the 8 mbarriers (64 B)
+  double2* const tws = sm + size_t(NW) * SM::PER_WARP + NW;  // after the 2 NW mbarriers
   if (w == 0) {
     if constexpr (TAB) {
       for (int j = 0; j < 16; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane * j) & (L - 1)));
@@ -154,7 +157,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, MINB) warp_row_conv_r16(WArgs a
   const bool b = lane >= 16;
   const int k1 = lane & 15;
   const auto I8 = std::make_integer_sequence<int, 8>{};
-  int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
+  int64_t line = int64_t(blockIdx.x) * NW + w;
   prefetch_in(line);
   prefetch_k(line);
   for (; line < nlines; line += stride) {
@@ -224,14 +227,23 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   }();
   const int64_t nl = int64_t(a.n_inner) * a.n_outer;
   if (nl >= (int64_t(1) << 31)) return 0;
-  const auto fn = tab ? warp_row_conv_r16<FUSG_PP_MINB, true> : warp_row_conv_r16<FUSG_PP_MINB, false>;
-  const size_t smem = tab ? r16_smem_bytes<true>() : r16_smem_bytes<false>();
+  static const int nw = [] {  // FUSG_R16_NW: warps per CTA (2, 3, 4, 6; 12 warps per SM)
+    const char* e = getenv("FUSG_R16_NW");
+    const int v = e ? atoi(e) : 4;
+    return (v == 2 || v == 3 || v == 6) ? v : 4;
+  }();
+  using Fn = void (*)(WArgs);
+  const Fn fn = nw == 2   ? (tab ? warp_row_conv_r16<2, 6, true> : warp_row_conv_r16<2, 6, false>)
+                : nw == 3 ? (tab ? warp_row_conv_r16<3, 4, true> : warp_row_conv_r16<3, 4, false>)
+                : nw == 6 ? (tab ? warp_row_conv_r16<6, 2, true> : warp_row_conv_r16<6, 2, false>)
+                          : (tab ? warp_row_conv_r16<4, FUSG_PP_MINB, true> : warp_row_conv_r16<4, FUSG_PP_MINB, false>);
+  const size_t smem = tab ? r16_smem_bytes<true>(nw) : r16_smem_bytes<false>(nw);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
     set_error(FUSG_CUDA, "pass C (16x16x2): cannot configure shared memory");
     return -1;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kPPWarps * 32, smem) != cudaSuccess || per_sm < 1) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     return 0;
   }
@@ -243,8 +255,8 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     const char* e = getenv("FUSG_R16_WAVES");
     return e ? std::max(1, atoi(e)) : 8;
   }();
-  const int64_t grid = std::min<int64_t>((lines + kPPWarps - 1) / kPPWarps, int64_t(per_sm) * ctx->num_sms * waves);
-  fn<<<unsigned(grid), kPPWarps * 32, smem, s>>>(a);
+  const int64_t grid = std::min<int64_t>((lines + nw - 1) / nw, int64_t(per_sm) * ctx->num_sms * waves);
+  fn<<<unsigned(grid), nw * 32, smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
