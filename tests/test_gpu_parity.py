@@ -403,7 +403,9 @@ def test_cpp_dropin_api_all_cases(ctx):
 
 
 @pytest.mark.parametrize("dims,G", [((37, 20, 19), 2), ((37, 20, 19), 3), ((64, 64, 64), 4),
-                                    ((16, 24, 9), 8), ((25, 30, 7), 7)])
+                                    ((16, 24, 9), 8), ((25, 30, 7), 7),
+                                    # Pz = 512: the 16x16x2 pass C on kx slabs (kx offset, no mirror order)
+                                    ((37, 20, 150), 2), ((37, 20, 150), 3)])
 def test_slab_sharded_apply_loopback_is_bitwise_unsharded(ctx, dims, G):
     # the sharded apply uses the same pass kernels and differs only in data
     # movement, so every decomposition must reproduce the single-GPU apply bit for bit.
