@@ -124,10 +124,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   const int64_t stride = int64_t(gridDim.x) * NW;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
-    const unsigned l = unsigned(line), ni = unsigned(a.n_inner);
-    const unsigned q = l / ni;
-    ky = interleave_index(int(l - q * ni), a.ko.Py);
-    kx = mirror ? interleave_index(int(q), a.ko.Px) : int(q);
+    conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
   auto prefetch_in = [&](int64_t line) {
     if (line < nlines && lane == 0) {

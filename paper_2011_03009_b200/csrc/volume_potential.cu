@@ -539,8 +539,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
   const int64_t stride = int64_t(gridDim.x) * kPPWarps;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {
-    ky = interleave_index(int(unsigned(line) % unsigned(a.n_inner)), a.ko.Py);
-    kx = mirror ? interleave_index(int(unsigned(line) / unsigned(a.n_inner)), a.ko.Px) : int(unsigned(line) / unsigned(a.n_inner));
+    conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
   // staged position p lives at S[swz(p)] (PRUNED: p < L/2, so the swizzle stays inside S)
   auto prefetch_in = [&](int64_t line) {
@@ -665,8 +664,7 @@ __global__ void __launch_bounds__(GROUPS * LANES, MINB) warp_row_conv_pp64(WArgs
   const int64_t stride = int64_t(gridDim.x) * GROUPS;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) {
-    ky = interleave_index(int(unsigned(line) % unsigned(a.n_inner)), a.ko.Py);
-    kx = mirror ? interleave_index(int(unsigned(line) / unsigned(a.n_inner)), a.ko.Px) : int(unsigned(line) / unsigned(a.n_inner));
+    conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
   auto prefetch_in = [&](int64_t line) {
     if (line < nlines) {
@@ -1506,6 +1504,17 @@ fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s) {
                             GStoreF{GStore{K->bufA, 1, Ny, int64_t(nz) * Ny, Px, 1.0}}, s, kKindRow);
 }
 
+// FUSG_CONV_QUAD=1: pass-C lines in quad order (kx mirror pairs interleaved at the finest
+// level, conv_line_coords in warp_args.cuh) instead of kx-slow order.  Measured neutral to
+// slightly slower (512: 0.703 -> 0.711 ms, 768: 2.88 -> 2.90, 1536: 34.0 -> 34.0), so off.
+static int conv_quad() {
+  static const int q = [] {
+    const char* e = getenv("FUSG_CONV_QUAD");
+    return (e && atoi(e) != 0) ? 1 : 0;
+  }();
+  return q;
+}
+
 // passes B, C on the x-slab X [nx][Nz][Ny] into B (ev, optional: marks after B and after C)
 static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEvent_t* ev) {
   const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
@@ -1518,7 +1527,7 @@ static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   if (ev) cudaEventRecord(ev[0], s);
   FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
                        GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
-                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0}, s));
+                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0, conv_quad()}, s));
   if (ev) cudaEventRecord(ev[1], s);
   return FUSG_OK;
 }
@@ -1594,7 +1603,7 @@ fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s) {
   const int64_t PyNz = int64_t(Py) * Nz;
   return launch_conv(K->ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
                      GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
-                     KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0}, s);
+                     KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0, conv_quad()}, s);
 }
 
 fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s) {

@@ -29,6 +29,39 @@ __device__ __forceinline__ int interleave_index(int r, int P) {
   return (r & 1) ? m : P - m;
 }
 
+// (ky, kx) of pass-C line `line` of n_inner (ky) x n_outer (kx) lines.  Unsharded (mirror) with
+// quad order: the kx interleave index r runs 0 | (1, 2) | (3, 4) | ... (| Px - 1 when Px is
+// even); inside a pair the two kx alternate at the finest level and ky runs mirror-interleaved,
+// so the (up to) four lines reading one folded K^ row are consecutive.  Otherwise kx slow, ky
+// mirror-interleaved fast (the partner kx row then follows Py lines later).
+__device__ __forceinline__ void conv_line_coords(unsigned line, const KOct& ko, int n_inner, bool mirror, int& ky,
+                                                 int& kx) {
+  const unsigned ni = unsigned(n_inner);
+  if (!mirror || !ko.quad) {
+    const unsigned q = line / ni;
+    ky = interleave_index(int(line - q * ni), ko.Py);
+    kx = mirror ? interleave_index(int(q), ko.Px) : int(q);
+    return;
+  }
+  if (line < ni) {
+    ky = interleave_index(int(line), ko.Py);
+    kx = 0;
+    return;
+  }
+  unsigned l = line - ni;
+  const unsigned npairs = unsigned(ko.Px - 1) / 2u;
+  const unsigned g = l / (2u * ni);
+  if (g < npairs) {
+    const unsigned within = l - g * 2u * ni;
+    ky = interleave_index(int(within >> 1), ko.Py);
+    kx = interleave_index(int(2u * g + 1u + (within & 1u)), ko.Px);
+    return;
+  }
+  l -= npairs * 2u * ni;  // Px even: the self-mirror column r = Px - 1 (kx = Px / 2)
+  ky = interleave_index(int(l), ko.Py);
+  kx = interleave_index(ko.Px - 1, ko.Px);
+}
+
 constexpr int kPPWarps = 4;  // warps per CTA
 #ifndef FUSG_PP_MINB
 #define FUSG_PP_MINB 3  // CTAs per SM the register budget targets (3: <= 168 registers)
