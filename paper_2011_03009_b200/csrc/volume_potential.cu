@@ -926,7 +926,8 @@ struct MWVariant {
 // Variants per (length, direction); FUSG_MW_<L>_R2C / _C2R = index among them (-1: static
 // kernels), else the one marked default.  Measured (tools/pass_times.py, ms for A B D E):
 //   1536 (768^3): static 8.8 17.4 17.8 8.5 -> 6.7 12.7 11.0 6.3 (apply 86.1 -> 70.4 ms);
-//                 T = 2 tiles: 12.5 14.0 10.8 11.6
+//                 T = 2 tiles: 12.5 14.0 10.8 11.6; 128-lane lines (12 points per lane, radices
+//                 4,4,4,4,2,3, 16 warps per SM): 8.8 17.4 17.9 8.6 (pass C 4,4,2,3,4,4: 63 vs 34 ms)
 //   1024 (512^3): static 1.95 3.75 3.93 2.03 -> r2c 1.96 3.76 (kept static), c2r 3.33 1.88
 //   512 (cfg2): pp warp kernels 0.156 0.297 0.344 0.178 -> c2r on 4-line tiles (3 CTAs, 12
 //                 warps per SM) 0.295 0.166 (apply 1.861 -> 1.800 ms); 8-line tiles 0.348 0.180;
