@@ -97,22 +97,26 @@ __device__ __forceinline__ int r16_ex(int row, int col) { return row * 32 + (col
 
 // per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
 template <bool TAB>
-constexpr size_t r16_smem_bytes(int nw) {
-  return size_t(nw) * PPConvSmem<512, true>::PER_WARP * sizeof(double2) + nw * 2 * sizeof(uint64_t) +
-         (TAB ? 16 : 4) * 32 * sizeof(double2);
+constexpr size_t r16_smem_bytes(int nw, bool kl2 = false) {
+  return size_t(nw) * (kl2 ? 512 + PPConvSmem<512, true>::STAGE : PPConvSmem<512, true>::PER_WARP) * sizeof(double2) +
+         nw * 2 * sizeof(uint64_t) + (TAB ? 16 : 4) * 32 * sizeof(double2);
 }
 
-template <int NW, int MINB, bool TAB>
+// KL2: the K^ row is not staged in shared memory; it is prefetched into L2 one line ahead
+// (cp.async.bulk.prefetch) and read at the multiply with read-only loads.  12 KB per warp
+// instead of 16 lets 16 warps share an SM (MINB 4, 128 registers).
+template <int NW, int MINB, bool TAB, bool KL2 = false>
 __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   constexpr int L = 512;
   constexpr int HZ = L / 2 + 1;
   using SM = PPConvSmem<L, true>;
+  constexpr int PW = KL2 ? L + SM::STAGE : SM::PER_WARP;  // double2 per warp
   extern __shared__ double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* const xb = sm + size_t(w) * SM::PER_WARP;
+  double2* const xb = sm + size_t(w) * PW;
   double2* const sb = xb + L;
-  double2* const kb = sb + SM::STAGE;
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(NW) * SM::PER_WARP) + 2 * w;
+  double2* const kb = sb + SM::STAGE;  // (unused when KL2)
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(NW) * PW) + 2 * w;
   if (lane == 0) {
     mbar_init(bars, 1);
     mbar_init(bars + 1, 1);
@@ -137,10 +141,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     if (line < nlines && lane == 0) {
       int ky, kx;
       coords(line, ky, kx);
-      bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
+      if constexpr (KL2) {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.ko.line(ky, kx)), "r"(unsigned(HZ * sizeof(double2)))
+                     : "memory");
+      } else {
+        bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
+      }
     }
   };
-  double2* const tws = sm + size_t(NW) * SM::PER_WARP + NW;  // after the 2 NW mbarriers
+  double2* const tws = sm + size_t(NW) * PW + NW;  // after the 2 NW mbarriers
   if (w == 0) {
     if constexpr (TAB) {
       for (int j = 0; j < 16; ++j) tws[32 * j + lane] = __ldg(a.tw + ((lane * j) & (L - 1)));
@@ -179,16 +188,29 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     // forward stage B and the cross-lane radix 2
     dft16<false>(v);
     r16_r2_all<false>(v, b, I8);
-    mbar_wait(bars + 1, ph_k);
-    ph_k ^= 1;
+    if constexpr (KL2) {
+      int ky, kx;
+      coords(line, ky, kx);
+      const double2* kl = a.ko.line(ky, kx);
+      prefetch_k(line + stride);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
-      v[i] = cmul(v[i], kb[p]);
-      v[i + 8] = cmul(v[i + 8], kb[256 - p]);
+      for (int i = 0; i < 8; ++i) {
+        const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
+        v[i] = cmul(v[i], __ldg(kl + p));
+        v[i + 8] = cmul(v[i + 8], __ldg(kl + 256 - p));
+      }
+    } else {
+      mbar_wait(bars + 1, ph_k);
+      ph_k ^= 1;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
+        v[i] = cmul(v[i], kb[p]);
+        v[i + 8] = cmul(v[i + 8], kb[256 - p]);
+      }
+      __syncwarp();  // K^ row consumed
+      prefetch_k(line + stride);
     }
-    __syncwarp();  // K^ row consumed
-    prefetch_k(line + stride);
     // inverse: radix 2 (in-lane) + half-exchange back, stage B, exchange, twiddle, stage A
     r16_r2_all<true>(v, b, I8);
     dft16<true>(v);
@@ -229,18 +251,24 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     const int v = e ? atoi(e) : 4;
     return (v == 2 || v == 3 || v == 6) ? v : 4;
   }();
+  static const int kl2 = [] {  // FUSG_R16_KL2=1: K^ rows through L2, 16 warps per SM
+    const char* e = getenv("FUSG_R16_KL2");
+    return e ? atoi(e) : 0;
+  }();
   using Fn = void (*)(WArgs);
-  const Fn fn = nw == 2   ? (tab ? warp_row_conv_r16<2, 6, true> : warp_row_conv_r16<2, 6, false>)
+  const Fn fn = kl2 ? warp_row_conv_r16<4, 4, false, true>
+                : nw == 2 ? (tab ? warp_row_conv_r16<2, 6, true> : warp_row_conv_r16<2, 6, false>)
                 : nw == 3 ? (tab ? warp_row_conv_r16<3, 4, true> : warp_row_conv_r16<3, 4, false>)
                 : nw == 6 ? (tab ? warp_row_conv_r16<6, 2, true> : warp_row_conv_r16<6, 2, false>)
                           : (tab ? warp_row_conv_r16<4, FUSG_PP_MINB, true> : warp_row_conv_r16<4, FUSG_PP_MINB, false>);
-  const size_t smem = tab ? r16_smem_bytes<true>(nw) : r16_smem_bytes<false>(nw);
+  const size_t smem = kl2 ? r16_smem_bytes<false>(4, true) : tab ? r16_smem_bytes<true>(nw) : r16_smem_bytes<false>(nw);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
     set_error(FUSG_CUDA, "pass C (16x16x2): cannot configure shared memory");
     return -1;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nw * 32, smem) != cudaSuccess || per_sm < 1) {
+  const int nwl = kl2 ? 4 : nw;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nwl * 32, smem) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
     return 0;
   }
@@ -252,8 +280,8 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     const char* e = getenv("FUSG_R16_WAVES");
     return e ? std::max(1, atoi(e)) : 8;
   }();
-  const int64_t grid = std::min<int64_t>((lines + nw - 1) / nw, int64_t(per_sm) * ctx->num_sms * waves);
-  fn<<<unsigned(grid), nw * 32, smem, s>>>(a);
+  const int64_t grid = std::min<int64_t>((lines + nwl - 1) / nwl, int64_t(per_sm) * ctx->num_sms * waves);
+  fn<<<unsigned(grid), nwl * 32, smem, s>>>(a);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
