@@ -449,31 +449,45 @@ __global__ void rhs_kernel(LowerPtrs lp, int n, int64_t count, double coeff,
 }
 
 // interpolate (src/grid.cpp:141-195), exact rounding
-__global__ void interp_kernel(GridDev s, const double2* __restrict__ f, GridDev t,
-                              double2* __restrict__ out) {
-  const int64_t count = int64_t(t.dims[0]) * t.dims[1] * t.dims[2];
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < count;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int ix = int(idx % t.dims[0]);
-    const int64_t r = idx / t.dims[0];
-    const int iy = int(r % t.dims[1]);
-    const int iz = int(r / t.dims[1]);
-    const int ii[3] = {ix, iy, iz};
-    int i0[3];
-    double tt[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const double p = centre(t.lo[a], ii[a], t.dx);
-      const double q = __dsub_rn(__ddiv_rn(__dsub_rn(p, s.lo[a]), s.dx), 0.5);
-      int base = int(floor(q));
-      const int hi = max(0, s.dims[a] - 2);
-      base = base < 0 ? 0 : (base > hi ? hi : base);
-      double frac = __dsub_rn(q, double(base));
-      if (frac < 0.0) frac = 0.0;
-      if (frac > 1.0) frac = s.dims[a] > 1 ? 1.0 : 0.0;
-      i0[a] = base;
-      tt[a] = frac;
-    }
+// Source cell and weight of target index i on axis a (src/grid.cpp:156-170): q = (p - lo_s)/dx_s
+// - 0.5, base = clamp(floor q, 0, max(0, n - 2)), t = clamp(q - base, 0, 1) (t > 1 -> 1, or 0
+// when n == 1); the same correctly rounded operations as the reference's non-FMA build.
+__device__ __forceinline__ void interp_axis(const GridDev& s, const GridDev& t, int a, int i, int& base,
+                                            double& frac) {
+  const double p = centre(t.lo[a], i, t.dx);
+  const double q = __dsub_rn(__ddiv_rn(__dsub_rn(p, s.lo[a]), s.dx), 0.5);
+  int b = int(floor(q));
+  const int hi = max(0, s.dims[a] - 2);
+  b = b < 0 ? 0 : (b > hi ? hi : b);
+  double fr = __dsub_rn(q, double(b));
+  if (fr < 0.0) fr = 0.0;
+  if (fr > 1.0) fr = s.dims[a] > 1 ? 1.0 : 0.0;
+  base = b;
+  frac = fr;
+}
+
+// Per-axis cells and weights (they depend on one index each), computed once per call.
+__global__ void interp_axes_kernel(GridDev s, GridDev t, int* __restrict__ base, double* __restrict__ frac) {
+  const int n = t.dims[0] + t.dims[1] + t.dims[2];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int a = j < t.dims[0] ? 0 : (j < t.dims[0] + t.dims[1] ? 1 : 2);
+    const int i = a == 0 ? j : (a == 1 ? j - t.dims[0] : j - t.dims[0] - t.dims[1]);
+    interp_axis(s, t, a, i, base[j], frac[j]);
+  }
+}
+
+// Trilinear gather (src/grid.cpp:171-192) from the per-axis tables: 32-bit index arithmetic,
+// no divisions per point; consecutive threads take consecutive x.
+__global__ void __launch_bounds__(256) interp_kernel(GridDev s, const double2* __restrict__ f, GridDev t,
+                                                     const int* __restrict__ base, const double* __restrict__ frac,
+                                                     double2* __restrict__ out) {
+  const unsigned nx = unsigned(t.dims[0]), ny = unsigned(t.dims[1]);
+  const unsigned count = nx * ny * unsigned(t.dims[2]);
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < count; idx += gridDim.x * blockDim.x) {
+    const unsigned r = idx / nx, ix = idx - r * nx;
+    const unsigned iz = r / ny, iy = r - iz * ny;
+    const int i0[3] = {__ldg(base + ix), __ldg(base + nx + iy), __ldg(base + nx + ny + iz)};
+    const double tt[3] = {__ldg(frac + ix), __ldg(frac + nx + iy), __ldg(frac + nx + ny + iz)};
     double re = 0.0, im = 0.0;
 #pragma unroll
     for (int cz = 0; cz < 2; ++cz)
@@ -489,7 +503,7 @@ __global__ void interp_kernel(GridDev s, const double2* __restrict__ f, GridDev 
           const int jx = min(max(i0[0] + cx, 0), s.dims[0] - 1);
           const int jy = min(max(i0[1] + cy, 0), s.dims[1] - 1);
           const int jz = min(max(i0[2] + cz, 0), s.dims[2] - 1);
-          const double2 v = f[jx + int64_t(s.dims[0]) * (jy + int64_t(s.dims[1]) * jz)];
+          const double2 v = __ldg(f + jx + int64_t(s.dims[0]) * (jy + int64_t(s.dims[1]) * jz));
           re = __dadd_rn(re, __dmul_rn(wgt, v.x));
           im = __dadd_rn(im, __dmul_rn(wgt, v.y));
         }
@@ -644,7 +658,17 @@ fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* 
       return set_error(FUSG_INVALID_ARGUMENT,
                        "interpolate: target extends more than one source voxel beyond the source domain");
   const int64_t count = int64_t(tgt.dims[0]) * tgt.dims[1] * tgt.dims[2];
-  interp_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(to_dev(src), f, to_dev(tgt), out);
+  if (count >= (int64_t(1) << 32))
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate: target above 2^32 voxels");
+  const int nax = tgt.dims[0] + tgt.dims[1] + tgt.dims[2];
+  void* tabs = nullptr;
+  FUSG_CUDA_TRY(cudaMallocAsync(&tabs, size_t(nax) * (sizeof(int) + sizeof(double)) + 16, s));
+  double* frac = static_cast<double*>(tabs);
+  int* base = reinterpret_cast<int*>(frac + nax);
+  interp_axes_kernel<<<(nax + 255) / 256, 256, 0, s>>>(to_dev(src), to_dev(tgt), base, frac);
+  interp_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(to_dev(src), f, to_dev(tgt), base, frac, out);
+  ctx->launches++;
+  FUSG_CUDA_TRY(cudaFreeAsync(tabs, s));
   ctx->launches++;
   FUSG_LAUNCH_CHECK("interp_kernel");
   return FUSG_OK;
