@@ -171,9 +171,12 @@ __device__ __forceinline__ void stage_sources(const double* src, int n_src, int 
 // kVPT adjacent voxels of one x-row per thread: the (y, z) part of the squared distance is
 // shared, the source loads are amortised and the thread carries kVPT independent chains.
 constexpr int kVPT = 4;
+#ifndef FUSG_MONO_MINB
+#define FUSG_MONO_MINB 1  // CTAs per SM the grid kernel's register budget targets (4: 64 registers, measured equal: FP64-bound)
+#endif
 
 template <int ATT>
-__global__ void __launch_bounds__(256) monopole_grid_kernel(const double* __restrict__ src, int n_src,
+__global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(const double* __restrict__ src, int n_src,
                                                             GridDev g, double k1, double kim,
                                                             double amp, double2* __restrict__ out,
                                                             int* flag, int n_eh = 0) {
