@@ -58,18 +58,30 @@ constexpr double kPolyAttMax = 0.03;
 constexpr int kPhaseBits = 11;
 constexpr int kPhaseN = 1 << kPhaseBits;
 constexpr double kTwoPi = 6.283185307179586476925;
-constexpr double kPhC = kTwoPi / kPhaseN;  // radians per table step
-constexpr double kS1 = kPhC, kS3 = -kPhC * kPhC * kPhC / 6.0;
-constexpr double kC2 = -kPhC * kPhC / 2.0, kC4 = kPhC * kPhC * kPhC * kPhC / 24.0;
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 
 // table scale: the host passes k1 = Re k * N / (2 pi)
-inline double phase_scale(double kre) { return kre * double(kPhaseN) / kTwoPi; }
+inline double phase_scale(double kre, int bits = kPhaseBits) { return kre * double(1 << bits) / kTwoPi; }
 
+// Phase-table geometry for N = 2^BITS entries.  The grid kernel (the Rayleigh p1 sum) uses
+// 4096 entries in dynamic shared memory: the residual |2 pi v / N| <= 7.7e-4 lets cos drop to
+// degree 2 (error < 1.5e-14); the other kernels keep 2048 entries in static shared memory.
+constexpr int kGridPhaseBits = 12;
+template <int BITS>
+struct PhaseSpec {
+  static constexpr int N = 1 << BITS;
+  static constexpr double PhC = kTwoPi / N;
+  static constexpr double S1 = PhC, S3 = -PhC * PhC * PhC / 6.0;
+  static constexpr double C2 = -PhC * PhC / 2.0, C4 = PhC * PhC * PhC * PhC / 24.0;
+  static constexpr bool kCos2 = BITS >= 12;  // cos to degree 2
+};
+
+template <int BITS = kPhaseBits>
 __device__ __forceinline__ void fill_phase_table(double2* tab) {
-  for (int j = threadIdx.x; j < kPhaseN; j += blockDim.x) {
+  constexpr int N = 1 << BITS;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
     double sn, cs;
-    sincospi(2.0 * j / kPhaseN, &sn, &cs);  // exact argument (power-of-two denominator)
+    sincospi(2.0 * j / N, &sn, &cs);  // exact argument (power-of-two denominator)
     tab[j] = make_double2(cs * kInv4Pi, sn * kInv4Pi);
   }
 }
@@ -77,14 +89,16 @@ __device__ __forceinline__ void fill_phase_table(double2* tab) {
 // ATT 3 tables (monopole_grid_kernel): rows e^{2 pi i j / N} e^{-alpha j} / (4 pi) and the
 // coarse factors eh[m] = e^{-alpha N m}, m < n_eh (the host bounds Re k d / (2 pi) N by N n_eh).
 constexpr int kEhMax = 512;
+template <int BITS = kPhaseBits>
 __device__ __forceinline__ void fill_att_tables(double2* tab, double* eh, double alpha, int n_eh) {
-  for (int j = threadIdx.x; j < kPhaseN; j += blockDim.x) {
+  constexpr int N = 1 << BITS;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
     double sn, cs;
-    sincospi(2.0 * j / kPhaseN, &sn, &cs);
+    sincospi(2.0 * j / N, &sn, &cs);
     const double a = exp(-alpha * j) * kInv4Pi;
     tab[j] = make_double2(cs * a, sn * a);
   }
-  for (int m = threadIdx.x; m < n_eh; m += blockDim.x) eh[m] = exp(-alpha * double(kPhaseN) * m);
+  for (int m = threadIdx.x; m < n_eh; m += blockDim.x) eh[m] = exp(-alpha * double(N) * m);
 }
 
 __device__ __forceinline__ double rsqrt_refined(double x) {
@@ -118,7 +132,7 @@ __device__ __forceinline__ double attenuation(double t) {  // e^{-t}, t = Im k *
 // SC (scaled coordinates, monopole_grid_kernel): coordinates arrive pre-multiplied by k1, so d2
 // is already in table turns squared, u = d, the magnitude 1/d carries a factor 1/k1 the caller
 // restores once per voxel, and the coincidence bound is (k1 1e-12)^2 (bits in tiny_bits).
-template <int ATT, bool SC = false>
+template <int ATT, bool SC = false, int BITS = kPhaseBits>
 __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
                                                  const double2* __restrict__ tab, double2& acc,
                                                  bool& bad, const double* __restrict__ eh = nullptr,
@@ -130,18 +144,19 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
   const double d = d2 * ir;
   const double u = SC ? d : d * k1;
   const double t = u + kRoundMagic;
-  const int j = __double2loint(t) & (kPhaseN - 1);
+  using PS = PhaseSpec<BITS>;
+  const int j = __double2loint(t) & (PS::N - 1);
   const double v = u - (t - kRoundMagic);
   const double v2 = v * v;
-  const double sn = v * fma(v2, kS3, kS1);
-  const double cs = fma(v2, fma(v2, kC4, kC2), 1.0);
+  const double sn = v * fma(v2, PS::S3, PS::S1);
+  const double cs = PS::kCos2 ? fma(v2, PS::C2, 1.0) : fma(v2, fma(v2, PS::C4, PS::C2), 1.0);
   const double2 w = tab[j];
   double mag;
   if constexpr (ATT == 3) {
     // tabulated attenuation: kim carries alpha = Im k / k1, the table rows already hold
     // e^{-alpha (j mod N)}, eh[m] = e^{-alpha N m}, and e^{-alpha v} = 1 - alpha v to
     // (alpha v)^2 / 2 < 1e-18
-    mag = ir * eh[__double2loint(t) >> kPhaseBits] * fma(-kim, v, 1.0);
+    mag = ir * eh[__double2loint(t) >> BITS] * fma(-kim, v, 1.0);
   } else {
     mag = ATT == 0 ? ir : ir * attenuation<ATT>(kim * d);
   }
@@ -182,11 +197,12 @@ __global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(cons
                                                             int* flag, int n_eh = 0) {
   // coordinates scaled by k1 (distances in table turns, SC terms); kim arrives as Im k / k1
   __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
-  __shared__ double2 tab[kPhaseN];
-  __shared__ double eh[ATT == 3 ? kEhMax : 1];
+  extern __shared__ double2 dyn_tab[];  // phase table (2^kGridPhaseBits) + ATT 3 coarse table
+  double2* const tab = dyn_tab;
+  double* const eh = reinterpret_cast<double*>(dyn_tab + (1 << kGridPhaseBits));
   // visible after the first barrier of the source loop
-  if constexpr (ATT == 3) fill_att_tables(tab, eh, kim, n_eh);
-  else fill_phase_table(tab);
+  if constexpr (ATT == 3) fill_att_tables<kGridPhaseBits>(tab, eh, kim, n_eh);
+  else fill_phase_table<kGridPhaseBits>(tab);
   const int row_threads = (g.dims[0] + kVPT - 1) / kVPT;
   const int64_t count = int64_t(row_threads) * g.dims[1] * g.dims[2];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -222,7 +238,7 @@ __global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(cons
 #pragma unroll
         for (int v = 0; v < kVPT; ++v) {
           const double ddx = x[v] - s0;
-          monopole_term_d2<ATT, true>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh, tiny_bits);
+          monopole_term_d2<ATT, true, kGridPhaseBits>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh, tiny_bits);
         }
       }
     }
@@ -631,7 +647,7 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   const int64_t count = int64_t((g.dims[0] + kVPT - 1) / kVPT) * g.dims[1] * g.dims[2];
   const int threads = 256;
   const unsigned blocks = unsigned((count + threads - 1) / threads);
-  const double k1 = phase_scale(kre);
+  const double k1 = phase_scale(kre, kGridPhaseBits);
   if (!(k1 > 0.0))  // the grid kernel measures distances in phase-table turns (Re k > 0)
     return set_error(FUSG_INVALID_ARGUMENT, "monopole_grid: Re k must be positive");
   // attenuating media: tabulated attenuation (ATT 3) when every Re k d / (2 pi) N fits the
@@ -641,12 +657,19 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
     return !(e && atoi(e) == 0);
   }();
   const double umax = dmax * k1;
-  const int n_eh = dmax >= 0.0 ? int(umax / kPhaseN) + 2 : kEhMax + 1;
+  const int n_eh = dmax >= 0.0 ? int(umax / (1 << kGridPhaseBits)) + 2 : kEhMax + 1;
+  const size_t dsm = sizeof(double2) * (size_t(1) << kGridPhaseBits) + sizeof(double) * kEhMax;
+  static const bool attr = [&] {
+    for (auto fn : {monopole_grid_kernel<0>, monopole_grid_kernel<1>, monopole_grid_kernel<2>, monopole_grid_kernel<3>})
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)) != cudaSuccess) return false;
+    return true;
+  }();
+  if (!attr) return set_error(FUSG_CUDA, "monopole_grid: cannot configure shared memory");
   if (att_table && kim > 0.0 && k1 > 0.0 && n_eh <= kEhMax && umax < 1e9) {
-    monopole_grid_kernel<3><<<blocks, threads, 0, s>>>(src_dev, n_src, to_dev(g), k1, kim / k1, amp, out,
-                                                       ctx->dev_flag, n_eh);
+    monopole_grid_kernel<3><<<blocks, threads, dsm, s>>>(src_dev, n_src, to_dev(g), k1, kim / k1, amp, out,
+                                                         ctx->dev_flag, n_eh);
   } else {
-    FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel, blocks, threads, 0, s>>>(
+    FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel, blocks, threads, dsm, s>>>(
                           src_dev, n_src, to_dev(g), k1, kim / k1, amp, out, ctx->dev_flag));
   }
   ctx->launches++;
