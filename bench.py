@@ -249,10 +249,10 @@ def nested_solve(ctx, reps=2):
             "grids": [list(cfg.plan.for_harmonic(i).grid.dims) for i in range(2, 6)],
             "rows": [{k: v for k, v in t.__dict__.items()} for t in rows],
             "rayleigh_terms_per_s": n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None,
-            # FP64 pipe fraction of the Rayleigh sum: 22.25 FP64 instructions per term (SASS of
-            # monopole_grid_kernel<0>'s inner loop: 267 per 12 terms) against the pipe's
+            # FP64 pipe fraction of the Rayleigh sum: 21.25 FP64 instructions per term (SASS of
+            # monopole_grid_kernel<0>'s inner loop: 255 per 12 terms) against the pipe's
             # 64 lanes/clk/SM x 148 SMs x 1.965 GHz
-            "rayleigh_fp64_pipe_frac": (n2 * len(cfg.transducer.source_points) / p1 * 22.25
+            "rayleigh_fp64_pipe_frac": (n2 * len(cfg.transducer.source_points) / p1 * 21.25
                                         / (64 * 148 * 1.965e9)) if p1 > 0 else None}
 
 
