@@ -626,11 +626,11 @@ __global__ void __launch_bounds__(256, 2) ab_fused_r16(ABFused f) {
 // transform's spectral layout, runs the inverse 16 x 16 x 2 transform with a private exchange
 // buffer and stores its cropped output row from registers (512 B per warp instruction).
 constexpr int kR16CT = 4;
-constexpr size_t kR16C2RBytes = (size_t(kR16CT) * 512 + size_t(512) * kR16CT + 4 * 32) * sizeof(double2);
+constexpr size_t r16_c2r_bytes(int T) { return (size_t(T) * 512 + size_t(512) * T + 4 * 32) * sizeof(double2); }
 
-template <int MINB>
-__global__ void __launch_bounds__(kR16CT * 32, MINB) col_to_row_r16(WArgs a) {
-  constexpr int L = 512, T = kR16CT;
+template <int MINB, int T = kR16CT>
+__global__ void __launch_bounds__(T * 32, MINB) col_to_row_r16(WArgs a) {
+  constexpr int L = 512;
   extern __shared__ double2 sm[];
   const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + g * L;
@@ -722,24 +722,30 @@ int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s
     }
     fn<<<unsigned(tiles8), 256, kR16TileBytes, s>>>(a);
   } else {
-    const auto fn = col_to_row_r16<3>;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kR16C2RBytes)) != cudaSuccess) {
+    // FUSG_R16_C2R_T: lines per tile (4: 3 CTAs of 4 warps per SM; 8: 128-byte tile segments,
+    // one CTA of 8 warps per SM)
+    static const int T = [] {
+      const char* e = getenv("FUSG_R16_C2R_T");
+      return (e && atoi(e) == 8) ? 8 : 4;
+    }();
+    const auto fn = T == 8 ? col_to_row_r16<1, 8> : col_to_row_r16<3, 4>;
+    const size_t bytes = r16_c2r_bytes(T);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) != cudaSuccess) {
       set_error(FUSG_CUDA, "transposing pass (16x16x2): cannot configure shared memory");
       return -1;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kR16CT * 32, kR16C2RBytes) != cudaSuccess ||
-        per_sm < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, T * 32, bytes) != cudaSuccess || per_sm < 1) {
       cudaGetLastError();
       return 0;
     }
-    const int64_t tiles = int64_t((a.n_inner + kR16CT - 1) / kR16CT) * a.n_outer;
+    const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
     static const int waves = [] {  // FUSG_R16_C2R_WAVES: CTAs per SM slot (1 = persistent)
       const char* e = getenv("FUSG_R16_C2R_WAVES");
       return e ? std::max(1, atoi(e)) : 1;
     }();
     const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * waves);
-    fn<<<unsigned(grid), kR16CT * 32, kR16C2RBytes, s>>>(a);
+    fn<<<unsigned(grid), T * 32, bytes, s>>>(a);
   }
   ctx->launches++;
   err = cudaGetLastError();
