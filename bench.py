@@ -385,6 +385,12 @@ def run_gpu(args, world, rank, local):
                          "peak_kind": hbm_kind, "unit": "GB/s", "frac": dom_gbs / hbm,
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": per_pass[names[dom]]},
+            # pass C is FP64/L1-latency bound, not HBM bound: its FP64 pipe fraction from the
+            # SASS instruction count of the 16x16x2 kernel (998 FP64 warp instructions per
+            # z-line, ncu: profiles/r1_ncu_summary.md) against 2 per clock per SM
+            "pass_c_fp64_pipe": ({"fp64_warp_instr_per_line": 998, "lines": P[0] * P[1],
+                                  "frac": 998.0 * P[0] * P[1] / (pass_ms[2] * 1e-3)
+                                  / (2 * 148 * 1.965e9)} if tuple(P) == (512, 512, 512) else None),
             "apply_roofline": {"algorithmic_bytes": total_bytes,
                                "achieved_gbs": total_bytes / (ms * 1e-3) / 1e9,
                                "frac": total_bytes / (ms * 1e-3) / 1e9 / hbm},
