@@ -48,8 +48,7 @@ void free_kernel(fusg_kernel* K) {
   cudaFree(K->stage_u);
   for (cudaEvent_t e : K->chunk_ev) cudaEventDestroy(e);
   if (K->copy_stream) cudaStreamDestroy(K->copy_stream);
-  for (auto* t : K->tw) cudaFree(t);
-  delete K;
+  delete K;  // (twiddle tables belong to the context's cache)
 }
 
 // CUDA-event stopwatch on a stream
@@ -136,6 +135,7 @@ fusg_status fusg_ctx_destroy(fusg_ctx* ctx) {
   destroy_nccl(ctx);
   cudaFree(ctx->dev_flag);
   if (ctx->phase_tab) cudaFree(ctx->phase_tab);
+  for (auto& kv : ctx->tw_cache) cudaFree(kv.second);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return FUSG_OK;

@@ -1,6 +1,7 @@
 // Internal (non-ABI) declarations shared by the library's translation units.
 #pragma once
 #include <cuda_runtime.h>
+#include <map>
 
 #include <atomic>
 #include <cstdint>
@@ -79,6 +80,10 @@ struct fusg_ctx {
   void* nccl = nullptr;  // ncclComm_t of a sharded job (fusg_ctx_attach_nccl)
   int nranks = 1, rank = 0;
   std::mutex mu;
+  // twiddle tables e^{-2 pi i m / L} per padded length, uploaded once per context and shared by
+  // its kernels (a build then needs no synchronous cudaMalloc / cudaMemcpy / cudaFree)
+  std::map<int, double2*> tw_cache;
+  std::mutex tw_mu;
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
 };
 

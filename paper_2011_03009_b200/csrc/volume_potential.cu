@@ -178,7 +178,13 @@ bool make_plan_radices(int L, AxisPlan& pl) {
   return true;
 }
 
-static fusg_status upload_twiddles(int L, double2** out) {
+static fusg_status upload_twiddles(fusg_ctx* ctx, int L, double2** out) {
+  std::lock_guard<std::mutex> lock(ctx->tw_mu);
+  auto it = ctx->tw_cache.find(L);
+  if (it != ctx->tw_cache.end()) {
+    *out = it->second;
+    return FUSG_OK;
+  }
   std::vector<double2> h(L);
   for (int m = 0; m < L; ++m) {
     // exp(-2 pi i m / L) with the angle reduced to the first octant for accuracy
@@ -187,6 +193,7 @@ static fusg_status upload_twiddles(int L, double2** out) {
   }
   FUSG_CUDA_TRY(cudaMalloc(out, sizeof(double2) * L));
   FUSG_CUDA_TRY(cudaMemcpy(*out, h.data(), sizeof(double2) * L, cudaMemcpyHostToDevice));
+  ctx->tw_cache[L] = *out;
   return FUSG_OK;
 }
 
@@ -1423,7 +1430,7 @@ fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank) {
 fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   for (int a = 0; a < 3; ++a) {
-    FUSG_TRY(upload_twiddles(K->P[a], &K->tw[a]));
+    FUSG_TRY(upload_twiddles(K->ctx, K->P[a], &K->tw[a]));
     K->plan[a].tw = K->tw[a];
   }
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
