@@ -33,6 +33,8 @@ void free_kernel(fusg_kernel* K) {
     }
   if (K->bar) cudaFree(K->bar);
   if (K->absync) cudaFree(K->absync);
+  for (cudaEvent_t e : K->ab_ev) cudaEventDestroy(e);
+  if (K->ab_stream) cudaStreamDestroy(K->ab_stream);
   if (K->ipc_bufs) {
     cudaStreamSynchronize(s);
     cudaFree(K->bufA);

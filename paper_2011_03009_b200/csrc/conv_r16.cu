@@ -421,6 +421,43 @@ __global__ void __launch_bounds__(256, 2) warp_row_to_col_r16(WArgs a) {
   r2c_tile<kR2CPlain>(a, a.in, a.out, a.n_inner, int(blockIdx.x - kq * ntiles) * 8, int(kq), tile);
 }
 
+// Pass B of one z-chunk read from an L2-resident ring slot [kx][zz][y] (CTA = one kx, all zz):
+// after the tile is stored, its input block is dead and its L2 lines are dropped without
+// write-back (the slot is rewritten by a later chunk's pass A).
+__global__ void __launch_bounds__(256, 2) warp_row_to_col_r16_ring(WArgs a) {
+  extern __shared__ double2 tile[];
+  const int k = blockIdx.x;  // n_inner <= 8: one tile per kx
+  r2c_tile<kR2CPlain>(a, a.in, a.out, a.n_inner, 0, k, tile);
+  const char* blk = reinterpret_cast<const char*>(a.in + int64_t(k) * a.in_sk);
+  const int lines = int((int64_t(a.n_inner) * a.in_si * int64_t(sizeof(double2)) + 127) / 128);
+  for (int l = threadIdx.x; l < lines; l += 256) l2_discard(blk + 128 * l);
+}
+
+// Passes A and B of a z-chunk on two streams through ring slot buffers (volume_potential.cu):
+// pass A of the chunk (rows of f -> slot) or pass B (slot -> B).  1 launched, -1 error.
+int launch_r16_chunk(fusg_ctx* ctx, bool pass_b, const WArgs& a, cudaStream_t s) {
+  const auto fn = pass_b ? warp_row_to_col_r16_ring : warp_row_to_col_r16;
+  static const bool attr = [] {
+    return cudaFuncSetAttribute(warp_row_to_col_r16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(kR16TileBytes)) == cudaSuccess &&
+           cudaFuncSetAttribute(warp_row_to_col_r16_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(kR16TileBytes)) == cudaSuccess;
+  }();
+  if (!attr) {
+    set_error(FUSG_CUDA, "z-chunk A/B: cannot configure shared memory");
+    return -1;
+  }
+  const unsigned blocks = pass_b ? unsigned(a.n_outer) : unsigned((a.n_inner + 7) / 8) * unsigned(a.n_outer);
+  fn<<<blocks, 256, kR16TileBytes, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "z-chunk A/B");
+    return -1;
+  }
+  return 1;
+}
+
 // Passes A and B fused through an L2-resident ring of z-slabs (8 planes each).  Pass A of slab
 // s writes its [kx][8][y] block into ring slot s % R; pass B of slab s reads it back (through
 // L2) as soon as every pass-A tile of the slab is done.  The ring replaces the full [kx][z][y]

@@ -118,6 +118,8 @@ struct fusg_kernel {
   std::vector<bool> peer_opened;  // IPC mappings to close on destroy
   int* bar = nullptr;             // 1-int NCCL barrier buffer
   int* absync = nullptr;          // fused A+B pass: ticket and per-slab completion counters
+  cudaStream_t ab_stream = nullptr;        // z-chunked A/B: pass-B stream (pass A on the caller's)
+  std::vector<cudaEvent_t> ab_ev;          // [2 * chunk + 0]: A done, [2 * chunk + 1]: B done
   uint64_t bytes = 0;
   std::mutex mu;  // serialises applies sharing the workspace
 };

@@ -1654,6 +1654,53 @@ static int try_ab_fused(fusg_kernel* K, const double2* f, cudaStream_t s) {
   return launch_ab_fused_r16(K->ctx, fa, s);
 }
 
+// Passes A and B z-chunk by z-chunk on two streams (FUSG_AB_CHUNKS=1): pass A of chunk c
+// (8 planes) writes ring slot c % R (R = 3, 16 MB each at cfg2, the head of bufA), pass B of
+// chunk c reads it on a second stream while pass A of chunk c + 1 runs, and drops the slot's L2
+// lines after reading them.  Regular (non-persistent) launches; events order the ring reuse.
+// 1 done, 0 not applicable, -1 error.
+static int try_ab_chunks(fusg_kernel* K, const double2* f, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = getenv("FUSG_AB_CHUNKS");
+    return e && atoi(e) != 0;
+  }();
+  const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
+  const int Px = K->P[0], Py = K->P[1];
+  if (!on || K->G != 1 || K->slab || Px != 512 || Py != 512 || 2 * Nx > Px || 2 * Ny > Py) return 0;
+  constexpr int kRing = 3;
+  const int64_t slot = int64_t(Px) * 8 * Ny;
+  if (kRing * slot > int64_t(Px) * Nz * Ny) return 0;
+  const int C = (Nz + 7) / 8;
+  if (!K->ab_stream && cudaStreamCreateWithFlags(&K->ab_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return -1;
+  while (int(K->ab_ev.size()) < 2 * C + 1) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return -1;
+    K->ab_ev.push_back(e);
+  }
+  cudaEvent_t* evA = K->ab_ev.data();  // evA[2c], evB[2c + 1], start = [2C]
+  // the B stream starts after everything already queued on s (e.g. the previous apply)
+  if (cudaEventRecord(K->ab_ev[2 * C], s) != cudaSuccess || cudaStreamWaitEvent(K->ab_stream, K->ab_ev[2 * C], 0))
+    return -1;
+  const int64_t PyNz = int64_t(Py) * Nz;
+  for (int c = 0; c < C; ++c) {
+    const int z0 = 8 * c, nzc = std::min(8, Nz - z0);
+    double2* const sl = K->bufA + int64_t(c % kRing) * slot;
+    if (c >= kRing && cudaStreamWaitEvent(s, evA[2 * (c - kRing) + 1], 0) != cudaSuccess) return -1;
+    const WArgs wa{f + int64_t(z0) * Nx * Ny, Nx, int64_t(Nx) * Ny, 1, Nx, sl, 1, Ny, 8 * int64_t(Ny), Px, 1.0,
+                   Ny, nzc, K->plan[0].tw, KOct{}};
+    if (launch_r16_chunk(K->ctx, false, wa, s) < 0) return -1;
+    if (cudaEventRecord(evA[2 * c], s) != cudaSuccess || cudaStreamWaitEvent(K->ab_stream, evA[2 * c], 0))
+      return -1;
+    const WArgs wb{sl, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB + z0, 1, PyNz, Nz, Py, 1.0, nzc, Px, K->plan[1].tw,
+                   KOct{}};
+    if (launch_r16_chunk(K->ctx, true, wb, K->ab_stream) < 0) return -1;
+    if (cudaEventRecord(evA[2 * c + 1], K->ab_stream) != cudaSuccess) return -1;
+  }
+  if (cudaStreamWaitEvent(s, evA[2 * (C - 1) + 1], 0) != cudaSuccess) return -1;
+  return 1;
+}
+
 fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u, double scale,
                                    cudaStream_t s, cudaEvent_t* ev) {
   if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: sharded kernel needs a slab apply");
@@ -1661,7 +1708,8 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
     if (ev) cudaEventRecord(ev[i], s);
   };
   mark(0);
-  const int fused = try_ab_fused(K, f, s);
+  int fused = try_ab_chunks(K, f, s);
+  if (fused == 0) fused = try_ab_fused(K, f, s);
   if (fused < 0) return FUSG_CUDA;
   if (fused) {  // A+B in one launch (both marks after it), then C, D, E
     const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];

@@ -91,6 +91,8 @@ struct ABFused {
   int mode = 0;     // FUSG_ABF_MODE experiment bits
 };
 int launch_ab_fused_r16(fusg_ctx* ctx, const ABFused& f, cudaStream_t s);
+// pass A (rows of f -> ring slot) or pass B (ring slot -> B, slot lines discarded) of one z-chunk
+int launch_r16_chunk(fusg_ctx* ctx, bool pass_b, const WArgs& a, cudaStream_t s);
 
 // passes A/B (r2c) or D/E at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error
 int launch_transpose_r16(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s);
