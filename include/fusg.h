@@ -151,6 +151,12 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* kernel, const double* f_host, do
 fusg_status fusg_monopole_grid(fusg_ctx* ctx, const double* src_host, int32_t n_src,
                                const fusg_grid* grid, double k_re, double k_im, double amp,
                                double* out_dev, void* stream);
+/* The z-slab [z0, z0 + nz) of fusg_monopole_grid's field (Nx * Ny * nz values, bitwise the
+ * same planes): the multi-GPU p1 shards the incident field by z-planes with no collective
+ * (SURVEY.md 8(e)); each rank evaluates its own slab. */
+fusg_status fusg_monopole_grid_zslab(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                                     const fusg_grid* grid, int32_t z0, int32_t nz, double k_re,
+                                     double k_im, double amp, double* out_dev, void* stream);
 fusg_status fusg_monopole_points(fusg_ctx* ctx, const double* src_host, int32_t n_src,
                                  const double* pts_dev, int64_t n_pts, double k_re, double k_im,
                                  double amp, double* out_dev, void* stream);

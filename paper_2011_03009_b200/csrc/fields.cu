@@ -24,6 +24,7 @@ struct GridDev {
   double lo[3];
   double dx;
   int dims[3];
+  int z_off = 0;  // z index of plane 0 (a z-slab of a larger grid: monopole_grid_kernel)
 };
 
 static GridDev to_dev(const fusg_grid& g) {
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(cons
     row = idx / row_threads;
     nv = min(kVPT, g.dims[0] - ix0);
     y = k1 * centre(g.lo[1], int(row % g.dims[1]), g.dx);
-    z = k1 * centre(g.lo[2], int(row / g.dims[1]), g.dx);
+    z = k1 * centre(g.lo[2], int(row / g.dims[1]) + g.z_off, g.dx);
   }
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) x[v] = k1 * centre(g.lo[0], ix0 + min(v, max(nv - 1, 0)), g.dx);  // tail: repeat the last voxel
@@ -643,8 +644,14 @@ static fusg_status check_flag(fusg_ctx* ctx, cudaStream_t s) {
 
 fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
                           double kre, double kim, double amp, double2* out, cudaStream_t s,
-                          double dmax) {
-  const int64_t count = int64_t((g.dims[0] + kVPT - 1) / kVPT) * g.dims[1] * g.dims[2];
+                          double dmax, int z0, int nz) {
+  GridDev gd = to_dev(g);
+  if (nz >= 0) {  // z-slab [z0, z0 + nz) of g (p1 shards by z-planes)
+    gd.dims[2] = nz;
+    gd.z_off = z0;
+  }
+  const int64_t count = int64_t((gd.dims[0] + kVPT - 1) / kVPT) * gd.dims[1] * gd.dims[2];
+  if (count == 0) return FUSG_OK;
   const int threads = 256;
   const unsigned blocks = unsigned((count + threads - 1) / threads);
   const double k1 = phase_scale(kre, kGridPhaseBits);
@@ -666,11 +673,11 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   }();
   if (!attr) return set_error(FUSG_CUDA, "monopole_grid: cannot configure shared memory");
   if (att_table && kim > 0.0 && k1 > 0.0 && n_eh <= kEhMax && umax < 1e9) {
-    monopole_grid_kernel<3><<<blocks, threads, dsm, s>>>(src_dev, n_src, to_dev(g), k1, kim / k1, amp, out,
+    monopole_grid_kernel<3><<<blocks, threads, dsm, s>>>(src_dev, n_src, gd, k1, kim / k1, amp, out,
                                                          ctx->dev_flag, n_eh);
   } else {
     FUSG_ATT_DISPATCH(att_mode(kim, dmax), monopole_grid_kernel, blocks, threads, dsm, s>>>(
-                          src_dev, n_src, to_dev(g), k1, kim / k1, amp, out, ctx->dev_flag));
+                          src_dev, n_src, gd, k1, kim / k1, amp, out, ctx->dev_flag));
   }
   ctx->launches++;
   FUSG_LAUNCH_CHECK("monopole_grid_kernel");
@@ -777,6 +784,26 @@ fusg_status fusg_monopole_grid(fusg_ctx* ctx, const double* src_host, int32_t n_
   if (st != FUSG_OK) return st;
   st = monopole_grid(ctx, src, n_src, *grid, k_re, k_im, amp, reinterpret_cast<double2*>(out_dev), s,
                      distance_bound(src_host, n_src, grid->lo, grid->hi));
+  cudaFreeAsync(src, s);
+  if (st != FUSG_OK) return st;
+  return check_flag(ctx, s);
+}
+
+fusg_status fusg_monopole_grid_zslab(fusg_ctx* ctx, const double* src_host, int32_t n_src,
+                                     const fusg_grid* grid, int32_t z0, int32_t nz, double k_re,
+                                     double k_im, double amp, double* out_dev, void* stream) {
+  if (!ctx || !grid || (nz > 0 && !out_dev))
+    return set_error(FUSG_INVALID_ARGUMENT, "monopole_grid_zslab: null argument");
+  if (z0 < 0 || nz < 0 || int64_t(z0) + nz > grid->dims[2])
+    return set_error(FUSG_INVALID_ARGUMENT, "monopole_grid_zslab: slab outside the grid");
+  if (nz == 0) return FUSG_OK;
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->pick(stream);
+  double* src = nullptr;
+  fusg_status st = upload_sources(src_host, n_src, &src, s);
+  if (st != FUSG_OK) return st;
+  st = monopole_grid(ctx, src, n_src, *grid, k_re, k_im, amp, reinterpret_cast<double2*>(out_dev), s,
+                     distance_bound(src_host, n_src, grid->lo, grid->hi), z0, nz);
   cudaFreeAsync(src, s);
   if (st != FUSG_OK) return st;
   return check_flag(ctx, s);

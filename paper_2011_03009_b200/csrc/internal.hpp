@@ -154,7 +154,7 @@ namespace fusg {
 fusg_status upload_sources(const double* src_host, int n_src, double** dev, cudaStream_t s);
 fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const fusg_grid& g,
                           double kre, double kim, double amp, double2* out, cudaStream_t s,
-                          double dmax);
+                          double dmax, int z0 = 0, int nz = -1);
 double distance_bound(const double* src_host, int n_src, const double lo[3], const double hi[3]);
 fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
                             const fusg_grid& tgt, double2* out, cudaStream_t s);

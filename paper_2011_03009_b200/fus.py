@@ -421,6 +421,24 @@ def evaluate_first_harmonic(t: BowlTransducer, m: Medium, grid: VoxelGrid, ampli
     return HarmonicField(grid, out, k1)
 
 
+def evaluate_first_harmonic_zslab(t: BowlTransducer, m: Medium, grid: VoxelGrid, amplitude_scale: float,
+                                  z0: int, nz: int, ctx: Optional[Context] = None):
+    """Planes [z0, z0 + nz) of evaluate_first_harmonic (src/transducer.cpp:179-196), bitwise the
+    same values: the multi-GPU incident field shards by z-planes with no collective (each rank
+    evaluates its own slab).  Returns a CUDA complex128 tensor of Nx*Ny*nz."""
+    ctx = ctx or context()
+    k1 = complex_wavenumber(m, t.f0, 1)
+    amp = amplitude_scale * t.cap_area() / float(len(t.source_points))
+    nx, ny, _ = grid.dims
+    out = torch.empty(nx * ny * nz, dtype=torch.complex128, device=f"cuda:{ctx.device}")
+    sp, n = t._src()
+    g = grid.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_monopole_grid_zslab(ctx.handle, sp, n, C.byref(g), int(z0), int(nz), k1.k.real,
+                                         k1.k.imag, amp, out.data_ptr() if nz > 0 else None, None))
+    return out
+
+
 def evaluate_source_field(t: BowlTransducer, m: Medium, grid: VoxelGrid):
     """src/transducer.cpp:198-206 -> (field, normalization)"""
     k1 = complex_wavenumber(m, t.f0, 1)
