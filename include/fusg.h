@@ -189,6 +189,16 @@ fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower
 /* interpolate (src/grid.cpp:141-195): trilinear transfer onto target voxel centres. */
 fusg_status fusg_interpolate(fusg_ctx* ctx, const fusg_grid* src, const double* f_dev,
                              const fusg_grid* target, double* out_dev, void* stream);
+/* z-slab transfer for the multi-GPU cascade: target planes [tz0, tz0 + tnz)
+ * from source planes [sz0, sz0 + snz) held in f_slab_dev (a source z-slab with its halo);
+ * bitwise the same values as fusg_interpolate.  fusg_interpolate_source_planes gives the
+ * source plane range [z_lo, z_hi] a target slab reads (nested grids: its own planes plus a
+ * one-plane halo).  FUSG_INVALID_ARGUMENT when the slab lacks a needed plane. */
+fusg_status fusg_interpolate_source_planes(const fusg_grid* src, const fusg_grid* target, int32_t tz0,
+                                           int32_t tnz, int32_t* z_lo, int32_t* z_hi);
+fusg_status fusg_interpolate_zslab(fusg_ctx* ctx, const fusg_grid* src, int32_t sz0, int32_t snz,
+                                   const double* f_slab_dev, const fusg_grid* target, int32_t tz0, int32_t tnz,
+                                   double* out_dev, void* stream);
 
 /* ---------------------------------------------------------------- recursion
  * run_cascade (src/cascade.cpp:42-107), device resident. grids[i] is the planned grid of

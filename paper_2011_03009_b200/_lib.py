@@ -93,6 +93,10 @@ SIGNATURES = {
     "fusg_kernel_apply_host": (C.c_int, [_vp, _vp, _vp, C.c_double]),
     "fusg_monopole_grid": (C.c_int, [_vp, _dp, C.c_int32, C.POINTER(Grid), C.c_double, C.c_double,
                                      C.c_double, _vp, _vp]),
+    "fusg_interpolate_source_planes": (C.c_int, [C.POINTER(Grid), C.POINTER(Grid), C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fusg_interpolate_zslab": (C.c_int, [_vp, C.POINTER(Grid), C.c_int32, C.c_int32, _vp, C.POINTER(Grid),
+                                         C.c_int32, C.c_int32, _vp, _vp]),
     "fusg_monopole_grid_zslab": (C.c_int, [_vp, _dp, C.c_int32, C.POINTER(Grid), C.c_int32, C.c_int32,
                                            C.c_double, C.c_double, C.c_double, _vp, _vp]),
     "fusg_monopole_points": (C.c_int, [_vp, _dp, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double,

@@ -487,11 +487,12 @@ __device__ __forceinline__ void interp_axis(const GridDev& s, const GridDev& t, 
 }
 
 // Per-axis cells and weights (they depend on one index each), computed once per call.
+// (t.dims[2] is the number of target planes computed, starting at target plane t.z_off.)
 __global__ void interp_axes_kernel(GridDev s, GridDev t, int* __restrict__ base, double* __restrict__ frac) {
   const int n = t.dims[0] + t.dims[1] + t.dims[2];
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const int a = j < t.dims[0] ? 0 : (j < t.dims[0] + t.dims[1] ? 1 : 2);
-    const int i = a == 0 ? j : (a == 1 ? j - t.dims[0] : j - t.dims[0] - t.dims[1]);
+    const int i = a == 0 ? j : (a == 1 ? j - t.dims[0] : j - t.dims[0] - t.dims[1] + t.z_off);
     interp_axis(s, t, a, i, base[j], frac[j]);
   }
 }
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(256) interp_kernel(GridDev s, const double2* _
           const int jx = min(max(i0[0] + cx, 0), s.dims[0] - 1);
           const int jy = min(max(i0[1] + cy, 0), s.dims[1] - 1);
           const int jz = min(max(i0[2] + cz, 0), s.dims[2] - 1);
-          const double2 v = __ldg(f + jx + int64_t(s.dims[0]) * (jy + int64_t(s.dims[1]) * jz));
+          const double2 v = __ldg(f + jx + int64_t(s.dims[0]) * (jy + int64_t(s.dims[1]) * (jz - s.z_off)));
           re = __dadd_rn(re, __dmul_rn(wgt, v.x));
           im = __dadd_rn(im, __dmul_rn(wgt, v.y));
         }
@@ -684,27 +685,63 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   return FUSG_OK;
 }
 
-fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
-                            const fusg_grid& tgt, double2* out, cudaStream_t s) {
+// Host restatement of interp_axis's z cell (same IEEE operations, no contraction): the source
+// planes [lo, hi] the target planes [tz0, tz0 + tnz) read (the z-slab transfer's halo).
+static void interp_source_planes(const fusg_grid& src, const fusg_grid& tgt, int tz0, int tnz, int* lo, int* hi) {
+  int mn = INT_MAX, mx = INT_MIN;
+  for (int iz = tz0; iz < tz0 + tnz; ++iz) {
+    const double p = tgt.lo[2] + (double(iz) + 0.5) * tgt.dx;
+    const double q = (p - src.lo[2]) / src.dx - 0.5;
+    int b = int(std::floor(q));
+    const int top = std::max(0, src.dims[2] - 2);
+    b = b < 0 ? 0 : (b > top ? top : b);
+    mn = std::min(mn, b);
+    mx = std::max(mx, std::min(b + 1, src.dims[2] - 1));
+  }
+  *lo = mn;
+  *hi = mx;
+}
+
+// Target planes [tz0, tz0 + tnz) from source planes [sz0, sz0 + snz) held in f (a z-slab of the
+// source field, halo included); the full transfer is tz0 = sz0 = 0, tnz = tgt dims, snz = src dims.
+static fusg_status interpolate_slab_dev(fusg_ctx* ctx, const fusg_grid& src, int sz0, int snz, const double2* f,
+                                        const fusg_grid& tgt, int tz0, int tnz, double2* out, cudaStream_t s) {
   for (int a = 0; a < 3; ++a)
     if (tgt.lo[a] < src.lo[a] - src.dx || tgt.hi[a] > src.hi[a] + src.dx)
       return set_error(FUSG_INVALID_ARGUMENT,
                        "interpolate: target extends more than one source voxel beyond the source domain");
-  const int64_t count = int64_t(tgt.dims[0]) * tgt.dims[1] * tgt.dims[2];
+  if (tz0 < 0 || tnz < 0 || int64_t(tz0) + tnz > tgt.dims[2] || sz0 < 0 || snz < 0 ||
+      int64_t(sz0) + snz > src.dims[2])
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate: slab outside the grid");
+  if (tnz == 0) return FUSG_OK;
+  int need_lo, need_hi;
+  interp_source_planes(src, tgt, tz0, tnz, &need_lo, &need_hi);
+  if (need_lo < sz0 || need_hi >= sz0 + snz)
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate: the source slab lacks planes " + std::to_string(need_lo) +
+                                                ".." + std::to_string(need_hi) + " the target slab reads");
+  const int64_t count = int64_t(tgt.dims[0]) * tgt.dims[1] * tnz;
   if (count >= (int64_t(1) << 32))
     return set_error(FUSG_INVALID_ARGUMENT, "interpolate: target above 2^32 voxels");
-  const int nax = tgt.dims[0] + tgt.dims[1] + tgt.dims[2];
+  GridDev sd = to_dev(src), td = to_dev(tgt);
+  sd.z_off = sz0;
+  td.dims[2] = tnz;
+  td.z_off = tz0;
+  const int nax = tgt.dims[0] + tgt.dims[1] + tnz;
   void* tabs = nullptr;
   FUSG_CUDA_TRY(cudaMallocAsync(&tabs, size_t(nax) * (sizeof(int) + sizeof(double)) + 16, s));
   double* frac = static_cast<double*>(tabs);
   int* base = reinterpret_cast<int*>(frac + nax);
-  interp_axes_kernel<<<(nax + 255) / 256, 256, 0, s>>>(to_dev(src), to_dev(tgt), base, frac);
-  interp_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(to_dev(src), f, to_dev(tgt), base, frac, out);
-  ctx->launches++;
+  interp_axes_kernel<<<(nax + 255) / 256, 256, 0, s>>>(sd, td, base, frac);
+  interp_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(sd, f, td, base, frac, out);
+  ctx->launches += 2;
   FUSG_CUDA_TRY(cudaFreeAsync(tabs, s));
-  ctx->launches++;
   FUSG_LAUNCH_CHECK("interp_kernel");
   return FUSG_OK;
+}
+
+fusg_status interpolate_dev(fusg_ctx* ctx, const fusg_grid& src, const double2* f,
+                            const fusg_grid& tgt, double2* out, cudaStream_t s) {
+  return interpolate_slab_dev(ctx, src, 0, src.dims[2], f, tgt, 0, tgt.dims[2], out, s);
 }
 
 fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t count, double coeff,
@@ -967,6 +1004,27 @@ fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower
   const double coeff = fusg_rhs_coefficient(m, omega, n);
   return rhs_dev(ctx, n, reinterpret_cast<const double2* const*>(lower_dev), count, coeff,
                  reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
+}
+
+fusg_status fusg_interpolate_source_planes(const fusg_grid* src, const fusg_grid* target, int32_t tz0,
+                                           int32_t tnz, int32_t* z_lo, int32_t* z_hi) {
+  if (!src || !target || !z_lo || !z_hi || tnz < 1 || tz0 < 0 || int64_t(tz0) + tnz > target->dims[2])
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate_source_planes: bad argument");
+  int lo, hi;
+  interp_source_planes(*src, *target, tz0, tnz, &lo, &hi);
+  *z_lo = lo;
+  *z_hi = hi;
+  return FUSG_OK;
+}
+
+fusg_status fusg_interpolate_zslab(fusg_ctx* ctx, const fusg_grid* src, int32_t sz0, int32_t snz,
+                                   const double* f_slab_dev, const fusg_grid* target, int32_t tz0, int32_t tnz,
+                                   double* out_dev, void* stream) {
+  if (!ctx || !src || !target || (tnz > 0 && (!f_slab_dev || !out_dev)))
+    return set_error(FUSG_INVALID_ARGUMENT, "interpolate_zslab: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  return interpolate_slab_dev(ctx, *src, sz0, snz, reinterpret_cast<const double2*>(f_slab_dev), *target, tz0, tnz,
+                              reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
 }
 
 fusg_status fusg_interpolate(fusg_ctx* ctx, const fusg_grid* src, const double* f_dev,

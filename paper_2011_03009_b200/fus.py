@@ -517,6 +517,32 @@ def interpolate(fld: HarmonicField, target: VoxelGrid, ctx: Optional[Context] = 
 
 
 # ------------------------------------------------------------------------ cascade
+def interpolate_source_planes(src: VoxelGrid, target: VoxelGrid, tz0: int, tnz: int) -> tuple:
+    """Source planes (z_lo, z_hi) that target planes [tz0, tz0 + tnz) of interpolate read."""
+    lo, hi = C.c_int32(), C.c_int32()
+    gs, gt = src.c(), target.c()
+    check(lib().fusg_interpolate_source_planes(C.byref(gs), C.byref(gt), int(tz0), int(tnz), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def interpolate_zslab(src: VoxelGrid, f_slab, sz0: int, target: VoxelGrid, tz0: int, tnz: int,
+                      ctx: Optional[Context] = None):
+    """Target planes [tz0, tz0 + tnz) of interpolate (src/grid.cpp:141-195) from a source z-slab
+    f_slab holding planes [sz0, sz0 + len/(Nx Ny)) (halo included): the multi-GPU transfer,
+    bitwise the full transfer's planes."""
+    ctx = ctx or context()
+    fs = _on_device(f_slab, ctx)
+    nxs, nys, _ = src.dims
+    snz = fs.numel() // (nxs * nys)
+    nx, ny, _ = target.dims
+    out = torch.empty(nx * ny * tnz, dtype=torch.complex128, device=f"cuda:{ctx.device}")
+    gs, gt = src.c(), target.c()
+    _sync_torch_to(ctx)
+    check(lib().fusg_interpolate_zslab(ctx.handle, C.byref(gs), int(sz0), int(snz), fs.data_ptr(), C.byref(gt),
+                                       int(tz0), int(tnz), out.data_ptr() if tnz > 0 else None, None))
+    return out
+
+
 def rhs_source(n: int, lower: Sequence[HarmonicField], m: Medium, omega: float,
                ctx: Optional[Context] = None):
     """src/cascade.cpp:21-40; returns a CUDA tensor."""

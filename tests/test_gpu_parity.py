@@ -531,3 +531,28 @@ def test_incident_field_zslabs_are_bitwise_the_full_field(ctx, G):
     assert torch.equal(torch.cat(parts), full)
     with pytest.raises(ValueError):
         fus.evaluate_first_harmonic_zslab(t, w, g, 3.0, nz - 1, 2)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_interpolate_zslabs_with_halo_are_bitwise_the_full_transfer(ctx, G):
+    # each target z-slab reads one contiguous source plane range (its planes plus
+    # a one-plane halo); the slab transfer must reproduce the full transfer bit for bit
+    t = fus.transducer_preset("H131", 100.0, 512)
+    w = water()
+    plan = fus.plan_nested_meshes(t, w, 6e-3, 2, 3, 0.3)
+    gs, gt = plan.for_harmonic(2).grid, plan.for_harmonic(3).grid
+    f = torch.from_numpy(fus.random_vector(gs.count(), 21)).cuda()
+    full = fus.interpolate(fus.HarmonicField(gs, f, fus.complex_wavenumber(w, t.f0, 2)), gt).values
+    nxy = gs.dims[0] * gs.dims[1]
+    nz = gt.dims[2]
+    parts, z0 = [], 0
+    for r in range(G):
+        n = nz // G + (1 if r < nz % G else 0)
+        lo, hi = fus.interpolate_source_planes(gs, gt, z0, n)
+        assert 0 <= lo <= hi < gs.dims[2]
+        parts.append(fus.interpolate_zslab(gs, f[lo * nxy:(hi + 1) * nxy], lo, gt, z0, n))
+        if lo > 0 and n > 0:  # a slab without its first needed plane is refused
+            with pytest.raises(ValueError, match="lacks planes"):
+                fus.interpolate_zslab(gs, f[(lo + 1) * nxy:(hi + 1) * nxy], lo + 1, gt, z0, n)
+        z0 += n
+    assert torch.equal(torch.cat(parts), full)
