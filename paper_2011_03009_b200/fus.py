@@ -629,6 +629,80 @@ def run_cascade(cfg: CascadeConfig, ctx: Optional[Context] = None) -> CascadeRes
     return res
 
 
+def _zsplit(n: int, G: int):
+    """Ragged z-slabs [(z0, nz)] of n planes over G ranks (the first n mod G take one more)."""
+    out, z0 = [], 0
+    for r in range(G):
+        nz = n // G + (1 if r < n % G else 0)
+        out.append((z0, nz))
+        z0 += nz
+    return out
+
+
+def run_cascade_zslab_loopback(cfg: CascadeConfig, nranks: int, ctx: Optional[Context] = None,
+                               transport: str = "auto") -> CascadeResult:
+    """The cascade of run_cascade (src/cascade.cpp:42-107) decomposed into z-slabs as a multi-GPU
+    run would be, all ranks in this process on one GPU: the incident field per
+    slab (no collective), each lower harmonic brought onto the next grid per target slab from
+    its source slab plus the halo planes a neighbour would send (fusg_interpolate_zslab), the
+    source term per slab, and the apply through the slab-sharded operator (fused peer-store
+    transposes where the padded x / y lengths have transposing warp kernels, else NCCL; "auto").
+    The result must equal run_cascade's bit for bit."""
+    ctx = ctx or context()
+    n = int(cfg.n_harmonics)
+    if n < 2:
+        raise ValueError("run_cascade: n_harmonics must be >= 2")
+    t, med = cfg.transducer, cfg.medium
+    grid_of = lambda i: cfg.plan.for_harmonic(max(i, 2)).grid  # p1 lives on D_2's grid
+    k1 = complex_wavenumber(med, t.f0, 1)
+    scale = power_scale_factor(t, med, k1)
+    norm = scale if scale > 0.0 else 1.0
+    g1 = grid_of(1)
+    fields = [torch.cat([evaluate_first_harmonic_zslab(t, med, g1, scale, z0, nz, ctx)
+                         for z0, nz in _zsplit(g1.dims[2], nranks)])]
+    res = CascadeResult(source_normalization=norm)
+    res.harmonics.append(HarmonicField(g1, fields[0], k1))
+
+    class _Slab:  # rhs_source only reads .values
+        def __init__(self, v):
+            self.values = v
+
+    for i in range(2, n + 1):
+        gi = grid_of(i)
+        ki = complex_wavenumber(med, t.f0, i)
+        plane = gi.dims[0] * gi.dims[1]
+        rhs_slabs = []
+        for z0, nz in _zsplit(gi.dims[2], nranks):
+            lower = []
+            for m in range(1, i):
+                gm, pm = grid_of(m), fields[m - 1]
+                if same_grid(gm, gi):
+                    lower.append(_Slab(pm[z0 * plane:(z0 + nz) * plane]))
+                    continue
+                if cfg.recompute_p1_each_grid and m == 1:
+                    lower.append(_Slab(evaluate_first_harmonic_zslab(t, med, gi, scale, z0, nz, ctx)))
+                    continue
+                if nz == 0:
+                    lower.append(_Slab(torch.empty(0, dtype=torch.complex128, device=pm.device)))
+                    continue
+                lo, hi = interpolate_source_planes(gm, gi, z0, nz)
+                pl = gm.dims[0] * gm.dims[1]
+                lower.append(_Slab(interpolate_zslab(gm, pm[lo * pl:(hi + 1) * pl], lo, gi, z0, nz, ctx)))
+            rhs_slabs.append(rhs_source(i, lower, med, ki.omega, ctx) if nz > 0 else
+                             torch.empty(0, dtype=torch.complex128, device=fields[0].device))
+        f = torch.cat(rhs_slabs)
+        gk = VoxelGrid(gi.lo, gi.hi, gi.dx, gi.dims, i)
+        tr = transport
+        if tr == "auto":
+            px, py = padded_dims(gk)[:2]
+            warp = {256, 512, 768, 1024, 1536}
+            tr = "p2p" if px in warp and py in warp else "nccl"
+        u = apply_slab_loopback(gk, ki, f, nranks, -1.0, ctx, tr)
+        fields.append(u)
+        res.harmonics.append(HarmonicField(gi, u, ki))
+    return res
+
+
 # ------------------------------------------------------------------------ VIE mode
 # SURVEY.md 8(f) rank 2 (include/fus/vie.hpp, src/vie.cpp): heterogeneous media by a volume
 # integral equation solved with restarted GMRES, everything device resident.

@@ -556,3 +556,18 @@ def test_interpolate_zslabs_with_halo_are_bitwise_the_full_transfer(ctx, G):
                 fus.interpolate_zslab(gs, f[(lo + 1) * nxy:(hi + 1) * nxy], lo + 1, gt, z0, n)
         z0 += n
     assert torch.equal(torch.cat(parts), full)
+
+
+@pytest.mark.parametrize("G,transport", [(1, "auto"), (2, "auto"), (3, "nccl"), (4, "auto")])
+def test_cascade_zslab_loopback_is_bitwise_run_cascade(ctx, G, transport):
+    # the cascade decomposed into z-slabs (incident field per slab, halo
+    # transfers, slab-sharded applies) reproduces the single-GPU cascade bit for bit
+    t = fus.transducer_preset("H131", 100.0, 512)
+    w = water()
+    plan = fus.plan_nested_meshes(t, w, 6e-3, 2, 3, 0.3)
+    cfg = fus.CascadeConfig(w, t, plan, 3)
+    want = fus.run_cascade(cfg)
+    got = fus.run_cascade_zslab_loopback(cfg, G, transport=transport)
+    assert got.source_normalization == want.source_normalization
+    for a, b in zip(got.harmonics, want.harmonics):
+        assert torch.equal(a.values, b.values)
