@@ -321,6 +321,27 @@ fusg_status fusg_run_cascade(fusg_ctx* ctx, const fusg_cascade_desc* d, double* 
   if (st != FUSG_OK) return st;
   std::unique_ptr<double, void (*)(double*)> src_guard(src, [](double* p) { cudaFree(p); });
 
+  // Reserve the stream-ordered pool once for the largest stage (its kernel's buffers, the
+  // lower fields brought onto its grid and its source term): the per-harmonic allocations then
+  // come from memory the pool already maps, instead of growing it (and stalling) stage by stage.
+  {
+    size_t peak = 0;
+    for (int i = 2; i <= n; ++i) {
+      const fusg_grid& gi = grid_of(i);
+      size_t P[3], H[3];
+      for (int a = 0; a < 3; ++a) {
+        P[a] = size_t(fusg::device_padded_size(gi.dims[a], a));
+        H[a] = P[a] / 2 + 1;
+      }
+      const size_t cnt = size_t(count_of(gi));
+      const size_t e = P[0] * gi.dims[1] * gi.dims[2] + P[0] * P[1] * gi.dims[2] + H[0] * H[1] * H[2] + size_t(i) * cnt;
+      peak = std::max(peak, e * 16);
+    }
+    void* r = nullptr;
+    if (cudaMallocAsync(&r, peak + peak / 8, s) == cudaSuccess) cudaFreeAsync(r, s);
+    cudaGetLastError();
+  }
+
   // p1 on the D_2 grid: evaluate_source_field (src/transducer.cpp:198-206)
   EvTimer tm(s);
   tm.start();
