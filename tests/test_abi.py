@@ -114,3 +114,24 @@ def test_cpp_dropin_api_host_cases():
     out = subprocess.run([exe, "host"], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "OK:" in out.stdout
+
+
+def test_interpolate_source_planes_follow_the_reference_cell_rule():
+    # Host restatement (no GPU): the z-slab transfer's source range is the span of the
+    # reference's cell bases (src/grid.cpp:156-170: q = (p - lo_s)/dx_s - 0.5,
+    # base = clamp(floor q, 0, max(0, n - 2))) and base + 1, over the target slab's planes.
+    t = fus.transducer_preset("H131", 100.0, 64)
+    w = fus.medium_preset("water")
+    plan = fus.plan_nested_meshes(t, w, 6e-3, 2, 4, 0.3)
+    for a, b in [(2, 3), (3, 4), (2, 4)]:
+        gs, gt = plan.for_harmonic(a).grid, plan.for_harmonic(b).grid
+        n = gs.dims[2]
+        for z0, nz in [(0, 1), (0, gt.dims[2]), (3, 5), (gt.dims[2] - 2, 2)]:
+            bases = []
+            for iz in range(z0, z0 + nz):
+                p = gt.lo[2] + (iz + 0.5) * gt.dx
+                q = (p - gs.lo[2]) / gs.dx - 0.5
+                bases.append(min(max(math.floor(q), 0), max(0, n - 2)))
+            assert fus.interpolate_source_planes(gs, gt, z0, nz) == (min(bases), min(max(bases) + 1, n - 1))
+    with pytest.raises(ValueError):
+        fus.interpolate_source_planes(gs, gt, 0, 0)
