@@ -571,3 +571,19 @@ def test_cascade_zslab_loopback_is_bitwise_run_cascade(ctx, G, transport):
     assert got.source_normalization == want.source_normalization
     for a, b in zip(got.harmonics, want.harmonics):
         assert torch.equal(a.values, b.values)
+
+
+def test_apply_scale_and_host_path_on_the_512_kernels(ctx):
+    # The 16x16x2 kernels at padded length 512 on every axis: the scale argument is applied at
+    # the final store (a power of two scales exactly), and the z-chunked host-vector apply runs
+    # the same kernels (bitwise equal to the device apply).
+    dx = 1e-4
+    dims = (254, 253, 230)  # 2N - 1 > 504: every axis pads to 512
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    K = fus.GreenKernel(g, k)
+    assert K.padded == (512, 512, 512)
+    f = fus.random_vector(g.count(), 33)
+    u = K.apply(f)
+    assert torch.equal(K.apply(f, -0.5), -0.5 * u)
+    assert np.array_equal(K.apply_host(f), host(u))
