@@ -587,3 +587,32 @@ def test_apply_scale_and_host_path_on_the_512_kernels(ctx):
     u = K.apply(f)
     assert torch.equal(K.apply(f, -0.5), -0.5 * u)
     assert np.array_equal(K.apply_host(f), host(u))
+
+
+_ATT_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2011_03009_b200 import fus
+t = fus.transducer_preset("H131", 100.0, 1024)
+w = fus.medium_preset("water")
+plan = fus.plan_nested_meshes(t, w, 6e-3, 2, 2, 0.3)
+g = plan.for_harmonic(2).grid
+np.save(sys.argv[2], fus.evaluate_first_harmonic(t, w, g, 3.0).values.cpu().numpy())
+"""
+
+
+def test_tabulated_attenuation_matches_the_polynomial_and_exp_paths(tmp_path):
+    # The Rayleigh grid kernel's tabulated e^{-Im k d} (FUSG_ATT_TABLE=1, default) against the
+    # degree-6 interpolant / exp() modes (FUSG_ATT_TABLE=0) on an attenuating medium
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("1", "0"):
+        p = tmp_path / f"p{v}.npy"
+        r = subprocess.run([sys.executable, "-c", _ATT_CHILD, root, str(p)], env=dict(os.environ, FUSG_ATT_TABLE=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = np.load(p)
+    assert rel_l2(out["1"], out["0"]) <= 1e-13
