@@ -1,25 +1,30 @@
 #!/usr/bin/env python
 """Benchmark: volume-potential apply throughput (grid points/s, complex128) on B200.
 
-Workload (BASELINE.json configs[1], "cfg2"): one GreenKernel::apply on a 256^3 grid with a
-512^3 circulant embedding, k = 2k_1 at f = 1.1 MHz, c = 1540 m/s, h = lambda_2/6; the source
-is a seeded iid complex U[-1,1] field (libstdc++ mt19937, tests/acceptance.cpp:30-36) times a
-Gaussian envelope of std 0.2 x box width centred in the box.  A "step" is one apply with the
-kernel spectrum cached (include/fus/potential.hpp:25-27); the spectrum build is reported
-separately.  Inputs and workspaces (0.27 + 1.6 GB) exceed the 126 MB L2, so no flush is needed.
+Headline workload (BASELINE.json configs[4], "cfg5", the largest configuration that fits one
+GPU): one GreenKernel::apply on a 768^3 grid with a 1536^3 circulant embedding (~58 GB in the
+reference's form), k h = pi/3 (h = lambda/6 at f = 1.1 MHz, c = 1540 m/s), source = seeded iid
+complex U[-1,1] (libstdc++ mt19937 seed 768, tests/acceptance.cpp:30-36).  A "step" is one
+apply with the kernel spectrum cached (include/fus/potential.hpp:25-27); the spectrum build is
+reported separately.  Inputs (7.25 GB) and workspaces (43.5 GB) exceed the 126 MB L2, so no
+flush is needed.  cfg2 (256^3 / 512^3) is measured beside it as an extra key.
 
   python bench.py [--gpus N --steps K --warmup W]       # this framework (libfusg.so)
-  python bench.py --impl reference ...                   # the CPU reference path (oracle port)
+  python bench.py --impl reference ...                   # the reference's CPU path (oracle port)
 
-N > 1 (torchrun): the cfg2 apply is slab-sharded over the ranks (strong scaling): z-slabs of
-f/u, x-slabs of the spectrum, two NCCL all-to-all transposes over NVLink per apply
-(fusg_kernel_apply_slab); time = max over ranks of CUDA-event time.  --replicas runs
-independent per-rank applies instead (weak scaling).
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks.  N > 1: the cfg5 apply is slab-sharded over the ranks (strong scaling): z-slabs
+of f/u, x-slabs of the spectrum, the two 3D-FFT transposes fused into passes A/D as NVLink
+peer stores (fusg_kernel_apply_slab_p2p); time = max over ranks of CUDA-event time.
+
+The reference arm never imports the framework package (no libfusg.so): its inputs come from
+oracle/ and its config dict is the same object as the GPU arm's.
 """
 import argparse
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,35 +38,62 @@ sys.path.insert(0, ROOT)
 
 METRIC = "volume-potential grid pts/s (c128)"
 UNIT = "grid_pts/s"
-WORKLOAD = ("cfg2: single volume-potential apply, 256^3 grid, 512^3 circulant embedding, complex128, "
-            "k2=2k at f=1.1MHz c=1540, h=lambda2/6, iid U[-1,1] (mt19937 seed 2024) x Gaussian "
-            "envelope sigma=0.2*box")
-N_SIDE = 256
+
+# ---- workloads (plain constants: both arms build their config from these alone)
+C0, F0 = 1540.0, 1.1e6
+CFG5 = {"n": 768, "harmonic": 1, "seed": 768,
+        "workload": ("cfg5: single volume-potential apply, 768^3 grid, 1536^3 circulant embedding, "
+                     "complex128, k=2*pi*f/c at f=1.1MHz c=1540 (k h = pi/3, h = lambda/6), "
+                     "iid U[-1,1] source (mt19937 seed 768)")}
+CFG2 = {"n": 256, "harmonic": 2, "seed": 2024,
+        "workload": ("cfg2: single volume-potential apply, 256^3 grid, 512^3 circulant embedding, complex128, "
+                     "k2=2k at f=1.1MHz c=1540, h=lambda2/6, iid U[-1,1] (mt19937 seed 2024) x Gaussian "
+                     "envelope sigma=0.2*box")}
+
+
+def geometry(cfg):
+    """(h, k, omega) of a cube workload: h = lambda_n / 6, k = n * 2 pi f / c (real)."""
+    n = cfg["harmonic"]
+    h = (C0 / (n * F0)) / 6.0
+    return h, n * 2 * math.pi * F0 / C0, 2 * math.pi * F0
+
+
+def bench_config(cfg, world):
+    n = cfg["n"]
+    return {"workload": cfg["workload"], "grid": [n] * 3, "padded": [2 * n] * 3, "seed": cfg["seed"],
+            "parallelism": "single" if world == 1 else f"zslab{world}",
+            "l2": "inputs+workspace > 126 MB L2; no flush"}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return 6650.0, "fallback"
+        return 7672.0, "fallback (B200_PROFILING.md)"
 
 
-def cfg2_inputs():
+def gpu_inputs(cfg):
     from paper_2011_03009_b200 import fus
 
-    c, f0 = 1540.0, 1.1e6
-    h = (c / (2 * f0)) / 6.0
-    g = fus.make_grid([0, 0, 0], [N_SIDE * h] * 3, h, 2)
-    k = fus.Wavenumber(complex(2 * 2 * math.pi * f0 / c, 0.0), 2, 2 * math.pi * f0)
-    f = fus.random_vector(g.count(), 2024).reshape(g.dims[2], g.dims[1], g.dims[0])
-    cen = 0.5 * (g.lo + g.hi)
-    sig = 0.2 * (g.hi[0] - g.lo[0])
-    ax = [g.lo[a] + (np.arange(g.dims[a]) + 0.5) * g.dx - cen[a] for a in range(3)]
+    h, k, om = geometry(cfg)
+    n = cfg["n"]
+    g = fus.make_grid([0, 0, 0], [n * h] * 3, h, cfg["harmonic"])
+    kw = fus.Wavenumber(complex(k, 0.0), cfg["harmonic"], om)
+    f = fus.random_vector(g.count(), cfg["seed"])
+    if cfg is CFG2:
+        f = envelope(f, g.lo, g.hi, g.dx, g.dims)
+    return g, kw, f
+
+
+def envelope(f, lo, hi, dx, dims):
+    f = f.reshape(dims[2], dims[1], dims[0])
+    cen = 0.5 * (np.asarray(lo) + np.asarray(hi))
+    sig = 0.2 * (hi[0] - lo[0])
+    ax = [lo[a] + (np.arange(dims[a]) + 0.5) * dx - cen[a] for a in range(3)]
     r2 = (ax[0] ** 2)[None, None, :] + (ax[1] ** 2)[None, :, None] + (ax[2] ** 2)[:, None, None]
-    f = (f * np.exp(-r2 / (2 * sig * sig))).reshape(-1)
-    return g, k, f
+    return (f * np.exp(-r2 / (2 * sig * sig))).reshape(-1)
 
 
 def algorithmic_bytes(N, P):
@@ -168,59 +200,107 @@ def max_over_ranks(x, world, local):
     return float(t.item())
 
 
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_under_torchrun(n):
+    """--gpus N > 1 outside torchrun: run this script again as N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------------- CPU reference arm
-def cpu_apply_seconds(g, k, f, workers, max_steps, warmup, budget_s):
-    """Oracle port of GreenKernel::apply (src/potential.cpp:120-151) on the host: pocketfft
-    on exactly the reference's 2N box. Returns (seconds/apply, steps run)."""
+SAMPLE_PLANES = 32
+
+
+def cpu_sampled(cfg, workers, steps, warmup, budget_s):
+    """The reference's apply (src/potential.cpp:120-151) by the oracle port on the host, as a
+    bounded sample: SAMPLE_PLANES z-planes' share of every stage of the P-box apply at the full
+    line lengths (oracle.SampledApply), extrapolated to the whole apply.  Returns
+    (mean seconds per extrapolated apply, steps run, fraction, mean seconds per sample)."""
     from oracle import fus_oracle as orc
 
     orc.build()
-    go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 2)
-    K = orc.GreenKernel(go, orc.Wavenumber(k.k, 2, k.omega), workers=workers)
+    n = cfg["n"]
+    s = orc.SampledApply([n] * 3, [2 * n] * 3, SAMPLE_PLANES, workers, cfg["seed"])
     for _ in range(warmup):
-        K.apply(f)
-    times = []
-    t_all = time.perf_counter()
-    while len(times) < max_steps:
-        t0 = time.perf_counter()
-        K.apply(f)
-        times.append(time.perf_counter() - t0)
+        s.run()
+    t_all, raw = time.perf_counter(), []
+    while len(raw) < max(1, steps):
+        raw.append(s.run())
         if time.perf_counter() - t_all > budget_s:
             break
-    return statistics.mean(times), len(times)
+    mean = statistics.mean(raw)
+    return mean / s.fraction, len(raw), s.fraction, mean
+
+
+def cpu_baseline_record(cfg, steps, warmup, budget_s, one_thread=True):
+    cores = os.cpu_count() or 1
+    from oracle import fus_oracle as orc
+
+    orc.lib().orc_set_num_threads(cores)
+    sec, nst, frac, raw = cpu_sampled(cfg, cores, steps, warmup, budget_s)
+    n = cfg["n"] ** 3
+    rec = {"value": n / sec, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": (f"{nst} sample(s) of the reference apply (oracle port: pad, pocketfft x/y/z line batches "
+                      f"fwd+inv, spectrum multiply, 1/|P| scale, crop) on {SAMPLE_PLANES} of {2 * cfg['n']} "
+                      f"z-planes' share of every stage (fraction {frac:.5f}), {cores} FFT workers, "
+                      f"{raw:.3f} s per sample; extrapolated = sample / fraction"),
+           "extrapolated": True, "seconds_per_apply": sec, "steps_run": nst}
+    if one_thread:
+        # the reference's own FFT is single-threaded FFTW (proj/CMakeLists.txt:11,29): the
+        # faithful mirror, reported beside the all-core variant
+        s1, _, _, raw1 = cpu_sampled(cfg, 1, 1, 0, 1e9)
+        rec["fft_1thread"] = {"value": n / s1, "unit": UNIT, "cores": 1, "seconds_per_apply": s1,
+                              "sample": f"1 sample, 1 FFT worker, {raw1:.3f} s per sample, extrapolated"}
+    return rec
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu"] = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                info["mem_total"] = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
-    g, k, f = cfg2_inputs()
-    cores = os.cpu_count() or 1
-    orc_lib = None
-    try:
-        from oracle import fus_oracle as orc
-        orc_lib = orc.lib()
-        orc_lib.orc_set_num_threads(cores)
-    except Exception:
-        pass
-    # every requested warm-up apply runs (~1.4 s each); the timed steps stop after a 150 s budget
-    sec, steps = cpu_apply_seconds(g, k, f, cores, args.steps, args.warmup, 150.0)
-    v = g.count() / sec
+    cfg = CFG5
+    rec = cpu_baseline_record(cfg, args.steps, args.warmup, 240.0, one_thread=True)
+    n = cfg["n"] ** 3
+    sec = rec["seconds_per_apply"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "steps_requested": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "c128", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "grid": [N_SIDE] * 3, "padded": [2 * N_SIDE] * 3,
-                   "parallelism": "host cores"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{steps} full cfg2 applies (oracle/fus_oracle: pocketfft on the "
-                                   f"reference's 2N box, {cores} FFT workers; spectrum prebuilt)"},
-        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world,
+        "steps": rec["steps_run"], "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": bench_config(cfg, world),
+        "cpu_baseline": rec,
+        "host": host_info(),
+        "e2e": {"value": rec["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "host-vector apply by definition (the reference is CPU-only); n=%d voxels" % n,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------------- GPU helpers
 def nested_solve(ctx, reps=2):
     """BASELINE metric part 2: wall time of the nested 5-harmonic recursion (run_cascade) on
     config 4's geometry at the desk frequency 0.275 MHz (full size needs >= 4 GPUs: SURVEY.md
@@ -243,184 +323,213 @@ def nested_solve(ctx, reps=2):
             best, rows = dt, r.timings
     n2 = cfg.plan.for_harmonic(2).grid.count()
     p1 = rows[0].p1_s
+    fp64 = rayleigh_fp64_profile()
+    tps = n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None
     return {"config": "cfg4 geometry (bowl R 7.5 cm, l 15 cm, c 1540, rho 1050, beta 4.5, 1 MPa) at "
                       "f0=0.275 MHz, 4096 points, nested n_w=6, 5 harmonics",
             "solve_s": best,
             "grids": [list(cfg.plan.for_harmonic(i).grid.dims) for i in range(2, 6)],
             "rows": [{k: v for k, v in t.__dict__.items()} for t in rows],
-            "rayleigh_terms_per_s": n2 * len(cfg.transducer.source_points) / p1 if p1 > 0 else None,
-            # FP64 pipe fraction of the Rayleigh sum: 21.25 FP64 instructions per term (SASS of
-            # monopole_grid_kernel<0>'s inner loop: 255 per 12 terms) against the pipe's
-            # 64 lanes/clk/SM x 148 SMs x 1.965 GHz
-            "rayleigh_fp64_pipe_frac": (n2 * len(cfg.transducer.source_points) / p1 * 21.25
-                                        / (64 * 148 * 1.965e9)) if p1 > 0 else None}
+            "rayleigh_terms_per_s": tps,
+            # FP64 pipe fraction of the Rayleigh sum: ncu-measured FP64 warp instructions per
+            # term (profiles/, same kernel build) x terms/s against 2 warp instructions per clock
+            # per SM x 148 SMs x the SM clock
+            "rayleigh_fp64_pipe_frac": (tps * fp64["fp64_thread_instr_per_term"] / (64 * 148 * 1.965e9))
+                                       if (tps and fp64) else None,
+            "rayleigh_fp64_source": fp64}
 
 
-# ------------------------------------------------------------------------- GPU arm
-def run_gpu(args, world, rank, local):
+def rayleigh_fp64_profile():
+    p = os.path.join(ROOT, "profiles", "r2_rayleigh_fp64.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def measure_apply(cfg, ctx, steps, warmup, world, local, sampler_on=True, e2e_steps=3):
+    """Device-resident apply on one GPU: K timed steps (CUDA events on the library stream),
+    per-pass events, e2e through the public host-vector call (pageable numpy, the
+    GreenKernel::apply(VectorXcd) drop-in) and pinned."""
+    import ctypes
+
     import torch
 
     from paper_2011_03009_b200 import _lib, fus
 
-    torch.cuda.set_device(local)
-    ctx = fus.context(local)
-    g, k, f = cfg2_inputs()
+    g, k, f = gpu_inputs(cfg)
     N = g.count()
     t0 = time.perf_counter()
     K = fus.GreenKernel(g, k, ctx=ctx)
+    ctx.synchronize()
     build_s = time.perf_counter() - t0
-    # the same build again: the first one also pays the context's first allocations and module
-    # loads; this is the "Evaluate G_k" cost of every further kernel (e.g. each cascade harmonic)
-    t0 = time.perf_counter()
-    K2 = fus.GreenKernel(g, k, ctx=ctx)
-    build_warm_s = time.perf_counter() - t0
-    del K2
     P = K.padded
-    fd = torch.from_numpy(f).to(f"cuda:{local}")
+    dev = f"cuda:{local}"
+    fd = torch.from_numpy(f).to(dev)
     ud = torch.empty_like(fd)
     torch.cuda.synchronize()
     L = _lib.lib()
-    stream = ctx.stream_ptr
 
     def step():
         _lib.check(L.fusg_kernel_apply(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, None))
 
-    for _ in range(max(args.warmup, 3)):
+    for _ in range(max(warmup, 3)):
         step()
     ctx.synchronize()
-
-    # ---- timed region: K back-to-back applies on the library stream, CUDA events
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    cs = torch.cuda.ExternalStream(stream)
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
+    cs = torch.cuda.ExternalStream(ctx.stream_ptr)
+    sampler = ClockSampler(local) if sampler_on else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
     barrier(world)
     ctx.synchronize()
     launches0 = ctx.launch_count()
     ev0.record(cs)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     ev1.record(cs)
     ev1.synchronize()
     launches = ctx.launch_count() - launches0
-    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = ev0.elapsed_time(ev1) / steps
     barrier(world)
-    clocks = sampler.stop()
-    ms = max_over_ranks(ms_local, world, local)
-    value = world * N / (ms * 1e-3)
+    clocks = sampler.stop() if sampler else None
 
-    # ---- per-pass durations (CUDA events between the passes, same stream)
-    pass_ms = (__import__("ctypes").c_double * 5)()
-    _lib.check(L.fusg_kernel_apply_timed(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, 20, pass_ms))
+    pass_ms = (ctypes.c_double * 5)()
+    _lib.check(L.fusg_kernel_apply_timed(K.handle, fd.data_ptr(), ud.data_ptr(), 1.0, 3, pass_ms))
     pass_ms = list(pass_ms)
-    per_pass, total_bytes = algorithmic_bytes(g.dims, P)
-    names = list(per_pass)
-    dom = int(np.argmax(pass_ms))
-    hbm, hbm_kind = peaks()
-    dom_gbs = per_pass[names[dom]] / (pass_ms[dom] * 1e-3) / 1e9
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):
-        try:
-            traffic = json.load(open(tr_path)).get(names[dom])
-        except Exception:
-            traffic = None
 
-    # ---- end to end through the C-ABI host-vector call (pinned host buffers, H2D+D2H inside)
+    # end to end through the public host-vector API (f and u in pageable host memory, the
+    # reference's VectorXcd case; H2D + apply + D2H inside the timed region, chunk-pipelined
+    # through the library's pinned staging ring), then the same with pinned host buffers
+    u_host = np.empty_like(f)
+    K.apply_host(f, out=u_host)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        K.apply_host(f, out=u_host)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
     fh = torch.from_numpy(f).pin_memory()
     uh = torch.empty_like(fh).pin_memory()
-    for _ in range(2):
-        _lib.check(L.fusg_kernel_apply_host(K.handle, fh.data_ptr(), uh.data_ptr(), 1.0))
-    e2e_steps = max(3, min(args.steps, 20))
-    barrier(world)
+    _lib.check(L.fusg_kernel_apply_host(K.handle, fh.data_ptr(), uh.data_ptr(), 1.0))
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         _lib.check(L.fusg_kernel_apply_host(K.handle, fh.data_ptr(), uh.data_ptr(), 1.0))
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, local)
-
-    # parity spot check of the timed output against the host path (same kernels)
+    e2e_pinned_s = (time.perf_counter() - t0) / e2e_steps
     ctx.synchronize()
-    assert torch.equal(ud.cpu(), uh), "device and host-vector applies disagree"
+    # the timed device output, the pageable and the pinned host paths run the same kernels
+    same = bool(torch.equal(ud.cpu(), uh)) and bool(np.array_equal(u_host, uh.numpy()))
+    del fh, uh, u_host
+    out = {"N": N, "dims": list(g.dims), "P": list(P), "ms": ms, "pass_ms": pass_ms, "launches": launches,
+           "clocks": clocks, "build_s": build_s, "e2e_s": e2e_s, "e2e_pinned_s": e2e_pinned_s,
+           "paths_bitwise_equal": same}
+    del K, fd, ud
+    torch.cuda.empty_cache()
+    return out
 
-    solve = None
+
+def roofline_of(m):
+    per_pass, total = algorithmic_bytes(m["dims"], m["P"])
+    names = list(per_pass)
+    dom = int(np.argmax(m["pass_ms"]))
+    hbm, kind = peaks()
+    gbs = per_pass[names[dom]] / (m["pass_ms"][dom] * 1e-3) / 1e9
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        key = "x".join(str(p) for p in m["P"])
+        traffic = tr.get(key, {}).get(names[dom]) if key in tr else None
+    except Exception:
+        pass
+    roof = {"bound": "hbm", "kernel": names[dom], "achieved": gbs, "peak": hbm, "peak_kind": kind,
+            "unit": "GB/s", "frac": gbs / hbm, "traffic": traffic,
+            "algorithmic_bytes_per_launch": per_pass[names[dom]],
+            "launch_ms": m["pass_ms"][dom], "share_of_step": m["pass_ms"][dom] / sum(m["pass_ms"])}
+    apply_roof = {"algorithmic_bytes": total, "achieved_gbs": total / (m["ms"] * 1e-3) / 1e9,
+                  "frac": total / (m["ms"] * 1e-3) / 1e9 / hbm,
+                  "per_pass_frac": {nm: per_pass[nm] / (t * 1e-3) / 1e9 / hbm
+                                    for nm, t in zip(names, m["pass_ms"])}}
+    return roof, apply_roof, dict(zip(names, m["pass_ms"]))
+
+
+# ------------------------------------------------------------------------- GPU arm (N = 1)
+def run_gpu(args, world, rank, local):
+    import torch
+
+    from paper_2011_03009_b200 import fus
+
+    torch.cuda.set_device(local)
+    ctx = fus.context(local)
+    m = measure_apply(CFG5, ctx, args.steps, args.warmup, world, local)
+    N = m["N"]
+    value = world * N / (m["ms"] * 1e-3)
+    roof, apply_roof, passes = roofline_of(m)
+
+    extras = {}
+    if not args.headline_only:
+        m2 = measure_apply(CFG2, ctx, 50, 3, world, local, sampler_on=False)
+        r2, a2, p2 = roofline_of(m2)
+        extras["cfg2"] = {"workload": CFG2["workload"], "value": m2["N"] / (m2["ms"] * 1e-3), "unit": UNIT,
+                          "ms_per_step": m2["ms"], "steps": 50, "roofline": r2, "apply_roofline": a2,
+                          "passes_ms": p2, "e2e_pageable": m2["N"] / m2["e2e_s"],
+                          "e2e_pinned": m2["N"] / m2["e2e_pinned_s"], "kernel_build_s": m2["build_s"]}
     if rank == 0 and not args.no_cascade:
-        solve = nested_solve(ctx)
-    # evaluate_potential_at at the reference's use (on-axis nodes of a
-    # D2-grid field), with the CPU oracle on a bounded sample when the CPU leg runs
-    off_grid = vie = acceptance = None
-    if rank == 0 and world == 1 and not args.no_cascade:
+        extras["nested_5_harmonic_solve"] = nested_solve(ctx)
+    if rank == 0 and world == 1 and not args.no_cascade and not args.headline_only:
         from tools import acceptance_bench, potential_at_bench, vie_bench
-        off_grid = potential_at_bench.run(cpu_points=0 if args.no_cpu_baseline else 16)
-        # a VIE solve at cfg2 size (liver slab), CPU oracle per iteration beside it
-        vie = vie_bench.run(cpu=not args.no_cpu_baseline)
-        # the reference's long acceptance workloads (recorded wall times in proj/test_output.txt)
+        # SURVEY.md 8(f) rank 1: evaluate_potential_at at the reference's use
+        extras["evaluate_potential_at"] = potential_at_bench.run(cpu_points=0 if args.no_cpu_baseline else 16)
+        # SURVEY.md 8(f) rank 2: a VIE solve at cfg2 size (liver slab)
+        extras["vie_solve"] = vie_bench.run(cpu=not args.no_cpu_baseline)
         acceptance_bench.criterion1()  # warm-up
-        acceptance = {"criterion_1": acceptance_bench.criterion1(), "criterion_6": acceptance_bench.criterion6(),
-                      "criterion_10_cascade": acceptance_bench.criterion10_cascade()}
+        extras["acceptance"] = {"criterion_1": acceptance_bench.criterion1(),
+                                "criterion_6": acceptance_bench.criterion6(),
+                                "criterion_10_cascade": acceptance_bench.criterion10_cascade()}
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
         try:
-            from oracle import fus_oracle as orc
-            orc.lib().orc_set_num_threads(cores)
-            sec, nst = cpu_apply_seconds(g, k, f, cores, 3, 0, 20.0)
-            cpu_baseline = {"value": N / sec, "unit": UNIT, "cores": cores, "kind": "port",
-                            "sample": f"{nst} full cfg2 apply(s) by oracle/fus_oracle (pocketfft on the "
-                                      f"reference's 2N box, {cores} FFT workers; spectrum prebuilt)"}
+            cpu_baseline = cpu_baseline_record(CFG5, 3, 1, 20.0, one_thread=True)
         except Exception as e:  # reported, never silently replaced
-            cpu_baseline = {"value": None, "unit": UNIT, "cores": cores, "kind": "port",
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                             "sample": f"failed: {e}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "warmup": max(args.warmup, 3), "ms_per_step": m["ms"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "grid": list(g.dims), "padded": list(P),
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs+workspace (1.9 GB) > 126 MB L2; no flush"},
-            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": dom_gbs, "peak": hbm,
-                         "peak_kind": hbm_kind, "unit": "GB/s", "frac": dom_gbs / hbm,
-                         "traffic": traffic,
-                         "algorithmic_bytes_per_launch": per_pass[names[dom]]},
-            # pass C is FP64/L1-latency bound, not HBM bound: its FP64 pipe fraction from the
-            # SASS instruction count of the 16x16x2 kernel (998 FP64 warp instructions per
-            # z-line, ncu: profiles/r1_ncu_summary.md) against 2 per clock per SM
-            "pass_c_fp64_pipe": ({"fp64_warp_instr_per_line": 998, "lines": P[0] * P[1],
-                                  "frac": 998.0 * P[0] * P[1] / (pass_ms[2] * 1e-3)
-                                  / (2 * 148 * 1.965e9)} if tuple(P) == (512, 512, 512) else None),
-            "apply_roofline": {"algorithmic_bytes": total_bytes,
-                               "achieved_gbs": total_bytes / (ms * 1e-3) / 1e9,
-                               "frac": total_bytes / (ms * 1e-3) / 1e9 / hbm},
-            "passes_ms": dict(zip(names, pass_ms)),
-            "kernel_build_s": build_s, "kernel_build_warm_s": build_warm_s,
-            "e2e": {"value": world * N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
-                    "d2h_bytes_per_step": 16 * N},
-            "gpu_launches": int(launches),
-            "clocks": clocks,
+            "config": bench_config(CFG5, world),
+            "roofline": roof,
+            "apply_roofline": apply_roof,
+            "passes_ms": passes,
+            "kernel_build_s": m["build_s"],
+            "e2e": {"value": world * N / m["e2e_s"], "unit": UNIT, "h2d_bytes_per_step": 16 * N,
+                    "d2h_bytes_per_step": 16 * N,
+                    "path": "GreenKernel.apply_host on pageable numpy buffers (fusg_kernel_apply_host)",
+                    "pinned_value": world * N / m["e2e_pinned_s"]},
+            "gpu_launches": int(m["launches"]),
+            "clocks": m["clocks"],
             "cpu_baseline": cpu_baseline,
-            "nested_5_harmonic_solve": solve,
-            "evaluate_potential_at": off_grid,
-            "vie_solve": vie,
-            "acceptance": acceptance,
+            "host": host_info(),
+            "paths_bitwise_equal": m["paths_bitwise_equal"],
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     return 0
 
 
+# ------------------------------------------------------------------------- GPU arm (N > 1)
 def run_gpu_sharded(args, world, rank, local):
-    """N > 1: one cfg2 apply slab-sharded over all ranks (strong scaling). Rank r owns z-planes
-    of f/u and kx columns of the spectrum; the two transposes are NCCL grouped send/recv over
-    NVLink (fusg_kernel_apply_slab). Time = max over ranks of CUDA-event time."""
-    import ctypes
-
+    """N > 1: one cfg5 apply slab-sharded over all ranks (strong scaling). Rank r owns z-planes
+    of f/u and kx columns of the spectrum; the two transposes are fused into passes A/D as NVLink
+    peer stores (or NCCL grouped send/recv with --transport nccl). Time = max over ranks of
+    CUDA-event time."""
     import torch
     import torch.distributed as dist
 
     from paper_2011_03009_b200 import _lib, fus
 
+    cfg = CFG5 if not args.cfg2 else CFG2
     torch.cuda.set_device(local)
     ctx = fus.context(local)
     uid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
@@ -429,15 +538,17 @@ def run_gpu_sharded(args, world, rank, local):
     if world > 1:
         dist.broadcast(uid, 0)
     fus.attach_nccl(ctx, world, rank, bytes(uid.cpu().numpy().tobytes()))
-    g, k, f = cfg2_inputs()
+    h, kk, om = geometry(cfg)
+    n = cfg["n"]
+    g = fus.make_grid([0, 0, 0], [n * h] * 3, h, cfg["harmonic"])
+    k = fus.Wavenumber(complex(kk, 0.0), cfg["harmonic"], om)
     N = g.count()
     t0 = time.perf_counter()
     K = fus.SlabKernel(g, k, world, rank, ctx)
     build_s = time.perf_counter() - t0
-    # fused peer-store transposes (default when the padded x/y lengths allow): gather every
-    # rank's CUDA IPC handles and map the peers' x-slab / A buffers
     transport = args.transport
-    if transport == "p2p" and not (set(K_padded(g)[:2]) <= {256, 512, 768, 1024, 1536, 2048}):
+    P = fus.padded_dims(g)
+    if transport == "p2p" and not (set(P[:2]) <= {256, 512, 768, 1024, 1536, 2048}):
         transport = "nccl"
     if transport == "p2p":
         mine = torch.frombuffer(bytearray(K.ipc_handles()), dtype=torch.uint8).to(f"cuda:{local}")
@@ -446,13 +557,15 @@ def run_gpu_sharded(args, world, rank, local):
             dist.all_gather(allh, mine)
         else:
             allh = [mine]
-        K.attach_peers(b"".join(bytes(h.cpu().numpy().tobytes()) for h in allh))
+        K.attach_peers(b"".join(bytes(x.cpu().numpy().tobytes()) for x in allh))
     plane = g.dims[0] * g.dims[1]
-    f_slab = np.ascontiguousarray(f[K.z0 * plane:(K.z0 + K.nz) * plane])
+    # this rank's z-slab of the seeded source (the mt19937 stream is sequential in x-fastest order)
+    f_pre = fus.random_vector((K.z0 + K.nz) * plane, cfg["seed"])
+    f_slab = np.ascontiguousarray(f_pre[K.z0 * plane:])
+    del f_pre
     fd = torch.from_numpy(f_slab).to(f"cuda:{local}")
     ud = torch.empty_like(fd)
     L = _lib.lib()
-
     apply_fn = L.fusg_kernel_apply_slab_p2p if transport == "p2p" else L.fusg_kernel_apply_slab
 
     def step():
@@ -481,7 +594,7 @@ def run_gpu_sharded(args, world, rank, local):
     # end to end through the public API: pinned host slab -> device, sharded apply, -> host
     fh = torch.from_numpy(f_slab).pin_memory()
     uh = torch.empty_like(fh).pin_memory()
-    e2e_steps = max(3, min(args.steps, 20))
+    e2e_steps = 3
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -491,31 +604,26 @@ def run_gpu_sharded(args, world, rank, local):
         ctx.synchronize()
         uh.copy_(ud)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps, world, local)
-    # all-to-all volume: every rank sends all but its own block in each of the two transposes
     plan = fus.slab_exchange_plan(g, world, rank)
     sent = 2 * 16 * int(plan["a_cnt"].sum() - plan["a_cnt"][rank])
     sent = max_over_ranks(float(sent), world, local)
-    per_pass, total_bytes = algorithmic_bytes(g.dims, K_padded(g))
+    per_pass, total_bytes = algorithmic_bytes(g.dims, P)
     hbm, hbm_kind = peaks()
+    nvl = 900.0
     if rank == 0:
         line = {
             "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic",
-            "transport": transport,
-            "config": {"workload": WORKLOAD + ("; z-slab sharded over ranks, transposes fused into passes A/D as "
-                                               "NVLink peer stores" if transport == "p2p" else
-                                               "; z-slab sharded over ranks, NCCL all-to-all transposes"),
-                       "grid": list(g.dims), "padded": list(K_padded(g)),
-                       "parallelism": f"slab{world}", "l2": "inputs+workspace > 126 MB L2; no flush"},
+            "data": "synthetic", "transport": transport,
+            "config": bench_config(cfg, world),
             "roofline": {"bound": "hbm+nvlink", "kernel": "sharded apply (passes A-E + 2 transposes)",
                          "achieved": total_bytes / world / (ms * 1e-3) / 1e9, "peak": hbm,
                          "peak_kind": hbm_kind, "unit": "GB/s",
                          "frac": total_bytes / world / (ms * 1e-3) / 1e9 / hbm, "traffic": None,
                          "nvlink_bytes_sent_per_gpu": sent,
                          "nvlink_gbs_if_serialised": sent / (ms * 1e-3) / 1e9,
-                         "nvlink_peak_gbs": 770.0},
+                         "nvlink_peak_gbs": nvl, "nvlink_frac_if_serialised": sent / (ms * 1e-3) / 1e9 / nvl},
             "kernel_build_s": build_s,
             "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
@@ -525,31 +633,27 @@ def run_gpu_sharded(args, world, rank, local):
     return 0
 
 
-def K_padded(g):
-    from paper_2011_03009_b200 import fus
-
-    return fus.padded_dims(g)
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="fusg", choices=["fusg", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cascade", action="store_true", help="skip the nested 5-harmonic solve")
+    ap.add_argument("--headline-only", action="store_true", help="cfg5 line only (no cfg2 / 8(f) extras)")
     ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N = 1")
+    ap.add_argument("--cfg2", action="store_true", help="sharded path on cfg2 instead of cfg5")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="sharded apply: transposes fused into passes A/D as peer stores, or NCCL all-to-all")
-    ap.add_argument("--replicas", action="store_true",
-                    help="N > 1: independent per-rank applies (weak scaling) instead of the sharded apply")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
     world, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":
             return run_reference(args, world, rank)
-        if (world > 1 or args.sharded) and not args.replicas:
+        if world > 1 or args.sharded:
             return run_gpu_sharded(args, world, rank, local)
         return run_gpu(args, world, rank, local)
     finally:

@@ -262,6 +262,63 @@ class GreenKernel:
         return HarmonicField(self.grid, self.apply(f.values), self.k)
 
 
+class SampledApply:
+    """Bounded sample of GreenKernel::apply (src/potential.cpp:128-149) for boxes too large to
+    run whole within a benchmark's time budget ("time a stated fraction
+    and report it as extrapolated").  The reference's apply is pad -> 3D FFT of the P box ->
+    multiply by the P-box spectrum -> inverse 3D FFT -> /|P| -> crop; its 3D FFTs are three
+    batches of one-dimensional transforms (one batch per axis).  One sample runs `planes`
+    z-planes' share of every stage at the full line lengths and strides:
+      * pad + crop + the spectrum multiply + the 1/|P| scale on a (planes, Py, Px) block;
+      * forward and inverse x-line and y-line transforms on that block;
+      * forward and inverse z-line transforms on a (Pz, planes*Py/Pz, Px) block.
+    That is the fraction F = planes/Pz of every stage's lines, so t_apply = t_sample / F.
+    Inputs are the first `planes` z-planes of the seeded source (random_vector(n, seed) is
+    sequential in x-fastest order); the multiply's factor block holds stand-in values (the
+    timing does not depend on them)."""
+
+    def __init__(self, dims, P, planes: int, workers: int, seed: int):
+        self.n = [int(v) for v in dims]
+        self.P = [int(v) for v in P]
+        self.planes = max(1, min(int(planes), self.P[2]))
+        self.workers = workers
+        n, P = self.n, self.P
+        self.nzf = min(self.planes, n[2])
+        self.f = random_vector(self.nzf * n[1] * n[0], seed).reshape(self.nzf, n[1], n[0])
+        self.khat = np.full((self.planes, P[1], P[0]), 1.0 + 0.5j, np.complex128)
+        self.zcols = max(1, self.planes * P[1] // P[2])
+        self.zb = np.ones((P[2], self.zcols, P[0]), np.complex128)
+        self.fraction = self.planes / P[2]
+
+    def run(self) -> float:
+        """One sample; returns its seconds."""
+        import scipy.fft as sf
+
+        n, P, w = self.n, self.P, self.workers
+        t0 = __import__("time").perf_counter()
+        work = np.zeros((self.planes, P[1], P[0]), np.complex128)  # pad (:130-134)
+        work[: self.nzf, : n[1], : n[0]] = self.f
+        for ax in (2, 1):  # forward x, y lines of the block
+            work = sf.fft(work, axis=ax, workers=w, overwrite_x=True)
+        self.zb = sf.fft(self.zb, axis=0, workers=w, overwrite_x=True)  # forward z lines
+        work *= self.khat  # (:137-139)
+        self.zb = sf.ifft(self.zb, axis=0, norm="forward", workers=w, overwrite_x=True)
+        for ax in (1, 2):
+            work = sf.ifft(work, axis=ax, norm="forward", workers=w, overwrite_x=True)
+        work /= float(P[0] * P[1] * P[2])  # (:141)
+        out = np.ascontiguousarray(work[: self.nzf, : n[1], : n[0]])  # crop (:143-149)
+        dt = __import__("time").perf_counter() - t0
+        del out, work
+        return dt
+
+
+def sampled_apply_seconds(dims, P, planes: int, workers: int, seed: int, reps: int = 1):
+    """(seconds per extrapolated apply, fraction, best seconds per sample) of SampledApply."""
+    s = SampledApply(dims, P, planes, workers, seed)
+    best = min(s.run() for _ in range(max(1, reps)))
+    return best / s.fraction, s.fraction, best
+
+
 def _fftn(a, workers):
     try:
         import scipy.fft as sf

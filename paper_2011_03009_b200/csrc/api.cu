@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "internal.hpp"
+#include "host_stage.hpp"
 
 
 using namespace fusg;
@@ -46,11 +47,33 @@ void free_kernel(fusg_kernel* K) {
   cudaFreeAsync(K->bufB, s);
   cudaFreeAsync(K->koct, s);
   if (K->rbuf) cudaFreeAsync(K->rbuf, s);
-  cudaFree(K->stage_f);
-  cudaFree(K->stage_u);
+  if (K->stage_f) cudaFree(K->stage_f);
+  if (K->stage_u) cudaFree(K->stage_u);
+  if (K->ring) {
+    static_cast<PinnedRing*>(K->ring)->destroy();
+    delete static_cast<PinnedRing*>(K->ring);
+  }
+  if (K->last_ev) cudaEventDestroy(K->last_ev);
   for (cudaEvent_t e : K->chunk_ev) cudaEventDestroy(e);
   if (K->copy_stream) cudaStreamDestroy(K->copy_stream);
   delete K;  // (twiddle tables belong to the context's cache)
+}
+
+// Applies of one kernel share its workspace: an apply enqueued on a stream other than the last
+// user's waits for the last user's work (an event), then records its own.  Callers hold K->mu.
+cudaError_t workspace_acquire(fusg_kernel* K, cudaStream_t s) {
+  if (!K->last_ev) {
+    cudaError_t e = cudaEventCreateWithFlags(&K->last_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  } else if (K->last_stream != s) {
+    cudaError_t e = cudaStreamWaitEvent(s, K->last_ev, 0);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+cudaError_t workspace_release(fusg_kernel* K, cudaStream_t s) {
+  K->last_stream = s;
+  return cudaEventRecord(K->last_ev, s);
 }
 
 // CUDA-event stopwatch on a stream
@@ -201,8 +224,12 @@ fusg_status fusg_kernel_apply(fusg_kernel* K, const double* f_dev, double* u_dev
     return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: output aliases input");
   FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
   std::lock_guard<std::mutex> lock(K->mu);
-  return volume_potential_apply(K, reinterpret_cast<const double2*>(f_dev),
-                                reinterpret_cast<double2*>(u_dev), scale, K->ctx->pick(stream));
+  cudaStream_t s = K->ctx->pick(stream);
+  FUSG_CUDA_TRY(workspace_acquire(K, s));
+  fusg_status st = volume_potential_apply(K, reinterpret_cast<const double2*>(f_dev),
+                                          reinterpret_cast<double2*>(u_dev), scale, s);
+  FUSG_CUDA_TRY(workspace_release(K, s));
+  return st;
 }
 
 fusg_status fusg_kernel_apply_timed(fusg_kernel* K, const double* f_dev, double* u_dev,
@@ -212,6 +239,7 @@ fusg_status fusg_kernel_apply_timed(fusg_kernel* K, const double* f_dev, double*
   FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
   std::lock_guard<std::mutex> lock(K->mu);
   cudaStream_t s = K->ctx->stream;
+  FUSG_CUDA_TRY(workspace_acquire(K, s));
   std::vector<cudaEvent_t> ev(6 * size_t(reps));
   for (auto& e : ev) FUSG_CUDA_TRY(cudaEventCreate(&e));
   fusg_status st = FUSG_OK;
@@ -231,24 +259,50 @@ fusg_status fusg_kernel_apply_timed(fusg_kernel* K, const double* f_dev, double*
     }
   }
   for (auto& e : ev) cudaEventDestroy(e);
+  FUSG_CUDA_TRY(workspace_release(K, s));
   return st;
 }
 
 fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double* u_host,
                                    double scale) {
   if (!K || !f_host || !u_host) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply: null argument");
+  if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_host: sharded kernel needs a slab apply");
   FUSG_CUDA_TRY(cudaSetDevice(K->ctx->device));
   const size_t bytes = size_t(count_of(K->grid)) * 16;
   cudaStream_t s = K->ctx->stream;
   std::lock_guard<std::mutex> lock(K->mu);
-  if (!K->stage_f) {  // device staging for host-vector applies, allocated once per kernel
+  if (!K->stage_f || !K->stage_u) {  // device staging for host-vector applies, allocated once per kernel
+    if (K->stage_f) cudaFree(K->stage_f);
+    if (K->stage_u) cudaFree(K->stage_u);
+    K->stage_f = K->stage_u = nullptr;
     if (cudaMalloc(&K->stage_f, bytes) != cudaSuccess || cudaMalloc(&K->stage_u, bytes) != cudaSuccess) {
       cudaGetLastError();
+      if (K->stage_f) cudaFree(K->stage_f);
+      K->stage_f = K->stage_u = nullptr;
       return set_error(FUSG_OOM, "kernel_apply_host: staging allocation failed");
     }
     K->bytes += 2 * bytes;
   }
-  if (K->G != 1) return set_error(FUSG_INVALID_ARGUMENT, "kernel_apply_host: sharded kernel needs a slab apply");
+  // Pageable host vectors (the VectorXcd case) go through the library's pinned staging ring;
+  // pinned ones are copied directly.
+  const bool pinned = host_pinned(f_host) && host_pinned(u_host);
+  PinnedRing* ring = nullptr;
+  if (!pinned) {
+    if (!K->ring) {
+      auto* r = new PinnedRing;
+      const char* env_t = getenv("FUSG_HOST_THREADS");
+      const int hw = int(std::thread::hardware_concurrency());
+      const int nt = env_t ? std::max(1, atoi(env_t)) : std::max(1, std::min(8, hw / 2));
+      if (r->init(4, size_t(32) << 20, nt) != cudaSuccess) {
+        cudaGetLastError();
+        r->destroy();
+        delete r;
+        return set_error(FUSG_OOM, "kernel_apply_host: pinned staging allocation failed");
+      }
+      K->ring = r;
+    }
+    ring = static_cast<PinnedRing*>(K->ring);
+  }
   // z-chunk pipeline: chunk c is copied in on the copy stream while the compute stream runs
   // passes A+B on chunk c-1; after pass C, passes D+E of chunk c overlap the copy-out of c-1.
   const int Nz = K->grid.dims[2];
@@ -263,23 +317,27 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
     FUSG_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     K->chunk_ev.push_back(e);
   }
+  FUSG_CUDA_TRY(workspace_acquire(K, s));
   cudaStream_t cs = K->copy_stream;
   auto z_of = [&](int c) { return int(int64_t(Nz) * c / nchunks); };
   auto* hf = reinterpret_cast<const char*>(f_host);
   auto* hu = reinterpret_cast<char*>(u_host);
+  auto* df = reinterpret_cast<char*>(K->stage_f);
+  auto* du = reinterpret_cast<char*>(K->stage_u);
   // the copy stream starts after the compute stream's earlier work (a previous apply's reads of
   // the staging buffers)
   FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[2 * nchunks], s));
   FUSG_CUDA_TRY(cudaStreamWaitEvent(cs, K->chunk_ev[2 * nchunks], 0));
-  for (int c = 0; c < nchunks; ++c) {
-    const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
-    FUSG_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(K->stage_f) + z0 * plane, hf + z0 * plane,
-                                  nzc * plane, cudaMemcpyHostToDevice, cs));
-    FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[c], cs));
-  }
   fusg_status st = FUSG_OK;
+  // host -> device, chunk by chunk; with the ring the host thread stages chunk c + 1 while the
+  // device computes passes A+B of chunk c, so the compute launches are interleaved with it
   for (int c = 0; c < nchunks && st == FUSG_OK; ++c) {
     const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
+    if (ring)
+      FUSG_CUDA_TRY(ring->h2d(df + z0 * plane, hf + z0 * plane, nzc * plane, cs));
+    else
+      FUSG_CUDA_TRY(cudaMemcpyAsync(df + z0 * plane, hf + z0 * plane, nzc * plane, cudaMemcpyHostToDevice, cs));
+    FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[c], cs));
     FUSG_CUDA_TRY(cudaStreamWaitEvent(s, K->chunk_ev[c], 0));
     st = apply_chunk_AB(K, K->stage_f + int64_t(z0) * (plane / 16), z0, nzc, s);
   }
@@ -290,12 +348,18 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
     if (st != FUSG_OK) break;
     FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[nchunks + c], s));
     FUSG_CUDA_TRY(cudaStreamWaitEvent(cs, K->chunk_ev[nchunks + c], 0));
-    FUSG_CUDA_TRY(cudaMemcpyAsync(hu + z0 * plane, reinterpret_cast<char*>(K->stage_u) + z0 * plane,
-                                  nzc * plane, cudaMemcpyDeviceToHost, cs));
+    if (!ring)
+      FUSG_CUDA_TRY(cudaMemcpyAsync(hu + z0 * plane, du + z0 * plane, nzc * plane, cudaMemcpyDeviceToHost, cs));
+  }
+  // with the ring the host drains chunk by chunk (each chunk's DMA waits for its passes D+E)
+  for (int c = 0; ring && c < nchunks && st == FUSG_OK; ++c) {
+    const int z0 = z_of(c), nzc = z_of(c + 1) - z0;
+    FUSG_CUDA_TRY(ring->d2h(hu + z0 * plane, du + z0 * plane, nzc * plane, cs));
   }
   // the compute stream's later work must not overwrite the staging buffers under the copies
   FUSG_CUDA_TRY(cudaEventRecord(K->chunk_ev[2 * nchunks], cs));
   FUSG_CUDA_TRY(cudaStreamWaitEvent(s, K->chunk_ev[2 * nchunks], 0));
+  FUSG_CUDA_TRY(workspace_release(K, s));
   FUSG_CUDA_TRY(cudaStreamSynchronize(cs));
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
   return st;

@@ -437,12 +437,13 @@ __global__ void __launch_bounds__(256, 2) warp_row_to_col_r16_ring(WArgs a) {
 // pass A of the chunk (rows of f -> slot) or pass B (slot -> B).  1 launched, -1 error.
 int launch_r16_chunk(fusg_ctx* ctx, bool pass_b, const WArgs& a, cudaStream_t s) {
   const auto fn = pass_b ? warp_row_to_col_r16_ring : warp_row_to_col_r16;
-  static const bool attr = [] {
+  static std::atomic<uint64_t> attr_mask{0};
+  const bool attr = once_per_device(attr_mask, [] {
     return cudaFuncSetAttribute(warp_row_to_col_r16, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(kR16TileBytes)) == cudaSuccess &&
            cudaFuncSetAttribute(warp_row_to_col_r16_ring, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(kR16TileBytes)) == cudaSuccess;
-  }();
+  });
   if (!attr) {
     set_error(FUSG_CUDA, "z-chunk A/B: cannot configure shared memory");
     return -1;

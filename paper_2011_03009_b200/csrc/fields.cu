@@ -667,11 +667,12 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   const double umax = dmax * k1;
   const int n_eh = dmax >= 0.0 ? int(umax / (1 << kGridPhaseBits)) + 2 : kEhMax + 1;
   const size_t dsm = sizeof(double2) * (size_t(1) << kGridPhaseBits) + sizeof(double) * kEhMax;
-  static const bool attr = [&] {
+  static std::atomic<uint64_t> attr_mask{0};
+  const bool attr = once_per_device(attr_mask, [&] {
     for (auto fn : {monopole_grid_kernel<0>, monopole_grid_kernel<1>, monopole_grid_kernel<2>, monopole_grid_kernel<3>})
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm)) != cudaSuccess) return false;
     return true;
-  }();
+  });
   if (!attr) return set_error(FUSG_CUDA, "monopole_grid: cannot configure shared memory");
   if (att_table && kim > 0.0 && k1 > 0.0 && n_eh <= kEhMax && umax < 1e9) {
     monopole_grid_kernel<3><<<blocks, threads, dsm, s>>>(src_dev, n_src, gd, k1, kim / k1, amp, out,

@@ -1,0 +1,196 @@
+// Pinned staging ring for host-vector applies on pageable memory.
+//
+// GreenKernel::apply(const VectorXcd&) (src/potential.cpp:120-151) hands the library ordinary
+// pageable host memory.  A cudaMemcpyAsync from pageable memory is staged by the driver through
+// a small bounce buffer and is synchronous for the calling thread, so the z-chunk overlap of
+// the host apply would be lost.  Here the library stages itself: the host copies a piece of
+// the caller's vector into one slot of a ring of pinned buffers (several threads, so the copy
+// keeps up with PCIe), one cudaMemcpyAsync moves the slot, and the slot is reused once the
+// event recorded after its DMA has completed.  Device-to-host runs the same ring backwards.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace fusg {
+
+// Fixed pool of worker threads running one parallel memcpy at a time (the caller takes a share).
+class CopyPool {
+ public:
+  explicit CopyPool(int nthreads) : n_(std::max(1, nthreads)) {
+    for (int i = 1; i < n_; ++i) th_.emplace_back([this, i] { worker(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void memcpy_par(void* dst, const void* src, size_t bytes) {
+    if (n_ == 1 || bytes < (size_t(4) << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> g(m_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(m_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+  }
+  int threads() const { return n_; }
+
+ private:
+  void part(int i) {
+    const size_t per = (bytes_ / n_ + 63) & ~size_t(63);
+    const size_t b = std::min(bytes_, per * size_t(i)), e = std::min(bytes_, b + per);
+    if (e > b) std::memcpy(dst_ + b, src_ + b, e - b);
+  }
+  void worker(int i) {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      part(i);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_cv_.notify_one();
+      }
+    }
+  }
+  int n_;
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  unsigned long long gen_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+  int pending_ = 0;
+};
+
+// Ring of pinned slots; each slot carries the event of the last DMA that used it.
+struct PinnedRing {
+  std::vector<void*> slot;
+  std::vector<cudaEvent_t> ev;
+  std::vector<bool> busy;
+  size_t slot_bytes = 0;
+  int next = 0;
+  CopyPool* pool = nullptr;
+
+  cudaError_t init(int nslots, size_t bytes, int threads) {
+    slot_bytes = bytes;
+    for (int i = 0; i < nslots; ++i) {
+      void* p = nullptr;
+      cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+      slot.push_back(p);
+      cudaEvent_t v;
+      e = cudaEventCreateWithFlags(&v, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+      ev.push_back(v);
+      busy.push_back(false);
+    }
+    pool = new CopyPool(threads);
+    return cudaSuccess;
+  }
+  void destroy() {
+    for (size_t i = 0; i < slot.size(); ++i) {
+      cudaEventSynchronize(ev[i]);
+      cudaFreeHost(slot[i]);
+      cudaEventDestroy(ev[i]);
+    }
+    slot.clear();
+    ev.clear();
+    busy.clear();
+    delete pool;
+    pool = nullptr;
+  }
+  // host -> device: pageable src -> slot -> dst on stream s
+  cudaError_t h2d(char* dst, const char* src, size_t bytes, cudaStream_t s) {
+    for (size_t off = 0; off < bytes; off += slot_bytes) {
+      const size_t n = std::min(slot_bytes, bytes - off);
+      const int i = next;
+      next = (next + 1) % int(slot.size());
+      if (busy[i]) {
+        cudaError_t e = cudaEventSynchronize(ev[i]);  // the slot's previous DMA has drained
+        if (e != cudaSuccess) return e;
+      }
+      pool->memcpy_par(slot[i], src + off, n);
+      cudaError_t e = cudaMemcpyAsync(dst + off, slot[i], n, cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) return e;
+      e = cudaEventRecord(ev[i], s);
+      if (e != cudaSuccess) return e;
+      busy[i] = true;
+    }
+    return cudaSuccess;
+  }
+  // device -> host: src on stream s -> slots (kept up to ring-size DMAs in flight) -> pageable dst
+  cudaError_t d2h(char* dst, const char* src, size_t bytes, cudaStream_t s) {
+    const int ns = int(slot.size());
+    const size_t npieces = (bytes + slot_bytes - 1) / slot_bytes;
+    std::vector<int> used(npieces);
+    size_t issued = 0, drained = 0;
+    auto issue = [&]() -> cudaError_t {
+      const size_t off = issued * slot_bytes, n = std::min(slot_bytes, bytes - off);
+      const int i = next;
+      next = (next + 1) % ns;
+      if (busy[i]) {
+        cudaError_t e = cudaEventSynchronize(ev[i]);
+        if (e != cudaSuccess) return e;
+      }
+      cudaError_t e = cudaMemcpyAsync(slot[i], src + off, n, cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) return e;
+      e = cudaEventRecord(ev[i], s);
+      busy[i] = true;
+      used[issued++] = i;
+      return e;
+    };
+    while (drained < npieces) {
+      while (issued < npieces && issued - drained < size_t(ns)) {
+        cudaError_t e = issue();
+        if (e != cudaSuccess) return e;
+      }
+      const int i = used[drained];
+      cudaError_t e = cudaEventSynchronize(ev[i]);
+      if (e != cudaSuccess) return e;
+      const size_t off = drained * slot_bytes, n = std::min(slot_bytes, bytes - off);
+      pool->memcpy_par(dst + off, slot[i], n);
+      busy[i] = false;
+      ++drained;
+    }
+    return cudaSuccess;
+  }
+};
+
+inline bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace fusg

@@ -102,6 +102,11 @@ struct fusg_kernel {
   double2* stage_u = nullptr;
   cudaStream_t copy_stream = nullptr;  // host-vector apply: chunked H2D / D2H beside the compute
   std::vector<cudaEvent_t> chunk_ev;   // one per z-chunk: copied in, then computed out
+  void* ring = nullptr;                // fusg::PinnedRing for pageable host vectors (host_stage.hpp)
+  // the workspace's last user: an apply on another stream waits for it (applies sharing one
+  // kernel are ordered, as the reference's reentrant const apply is safe to call concurrently)
+  cudaEvent_t last_ev = nullptr;
+  cudaStream_t last_stream = nullptr;
   // slab decomposition (unsharded: G = 1, rank 0 owns everything)
   int G = 1, rank = 0;
   bool slab = false;   // created by fusg_kernel_create_slab: owns exchange buffers even at G = 1
@@ -125,6 +130,18 @@ struct fusg_kernel {
 };
 
 namespace fusg {
+// Function attributes are per device: run `set` once for each device this process uses
+// (a mask over device ordinals 0..63; the current device is the one being launched on).
+template <class F>
+inline bool once_per_device(std::atomic<uint64_t>& mask, F&& set) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return set();
+  const uint64_t bit = uint64_t(1) << dev;
+  if (mask.load(std::memory_order_acquire) & bit) return true;
+  if (!set()) return false;
+  mask.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
+}
 // Padded sizes, FFT plans, twiddles and the slab decomposition (G ranks, this is `rank`).
 fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank);
 void slab_split(int n, int G, int r, int* begin, int* count);

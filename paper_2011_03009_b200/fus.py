@@ -276,6 +276,11 @@ class GreenKernel:
         if (f.numel() if torch is not None and isinstance(f, torch.Tensor) else np.size(f)) != n:
             raise ValueError("GreenKernel::apply: field size does not match kernel grid")
         fd = _on_device(f, self.ctx)
+        if out is not None:
+            if (not isinstance(out, torch.Tensor) or out.dtype != torch.complex128 or out.numel() != n
+                    or not out.is_contiguous() or out.device != fd.device):
+                raise ValueError("GreenKernel::apply: out must be a contiguous complex128 tensor of "
+                                 f"{n} elements on {fd.device}")
         u = out if out is not None else torch.empty(n, dtype=torch.complex128, device=fd.device)
         _sync_torch_to(self.ctx)
         check(lib().fusg_kernel_apply(self.handle, fd.data_ptr(), u.data_ptr(), float(scale), None))
@@ -286,12 +291,19 @@ class GreenKernel:
         """Raw device-pointer apply on `stream` (0 = context stream); no synchronisation."""
         check(lib().fusg_kernel_apply(self.handle, f_ptr, u_ptr, float(scale), stream or None))
 
-    def apply_host(self, f: np.ndarray, scale: float = 1.0) -> np.ndarray:
-        """Host-vector drop-in (GreenKernel::apply(const VectorXcd&)): H2D, apply, D2H."""
+    def apply_host(self, f: np.ndarray, scale: float = 1.0, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Host-vector drop-in (GreenKernel::apply(const VectorXcd&)): H2D, apply, D2H, chunk-
+        pipelined; pageable arrays are staged through the library's pinned ring."""
         f = np.ascontiguousarray(f, np.complex128).reshape(-1)
         if f.size != self._grid.count():
             raise ValueError("GreenKernel::apply: field size does not match kernel grid")
-        u = np.empty_like(f)
+        if out is not None:
+            if (not isinstance(out, np.ndarray) or out.dtype != np.complex128 or out.size != f.size
+                    or not out.flags.c_contiguous):
+                raise ValueError(f"GreenKernel::apply: out must be a contiguous complex128 array of {f.size} elements")
+            u = out.reshape(-1)
+        else:
+            u = np.empty_like(f)
         check(lib().fusg_kernel_apply_host(self.handle, f.ctypes.data, u.ctypes.data, float(scale)))
         return u
 
