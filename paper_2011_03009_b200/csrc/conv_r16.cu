@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "warp_args.cuh"
+#include "r16.cuh"
 
 namespace fusg {
 
@@ -20,81 +21,6 @@ namespace fusg {
 // X[k1 + 16 (i + 8 b)] and, in slot i + 8, X[k1 + 16 (i + 8 b) + 256].
 // Exchange buffer: row k1 (32 entries), column n2 ^ (k1 & 7): both access patterns are
 // bank-conflict-free (8 lanes of each 128-byte phase hit 8 distinct 16-byte bank groups).
-// TAB = false: from four exact table powers [w1, w2, w4, w8][lane] (<= 3 products);
-// TAB = true: all fifteen from an exact [k][lane] table (more shared loads, fewer FP64 ops).
-// Either table lives in shared memory, shared by the CTA's warps.
-template <bool CONJ>
-__device__ __forceinline__ void r16_twiddle(double2* v, double2 w1, double2 w2, double2 w4, double2 w8) {
-  auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
-  const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
-  v[1] = m(v[1], w1);
-  v[2] = m(v[2], w2);
-  v[3] = m(v[3], w3);
-  v[4] = m(v[4], w4);
-  v[5] = m(v[5], w5);
-  v[6] = m(v[6], w6);
-  v[7] = m(v[7], w7);
-  v[8] = m(v[8], w8);
-  v[9] = m(v[9], cmul(w8, w1));
-  v[10] = m(v[10], cmul(w8, w2));
-  v[11] = m(v[11], cmul(w8, w3));
-  v[12] = m(v[12], cmul(w8, w4));
-  v[13] = m(v[13], cmul(w8, w5));
-  v[14] = m(v[14], cmul(w8, w6));
-  v[15] = m(v[15], cmul(w8, w7));
-}
-
-template <bool TAB>
-struct R16Tw {  // W512^(n2 k) for k = 1..15
-  const double2* t;
-  int lane;
-  template <bool CONJ>
-  __device__ __forceinline__ void apply(double2* v) const {
-    auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
-    if constexpr (TAB) {
-#pragma unroll
-      for (int k = 1; k < 16; ++k) v[k] = m(v[k], t[32 * k + lane]);
-      return;
-    }
-    r16_twiddle<CONJ>(v, t[lane], t[32 + lane], t[64 + lane], t[96 + lane]);
-  }
-};
-
-__device__ __forceinline__ double2 shfl_xor_d2(double2 x, int m) {
-  return make_double2(__shfl_xor_sync(0xffffffffu, x.x, m), __shfl_xor_sync(0xffffffffu, x.y, m));
-}
-__device__ __forceinline__ double2 sel_d2(bool p, double2 a, double2 b) { return p ? a : b; }
-
-// radix 2 over n2lo with twiddle W32^(q1 n2lo), q1 = i + 8 b (forward), and its adjoint
-template <int I>
-__device__ __forceinline__ void r16_fwd_r2(double2* v, bool b) {
-  const double2 send = sel_d2(b, v[I], v[I + 8]);  // lane b keeps q1 in [8b, 8b + 8)
-  const double2 recv = shfl_xor_d2(send, 16);
-  const double2 z0 = sel_d2(b, recv, v[I]);
-  const double2 z1 = sel_d2(b, v[I + 8], recv);
-  double2 t = w32<false, I>(z1);
-  t = sel_d2(b, rot90<false>(t), t);  // W32^8 = -i
-  v[I] = cadd(z0, t);
-  v[I + 8] = csub(z0, t);
-}
-template <int I>
-__device__ __forceinline__ void r16_inv_r2(double2* v, bool b) {
-  const double2 z0 = cadd(v[I], v[I + 8]);
-  double2 z1 = w32<true, I>(csub(v[I], v[I + 8]));
-  z1 = sel_d2(b, rot90<true>(z1), z1);
-  const double2 send = sel_d2(b, z0, z1);  // lane b collects Z_b[q1] for every q1
-  const double2 recv = shfl_xor_d2(send, 16);
-  v[I] = sel_d2(b, recv, z0);
-  v[I + 8] = sel_d2(b, z1, recv);
-}
-template <bool INV, int... Is>
-__device__ __forceinline__ void r16_r2_all(double2* v, bool b, std::integer_sequence<int, Is...>) {
-  if constexpr (INV) (r16_inv_r2<Is>(v, b), ...);
-  else (r16_fwd_r2<Is>(v, b), ...);
-}
-
-__device__ __forceinline__ int r16_ex(int row, int col) { return row * 32 + (col ^ (row & 7)); }
-
 // per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
 template <bool TAB>
 constexpr size_t r16_smem_bytes(int nw, bool kl2 = false) {

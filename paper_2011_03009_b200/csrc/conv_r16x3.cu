@@ -1,0 +1,496 @@
+// Pass C of the apply at padded z length 1536 = 3 x 512: one CTA of three warps per line, warp
+// r owning the residue-r sub-transform, each a 16 x 16 x 2 warp transform (r16.cuh).
+//
+// Forward (decimation in frequency by 3; x[n] = 0 for n >= 768, the zero padding):
+//   X[3k' + r] = DFT512_k'( y_r ),  y_r[m] = W1536^(m r) (x[m] + W3^r x[m + 512]),  m < 512
+// (x[m + 1024] is padding).  The spectrum is multiplied by the folded K^ row in the warp's
+// half-exchanged layout.  Inverse (decimation in time by 3, unnormalised, cropped to n < 768):
+//   z_r = IDFT512( Z_r ),  t_r[n'] = W1536^(-n' r) z_r[n'],
+//   x[n'] = t0 + t1 + t2,  x[n' + 512] = t0 + W3^-1 t1 + W3^-2 t2   (n' < 256).
+// The per-lane part W1536^(lane r) of the input twiddle W1536^((32 n1 + lane) r) commutes with
+// stage A's in-lane radix 16 and is merged into its twiddle (r16_twiddle_u); the per-slot part
+// W48^(n1 r) is a warp-uniform table value.  The three t_r meet in shared memory and the CTA
+// writes the cropped row with coalesced stores.
+//
+// Per line (three warps): one 12 KB bulk copy of the input row and one of the folded K^ row,
+// both issued one line ahead; three shared exchanges plus shuffle half-exchanges per direction.
+// Against the 64-lane radix (8, 8, 3, 8) kernel it keeps 16 values per lane (no spills at
+// 4 CTAs = 12 warps per SM) and moves ~2000 instead of ~2800 shared wavefronts per line.
+#include <algorithm>
+#include <cstdlib>
+
+#include "r16.cuh"
+
+namespace fusg {
+
+// v[k] *= u * W512^(lane k), k = 0..15, from u and the exact powers w1, w2, w4, w8 (CONJ: by the
+// conjugates)
+template <bool CONJ>
+__device__ __forceinline__ void r16_twiddle_u(double2* v, double2 u, double2 w1, double2 w2, double2 w4, double2 w8) {
+  auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+  const double2 p1 = cmul(u, w1), p2 = cmul(u, w2), p4 = cmul(u, w4), p8 = cmul(u, w8);
+  const double2 p3 = cmul(p1, w2), p5 = cmul(p1, w4), p6 = cmul(p2, w4), p7 = cmul(p3, w4);
+  v[0] = m(v[0], u);
+  v[1] = m(v[1], p1);
+  v[2] = m(v[2], p2);
+  v[3] = m(v[3], p3);
+  v[4] = m(v[4], p4);
+  v[5] = m(v[5], p5);
+  v[6] = m(v[6], p6);
+  v[7] = m(v[7], p7);
+  v[8] = m(v[8], p8);
+  v[9] = m(v[9], cmul(p1, w8));
+  v[10] = m(v[10], cmul(p2, w8));
+  v[11] = m(v[11], cmul(p3, w8));
+  v[12] = m(v[12], cmul(p4, w8));
+  v[13] = m(v[13], cmul(p5, w8));
+  v[14] = m(v[14], cmul(p6, w8));
+  v[15] = m(v[15], cmul(p7, w8));
+}
+
+// shared-memory layout (double2 offsets) of one CTA
+struct X3Smem {
+  static constexpr int XB = 0;             // [3][512] exchange buffers, then the t_r rows
+  static constexpr int SB = 1536;          // staged input row (<= 768 positions)
+  static constexpr int KB = SB + 768;      // folded K^ row (769, padded to 770)
+  static constexpr int TW = KB + 770;      // [4][32] W512^(lane 2^j)
+  static constexpr int US = TW + 128;      // [3][32] W1536^(lane r)
+  static constexpr int C48 = US + 96;      // [48] W48^j
+  static constexpr int END = C48 + 48;
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
+};
+
+// Per-warp pieces of the 1536 = 3 x 512 transform (warp r owns residue r).
+struct X3Warp {
+  double2 u, w1, w2, w4, w8;  // W1536^(lane r); W512^(lane 2^j)
+  const double2* c48;         // W48^j (shared)
+  int r, k1;
+  bool b;
+  double c3, s3;              // W3^r = c3 + i s3
+  __device__ __forceinline__ X3Warp(const double2* sm_us, const double2* tws, const double2* c48_, int r_, int lane)
+      : c48(c48_), r(r_), k1(lane & 15), b(lane >= 16) {
+    u = sm_us[32 * r + lane];
+    w1 = tws[lane];
+    w2 = tws[32 + lane];
+    w4 = tws[64 + lane];
+    w8 = tws[96 + lane];
+    c3 = r == 0 ? 1.0 : -0.5;
+    s3 = r == 0 ? 0.0 : r == 1 ? -0.8660254037844386467637 : 0.8660254037844386467637;
+  }
+  // The three residues run the same instructions (residue 0 multiplies by exact ones), so the
+  // warps of a CTA reach its barriers together.
+  // y_r[32 n1 + lane] without its W1536 twiddle: x[m] + W3^r x[m + 512] (x zero beyond nv)
+  __device__ __forceinline__ void gather(double2* v, const double2* row, int nv, int lane) const {
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) {
+      const int m = 32 * n1 + lane;
+      double2 x0 = m < nv ? row[m] : make_double2(0.0, 0.0);
+      if (n1 < 8) {
+        const double2 x1 = m + 512 < nv ? row[m + 512] : make_double2(0.0, 0.0);
+        x0 = make_double2(fma(c3, x1.x, fma(-s3, x1.y, x0.x)), fma(c3, x1.y, fma(s3, x1.x, x0.y)));
+      }
+      v[n1] = x0;
+    }
+  }
+  // forward: y_r (gathered) -> X[3k' + r] in the half-exchanged layout (slot i: k' = k1 + 16 (i + 8 b),
+  // slot i + 8: k' + 256); xr: this warp's 512-entry exchange buffer
+  __device__ __forceinline__ void forward(double2* v, double2* xr, int lane) const {
+#pragma unroll
+    for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmul(v[n1], c48[n1 * r]);  // W48^(n1 r), n1 r < 48
+    dft16<false>(v);
+    r16_twiddle_u<false>(v, u, w1, w2, w4, w8);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 16; ++h) v[h] = xr[r16_ex(k1, 2 * h + int(b))];
+    dft16<false>(v);
+    r16_r2_all<false>(v, b, std::make_integer_sequence<int, 8>{});
+  }
+  // inverse: Z_r (half-exchanged layout) -> t_r[n'] = W1536^(-n' r) z_r[n'] in the natural
+  // layout (slot n1 = position 32 n1 + lane)
+  __device__ __forceinline__ void inverse(double2* v, double2* xr, int lane) const {
+    r16_r2_all<true>(v, b, std::make_integer_sequence<int, 8>{});
+    dft16<true>(v);
+#pragma unroll
+    for (int h = 0; h < 16; ++h) xr[r16_ex(k1, 2 * h + int(b))] = v[h];
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = xr[r16_ex(k, lane)];
+    r16_twiddle_u<true>(v, u, w1, w2, w4, w8);
+    dft16<true>(v);
+#pragma unroll
+    for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmulc(v[n1], c48[n1 * r]);
+  }
+};
+
+// cropped row from the three t_r rows: x[n'] = t0 + t1 + t2, x[n' + 512] = t0 + W3^-1 t1 + W3^-2 t2
+__device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* t1r, const double2* t2r, int n,
+                                             int onv, double sc, double2* out) {
+  constexpr double kS3 = 0.8660254037844386467637;
+  const double2 t0 = t0r[n], t1 = t1r[n], t2 = t2r[n];
+  const double2 s = cadd(t1, t2);
+  if (n < onv) {
+    const double2 o = cadd(t0, s);
+    out[n] = sc == 1.0 ? o : cscale(o, sc);
+  }
+  if (n + 512 < onv) {
+    const double2 d = csub(t1, t2);
+    const double2 o = make_double2(t0.x - 0.5 * s.x - kS3 * d.y, t0.y - 0.5 * s.y + kS3 * d.x);
+    out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
+  }
+}
+
+// the per-CTA twiddle tables: tws [4][32] W512^(lane 2^j), us [3][32] W1536^(lane r), c48 [48]
+__device__ __forceinline__ void x3_tables(const double2* tw1536, double2* tws, double2* us, double2* c48) {
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) tws[e] = __ldg(tw1536 + (((3 * (e & 31)) << (e >> 5)) % 1536));
+  for (int e = threadIdx.x; e < 96; e += blockDim.x) us[e] = __ldg(tw1536 + (e & 31) * (e >> 5));
+  for (int e = threadIdx.x; e < 48; e += blockDim.x) c48[e] = __ldg(tw1536 + 32 * e);
+}
+
+// ---------------------------------------------------------------------------- pass C
+// CTA of three warps, persistent over lines; the input and K^ rows are staged by 1-D bulk
+// copies one line ahead (the refill is issued after a CTA barrier: measured faster than
+// letting the warps drift apart with last-arriver refills or producer / consumer barriers,
+// 29.8 vs 32.8-33.6 ms at cfg5).
+__global__ void __launch_bounds__(96, 4) conv_r16x3(WArgs a) {
+  constexpr int HZ = 769;
+  extern __shared__ double2 sm[];
+  const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* const xb = sm + X3Smem::XB;
+  double2* const xr = xb + 512 * r;
+  double2* const sb = sm + X3Smem::SB;
+  double2* const kb = sm + X3Smem::KB;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + X3Smem::END);
+  x3_tables(a.tw, sm + X3Smem::TW, sm + X3Smem::US, sm + X3Smem::C48);
+  if (threadIdx.x == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const X3Warp W(sm + X3Smem::US, sm + X3Smem::TW, sm + X3Smem::C48, r, lane);
+  const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
+  const int64_t stride = gridDim.x;
+  const bool mirror = a.n_outer == a.ko.Px;
+  auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
+    conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
+  };
+  auto prefetch_in = [&](int64_t line) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
+      bulk_stage(sb, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(a.in_nvalid) * sizeof(double2), bars);
+    }
+  };
+  auto prefetch_k = [&](int64_t line) {
+    if (line < nlines) {
+      int ky, kx;
+      coords(line, ky, kx);
+      bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
+    }
+  };
+  const int nv = a.in_nvalid, onv = a.out_nvalid;
+  int64_t line = blockIdx.x;
+  if (threadIdx.x == 0) {
+    prefetch_in(line);
+    prefetch_k(line);
+  }
+  unsigned ph = 0;  // both staging barriers complete once per line
+  for (; line < nlines; line += stride, ph ^= 1) {
+    mbar_wait(bars, ph);
+    double2 v[16];
+    W.gather(v, sb, nv, lane);
+    __syncthreads();  // the staged row is read by all three warps: refill it
+    if (threadIdx.x == 0) prefetch_in(line + stride);
+    W.forward(v, xr, lane);
+    // X[3k' + r] times the folded K^ row
+    mbar_wait(bars + 1, ph);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int j = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;  // < 768; its partner j + 768 folds to 768 - j
+      v[i] = cmul(v[i], kb[j]);
+      v[i + 8] = cmul(v[i + 8], kb[768 - j]);
+    }
+    __syncthreads();  // K^ row read
+    if (threadIdx.x == 0) prefetch_k(line + stride);
+    W.inverse(v, xr, lane);
+    __syncwarp();  // every lane has read its exchange slots
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
+    __syncthreads();
+    int ky, kx;
+    coords(line, ky, kx);
+    double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + 512, xb + 1024, n, onv, a.scale, out);
+    __syncthreads();  // the t_r rows are read: the exchange buffers may be rewritten
+  }
+}
+
+// ---------------------------------------------------------------------------- passes A / B
+// Row -> column (forward, pruned input <= 768 of 1536): a CTA of 3T warps transforms T adjacent
+// lines (warp 3t + r: line t, residue r).  The T input rows (contiguous when the rows are
+// dense) arrive by 1-D bulk copy one tile ahead; the spectra meet in a swizzled [pos][T] tile
+// that aliases the twelve exchange buffers; the CTA stores 64-byte segments of T adjacent lines.
+template <int T>
+struct X3TSmem {
+  static constexpr int AREA = 0;              // [1536][T] tile = 3T exchange buffers
+  static constexpr int STAGE = 1536 * T;      // [T][768] staged input rows (r2c)
+  static constexpr int TW = STAGE + 768 * T;  // tables as in X3Smem
+  static constexpr int US = TW + 128;
+  static constexpr int C48 = US + 96;
+  static constexpr int END = C48 + 48;
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + sizeof(uint64_t);
+  // c2r: two [1536][T] tiles (double-buffered), then the tables
+  static constexpr int C_TW = 2 * 1536 * T;
+  static constexpr int C_US = C_TW + 128;
+  static constexpr int C_C48 = C_US + 96;
+  static constexpr int C_END = C_C48 + 48;
+  static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2);
+};
+
+template <int T>
+__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
+  using X3TSmem = fusg::X3TSmem<T>;
+  extern __shared__ double2 sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = w % 3, t = w / 3;
+  double2* const area = sm + X3TSmem::AREA;
+  double2* const xr = area + 512 * w;
+  double2* const stage = sm + X3TSmem::STAGE;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + X3TSmem::END);
+  x3_tables(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const X3Warp W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
+  const int nv = a.in_nvalid;
+  const int ntiles_i = (a.n_inner + T - 1) / T;
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto prefetch = [&](int64_t tix) {  // thread 0
+    if (tix < ntiles) {
+      const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+      const int k = int(unsigned(tix) / unsigned(ntiles_i));
+      const int lines_ok = min(T, a.n_inner - i0);
+      const double2* src = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
+      const unsigned row = unsigned(nv) * sizeof(double2);
+      mbar_expect_tx(bar, row * lines_ok);
+      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stage + tt * 768, src + tt * a.in_si, row, bar);
+    }
+  };
+  int64_t tix = blockIdx.x;
+  if (threadIdx.x == 0) prefetch(tix);
+  unsigned ph = 0;
+  for (; tix < ntiles; tix += gridDim.x, ph ^= 1) {
+    const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+    const int k = int(unsigned(tix) / unsigned(ntiles_i));
+    const int lines_ok = min(T, a.n_inner - i0);
+    mbar_wait(bar, ph);
+    double2 v[16];
+    W.gather(v, stage + (t < lines_ok ? t : 0) * 768, nv, lane);
+    __syncthreads();  // stage read by every warp: refill it with the next tile's rows
+    if (threadIdx.x == 0) prefetch(tix + gridDim.x);
+    W.forward(v, xr, lane);
+    __syncthreads();  // every exchange buffer is read out: the area becomes the tile
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
+      area[mtile_at<T>(p, t)] = v[i];
+      area[mtile_at<T>(p + 768, t)] = v[i + 8];
+    }
+    __syncthreads();  // all T spectra are in the tile
+    double2* const base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < a.out_nvalid * T; e += 96 * T) {
+      const int pos = e / T, tt = e % T;
+      if (tt < lines_ok) {
+        const double2 x = area[mtile_at<T>(pos, tt)];
+        const double2 y = (a.scale == 1.0) ? x : cscale(x, a.scale);
+        if (a.pm.n == 0) {
+          base[tt * a.out_si + pos * a.out_sp] = y;
+        } else {  // fused transpose: the segment goes straight to the rank owning it
+          const int q = a.pm.owner(a.pm.by_pos ? pos : i0 + tt);
+          a.pm.base[q][a.pm.off[q] + int64_t(i0 + tt) * a.out_si + int64_t(k) * a.pm.sk[q] + int64_t(pos) * a.out_sp] = y;
+        }
+      }
+    }
+    __syncthreads();  // the tile is read out before the next tile's exchanges
+  }
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
+}
+
+// ---------------------------------------------------------------------------- passes D / E
+// Column -> row (inverse, cropped output <= 768): a CTA of 3T warps; the [pos][T] column tiles
+// are double-buffered and filled by cp.async one tile ahead; each warp reads its residue's
+// spectrum from the tile, the exchanges and the t_r rows reuse the current tile, and the CTA
+// writes the T cropped rows with coalesced stores.
+template <int T>
+__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
+  using X3TSmem = fusg::X3TSmem<T>;
+  extern __shared__ double2 sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = w % 3, t = w / 3;
+  x3_tables(a.tw, sm + X3TSmem::C_TW, sm + X3TSmem::C_US, sm + X3TSmem::C_C48);
+  __syncthreads();
+  const X3Warp W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
+  const int ntiles_i = (a.n_inner + T - 1) / T;
+  const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
+  auto prefetch = [&](int64_t tix, double2* tile) {
+    if (tix < ntiles) {
+      const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+      const int k = int(unsigned(tix) / unsigned(ntiles_i));
+      const int lines_ok = min(T, a.n_inner - i0);
+      const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
+      for (int e = threadIdx.x; e < a.in_nvalid * T; e += 96 * T) {
+        const int pos = e / T, tt = e % T;
+        cp_async16_zfill(&tile[mtile_at<T>(pos, tt)], tt < lines_ok ? base + tt * a.in_si + pos * a.in_sp : a.in,
+                         tt < lines_ok);
+      }
+    }
+    cp_async_commit();
+  };
+  int64_t tix = blockIdx.x;
+  unsigned buf = 0;
+  prefetch(tix, sm);
+  for (; tix < ntiles; tix += gridDim.x, buf ^= 1) {
+    double2* const tile = sm + buf * (1536 * T);
+    const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+    const int k = int(unsigned(tix) / unsigned(ntiles_i));
+    const int lines_ok = min(T, a.n_inner - i0);
+    __syncthreads();  // the previous tile's t_r rows (in the other buffer) are read out
+    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (1536 * T));
+    cp_async_wait1();
+    __syncthreads();  // this tile's copies (issued by all threads) have landed
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int p = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
+      v[i] = p < a.in_nvalid ? tile[mtile_at<T>(p, t)] : make_double2(0.0, 0.0);
+      v[i + 8] = p + 768 < a.in_nvalid ? tile[mtile_at<T>(p + 768, t)] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();  // tile read by every warp: it becomes the exchange area
+    double2* const xr = tile + 512 * w;
+    W.inverse(v, xr, lane);
+    __syncwarp();
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
+    __syncthreads();  // all t_r rows are in the area
+    for (int e = threadIdx.x; e < 512 * T; e += 96 * T) {
+      const int tt = e >> 9, n = e & 511;
+      if (tt < lines_ok) {
+        const int line = i0 + tt;
+        double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
+        if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
+          const int q = a.pm.owner(line);
+          orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
+        }
+        const double2* x = tile + 512 * 3 * tt;
+        x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
+      }
+    }
+  }
+  cp_async_wait0();
+  if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
+}
+
+// pass C at L = 1536 (conv_r16x3): 1 launched, 0 not applicable, -1 error
+int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
+  static const bool on = [] {  // FUSG_CONV_R16X3=0 keeps the 64-lane radix (8, 8, 3, 8) pass C
+    const char* e = getenv("FUSG_CONV_R16X3");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on || a.in_nvalid < 1 || a.in_nvalid > 768 || a.out_nvalid > 768) return 0;
+  const int64_t nl = int64_t(a.n_inner) * a.n_outer;
+  if (nl >= (int64_t(1) << 31)) return 0;
+  const auto fn = conv_r16x3;
+  const size_t smem = X3Smem::BYTES;
+  static std::atomic<uint64_t> attr_mask{0};
+  if (!once_per_device(attr_mask, [&] {
+        return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) == cudaSuccess;
+      })) {
+    set_error(FUSG_CUDA, "pass C (1536 = 3 x 512): cannot configure shared memory");
+    return -1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 96, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  static const int waves = [] {  // CTAs per resident slot (1 = fully persistent)
+    const char* e = getenv("FUSG_X3_WAVES");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  const int64_t grid = std::min<int64_t>(nl, int64_t(per_sm) * ctx->num_sms * waves);
+  fn<<<unsigned(grid), 96, smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "pass C (1536 = 3 x 512)");
+    return -1;
+  }
+  return 1;
+}
+
+// passes A/B (r2c) or D/E at L = 1536: 1 launched, 0 not applicable, -1 error
+int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s) {
+  // FUSG_X3_T bitmask: 1 passes A/B, 2 passes D/E.  Default A/B only: at cfg5 the r2c kernel
+  // takes A 6.27 / B 10.64 ms against 6.75 / 13.59 for the 64-lane radix (8, 8, 3, 8) kernel,
+  // while this c2r kernel (12.9 / 7.2 ms) loses to it (11.6 / 6.37 ms).
+  static const int mask = [] {
+    const char* e = getenv("FUSG_X3_T");
+    return e ? atoi(e) : 1;
+  }();
+  if (!(mask & (r2c ? 1 : 2))) return 0;
+  if (r2c ? (a.in_nvalid > 768 || a.in_nvalid < 1 || a.in_sp != 1 || a.out_nvalid > 1536)
+          : (a.out_nvalid > 768 || a.out_sp != 1 || a.in_nvalid > 1536))
+    return 0;
+  // FUSG_X3_TL: lines per tile.  4 (default): one CTA of 12 warps per SM, 64-byte tile segments;
+  // 2: two CTAs of 6 warps per SM with 32-byte segments, measured 2x slower (A 13.4, B 25.7 ms).
+  static const int T = [] {
+    const char* e = getenv("FUSG_X3_TL");
+    return (e && atoi(e) == 2) ? 2 : 4;
+  }();
+  const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
+  if (tiles >= (int64_t(1) << 31)) return 0;
+  using Fn = void (*)(WArgs);
+  const Fn fn = T == 4 ? (r2c ? r16x3_row_to_col<4> : r16x3_col_to_row<4>)
+                       : (r2c ? r16x3_row_to_col<2> : r16x3_col_to_row<2>);
+  const size_t smem = T == 4 ? (r2c ? X3TSmem<4>::BYTES : X3TSmem<4>::C_BYTES)
+                             : (r2c ? X3TSmem<2>::BYTES : X3TSmem<2>::C_BYTES);
+  static std::atomic<uint64_t> attr_mask{0};
+  if (!once_per_device(attr_mask, [&] {
+        return cudaFuncSetAttribute(r16x3_row_to_col<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<4>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_row_to_col<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<2>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<2>::C_BYTES)) == cudaSuccess;
+      })) {
+    set_error(FUSG_CUDA, "transposing pass (1536 = 3 x 512): cannot configure shared memory");
+    return -1;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 96 * T, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  static const int waves = [] {  // FUSG_X3T_WAVES: CTAs per resident slot
+    const char* e = getenv("FUSG_X3T_WAVES");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * waves);
+  fn<<<unsigned(grid), 96 * T, smem, s>>>(a);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "transposing pass (1536 = 3 x 512)");
+    return -1;
+  }
+  return 1;
+}
+
+}  // namespace fusg

@@ -1308,7 +1308,8 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
     if (r2c || c2r) {
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
-      int r = pl.L == 512 ? launch_transpose_r16(ctx, r2c, wa, s) : 0;
+      int r = pl.L == 512 ? launch_transpose_r16(ctx, r2c, wa, s)
+              : pl.L == 1536 ? launch_transpose_r16x3(ctx, r2c, wa, s) : 0;
       if (r == 0) r = launch_mw(ctx, pl.L, r2c, wa, s);
       if (r == 0) r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
       if (r < 0) return FUSG_CUDA;
@@ -1377,7 +1378,8 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
   if (ld.g.sp == 1 && st.g.sp == 1 && ko.s_kz == 1) {
     const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                    st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, ko};
-    int r = launch_conv64(ctx, pl.L, wa, s);
+    int r = pl.L == 1536 ? launch_conv_r16x3(ctx, wa, s) : 0;
+    if (r == 0) r = launch_conv64(ctx, pl.L, wa, s);
     if (r == 0) r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
     if (r < 0) return FUSG_CUDA;
     if (r > 0) return FUSG_OK;
@@ -1549,7 +1551,8 @@ fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap&
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   WArgs a{f, Nx, int64_t(Ny) * Nx, 1, Nx, nullptr, 1, Ny, int64_t(Nz) * Ny, K->P[0], 1.0,
           Ny, K->nz, K->plan[0].tw, KOct{}, pm};
-  int r = K->P[0] == 512 ? launch_transpose_r16(K->ctx, true, a, s) : 0;
+  int r = K->P[0] == 512 ? launch_transpose_r16(K->ctx, true, a, s)
+          : K->P[0] == 1536 ? launch_transpose_r16x3(K->ctx, true, a, s) : 0;
   if (r == 0) r = launch_mw(K->ctx, K->P[0], true, a, s);
   if (r == 0) r = launch_warp(K->ctx, K->P[0], kWRowToCol, false, a, s);
   if (r < 0) return FUSG_CUDA;
@@ -1562,7 +1565,8 @@ fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t 
   const int Py = K->P[1];
   const int64_t PyNz = int64_t(Py) * Nz;
   WArgs a{K->bufB, 1, PyNz, Nz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
-  int r = Py == 512 ? launch_transpose_r16(K->ctx, false, a, s) : 0;
+  int r = Py == 512 ? launch_transpose_r16(K->ctx, false, a, s)
+          : Py == 1536 ? launch_transpose_r16x3(K->ctx, false, a, s) : 0;
   if (r == 0) r = launch_mw(K->ctx, Py, false, a, s);
   if (r == 0) r = launch_warp(K->ctx, Py, kWColToRow, true, a, s);
   if (r < 0) return FUSG_CUDA;

@@ -99,6 +99,9 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   # Nx / Ny = 512, 768, 1024: Px / Py = 1024, 1536, 2048 (multi-
                                   # warp-line transposing passes; ragged T-line tiles)
                                   (512, 5, 3), (3, 512, 4), (768, 3, 2), (2, 768, 3),
+                                  # Px / Py / Pz = 1536 = 3 x 512 kernels with fewer valid
+                                  # positions and ragged 4-line tiles
+                                  (700, 5, 3), (3, 650, 5), (601, 7, 2), (6, 5, 700), (9, 2, 601),
                                   (1024, 2, 2), (2, 1024, 2),
                                   # Nx / Ny in (128, 256]: Px / Py = 512 (16x16x2 transposing passes)
                                   (200, 3, 2), (3, 230, 4), (256, 7, 3),

@@ -69,8 +69,7 @@ def main():
     k = fus.Wavenumber(complex(2 * math.pi * f0 / c, 0.0), 1, 2 * math.pi * f0)
     res["cfg1"] = apply_rate(g, k, fus.random_vector(g.count(), 1234), 200)
     # cfg2: the bench workload
-    bench.N_SIDE = 256
-    g, k, f = bench.cfg2_inputs()
+    g, k, f = bench.gpu_inputs(bench.CFG2)
     res["cfg2"] = apply_rate(g, k, f, 100)
     # cfg5: 768^3 at 6 points per wavelength (harmonic-1 wavenumber), iid U[-1, 1]
     h = (c / f0) / 6.0

@@ -5,7 +5,7 @@ import torch
 import bench
 from paper_2011_03009_b200 import _lib, fus
 
-g, k, f = bench.cfg2_inputs()
+g, k, f = bench.gpu_inputs(bench.CFG2)
 K = fus.GreenKernel(g, k)
 fh = torch.from_numpy(f).pin_memory()
 uh = torch.empty_like(fh).pin_memory()

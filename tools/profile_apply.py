@@ -11,8 +11,7 @@ from paper_2011_03009_b200 import fus  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-bench.N_SIDE = n
-g, k, f = bench.cfg2_inputs()
+g, k, f = bench.gpu_inputs(bench.CFG2 if n == 256 else dict(bench.CFG5, n=n))
 K = fus.GreenKernel(g, k)
 fd = torch.from_numpy(f).cuda()
 u = None

@@ -12,7 +12,7 @@ from paper_2011_03009_b200 import _lib, fus  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 ctx = fus.context(0)
-g, k, f = bench.cfg2_inputs()
+g, k, f = bench.gpu_inputs(bench.CFG2)
 K = fus.GreenKernel(g, k, ctx=ctx)
 fd = torch.from_numpy(f).cuda()
 ud = torch.empty_like(fd)

@@ -2,7 +2,7 @@ import os, sys, json
 sys.path.insert(0, os.getcwd())
 import torch, bench
 from paper_2011_03009_b200 import _lib, fus
-g, k, f = bench.cfg2_inputs()
+g, k, f = bench.gpu_inputs(bench.CFG2)
 K = fus.GreenKernel(g, k)
 fd = torch.from_numpy(f).cuda(); ud = torch.empty_like(fd)
 L = _lib.lib(); ctx = K.ctx
