@@ -28,35 +28,44 @@ namespace fusg {
 template <bool CONJ>
 __device__ __forceinline__ void r16_twiddle_u(double2* v, double2 u, double2 w1, double2 w2, double2 w4, double2 w8) {
   auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
-  const double2 p1 = cmul(u, w1), p2 = cmul(u, w2), p4 = cmul(u, w4), p8 = cmul(u, w8);
-  const double2 p3 = cmul(p1, w2), p5 = cmul(p1, w4), p6 = cmul(p2, w4), p7 = cmul(p3, w4);
+  // each power p_k = u W512^(lane k) is applied to v[k] and, times w8, to v[k + 8] as soon as it
+  // exists, so few products are live at once
   v[0] = m(v[0], u);
-  v[1] = m(v[1], p1);
-  v[2] = m(v[2], p2);
-  v[3] = m(v[3], p3);
-  v[4] = m(v[4], p4);
-  v[5] = m(v[5], p5);
-  v[6] = m(v[6], p6);
-  v[7] = m(v[7], p7);
+  const double2 p8 = cmul(u, w8);
   v[8] = m(v[8], p8);
+  const double2 p1 = cmul(u, w1);
+  v[1] = m(v[1], p1);
   v[9] = m(v[9], cmul(p1, w8));
+  const double2 p2 = cmul(u, w2);
+  v[2] = m(v[2], p2);
   v[10] = m(v[10], cmul(p2, w8));
-  v[11] = m(v[11], cmul(p3, w8));
+  const double2 p4 = cmul(u, w4);
+  v[4] = m(v[4], p4);
   v[12] = m(v[12], cmul(p4, w8));
+  const double2 p3 = cmul(p1, w2);
+  v[3] = m(v[3], p3);
+  v[11] = m(v[11], cmul(p3, w8));
+  const double2 p5 = cmul(p1, w4);
+  v[5] = m(v[5], p5);
   v[13] = m(v[13], cmul(p5, w8));
+  const double2 p6 = cmul(p2, w4);
+  v[6] = m(v[6], p6);
   v[14] = m(v[14], cmul(p6, w8));
+  const double2 p7 = cmul(p3, w4);
+  v[7] = m(v[7], p7);
   v[15] = m(v[15], cmul(p7, w8));
 }
 
 // shared-memory layout (double2 offsets) of one CTA
+template <bool STAGED = true>
 struct X3Smem {
   static constexpr int XB = 0;             // [3][512] exchange buffers, then the t_r rows
-  static constexpr int SB = 1536;          // staged input row (<= 768 positions)
-  static constexpr int KB = SB + 768;      // folded K^ row (769, padded to 770)
+  static constexpr int KB = 1536;          // folded K^ row (769, padded to 770)
   static constexpr int TW = KB + 770;      // [4][32] W512^(lane 2^j)
   static constexpr int US = TW + 128;      // [3][32] W1536^(lane r)
   static constexpr int C48 = US + 96;      // [48] W48^j
-  static constexpr int END = C48 + 48;
+  static constexpr int SB = C48 + 48;      // staged input row (<= 768 positions), if staged
+  static constexpr int END = SB + (STAGED ? 768 : 0);
   static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
 };
 
@@ -148,13 +157,19 @@ __device__ __forceinline__ void x3_tables(const double2* tw1536, double2* tws, d
   for (int e = threadIdx.x; e < 48; e += blockDim.x) c48[e] = __ldg(tw1536 + 32 * e);
 }
 
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 // ---------------------------------------------------------------------------- pass C
 // CTA of three warps, persistent over lines; the input and K^ rows are staged by 1-D bulk
 // copies one line ahead (the refill is issued after a CTA barrier: measured faster than
 // letting the warps drift apart with last-arriver refills or producer / consumer barriers,
 // 29.8 vs 32.8-33.6 ms at cfg5).
-__global__ void __launch_bounds__(96, 4) conv_r16x3(WArgs a) {
+// STAGED = false: the input row is read straight from global memory (prefetched into L2 one
+// line ahead), which frees 12 KB per CTA for a fifth CTA (15 warps) per SM.
+template <bool STAGED>
+__global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
   constexpr int HZ = 769;
+  using X3Smem = fusg::X3Smem<STAGED>;
   extern __shared__ double2 sm[];
   const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + X3Smem::XB;
@@ -180,7 +195,13 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3(WArgs a) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
-      bulk_stage(sb, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(a.in_nvalid) * sizeof(double2), bars);
+      const double2* src = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
+      if constexpr (STAGED) {
+        bulk_stage(sb, src, unsigned(a.in_nvalid) * sizeof(double2), bars);
+      } else {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(unsigned(a.in_nvalid) * 16u)
+                     : "memory");
+      }
     }
   };
   auto prefetch_k = [&](int64_t line) {
@@ -198,9 +219,15 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3(WArgs a) {
   }
   unsigned ph = 0;  // both staging barriers complete once per line
   for (; line < nlines; line += stride, ph ^= 1) {
-    mbar_wait(bars, ph);
     double2 v[16];
-    W.gather(v, sb, nv, lane);
+    if constexpr (STAGED) {
+      mbar_wait(bars, ph);
+      W.gather(v, sb, nv, lane);
+    } else {
+      int ky, kx;
+      coords(line, ky, kx);
+      W.gather(v, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, nv, lane);
+    }
     __syncthreads();  // the staged row is read by all three warps: refill it
     if (threadIdx.x == 0) prefetch_in(line + stride);
     W.forward(v, xr, lane);
@@ -223,7 +250,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3(WArgs a) {
     coords(line, ky, kx);
     double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
     for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + 512, xb + 1024, n, onv, a.scale, out);
-    __syncthreads();  // the t_r rows are read: the exchange buffers may be rewritten
+    // (the next line's staging barrier orders these reads before its exchange writes)
   }
 }
 
@@ -316,7 +343,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
         }
       }
     }
-    __syncthreads();  // the tile is read out before the next tile's exchanges
+    // (the next tile's staging barrier orders these reads before its exchange writes)
   }
   if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
@@ -359,10 +386,9 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
     const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
     const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
-    __syncthreads();  // the previous tile's t_r rows (in the other buffer) are read out
-    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (1536 * T));
-    cp_async_wait1();
-    __syncthreads();  // this tile's copies (issued by all threads) have landed
+    cp_async_wait0();
+    __syncthreads();  // this tile's copies (issued by all threads) have landed; the previous
+                      // tile's t_r rows (other buffer) are read out
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -371,24 +397,23 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
       v[i + 8] = p + 768 < a.in_nvalid ? tile[mtile_at<T>(p + 768, t)] : make_double2(0.0, 0.0);
     }
     __syncthreads();  // tile read by every warp: it becomes the exchange area
+    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (1536 * T));
     double2* const xr = tile + 512 * w;
     W.inverse(v, xr, lane);
     __syncwarp();
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
-    __syncthreads();  // all t_r rows are in the area
-    for (int e = threadIdx.x; e < 512 * T; e += 96 * T) {
-      const int tt = e >> 9, n = e & 511;
-      if (tt < lines_ok) {
-        const int line = i0 + tt;
-        double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
-        if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
-          const int q = a.pm.owner(line);
-          orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
-        }
-        const double2* x = tile + 512 * 3 * tt;
-        x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
+    nbar_sync(1 + t, 96);  // line t's three t_r rows are in the area
+    if (t < lines_ok) {
+      const int line = i0 + t;
+      double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
+      if (a.pm.n) {  // fused transpose: the row goes straight to the rank owning line (z)
+        const int q = a.pm.owner(line);
+        orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
       }
+      const double2* x = tile + 512 * 3 * t;
+      for (int n = threadIdx.x - 96 * t; n < 512; n += 96)
+        x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
     }
   }
   cp_async_wait0();
@@ -404,11 +429,19 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   if (!on || a.in_nvalid < 1 || a.in_nvalid > 768 || a.out_nvalid > 768) return 0;
   const int64_t nl = int64_t(a.n_inner) * a.n_outer;
   if (nl >= (int64_t(1) << 31)) return 0;
-  const auto fn = conv_r16x3;
-  const size_t smem = X3Smem::BYTES;
+  static const bool staged = [] {  // FUSG_X3_STAGED=0: input rows from L2 (5 CTAs per SM)
+    const char* e = getenv("FUSG_X3_STAGED");
+    return !(e && atoi(e) == 0);
+  }();
+  const auto fn = staged ? conv_r16x3<true> : conv_r16x3<false>;
+  // unstaged: the staging row is not allocated (it is the last region before the tables)
+  const size_t smem = staged ? X3Smem<true>::BYTES : X3Smem<false>::BYTES;
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
-        return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) == cudaSuccess;
+        return cudaFuncSetAttribute(conv_r16x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<true>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(conv_r16x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<false>::BYTES)) == cudaSuccess;
       })) {
     set_error(FUSG_CUDA, "pass C (1536 = 3 x 512): cannot configure shared memory");
     return -1;
@@ -435,12 +468,12 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
 
 // passes A/B (r2c) or D/E at L = 1536: 1 launched, 0 not applicable, -1 error
 int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s) {
-  // FUSG_X3_T bitmask: 1 passes A/B, 2 passes D/E.  Default A/B only: at cfg5 the r2c kernel
-  // takes A 6.27 / B 10.64 ms against 6.75 / 13.59 for the 64-lane radix (8, 8, 3, 8) kernel,
-  // while this c2r kernel (12.9 / 7.2 ms) loses to it (11.6 / 6.37 ms).
+  // FUSG_X3_T bitmask: 1 passes A/B, 2 passes D/E (default both).  At cfg5: A 6.3 / B 10.5 /
+  // D 10.9 / E 6.35 ms against 6.75 / 13.6 / 11.6 / 6.37 for the 64-lane radix (8, 8, 3, 8)
+  // kernels.
   static const int mask = [] {
     const char* e = getenv("FUSG_X3_T");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 3;
   }();
   if (!(mask & (r2c ? 1 : 2))) return 0;
   if (r2c ? (a.in_nvalid > 768 || a.in_nvalid < 1 || a.in_sp != 1 || a.out_nvalid > 1536)
