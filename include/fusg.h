@@ -91,6 +91,9 @@ double fusg_equivalent_sphere_radius(double dx);
 /* next_fast_size (src/potential.cpp:36-43) and the padded box the device path uses. */
 int32_t fusg_next_fast_size(int32_t n);
 fusg_status fusg_padded_dims(const fusg_grid* g, int32_t pad_small_primes, int32_t out[3]);
+/* Padded lengths with compile-time-planned kernels (conv = 0: x / y passes, 1: z pass C),
+ * ascending; writes up to cap of them to out and returns how many exist. */
+int32_t fusg_static_lengths(int32_t conv, int32_t* out, int32_t cap);
 /* distribute_points (src/transducer.cpp:22-70): out_host is n_points x 3. */
 fusg_status fusg_distribute_points(double focal_length, double outer_radius, int32_t n_points,
                                    double* out_host);

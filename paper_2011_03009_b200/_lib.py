@@ -73,6 +73,7 @@ SIGNATURES = {
     "fusg_equivalent_sphere_radius": (C.c_double, [C.c_double]),
     "fusg_next_fast_size": (C.c_int32, [C.c_int32]),
     "fusg_padded_dims": (C.c_int, [C.POINTER(Grid), C.c_int32, C.POINTER(C.c_int32)]),
+    "fusg_static_lengths": (C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.c_int32]),
     "fusg_distribute_points": (C.c_int, [C.c_double, C.c_double, C.c_int32, _dp]),
     "fusg_plan_nested_meshes": (C.c_int, [C.POINTER(Bowl), C.POINTER(MediumC), C.c_double, C.c_int32,
                                           C.c_int32, C.c_double, C.c_int32, C.POINTER(Grid), _dp, _dp,

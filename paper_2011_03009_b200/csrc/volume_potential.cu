@@ -311,6 +311,15 @@ static const std::vector<int>& static_lengths(bool conv) {
   return lens[conv ? 1 : 0];
 }
 
+}  // namespace fusg
+
+extern "C" int32_t fusg_static_lengths(int32_t conv, int32_t* out, int32_t cap) {
+  const auto& v = fusg::static_lengths(conv != 0);
+  for (int32_t i = 0; out && i < cap && i < int32_t(v.size()); ++i) out[i] = v[size_t(i)];
+  return int32_t(v.size());
+}
+
+namespace fusg {
 // ---------------------------------------------------------------------------- warp engine
 // Warp-per-line kernels (fft_warp.cuh) for L <= 512: rows (x passes) are read and written
 // straight from global memory by their own lane group; columns (y, z passes) are staged as a

@@ -316,6 +316,14 @@ class GreenKernel:
             pass
 
 
+def static_lengths(conv: bool = False) -> list:
+    """Padded lengths with compile-time-planned kernels (x/y passes, or pass C on z)."""
+    n = int(lib().fusg_static_lengths(int(conv), None, 0))
+    out = (C.c_int32 * n)()
+    lib().fusg_static_lengths(int(conv), out, n)
+    return list(out)
+
+
 def padded_dims(grid: VoxelGrid, pad_small_primes: bool = False) -> tuple:
     out = (C.c_int32 * 3)()
     g = grid.c()

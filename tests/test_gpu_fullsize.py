@@ -1,7 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, where the CPU oracle cannot run the whole problem.
 
 * cfg5: one 768^3 apply (1536^3 embedding, the L = 1536 kernels) against the oracle's direct sum
-  (direct_potential_oracle, src/potential.cpp:203-238) at sampled voxels, plus the exact
+  (direct_potential_oracle, src/potential.cpp:203-238) at >= 64 sampled voxels (corners, face
+  centres, random interior), plus the exact
   scaling property apply(2 f) == 2 apply(f) bit for bit.
 * cfg3: the full uniform-grid 3-harmonic recursion (1.2e8 voxels, 4096 sources). Each stage is
   checked given the device's previous stage, so errors cannot hide behind each other:
@@ -33,9 +34,15 @@ def ctx():
     return fus.context(0)
 
 
-def _sample(count, n, seed):
+def _sample(dims, n, seed):
+    """Flat indices of the 8 corners, the 6 face centres, the centre and n random voxels."""
+    nx, ny, nz = dims
+    pts = [(x, y, z) for x in (0, nx - 1) for y in (0, ny - 1) for z in (0, nz - 1)]
+    pts += [(0, ny // 2, nz // 2), (nx - 1, ny // 2, nz // 2), (nx // 2, 0, nz // 2), (nx // 2, ny - 1, nz // 2),
+            (nx // 2, ny // 2, 0), (nx // 2, ny // 2, nz - 1), (nx // 2, ny // 2, nz // 2)]
     rng = np.random.default_rng(seed)
-    return np.unique(np.concatenate([[0, count - 1, count // 2], rng.integers(0, count, n)]))
+    ijk = np.concatenate([np.array(pts), rng.integers(0, [nx, ny, nz], size=(n, 3))])
+    return np.unique(ijk[:, 0] + nx * (ijk[:, 1] + ny * ijk[:, 2]))
 
 
 def _close(got, ref, tol=1e-10):
@@ -58,7 +65,8 @@ def test_cfg5_768cubed_apply_at_sampled_voxels(ctx, orc):
     u = K.apply(fd)
     # exact: scaling the source by 2 scales every rounding step by 2
     assert torch.equal(K.apply(fd * 2.0), u * 2.0)
-    idx = _sample(g.count(), 3, 7)
+    idx = _sample(g.dims, 56, 7)
+    assert idx.size >= 64
     got = u[torch.from_numpy(idx).cuda()].cpu().numpy()
     del u, fd
     go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 1)
@@ -77,7 +85,8 @@ def test_cfg3_full_cascade_stage_by_stage(ctx, orc):
     assert k1o.k.imag > 0.0  # attenuating water: the complex-k paths
     assert r.source_normalization == pytest.approx(orc.power_scale_factor(to, medo, k1o), rel=1e-12)
     go = orc.VoxelGrid(g.lo, g.hi, g.dx, g.dims, 2)
-    idx = _sample(g.count(), 5, 11)
+    idx = _sample(g.dims, 56, 11)
+    assert idx.size >= 64
     ix, iy, iz = idx % g.dims[0], (idx // g.dims[0]) % g.dims[1], idx // (g.dims[0] * g.dims[1])
     pts = np.stack([g.lo[0] + (ix + 0.5) * g.dx, g.lo[1] + (iy + 0.5) * g.dx, g.lo[2] + (iz + 0.5) * g.dx], 1)
     sel = torch.from_numpy(idx).cuda()
