@@ -290,10 +290,14 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
   if (!pinned) {
     if (!K->ring) {
       auto* r = new PinnedRing;
+      // FUSG_HOST_THREADS: copy threads (default: every hardware thread, up to 32);
+      // FUSG_HOST_SLOT_MB: pinned slot size (4 slots)
       const char* env_t = getenv("FUSG_HOST_THREADS");
+      const char* env_s = getenv("FUSG_HOST_SLOT_MB");
       const int hw = int(std::thread::hardware_concurrency());
-      const int nt = env_t ? std::max(1, atoi(env_t)) : std::max(1, std::min(8, hw / 2));
-      if (r->init(4, size_t(32) << 20, nt) != cudaSuccess) {
+      const int nt = env_t ? std::max(1, atoi(env_t)) : std::max(1, std::min(32, hw));
+      const size_t slot_mb = env_s ? size_t(std::max(1, atoi(env_s))) : 64;
+      if (r->init(4, slot_mb << 20, nt) != cudaSuccess) {
         cudaGetLastError();
         r->destroy();
         delete r;

@@ -7,10 +7,15 @@
 // the caller's vector into one slot of a ring of pinned buffers (several threads, so the copy
 // keeps up with PCIe), one cudaMemcpyAsync moves the slot, and the slot is reused once the
 // event recorded after its DMA has completed.  Device-to-host runs the same ring backwards.
+// Measured at cfg5 (7.25 GB each way, 16 host threads): 0.40 s per apply against 0.30 s for
+// pinned buffers.  The staged path moves every byte through host memory three times (read the
+// caller's vector, write the slot, DMA read) against once, and the copy threads saturate at
+// ~36 GB/s (non-temporal stores measured no faster).
 #pragma once
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
@@ -32,6 +37,7 @@ class CopyPool {
       std::lock_guard<std::mutex> g(m_);
       stop_ = true;
       ++gen_;
+      gen_atomic_.store(gen_, std::memory_order_release);
     }
     cv_.notify_all();
     for (auto& t : th_) t.join();
@@ -48,6 +54,7 @@ class CopyPool {
       bytes_ = bytes;
       pending_ = n_ - 1;
       ++gen_;
+      gen_atomic_.store(gen_, std::memory_order_release);
     }
     cv_.notify_all();
     part(0);
@@ -65,6 +72,9 @@ class CopyPool {
   void worker(int i) {
     unsigned long long seen = 0;
     for (;;) {
+      // spin briefly (back-to-back slots of one apply arrive within microseconds), then block
+      for (int spin = 0; spin < 20000 && gen_atomic_.load(std::memory_order_acquire) == seen; ++spin) {
+      }
       {
         std::unique_lock<std::mutex> lk(m_);
         cv_.wait(lk, [&] { return gen_ != seen; });
@@ -83,6 +93,7 @@ class CopyPool {
   std::mutex m_;
   std::condition_variable cv_, done_cv_;
   unsigned long long gen_ = 0;
+  std::atomic<unsigned long long> gen_atomic_{0};
   bool stop_ = false;
   char* dst_ = nullptr;
   const char* src_ = nullptr;
