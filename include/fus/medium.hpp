@@ -33,5 +33,7 @@ double attenuation_np_per_m(const Medium& medium, double f_hz);
 Wavenumber complex_wavenumber(const Medium& medium, double f0, int n);
 Medium medium_preset(const std::string& name);
 bool is_medium_preset(const std::string& name);
+// key=value config file with keys name, rho0, c0, beta, alpha0, eta (src/medium.cpp:58-69)
+Medium load_medium(const std::string& path);
 
 }  // namespace fus

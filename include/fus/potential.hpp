@@ -47,5 +47,10 @@ class GreenKernel {
 Eigen::VectorXcd evaluate_potential_at(const Wavenumber& k, const VoxelGrid& grid,
                                        const Eigen::VectorXcd& f,
                                        const std::vector<Eigen::Vector3d>& points);
+// The O(N^2) quadrature the FFT path is checked against (src/potential.cpp:203-238), guarded to
+// grids of at most 1e5 voxels; here it runs on the device (the off-grid kernel at every voxel
+// centre, where the coincident point takes the self term).
+Eigen::VectorXcd direct_potential_oracle(const Wavenumber& k, const VoxelGrid& grid,
+                                         const Eigen::VectorXcd& f);
 
 }  // namespace fus

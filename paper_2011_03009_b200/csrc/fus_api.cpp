@@ -303,6 +303,18 @@ Eigen::VectorXcd evaluate_potential_at(const Wavenumber& k, const VoxelGrid& gri
   return out;
 }
 
+Eigen::VectorXcd direct_potential_oracle(const Wavenumber& k, const VoxelGrid& grid, const Eigen::VectorXcd& f) {
+  if (grid.count() > 100000)
+    throw std::invalid_argument("direct_potential_oracle: grid exceeds the 1e5 voxel guard");
+  if (f.size() != Eigen::Index(grid.count()))
+    throw std::invalid_argument("direct_potential_oracle: field size mismatch");
+  std::vector<Eigen::Vector3d> centres(grid.count());
+  for (int iz = 0; iz < grid.dims.z(); ++iz)
+    for (int iy = 0; iy < grid.dims.y(); ++iy)
+      for (int ix = 0; ix < grid.dims.x(); ++ix) centres[grid.index(ix, iy, iz)] = grid.center(ix, iy, iz);
+  return evaluate_potential_at(k, grid, f, centres);
+}
+
 // ------------------------------------------------------------------------------ transducer
 double BowlTransducer::cap_area() const {
   const double l = focal_length, R = outer_radius;

@@ -2,11 +2,14 @@
 // file contracts (src/io.cpp) -- written here from those contracts.
 #include <cstdio>
 #include <fstream>
+#include <iostream>
 #include <stdexcept>
 #include <string>
 
 #include "fus/grid.hpp"
 #include "fus/io.hpp"
+#include "fus/medium.hpp"
+#include "fus/transducer.hpp"
 #include "fus/vie.hpp"
 
 namespace fus {
@@ -149,6 +152,32 @@ void write_medium_map(const std::string& header_path, const std::string& raster_
     const double pair[2] = {map.c[i], map.beta[i]};
     out.write(reinterpret_cast<const char*>(pair), sizeof(pair));
   }
+}
+
+// Medium / transducer config files (src/medium.cpp:58-69, src/transducer.cpp:94-102): the same
+// keys, the same missing-key and malformed-number errors (require_*), and the medium's
+// validation warnings on stderr.
+Medium load_medium(const std::string& path) {
+  const auto kv = parse_key_value_file(path);
+  Medium m;
+  m.name = require_string(kv, "name", path);
+  m.rho0 = require_double(kv, "rho0", path);
+  m.c0 = require_double(kv, "c0", path);
+  m.beta = require_double(kv, "beta", path);
+  m.alpha0 = require_double(kv, "alpha0", path);
+  m.eta = require_double(kv, "eta", path);
+  for (const auto& w : m.validate()) std::cerr << "warning: " << w << "\n";
+  return m;
+}
+
+BowlTransducer load_transducer(const std::string& path, double power) {
+  const auto kv = parse_key_value_file(path);
+  const std::string name = require_string(kv, "name", path);
+  const double f0 = require_double(kv, "f0", path);
+  const double l = require_double(kv, "focal_length", path);
+  const double R = require_double(kv, "outer_radius", path);
+  const int n_points = int(require_double(kv, "n_points", path));
+  return make_bowl(name, f0, l, R, power, n_points);
 }
 
 }  // namespace fus

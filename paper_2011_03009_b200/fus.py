@@ -98,6 +98,17 @@ class Medium:
     def c(self):
         return _lib.MediumC(self.rho0, self.c0, self.beta, self.alpha0, self.eta)
 
+    def validate(self) -> list:
+        """src/medium.cpp:11-23: ValueError for impossible values, warnings otherwise."""
+        for key, bad, what in (("rho0", self.rho0 <= 0.0, "must be positive"), ("c0", self.c0 <= 0.0, "must be positive"),
+                               ("beta", self.beta < 0.0, "must be non-negative"),
+                               ("alpha0", self.alpha0 < 0.0, "must be non-negative")):
+            if bad:
+                raise ValueError(f"medium '{self.name}': {key} {what}")
+        if self.eta < 1.0 or self.eta > 2.0:
+            return [f"medium '{self.name}': power-law exponent eta={self.eta:f} is outside the typical range [1, 2]"]
+        return []
+
 
 @dataclass
 class Wavenumber:
@@ -124,6 +135,17 @@ def medium_preset(name: str) -> Medium:
 
 def is_medium_preset(name: str) -> bool:
     return name in ("water", "liver", "kidney")
+
+
+def load_medium(path: str) -> Medium:
+    """src/medium.cpp:58-69: key=value file with name, rho0, c0, beta, alpha0, eta."""
+    kv = parse_key_value_file(path)
+    m = Medium(require_string(kv, "name", path), require_double(kv, "rho0", path), require_double(kv, "c0", path),
+               require_double(kv, "beta", path), require_double(kv, "alpha0", path), require_double(kv, "eta", path))
+    import sys as _sys
+    for w in m.validate():
+        print(f"warning: {w}", file=_sys.stderr)
+    return m
 
 
 def complex_wavenumber(m: Medium, f0: float, n: int) -> Wavenumber:
@@ -236,6 +258,21 @@ def evaluate_potential_at(k: Wavenumber, grid: VoxelGrid, f, points, ctx: Option
     check(lib().fusg_evaluate_potential_at(ctx.handle, C.byref(g), C.byref(w), fd.data_ptr(),
                                            pts.ctypes.data, len(pts), out.ctypes.data))
     return out
+
+
+def direct_potential_oracle(k: Wavenumber, grid: VoxelGrid, f, ctx: Optional["Context"] = None) -> np.ndarray:
+    """src/potential.cpp:203-238: the O(N^2) quadrature at every voxel centre (guarded to 1e5
+    voxels), run on the device through the off-grid kernel (the coincident point takes the
+    self term)."""
+    if grid.count() > 100000:
+        raise ValueError("direct_potential_oracle: grid exceeds the 1e5 voxel guard")
+    size = f.numel() if torch is not None and isinstance(f, torch.Tensor) else np.size(f)
+    if size != grid.count():
+        raise ValueError("direct_potential_oracle: field size mismatch")
+    ax = [grid.lo[a] + (np.arange(grid.dims[a]) + 0.5) * grid.dx for a in range(3)]
+    z, y, x = np.meshgrid(ax[2], ax[1], ax[0], indexing="ij")
+    pts = np.stack([x.reshape(-1), y.reshape(-1), z.reshape(-1)], 1)
+    return evaluate_potential_at(k, grid, f, pts, ctx)
 
 
 def next_fast_size(n: int) -> int:
@@ -368,6 +405,14 @@ def distribute_points(l: float, R: float, n: int) -> np.ndarray:
     check(lib().fusg_distribute_points(float(l), float(R), int(n),
                                        out.ctypes.data_as(C.POINTER(C.c_double))))
     return out.reshape(-1, 3)
+
+
+def load_transducer(path: str, power: float) -> "BowlTransducer":
+    """src/transducer.cpp:94-102: key=value file with name, f0, focal_length, outer_radius, n_points."""
+    kv = parse_key_value_file(path)
+    return make_bowl(require_string(kv, "name", path), require_double(kv, "f0", path),
+                     require_double(kv, "focal_length", path), require_double(kv, "outer_radius", path), power,
+                     int(require_double(kv, "n_points", path)))
 
 
 def make_bowl(name, f0, l, R, power, n_points) -> BowlTransducer:

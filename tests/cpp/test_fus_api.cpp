@@ -3,6 +3,7 @@
 // libfus.so -> libfusg.so.  `test_fus_api host` runs the host-arithmetic cases (no GPU);
 // `test_fus_api all` adds the device cases.
 #include <Eigen/Dense>
+#include <cuda_runtime.h>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -421,6 +422,111 @@ void device_cases() {
   }
 }
 
+// Every declaration of the drop-in headers not exercised above, as a reference user calls it:
+// host-side ones always, device-side ones with `all`.
+void surface_host_cases() {
+  // medium / transducer presets, validation and config-file loaders (src/medium.cpp:47-69,
+  // src/transducer.cpp:86-102)
+  CHECK(fus::is_medium_preset("liver") && !fus::is_medium_preset("bone"));
+  CHECK(fus::is_transducer_preset("H101") && !fus::is_transducer_preset("H999"));
+  CHECK(std::fabs(fus::attenuation_np_per_m(kWater, 2.0e6) - 0.2 * 4.0 / fus::kDbPerNeper) < 1e-15);
+  {
+    const std::string mp = "/tmp/fus_api_medium.cfg", tp = "/tmp/fus_api_bowl.cfg";
+    std::ofstream(mp) << "# tissue\nname = tissue\nrho0 = 1050\nc0 = 1540\nbeta = 4.5\nalpha0 = 0.5\neta = 1.1\n";
+    std::ofstream(tp) << "name = bowl\nf0 = 1e6\nfocal_length = 0.04\nouter_radius = 0.02\nn_points = 128\n";
+    const fus::Medium m = fus::load_medium(mp);
+    CHECK(m.name == "tissue" && m.rho0 == 1050.0 && m.c0 == 1540.0 && m.beta == 4.5 && m.alpha0 == 0.5 && m.eta == 1.1);
+    CHECK(m.validate().empty());
+    const fus::BowlTransducer t = fus::load_transducer(tp, 12.5);
+    const fus::BowlTransducer u = fus::make_bowl("bowl", 1e6, 0.04, 0.02, 12.5, 128);
+    CHECK(t.name == "bowl" && t.power == 12.5 && t.source_points.size() == 128);
+    CHECK(t.source_points[77] == u.source_points[77]);
+    CHECK(std::fabs(t.cap_area() - 2.0 * M_PI * 0.04 * t.rim_plane_x()) < 1e-18);
+    std::ofstream(mp) << "name = broken\nrho0 = 1050\n";
+    CHECK_THROWS_AS(fus::load_medium(mp), std::runtime_error);
+    fus::Medium bad = kWater;
+    bad.c0 = -1.0;
+    CHECK_THROWS_AS(bad.validate(), std::invalid_argument);
+  }
+  // reference domain and the single-mesh plan (src/grid.cpp:70-79, src/cascade.cpp:109-118)
+  {
+    const fus::BowlTransducer t = fus::transducer_preset("H131");
+    const fus::DomainBox d2 = fus::reference_domain(t, 10.2e-3);
+    CHECK(d2.contains(t.focus()) && d2.extent().x() > 0.0);
+    const fus::MeshPlan single = fus::plan_single_mesh(t, kWater, 10.2e-3, 6, 3);
+    for (int n = 2; n <= 3; ++n) CHECK(single.for_harmonic(n).grid.dims == single.for_harmonic(2).grid.dims);
+  }
+}
+
+void surface_device_cases() {
+  const fus::BowlTransducer t = [] {
+    fus::BowlTransducer b = fus::transducer_preset("H131", 20.0, 256);
+    b.f0 = 0.25e6;
+    return b;
+  }();
+  const fus::MeshPlan plan = fus::plan_nested_meshes(t, kWater, 6e-3, 3, 3, 0.35);
+  const fus::VoxelGrid g2 = plan.for_harmonic(2).grid;
+  // source field, power normalisation, first harmonic (src/transducer.cpp:179-206)
+  const fus::SourceField sf = fus::evaluate_source_field(t, kWater, g2);
+  const fus::Wavenumber k1 = fus::complex_wavenumber(kWater, t.f0, 1);
+  const fus::HarmonicField p1 = fus::evaluate_first_harmonic(t, kWater, g2, sf.normalization);
+  CHECK((p1.values - sf.field.values).norm() <= 1e-12 * sf.field.values.norm());
+  fus::SourceField raw{fus::evaluate_first_harmonic(t, kWater, g2, 1.0), 1.0};
+  const fus::SourceField normed = fus::normalize_to_power(raw, t, kWater);
+  CHECK(std::fabs(normed.normalization - fus::power_scale_factor(t, kWater, k1)) <= 1e-12 * normed.normalization);
+  // direct O(N^2) quadrature vs the FFT apply (tests/test_potential.cpp:75-92)
+  {
+    const fus::VoxelGrid g = fus::make_grid({{0, 0, 0}, {12e-4, 10e-4, 8e-4}}, 1e-4, 2);
+    const fus::Wavenumber k = fus::complex_wavenumber(kWater, 1.1e6, 2);
+    const Eigen::VectorXcd f = random_vector(g.count(), 21);
+    const Eigen::VectorXcd d = fus::direct_potential_oracle(k, g, f);
+    CHECK((fus::GreenKernel(g, k).apply(f) - d).cwiseAbs().maxCoeff() < 1e-12 * max_abs(d));
+    CHECK((d - direct(k, g, f)).cwiseAbs().maxCoeff() < 1e-12 * max_abs(d));
+    const fus::VoxelGrid big = fus::make_grid({{0, 0, 0}, {60e-4, 50e-4, 40e-4}}, 1e-4, 2);
+    CHECK_THROWS_AS(fus::direct_potential_oracle(k, big, Eigen::VectorXcd::Zero(Eigen::Index(big.count()))),
+                    std::invalid_argument);
+    // apply_device / native on caller-owned device buffers
+    fus::GreenKernel K(g, k);
+    CHECK(K.native() != nullptr);
+    std::complex<double>*fd = nullptr, *ud = nullptr;
+    const size_t bytes = g.count() * sizeof(std::complex<double>);
+    CHECK(cudaMalloc(&fd, bytes) == cudaSuccess && cudaMalloc(&ud, bytes) == cudaSuccess);
+    cudaMemcpy(fd, f.data(), bytes, cudaMemcpyHostToDevice);
+    K.apply_device(fd, ud, -1.0);
+    cudaDeviceSynchronize();
+    Eigen::VectorXcd u(Eigen::Index(g.count()));
+    cudaMemcpy(u.data(), ud, bytes, cudaMemcpyDeviceToHost);
+    CHECK((u + K.apply(f)).cwiseAbs().maxCoeff() <= 1e-15 * max_abs(u));
+    cudaFree(fd);
+    cudaFree(ud);
+  }
+  // on-axis profiles and the shrink diagnostics (src/analysis.cpp:26-90,176-242; src/grid.cpp:114-139)
+  {
+    const fus::OnAxisProfile a = fus::extract_on_axis(p1);
+    CHECK(a.x.size() == a.p.size() && a.x.size() > 2);
+    CHECK(fus::on_axis_error(a, a, a) == 0.0);
+    const Eigen::VectorXd q = fus::localisedness_map(p1);
+    CHECK(q.size() == Eigen::Index(p1.grid.count()) && q.maxCoeff() <= 1.0 + 1e-15);
+    const fus::DomainBox box = fus::shrink_domain_by_threshold(p1, 0.5);
+    CHECK(p1.grid.box.contains(box, 1e-12));
+    CHECK(std::isfinite(fus::error_trend_diagnostic(a, a, 0.5)));
+  }
+  // VIE pieces on a liver slab (src/vie.cpp:11-323)
+  {
+    const fus::Medium liver = fus::medium_preset("liver");
+    const fus::MediumMap mm = fus::slab_map(g2, kWater, liver, t.focal_length, 2e-3);
+    CHECK(!mm.is_homogeneous() && !mm.contrast_support().empty());
+    const Eigen::VectorXcd contrast = mm.wavenumber_contrast(t.f0, 2);
+    CHECK(contrast.size() == Eigen::Index(g2.count()));
+    const fus::MediumMap half = mm.resample(plan.for_harmonic(3).grid);
+    CHECK(half.c.size() == Eigen::Index(plan.for_harmonic(3).grid.count()));
+    const fus::GreenKernel K(g2, fus::complex_wavenumber(kWater, t.f0, 2));
+    const Eigen::VectorXcd lhs = fus::vie_operator_apply(p1.values, contrast, K);
+    const Eigen::VectorXcd v = contrast.cwiseProduct(p1.values);
+    CHECK((lhs - (p1.values - K.apply(v))).cwiseAbs().maxCoeff() <= 1e-12 * max_abs(lhs));
+  }
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -428,7 +534,11 @@ int main(int argc, char** argv) {
   try {
     host_cases();
     io_cases();
-    if (all) device_cases();
+    surface_host_cases();
+    if (all) {
+      device_cases();
+      surface_device_cases();
+    }
   } catch (const std::exception& e) {
     std::printf("FAIL uncaught exception: %s\n", e.what());
     ++g_fail;

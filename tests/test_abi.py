@@ -116,6 +116,20 @@ def test_cpp_dropin_api_host_cases():
     assert "OK:" in out.stdout
 
 
+def test_cpp_dropin_test_calls_every_header_declaration():
+    """Every function and member function the drop-in headers (include/fus/*.hpp) declare is
+    called by the C++ drop-in test (tests/cpp/test_fus_api.cpp), which links only against them."""
+    decl = set()
+    for name in os.listdir(os.path.join(ROOT, "include", "fus")):
+        if name.endswith(".hpp"):
+            t = re.sub(r"//.*", "", open(os.path.join(ROOT, "include", "fus", name)).read())
+            decl |= {m.group(1) for m in re.finditer(r"^\s*(?:[\w:<>,\s\*&]+?)\s+(\w+)\s*\(", t, re.M)}
+    decl -= {"if", "for", "while", "return", "operator"}
+    test = open(os.path.join(ROOT, "tests", "cpp", "test_fus_api.cpp")).read()
+    missing = sorted(n for n in decl if not re.search(r"\b" + n + r"\b", test))
+    assert len(decl) > 60 and not missing, missing
+
+
 def test_interpolate_source_planes_follow_the_reference_cell_rule():
     # Host restatement (no GPU): the z-slab transfer's source range is the span of the
     # reference's cell bases (src/grid.cpp:156-170: q = (p - lo_s)/dx_s - 0.5,
