@@ -10,6 +10,23 @@
 #include "host_stage.hpp"
 
 
+namespace fusg {
+void ctx_retain(fusg_ctx* ctx) { ctx->refs.fetch_add(1); }
+
+void ctx_release(fusg_ctx* ctx) {
+  if (ctx->refs.fetch_sub(1) != 1) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  destroy_nccl(ctx);
+  cudaFree(ctx->dev_flag);
+  if (ctx->phase_tab) cudaFree(ctx->phase_tab);
+  for (auto& kv : ctx->tw_cache) cudaFree(kv.second);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+}  // namespace fusg
+
 using namespace fusg;
 
 namespace {
@@ -56,7 +73,9 @@ void free_kernel(fusg_kernel* K) {
   if (K->last_ev) cudaEventDestroy(K->last_ev);
   for (cudaEvent_t e : K->chunk_ev) cudaEventDestroy(e);
   if (K->copy_stream) cudaStreamDestroy(K->copy_stream);
+  fusg_ctx* ctx = K->ctx;
   delete K;  // (twiddle tables belong to the context's cache)
+  ctx_release(ctx);
 }
 
 // Applies of one kernel share its workspace: an apply enqueued on a stream other than the last
@@ -154,15 +173,7 @@ fusg_status fusg_ctx_create(int32_t device, fusg_ctx** out) {
 }
 
 fusg_status fusg_ctx_destroy(fusg_ctx* ctx) {
-  if (!ctx) return FUSG_OK;
-  cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  destroy_nccl(ctx);
-  cudaFree(ctx->dev_flag);
-  if (ctx->phase_tab) cudaFree(ctx->phase_tab);
-  for (auto& kv : ctx->tw_cache) cudaFree(kv.second);
-  cudaStreamDestroy(ctx->stream);
-  delete ctx;
+  if (ctx) ctx_release(ctx);
   return FUSG_OK;
 }
 
@@ -191,6 +202,7 @@ fusg_status fusg_kernel_create(fusg_ctx* ctx, const fusg_grid* grid, const fusg_
   if (st != FUSG_OK) return st;
   auto* K = new fusg_kernel;
   K->ctx = ctx;
+  ctx_retain(ctx);
   K->grid = *grid;
   K->k = *k;
   st = kernel_init_geometry(K, 1, 0);

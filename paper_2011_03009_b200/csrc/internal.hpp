@@ -85,6 +85,9 @@ struct fusg_ctx {
   std::map<int, double2*> tw_cache;
   std::mutex tw_mu;
   cudaStream_t pick(void* s) const { return s ? static_cast<cudaStream_t>(s) : stream; }
+  // the owner's reference plus one per live kernel: a context outlives its kernels whatever
+  // order their owners release them in (fusg_ctx_destroy drops the owner's reference)
+  std::atomic<int> refs{1};
 };
 
 struct fusg_kernel {
@@ -130,6 +133,8 @@ struct fusg_kernel {
 };
 
 namespace fusg {
+void ctx_retain(fusg_ctx* ctx);
+void ctx_release(fusg_ctx* ctx);  // frees the context with its last reference
 // Function attributes are per device: run `set` once for each device this process uses
 // (a mask over device ordinals 0..63; the current device is the one being launched on).
 template <class F>

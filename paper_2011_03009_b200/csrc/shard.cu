@@ -103,6 +103,7 @@ fusg_status create_slab(fusg_ctx* ctx, const fusg_grid* grid, const fusg_wavenum
   if (st != FUSG_OK) return st;
   auto* K = new fusg_kernel;
   K->ctx = ctx;
+  ctx_retain(ctx);
   K->grid = *grid;
   K->k = *k;
   K->slab = true;

@@ -619,3 +619,46 @@ def test_tabulated_attenuation_matches_the_polynomial_and_exp_paths(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         out[v] = np.load(p)
     assert rel_l2(out["1"], out["0"]) <= 1e-13
+
+
+@pytest.mark.parametrize("transport", ["nccl", "auto"])
+def test_multiprocess_zslab_cascade_single_rank_is_bitwise_run_cascade(transport):
+    # The multi-process sharded cascade (paper_2011_03009_b200/zslab.py) on a one-rank NCCL
+    # communicator: every piece runs (slab incident field, halo plan, slab transfers, rhs, the
+    # slab-sharded apply with its NCCL / IPC machinery); bitwise = run_cascade.
+    from paper_2011_03009_b200 import zslab
+
+    med, t, k1 = _reduced_cfg4(fus)
+    t.power = fus.radiated_power(t, med, k1, 2.0 * k1.k.real * 1.0e6)
+    cfg = fus.CascadeConfig(med, t, fus.plan_nested_meshes(t, med, 10.2e-3, 6, 4), 4)
+    want = fus.run_cascade(cfg)
+    c = fus.Context(0)
+    fus.attach_nccl(c, 1, 0, fus.nccl_unique_id())
+    got = zslab.run_cascade_zslab(cfg, zslab.Comm(), c, transport)
+    assert got.source_normalization == want.source_normalization
+    for n in range(1, 5):
+        assert got.slabs_z[n - 1] == (0, want.p(n).grid.dims[2])
+        assert torch.equal(got.slabs[n - 1], want.p(n).values), n
+    assert [row["harmonic"] for row in got.rows] == [2, 3, 4]
+
+
+def test_context_outlives_its_kernels_in_any_release_order():
+    # Owners may be released in any order (e.g. Python finalising a traceback's frames): the
+    # context is freed with its last kernel, not under a live one.
+    from paper_2011_03009_b200 import _lib
+
+    L = _lib.lib()
+    c = fus.Context(0)
+    g = fus.make_grid([0, 0, 0], [16e-4, 12e-4, 8e-4], 1e-4, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    K = fus.GreenKernel(g, k, ctx=c)
+    f = fus.random_vector(g.count(), 3)
+    want = K.apply(f).clone()
+    L.fusg_ctx_destroy(c.handle)  # the owner lets go first
+    c.handle = None
+    fd = torch.from_numpy(f).cuda()
+    u = torch.empty_like(fd)
+    _lib.check(L.fusg_kernel_apply(K.handle, fd.data_ptr(), u.data_ptr(), 1.0, None))  # still works
+    torch.cuda.synchronize()
+    assert torch.equal(u, want)
+    del K  # and frees the context with it
