@@ -610,6 +610,27 @@ def run_gpu_sharded(args, world, rank, local):
     per_pass, total_bytes = algorithmic_bytes(g.dims, P)
     hbm, hbm_kind = peaks()
     nvl = 900.0
+    del K, fd, ud, fh, uh
+    torch.cuda.empty_cache()
+    # the nested 5-harmonic recursion sharded over the ranks (paper_2011_03009_b200/zslab.py):
+    # config 4's geometry at the desk frequency by default, the full 1.1 MHz config with
+    # --cascade-full (per-GPU memory budget)
+    solve = None
+    if not args.no_cascade:
+        from paper_2011_03009_b200 import zslab
+        from tools import cascades
+
+        ccfg = cascades.cfg4(fus, desk=not args.cascade_full)
+        comm = zslab.Comm()
+        if not args.cascade_full:
+            zslab.run_cascade_zslab(ccfg, comm, ctx)  # warm-up
+        rc = zslab.run_cascade_zslab(ccfg, comm, ctx)
+        solve = {"config": ("cfg4 geometry (bowl R 7.5 cm, l 15 cm, c 1540, rho 1050, beta 4.5, 1 MPa), "
+                            f"f0={ccfg.transducer.f0 / 1e6:g} MHz, 4096 points, nested n_w=6, 5 harmonics"),
+                 "solve_s": rc.solve_s, "grids": [list(gr.dims) for gr in rc.grids], "rows": rc.rows,
+                 "sharding": f"zslab{world}", "time": "wall clock of the whole recursion, max over ranks"}
+        del rc
+        torch.cuda.empty_cache()
     if rank == 0:
         line = {
             "metric": METRIC, "value": N / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -628,6 +649,7 @@ def run_gpu_sharded(args, world, rank, local):
             "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
             "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": None,
+            "nested_5_harmonic_solve": solve,
         }
         print(json.dumps(line), flush=True)
     return 0
@@ -644,6 +666,8 @@ def main():
     ap.add_argument("--headline-only", action="store_true", help="cfg5 line only (no cfg2 / 8(f) extras)")
     ap.add_argument("--sharded", action="store_true", help="use the sharded path even at N = 1")
     ap.add_argument("--cfg2", action="store_true", help="sharded path on cfg2 instead of cfg5")
+    ap.add_argument("--cascade-full", action="store_true",
+                    help="N > 1: the sharded nested solve on the full 1.1 MHz config 4 (needs >= 4 GPUs)")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="sharded apply: transposes fused into passes A/D as peer stores, or NCCL all-to-all")
     args = ap.parse_args()
