@@ -113,6 +113,9 @@ struct fusg_kernel {
   // slab decomposition (unsharded: G = 1, rank 0 owns everything)
   int G = 1, rank = 0;
   bool slab = false;   // created by fusg_kernel_create_slab: owns exchange buffers even at G = 1
+  // layout of the x-transformed intermediate A (and X): [kx][z][y] (az = Ny, akx = Nz Ny), or
+  // [z][kx][y] for unsharded kernels with FUSG_A_ZKY (az = Px Ny, akx = Ny)
+  int64_t az = 0, akx = 0;
   int z0 = 0, nz = 0;  // this rank's z-planes of f/u
   int x0 = 0, nx = 0;  // this rank's spectral kx columns
   std::vector<int> zs, nzs, xs, nxs;  // all ranks' ranges (exchange offsets)

@@ -1435,6 +1435,22 @@ fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank) {
   K->nz = K->nzs[rank];
   K->x0 = K->xs[rank];
   K->nx = K->nxs[rank];
+  // Unsharded kernels keep A as [z][kx][y]: passes A and E then move their 64/128-byte kx
+  // segments at an Ny-element stride instead of Nz*Ny, staying within DRAM pages (cfg5: A 6.25
+  // -> 5.22 ms, E 6.30 -> 5.45 ms; cfg2 neutral).  FUSG_A_ZKY=0 restores [kx][z][y], the
+  // layout of the sharded kernels' x-slabs.
+  static const bool zky = [] {
+    const char* e = getenv("FUSG_A_ZKY");
+    return !(e && atoi(e) == 0);
+  }();
+  const int64_t Ny = K->grid.dims[1];
+  if (zky && G == 1 && !K->slab) {
+    K->az = int64_t(K->P[0]) * Ny;
+    K->akx = Ny;
+  } else {
+    K->az = Ny;
+    K->akx = int64_t(K->nz) * Ny;  // x-slab X and the A slab: [kx][z in slab][y]
+  }
   return FUSG_OK;
 }
 
@@ -1520,7 +1536,7 @@ fusg_status apply_phase_A(fusg_kernel* K, const double2* f, cudaStream_t s) {
   const int Px = K->P[0], nz = K->nz;
   return launch_axis<false>(K->ctx, K->plan[0], Ny, nz,
                             GLoadF{GLoad{f, Nx, int64_t(Ny) * Nx, 1, Nx}},
-                            GStoreF{GStore{K->bufA, 1, Ny, int64_t(nz) * Ny, Px, 1.0}}, s, kKindRow);
+                            GStoreF{GStore{K->bufA, 1, K->az, K->akx, Px, 1.0}}, s, kKindRow);
 }
 
 // FUSG_CONV_QUAD=1: pass-C lines in quad order (kx mirror pairs interleaved at the finest
@@ -1540,8 +1556,10 @@ static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
   const int Hy = K->H[1], Hz = K->H[2];
   const int nx = K->nx;
-  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
-  FUSG_TRY(launch_axis<false>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{X, Ny, NzNy, 1, Ny}},
+  const int64_t PyNz = int64_t(Py) * Nz;
+  // X: [kx][z][y] (x-slab) or A in the kernel's layout (unsharded)
+  const int64_t xz = X == K->bufA ? K->az : Ny, xkx = X == K->bufA ? K->akx : int64_t(Nz) * Ny;
+  FUSG_TRY(launch_axis<false>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{X, xz, xkx, 1, Ny}},
                               GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
   if (ev) cudaEventRecord(ev[0], s);
   FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
@@ -1588,19 +1606,21 @@ fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Py = K->P[1];
   const int nx = K->nx;
-  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  const int64_t PyNz = int64_t(Py) * Nz;
+  const int64_t xz = X == K->bufA ? K->az : Ny, xkx = X == K->bufA ? K->akx : int64_t(Nz) * Ny;
   FUSG_TRY(phase_BC(K, X, s, ev));
   // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of X, keep Ny
   return launch_axis<true>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
-                           GStoreF{GStore{X, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol);
+                           GStoreF{GStore{X, xz, xkx, 1, Ny, 1.0}}, s, kKindCol);
 }
 
 fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t s) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1];
   const int Px = K->P[0], nz = K->nz;
   const double total = double(K->P[0]) * double(K->P[1]) * double(K->P[2]);
+  (void)nz;
   return launch_axis<true>(K->ctx, K->plan[0], Ny, nz,
-                           GLoadF{GLoad{K->bufA, 1, Ny, int64_t(nz) * Ny, Px}},
+                           GLoadF{GLoad{K->bufA, 1, K->az, K->akx, Px}},
                            GStoreF{GStore{u, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
 }
 
@@ -1611,10 +1631,11 @@ fusg_status apply_chunk_AB(fusg_kernel* K, const double2* f_z0, int z0, int nzc,
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1];
   const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
-  double2* A = K->bufA + int64_t(z0) * Ny;
+  (void)NzNy;
+  double2* A = K->bufA + int64_t(z0) * K->az;
   FUSG_TRY(launch_axis<false>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{f_z0, Nx, int64_t(Ny) * Nx, 1, Nx}},
-                              GStoreF{GStore{A, 1, Ny, NzNy, Px, 1.0}}, s, kKindRow));
-  return launch_axis<false>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{A, Ny, NzNy, 1, Ny}},
+                              GStoreF{GStore{A, 1, K->az, K->akx, Px, 1.0}}, s, kKindRow));
+  return launch_axis<false>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{A, K->az, K->akx, 1, Ny}},
                             GStoreF{GStore{K->bufB + z0, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow);
 }
 
@@ -1632,10 +1653,11 @@ fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, doubl
   const int Px = K->P[0], Py = K->P[1];
   const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
   const double total = double(K->P[0]) * double(K->P[1]) * double(K->P[2]);
-  double2* A = K->bufA + int64_t(z0) * Ny;
+  (void)NzNy;
+  double2* A = K->bufA + int64_t(z0) * K->az;
   FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{K->bufB + z0, 1, PyNz, Nz, Py}},
-                             GStoreF{GStore{A, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
-  return launch_axis<true>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{A, 1, Ny, NzNy, Px}},
+                             GStoreF{GStore{A, K->az, K->akx, 1, Ny, 1.0}}, s, kKindCol));
+  return launch_axis<true>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{A, 1, K->az, K->akx, Px}},
                            GStoreF{GStore{u_z0, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
 }
 
@@ -1646,6 +1668,7 @@ static int try_ab_fused(fusg_kernel* K, const double2* f, cudaStream_t s) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1];
   if (K->G != 1 || K->slab || Px != 512 || Py != 512 || 2 * Nx > Px || 2 * Ny > Py) return 0;
+  if (K->az != Ny) return 0;  // the ring assumes A as [kx][z][y]
   constexpr int kRing = 3;
   const int64_t slot = int64_t(Px) * 8 * Ny;
   if (slot * int64_t(sizeof(double2)) > (int64_t(24) << 20) || kRing * slot > int64_t(Px) * Nz * Ny) return 0;
@@ -1680,6 +1703,7 @@ static int try_ab_chunks(fusg_kernel* K, const double2* f, cudaStream_t s) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1];
   if (!on || K->G != 1 || K->slab || Px != 512 || Py != 512 || 2 * Nx > Px || 2 * Ny > Py) return 0;
+  if (K->az != Ny) return 0;  // the ring assumes A as [kx][z][y]
   constexpr int kRing = 3;
   const int64_t slot = int64_t(Px) * 8 * Ny;
   if (kRing * slot > int64_t(Px) * Nz * Ny) return 0;
@@ -1731,8 +1755,9 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
     mark(2);
     FUSG_TRY(apply_phase_C(K, s));
     mark(3);
+    (void)NzNy;
     FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], Nz, K->P[0], GLoadF{GLoad{K->bufB, 1, PyNz, Nz, K->P[1]}},
-                               GStoreF{GStore{K->bufA, Ny, NzNy, 1, Ny, 1.0}}, s, kKindCol));
+                               GStoreF{GStore{K->bufA, K->az, K->akx, 1, Ny, 1.0}}, s, kKindCol));
     mark(4);
     FUSG_TRY(apply_phase_E(K, u, scale, s));
     mark(5);
