@@ -585,6 +585,27 @@ def rhs_source(n: int, lower: List[HarmonicField], m: Medium, omega: float) -> n
     return out
 
 
+def rhs_source_full(n: int, fields: List[HarmonicField], m: Medium, omega: float) -> np.ndarray:
+    """The paper's full quadratic source, Eq. (cascade_1), truncated at
+    M = len(fields) harmonics: coeff * [sum_{m=1}^{n-1} p_m p_{n-m} + 2 sum_{m=n+1}^{M} p_m conj(p_{m-n})].
+    The reference implements only the first sum (src/cascade.cpp:36-39), so this is parity
+    unpinned beyond M = n - 1; plain numpy in the device kernel's accumulation order."""
+    M = len(fields)
+    coeff = m.beta * omega * omega * n * n / (2.0 * m.rho0 * m.c0 ** 4)  # src/cascade.cpp:32-34
+    count = fields[0].values.size
+    re = np.zeros(count)
+    im = np.zeros(count)
+    for k in range(1, n):
+        a, b = fields[k - 1].values, fields[n - k - 1].values
+        re = re + (a.real * b.real - a.imag * b.imag)
+        im = im + (a.real * b.imag + a.imag * b.real)
+    for k in range(n + 1, M + 1):
+        a, b = fields[k - 1].values, fields[k - n - 1].values
+        re = re + 2.0 * (a.real * b.real + a.imag * b.imag)
+        im = im + 2.0 * (a.imag * b.real - a.real * b.imag)
+    return coeff * re + 1j * (coeff * im)
+
+
 def same_grid(a: VoxelGrid, b: VoxelGrid) -> bool:
     """src/cascade.cpp:15-17"""
     return tuple(a.dims) == tuple(b.dims) and a.dx == b.dx and bool(np.all(a.lo == b.lo))

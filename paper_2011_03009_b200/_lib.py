@@ -111,6 +111,8 @@ SIGNATURES = {
                                       C.c_int32, _dp]),
     "fusg_rhs_source": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), C.c_int64, C.POINTER(MediumC),
                                   C.c_double, _vp, _vp]),
+    "fusg_rhs_source_full": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), C.c_int32, C.c_int64,
+                                       C.POINTER(MediumC), C.c_double, _vp, _vp]),
     "fusg_interpolate": (C.c_int, [_vp, C.POINTER(Grid), _vp, C.POINTER(Grid), _vp, _vp]),
     "fusg_run_cascade": (C.c_int, [_vp, C.POINTER(CascadeDesc), C.POINTER(_vp),
                                    C.POINTER(StageTiming), _dp]),

@@ -468,6 +468,32 @@ __global__ void rhs_kernel(LowerPtrs lp, int n, int64_t count, double coeff,
   }
 }
 
+// The full quadratic source of the paper's Eq. (cascade_1), truncated at the
+// M harmonics held: sum_{m=1}^{n-1} p_m p_{n-m} + 2 sum_{m=n+1}^{M} p_m conj(p_{m-n}). The first
+// sum is accumulated exactly as rhs_kernel (so M = n - 1 is bitwise fusg_rhs_source); the
+// conjugate terms follow in increasing m. Used by iterated (Gauss-Seidel) sweeps, where the
+// higher harmonics of the previous sweep are available.
+__global__ void rhs_full_kernel(LowerPtrs lp, int n, int M, int64_t count, double coeff,
+                                double2* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double re = 0.0, im = 0.0;
+    for (int m = 1; m <= n - 1; ++m) {
+      const double2 a = lp.p[m - 1][i], b = lp.p[n - m - 1][i];
+      re = __dadd_rn(re, __dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)));
+      im = __dadd_rn(im, __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+    }
+    for (int m = n + 1; m <= M; ++m) {  // a * conj(b) = (ac + bd, bc - ad) with b = (c, d)
+      const double2 a = lp.p[m - 1][i], b = lp.p[m - n - 1][i];
+      const double pr = __dadd_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y));
+      const double pi = __dsub_rn(__dmul_rn(a.y, b.x), __dmul_rn(a.x, b.y));
+      re = __dadd_rn(re, __dmul_rn(2.0, pr));
+      im = __dadd_rn(im, __dmul_rn(2.0, pi));
+    }
+    out[i] = make_double2(__dmul_rn(coeff, re), __dmul_rn(coeff, im));
+  }
+}
+
 // interpolate (src/grid.cpp:141-195), exact rounding
 // Source cell and weight of target index i on axis a (src/grid.cpp:156-170): q = (p - lo_s)/dx_s
 // - 0.5, base = clamp(floor q, 0, max(0, n - 2)), t = clamp(q - base, 0, 1) (t > 1 -> 1, or 0
@@ -760,6 +786,23 @@ fusg_status rhs_dev(fusg_ctx* ctx, int n, const double2* const* lower, int64_t c
   return FUSG_OK;
 }
 
+fusg_status rhs_full_dev(fusg_ctx* ctx, int n, const double2* const* fields, int M, int64_t count,
+                         double coeff, double2* out, cudaStream_t s) {
+  if (n < 2) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source: harmonic index must be >= 2");
+  if (M < n - 1) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: need p_1 .. p_{n-1}");
+  if (M > 32) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: at most 32 harmonics");
+  LowerPtrs lp{};
+  for (int m = 0; m < M; ++m) {
+    if (m == n - 1) continue;  // p_n itself never enters its own source
+    if (!fields[m]) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: null harmonic field");
+    lp.p[m] = fields[m];
+  }
+  rhs_full_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(lp, n, M, count, coeff, out);
+  ctx->launches++;
+  FUSG_LAUNCH_CHECK("rhs_full_kernel");
+  return FUSG_OK;
+}
+
 fusg_status max_abs_dev(fusg_ctx* ctx, const double2* v, int64_t n, double* out, cudaStream_t s) {
   unsigned long long* d = nullptr;
   FUSG_CUDA_TRY(cudaMallocAsync(&d, sizeof(unsigned long long), s));
@@ -1005,6 +1048,17 @@ fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower
   const double coeff = fusg_rhs_coefficient(m, omega, n);
   return rhs_dev(ctx, n, reinterpret_cast<const double2* const*>(lower_dev), count, coeff,
                  reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
+}
+
+fusg_status fusg_rhs_source_full(fusg_ctx* ctx, int32_t n, const double* const* fields_dev, int32_t M,
+                                 int64_t count, const fusg_medium* m, double omega, double* out_dev,
+                                 void* stream) {
+  if (!ctx || !m || !fields_dev || !out_dev)
+    return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: null argument");
+  FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
+  const double coeff = fusg_rhs_coefficient(m, omega, n);
+  return rhs_full_dev(ctx, n, reinterpret_cast<const double2* const*>(fields_dev), M, count, coeff,
+                      reinterpret_cast<double2*>(out_dev), ctx->pick(stream));
 }
 
 fusg_status fusg_interpolate_source_planes(const fusg_grid* src, const fusg_grid* target, int32_t tz0,

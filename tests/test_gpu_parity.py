@@ -310,6 +310,30 @@ def test_rhs_source_bit_exact(ctx, orc):
         fus.rhs_source(1, [], w, omega)
 
 
+@pytest.mark.gpu
+def test_rhs_source_full_conjugate_terms(ctx, orc):
+    """Eq. (cascade_1) with the p_m conj(p_{m-n}) terms (north_star (2)); M = n - 1 is rhs_source."""
+    w, wo = water(), orc.medium_preset("water")
+    g = fus.make_grid([0, 0, 0], [10e-3, 7e-3, 5e-3], 1e-3, 1)
+    omega = 2 * math.pi * 1.1e6
+    fields = [fus.random_vector(g.count(), 40 + i) for i in range(6)]
+    hf = [fus.HarmonicField(g, v, None) for v in fields]
+    ho = [orc.HarmonicField(None, v, None) for v in fields]
+    for n in (2, 3, 4):
+        assert np.array_equal(host(fus.rhs_source_full(n, hf[: n - 1], w, omega)),
+                              host(fus.rhs_source(n, hf[: n - 1], w, omega)))
+        for M in range(n, 7):
+            got = host(fus.rhs_source_full(n, hf[:M], w, omega))
+            assert np.array_equal(got, orc.rhs_source_full(n, ho[:M], wo, omega)), (n, M)
+    # p_n itself is not read: passing None in its slot gives the same source
+    withnone = list(hf[:5])
+    withnone[2] = None
+    assert np.array_equal(host(fus.rhs_source_full(3, withnone, w, omega)),
+                          host(fus.rhs_source_full(3, hf[:5], w, omega)))
+    with pytest.raises(ValueError):
+        fus.rhs_source_full(4, hf[:2], w, omega)
+
+
 # ------------------------------------------------------------------ recursion
 def tiny(n_h, power, lib):
     w = lib.medium_preset("water")
