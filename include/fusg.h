@@ -267,7 +267,8 @@ fusg_status fusg_device_copy(fusg_ctx* ctx, void* dst_dev, const void* src_dev, 
  * rank r of G owns z-planes [z0, z0+nz) of f and u (ragged split: the first
  * N mod G ranks take one extra plane) and spectral kx columns [x0, x0+nx) of the padded box.
  * The apply transposes z-slab -> x-slab after the forward x pass and back before the inverse
- * x pass (one all-to-all each way); the kernel spectrum is replicated. */
+ * x pass (one all-to-all each way). The kernel spectrum is held per x-slab: a rank keeps only
+ * the folded octant rows its kx columns need (fusg_kernel_octant_rows). */
 fusg_status fusg_slab_range(int32_t n, int32_t nranks, int32_t rank, int32_t* begin, int32_t* count);
 /* Exchange plan of rank `rank` (arrays of nranks, complex128 element offsets/counts):
  * a_off/a_cnt[q]: block of A_r [Px][nz_r][Ny] holding rank q's kx columns (sent to q in the
@@ -282,6 +283,9 @@ fusg_status fusg_ctx_attach_nccl(fusg_ctx* ctx, int32_t nranks, int32_t rank, co
 fusg_status fusg_kernel_create_slab(fusg_ctx* ctx, const fusg_grid* global_grid,
                                     const fusg_wavenumber* k, int32_t pad_small_primes,
                                     int32_t nranks, int32_t rank, fusg_kernel** out);
+/* Folded kx rows [kf0, kf0 + knf) of the octant spectrum this kernel holds (unsharded: 0 and
+ * Px/2 + 1; x-slab kernels: the fold of their kx columns). */
+fusg_status fusg_kernel_octant_rows(const fusg_kernel* kernel, int32_t* kf0, int32_t* knf);
 fusg_status fusg_kernel_slab(const fusg_kernel* kernel, int32_t* z0, int32_t* nz, int32_t* x0,
                              int32_t* nx);
 /* This rank's apply: f_dev/u_dev are its z-slab [nz][Ny][Nx]; collective over the context's

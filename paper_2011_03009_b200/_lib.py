@@ -125,6 +125,7 @@ SIGNATURES = {
     "fusg_ctx_attach_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(C.c_uint8)]),
     "fusg_kernel_create_slab": (C.c_int, [_vp, C.POINTER(Grid), C.POINTER(Wave), C.c_int32, C.c_int32,
                                           C.c_int32, C.POINTER(_vp)]),
+    "fusg_kernel_octant_rows": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "fusg_kernel_slab": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                    C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "fusg_kernel_apply_slab": (C.c_int, [_vp, _vp, _vp, C.c_double, _vp]),

@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
       const int lines_ok = min(T, a.n_inner - i0);
       const double2* src = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
       const unsigned row = unsigned(nv) * sizeof(double2);
+      refill_fence();
       mbar_expect_tx(bar, row * lines_ok);
       for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stage + tt * 768, src + tt * a.in_si, row, bar);
     }

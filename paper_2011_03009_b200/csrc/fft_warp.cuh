@@ -239,8 +239,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
-// stage `bytes` from src into dst (lane 0 of the caller's group issues; bytes > 0)
+// Orders this thread's earlier generic-proxy shared-memory accesses -- and, through the
+// barrier that precedes every refill, the other threads' reads of the buffer -- before the
+// async-proxy (bulk copy) writes that follow.  Without it a refill could land while a lane's
+// shared load of the old contents is still queued: measured on the B200 as rare bitwise
+// differences between repeated applies (pass C at L = 256, one apply in ~10 at 224 x 224 lines).
+__device__ __forceinline__ void refill_fence() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// stage `bytes` from src into dst (lane 0 of the caller's group issues; bytes > 0), after the
+// buffer's previous contents were read by the generic proxy
 __device__ __forceinline__ void bulk_stage(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  refill_fence();
   mbar_expect_tx(bar, bytes);
   bulk_g2s(dst, src, bytes, bar);
 }

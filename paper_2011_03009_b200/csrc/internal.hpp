@@ -99,6 +99,9 @@ struct fusg_kernel {
   fusg::AxisPlan plan[3]{};
   double2* tw[3] = {nullptr, nullptr, nullptr};
   double2* koct = nullptr;  // kernel spectrum octant [kx][ky][kz]  (Hx x Hy x Hz)
+  // folded kx rows of the octant held here: [kf0, kf0 + knf) (unsharded: all Hx rows; slab
+  // kernels keep only the rows their kx columns fold to, SURVEY.md 8(e) "octant per x-slab")
+  int kf0 = 0, knf = 0;
   double2* bufA = nullptr;  // [kx][z][y]  (Px x Nz x Ny)
   double2* bufB = nullptr;  // [kx][ky][z]  (Px x Py x Nz)
   double2* stage_f = nullptr;  // host-vector apply staging (lazily allocated)

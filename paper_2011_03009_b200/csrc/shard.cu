@@ -4,7 +4,8 @@
 //   phase A on the z-slab writes A_r [Px][nz_r][Ny]; A_r's kx-range slices ARE the send blocks
 //   exchange 1: rank r receives [nx_r][nz_p][Ny] from every p into rbuf, unpacked (2D copy) into
 //              the x-slab X_r [nx_r][Nz][Ny]
-//   phases B, C, D run locally on X_r (the octant K^ is replicated; kx folded globally)
+//   phases B, C, D run locally on X_r (K^ octant rows held per x-slab: the folded kx window
+//              [kf0, kf0 + knf) of this rank's columns, built without a collective)
 //   exchange 2: X_r rows of z-slab q are packed (2D copy) into rbuf and sent to q, which
 //              receives them straight into its A_q kx-slice
 //   phase E on the z-slab.
@@ -253,6 +254,13 @@ fusg_status fusg_kernel_create_slab(fusg_ctx* ctx, const fusg_grid* global_grid,
   if (!ctx || !global_grid || !k || !out) return set_error(FUSG_INVALID_ARGUMENT, "kernel_create_slab: null argument");
   FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
   return create_slab(ctx, global_grid, k, nranks, rank, out);
+}
+
+fusg_status fusg_kernel_octant_rows(const fusg_kernel* K, int32_t* kf0, int32_t* knf) {
+  if (!K) return set_error(FUSG_INVALID_ARGUMENT, "kernel_octant_rows: null kernel");
+  if (kf0) *kf0 = K->kf0;
+  if (knf) *knf = K->knf;
+  return FUSG_OK;
 }
 
 fusg_status fusg_kernel_slab(const fusg_kernel* K, int32_t* z0, int32_t* nz, int32_t* x0, int32_t* nx) {

@@ -102,8 +102,9 @@ struct KOct {
   int64_t s_kx, s_ky, s_kz;
   int kx_off;
   int quad = 0;  // pass-C line order of the persistent kernels: kx mirror pairs interleaved (1)
+  int kx_base = 0;  // first folded kx row stored at p (x-slab kernels hold a row window)
   __device__ __forceinline__ const double2* line(int ky, int kx) const {
-    return p + fold_index(kx + kx_off, Px) * s_kx + fold_index(ky, Py) * s_ky;
+    return p + (fold_index(kx + kx_off, Px) - kx_base) * s_kx + fold_index(ky, Py) * s_ky;
   }
 };
 

@@ -1465,7 +1465,19 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   // rank-local apply buffers (unsharded: nz = Nz, nx = Px and X aliases A); the full octant
   // is built on every rank (it depends only on the grid and k)
   const size_t nA = size_t(Px) * Ny * K->nz, nB = size_t(K->nx) * Py * Nz;
-  const size_t nK = size_t(Hx) * Hy * Hz;
+  // folded kx rows this kernel's kx columns [x0, x0 + nx) need (all Hx when unsharded)
+  {
+    int lo = Hx, hi = -1;
+    for (int kx = K->x0; kx < K->x0 + K->nx; ++kx) {
+      const int f = fusg::fold_index(kx, Px);
+      lo = std::min(lo, f);
+      hi = std::max(hi, f);
+    }
+    K->kf0 = hi < lo ? 0 : lo;
+    K->knf = hi < lo ? 0 : hi - lo + 1;
+  }
+  const int kf0 = K->kf0, knf = K->knf;
+  const size_t nK = size_t(std::max(knf, 1)) * Hy * Hz;
   const size_t nX = (K->G > 1 || K->slab) ? size_t(K->nx) * Nz * Ny : 0;
   // stream-ordered allocations: the context's pool keeps freed workspaces for the next kernel
   // (a cascade builds one GreenKernel per harmonic)
@@ -1488,7 +1500,7 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   // build scratch: the apply workspaces are idle during the build, so G1/G2 live in bufA/bufB
   // whenever they fit (always unsharded) -- the peak stays at the apply's own footprint, which
   // is what lets a 1024^3 grid (2048^3 embedding) fit in one B200
-  const size_t n1 = size_t(Hx) * Ny * Nz, n2 = size_t(Hx) * Hy * Nz;
+  const size_t n1 = size_t(Hx) * Ny * Nz, n2 = size_t(Hx) * Hy * Nz;  // (G2 only fills kx rows [kf0, kf0 + knf))
   const bool g1_in_A = n1 <= nA, g2_in_B = n2 <= nB;
   g1 = g1_in_A ? K->bufA : nullptr;
   g2 = g2_in_B ? K->bufB : nullptr;
@@ -1507,14 +1519,18 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   KGenF gen{Nx, Ny, Px, dx, dx * dx * dx, K->k.k_re, K->k.k_im, self};
   GStoreF s1{GStore{g1, Hx, 0, 1, Hx, 1.0}};
   FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, gen, s1, s));
-  // G2: even extension along y, forward y, keep ky <= Py/2
-  FoldF l2{g1, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
-  GStoreF s2{GStore{g2, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[1], Hx, Nz, l2, s2, s));
-  // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant
-  FoldF l3{g2, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
-  GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx][ky][kz]
-  FUSG_TRY(launch_axis<false>(ctx, K->plan[2], Hx, Hy, l3, s3, s));
+  // G2: even extension along y, forward y, keep ky <= Py/2 (kx rows [kf0, kf0 + knf) only:
+  // the y and z transforms are independent per kx, so an x-slab kernel builds just its window;
+  // the x pass above is the replicated part of a sharded build, and no collective is needed)
+  if (knf > 0) {
+    FoldF l2{g1 + kf0, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
+    GStoreF s2{GStore{g2 + kf0, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
+    FUSG_TRY(launch_axis<false>(ctx, K->plan[1], knf, Nz, l2, s2, s));
+    // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant rows [kf0, kf0 + knf)
+    FoldF l3{g2 + kf0, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
+    GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx - kf0][ky][kz]
+    FUSG_TRY(launch_axis<false>(ctx, K->plan[2], knf, Hy, l3, s3, s));
+  }
   if (!g1_in_A) cudaFreeAsync(g1, s);
   if (!g2_in_B) cudaFreeAsync(g2, s);
   FUSG_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1564,7 +1580,7 @@ static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   if (ev) cudaEventRecord(ev[0], s);
   FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
                        GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
-                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0, conv_quad()}, s));
+                       KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0, conv_quad(), K->kf0}, s));
   if (ev) cudaEventRecord(ev[1], s);
   return FUSG_OK;
 }
@@ -1645,7 +1661,7 @@ fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s) {
   const int64_t PyNz = int64_t(Py) * Nz;
   return launch_conv(K->ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
                      GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
-                     KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0, conv_quad()}, s);
+                     KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0, conv_quad(), K->kf0}, s);
 }
 
 fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s) {

@@ -1316,6 +1316,9 @@ class SlabKernel:
         v = [C.c_int32() for _ in range(4)]
         check(lib().fusg_kernel_slab(h, *[C.byref(x) for x in v]))
         self.z0, self.nz, self.x0, self.nx = (x.value for x in v)
+        kf0, knf = C.c_int32(), C.c_int32()
+        check(lib().fusg_kernel_octant_rows(h, C.byref(kf0), C.byref(knf)))
+        self.octant_rows = (kf0.value, knf.value)  # folded kx rows of K^ held by this rank
 
     def slab_count(self) -> int:
         return self.nz * int(self.grid.dims[1]) * int(self.grid.dims[0])

@@ -429,6 +429,23 @@ def test_cpp_dropin_api_all_cases(ctx):
     assert out.returncode == 0, out.stdout + out.stderr
 
 
+@pytest.mark.parametrize("dims,applies", [((106, 105, 105), 40), ((130, 105, 127), 40), ((256, 256, 256), 12),
+                                          ((64, 64, 700), 12), ((100, 100, 380), 12), ((200, 200, 490), 6)])
+def test_repeated_applies_are_bitwise_identical(ctx, dims, applies):
+    # Every staged pass C (L = 256 / 512 / 1536 / 768 / 1024) refills its shared buffers with bulk
+    # copies while other lanes have just read them; without the async-proxy fence the refill
+    # occasionally overtook a queued shared load (about one apply in ten at 224 x 224 lines of
+    # L = 256 differed, up to 0.7 % in max norm). Repeated applies must agree bit for bit.
+    dx = 1e-4
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 4)
+    k = fus.complex_wavenumber(water(), 0.8e6, 4)
+    f = torch.from_numpy(fus.random_vector(g.count(), 4)).cuda()
+    K = fus.GreenKernel(g, k)
+    ref = K.apply(f)
+    for _ in range(applies):
+        assert torch.equal(K.apply(f), ref)
+
+
 @pytest.mark.parametrize("dims,G", [((37, 20, 19), 2), ((37, 20, 19), 3), ((64, 64, 64), 4),
                                     ((16, 24, 9), 8), ((25, 30, 7), 7),
                                     # Pz = 512: the 16x16x2 pass C on kx slabs (kx offset, no mirror order)
@@ -461,6 +478,30 @@ def test_slab_fused_peer_transposes_loopback_is_bitwise_unsharded(ctx, dims, G):
     want = fus.GreenKernel(g, k).apply(f, 0.5)
     got = fus.apply_slab_loopback(g, k, f, G, 0.5, transport="p2p")
     assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("dims,G", [((37, 20, 19), 2), ((64, 64, 64), 4), ((25, 30, 7), 7), ((128, 128, 40), 8)])
+def test_slab_kernels_hold_only_their_octant_rows(ctx, dims, G):
+    # SURVEY.md 8(e) "octant kept per x-slab": rank r keeps the folded kx rows of its columns
+    # [x0, x0 + nx) (built without a collective); together the ranks cover the whole octant,
+    # each holds about 2/G of it, and the applies above stay bitwise the unsharded ones.
+    dx = 1e-4
+    g = fus.make_grid([0, 0, 0], [d * dx for d in dims], dx, 2)
+    k = fus.complex_wavenumber(water(), 1.1e6, 2)
+    Px = fus.padded_dims(g)[0]
+    Hx = Px // 2 + 1
+    full = fus.GreenKernel(g, k)
+    covered = set()
+    for r in range(G):
+        sk = fus.SlabKernel(g, k, G, r)
+        kf0, knf = sk.octant_rows
+        folds = {min(x, Px - x) for x in range(sk.x0, sk.x0 + sk.nx)}
+        assert folds == set(range(kf0, kf0 + knf)), (r, kf0, knf)
+        assert knf <= sk.nx and (G < 4 or knf < Hx)
+        covered |= folds
+    assert covered == set(range(Hx))
+    f = fus.random_vector(g.count(), 17)
+    assert torch.equal(fus.apply_slab_loopback(g, k, f, G), full.apply(f))
 
 
 def test_slab_fused_transposes_need_warp_lengths(ctx):
