@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "r16.cuh"
+#include "tma.cuh"
 
 namespace fusg {
 
@@ -104,10 +105,18 @@ struct X3Warp {
   // forward: y_r (gathered) -> X[3k' + r] in the half-exchanged layout (slot i: k' = k1 + 16 (i + 8 b),
   // slot i + 8: k' + 256); xr: this warp's 512-entry exchange buffer
   __device__ __forceinline__ void forward(double2* v, double2* xr, int lane) const {
+    forward_a(v);
+    forward_b(v, xr, lane);
+  }
+  // stage A of the forward transform (registers only)
+  __device__ __forceinline__ void forward_a(double2* v) const {
 #pragma unroll
     for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmul(v[n1], c48[n1 * r]);  // W48^(n1 r), n1 r < 48
     dft16<false>(v);
     r16_twiddle_u<false>(v, u, w1, w2, w4, w8);
+  }
+  // the exchange through xr and stage B
+  __device__ __forceinline__ void forward_b(double2* v, double2* xr, int lane) const {
 #pragma unroll
     for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
     __syncwarp();
@@ -273,13 +282,16 @@ struct X3TSmem {
   static constexpr int C_US = C_TW + 128;
   static constexpr int C_C48 = C_US + 96;
   static constexpr int C_END = C_C48 + 48;
-  static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2);
+  static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2) + 2 * sizeof(uint64_t);
 };
 
-template <int T>
-__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
+// TMA (T = 4): the finished tile leaves by tensor-map box stores issued by one thread, and the
+// next tile's stage-A arithmetic overlaps them; the area is rewritten (first exchange) only after
+// the stores have read it.
+template <int T, bool TMA>
+__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
   using X3TSmem = fusg::X3TSmem<T>;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = w % 3, t = w / 3;
   double2* const area = sm + X3TSmem::AREA;
@@ -318,9 +330,17 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
     mbar_wait(bar, ph);
     double2 v[16];
     W.gather(v, stage + (t < lines_ok ? t : 0) * 768, nv, lane);
+    if constexpr (TMA) {
+      W.forward_a(v);
+      if (threadIdx.x == 0) bulk_wait_read0();  // the previous tile's box stores have read the area
+    }
     __syncthreads();  // stage read by every warp: refill it with the next tile's rows
     if (threadIdx.x == 0) prefetch(tix + gridDim.x);
-    W.forward(v, xr, lane);
+    if constexpr (TMA) {
+      W.forward_b(v, xr, lane);
+    } else {
+      W.forward(v, xr, lane);
+    }
     __syncthreads();  // every exchange buffer is read out: the area becomes the tile
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -329,6 +349,14 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
       area[mtile_at<T>(p + 768, t)] = v[i + 8];
     }
     __syncthreads();  // all T spectra are in the tile
+    if constexpr (TMA) {
+      if (threadIdx.x == 0) {
+        smem_to_async_fence();
+        for (int p0 = 0; p0 < a.out_nvalid; p0 += 256) tma_store_tile_box(&tm, area + p0 * T, 2 * i0, p0, k);
+        bulk_commit();
+      }
+      continue;
+    }
     double2* const base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
 #pragma unroll 4
     for (int e = threadIdx.x; e < a.out_nvalid * T; e += 96 * T) {
@@ -346,6 +374,9 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
     }
     // (the next tile's staging barrier orders these reads before its exchange writes)
   }
+  if constexpr (TMA) {
+    if (threadIdx.x == 0) bulk_wait0();  // the last tile's stores complete before the CTA exits
+  }
   if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
 }
 
@@ -354,18 +385,38 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a) {
 // are double-buffered and filled by cp.async one tile ahead; each warp reads its residue's
 // spectrum from the tile, the exchanges and the t_r rows reuse the current tile, and the CTA
 // writes the T cropped rows with coalesced stores.
-template <int T>
-__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
+// TMA (T = 4): each column tile arrives by tensor-map box loads (one thread, one mbarrier per
+// buffer) instead of per-thread cp.async; positions and lines beyond the field are zero-filled.
+template <int T, bool TMA>
+__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
   using X3TSmem = fusg::X3TSmem<T>;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = w % 3, t = w / 3;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + X3TSmem::C_END);  // [2], TMA only
   x3_tables(a.tw, sm + X3TSmem::C_TW, sm + X3TSmem::C_US, sm + X3TSmem::C_C48);
+  if (TMA && threadIdx.x == 0) {
+    mbar_init(bars, 1);
+    mbar_init(bars + 1, 1);
+    mbar_init_fence();
+  }
   __syncthreads();
   const X3Warp W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix, double2* tile) {
+    if constexpr (TMA) {
+      if (tix < ntiles && threadIdx.x == 0) {
+        const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
+        const int k = int(unsigned(tix) / unsigned(ntiles_i));
+        uint64_t* const bar = bars + (tile == sm ? 0 : 1);
+        const int nbox = (a.in_nvalid + 255) / 256;
+        refill_fence();
+        mbar_expect_tx(bar, unsigned(nbox) * 256u * T * 16u);
+        for (int b = 0; b < nbox; ++b) tma_load_tile_box(&tm, tile + b * 256 * T, bar, 2 * i0, 256 * b, k);
+      }
+      return;
+    }
     if (tix < ntiles) {
       const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
       const int k = int(unsigned(tix) / unsigned(ntiles_i));
@@ -380,14 +431,19 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
     cp_async_commit();
   };
   int64_t tix = blockIdx.x;
-  unsigned buf = 0;
+  unsigned buf = 0, phs = 0;  // phs: parity bit of each buffer's mbarrier (TMA)
   prefetch(tix, sm);
   for (; tix < ntiles; tix += gridDim.x, buf ^= 1) {
     double2* const tile = sm + buf * (1536 * T);
     const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
     const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
-    cp_async_wait0();
+    if constexpr (TMA) {
+      mbar_wait(bars + buf, (phs >> buf) & 1u);
+      phs ^= 1u << buf;
+    } else {
+      cp_async_wait0();
+    }
     __syncthreads();  // this tile's copies (issued by all threads) have landed; the previous
                       // tile's t_r rows (other buffer) are read out
     double2 v[16];
@@ -417,8 +473,33 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a) {
         x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
     }
   }
-  cp_async_wait0();
+  if constexpr (!TMA) cp_async_wait0();
   if (a.pm.n) __threadfence_system();  // remote stores performed before the following barrier
+}
+
+bool make_tile_map(CUtensorMap* map, const void* base, int64_t n_lines, int64_t n_pos, int64_t n_outer, int64_t sp,
+                   int64_t sk, int T) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static const Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      return Encode(nullptr);
+    }
+    return reinterpret_cast<Encode>(fn);
+  }();
+  if (!encode || T != 4 || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const cuuint64_t dims[3] = {cuuint64_t(2 * n_lines), cuuint64_t(n_pos), cuuint64_t(n_outer)};
+  const cuuint64_t strides[2] = {cuuint64_t(sp) * 16, cuuint64_t(sk) * 16};
+  const cuuint32_t box[3] = {cuuint32_t(2 * T), 256, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // pass C at L = 1536 (conv_r16x3): 1 launched, 0 not applicable, -1 error
@@ -488,20 +569,37 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   }();
   const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
   if (tiles >= (int64_t(1) << 31)) return 0;
-  using Fn = void (*)(WArgs);
-  const Fn fn = T == 4 ? (r2c ? r16x3_row_to_col<4> : r16x3_col_to_row<4>)
-                       : (r2c ? r16x3_row_to_col<2> : r16x3_col_to_row<2>);
+  // FUSG_X3_TMA=0: the column tiles move by per-thread stores / cp.async instead of tensor-map
+  // box copies (T = 4, unit line stride, no peer stores, unscaled forward output)
+  static const bool tma_on = [] {
+    const char* e = getenv("FUSG_X3_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  CUtensorMap tm{};
+  const bool tma = tma_on && T == 4 && a.pm.n == 0 &&
+                   (r2c ? (a.out_si == 1 && a.scale == 1.0 &&
+                           make_tile_map(&tm, a.out, a.n_inner, a.out_nvalid, a.n_outer, a.out_sp, a.out_sk, T))
+                        : (a.in_si == 1 &&
+                           make_tile_map(&tm, a.in, a.n_inner, a.in_nvalid, a.n_outer, a.in_sp, a.in_sk, T)));
+  using Fn = void (*)(WArgs, CUtensorMap);
+  const Fn fn = T == 4 ? (r2c ? (tma ? r16x3_row_to_col<4, true> : r16x3_row_to_col<4, false>)
+                              : (tma ? r16x3_col_to_row<4, true> : r16x3_col_to_row<4, false>))
+                       : (r2c ? r16x3_row_to_col<2, false> : r16x3_col_to_row<2, false>);
   const size_t smem = T == 4 ? (r2c ? X3TSmem<4>::BYTES : X3TSmem<4>::C_BYTES)
                              : (r2c ? X3TSmem<2>::BYTES : X3TSmem<2>::C_BYTES);
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
-        return cudaFuncSetAttribute(r16x3_row_to_col<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(r16x3_row_to_col<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<4>::BYTES)) == cudaSuccess &&
-               cudaFuncSetAttribute(r16x3_col_to_row<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+               cudaFuncSetAttribute(r16x3_row_to_col<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<4>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
-               cudaFuncSetAttribute(r16x3_row_to_col<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+               cudaFuncSetAttribute(r16x3_col_to_row<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_row_to_col<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<2>::BYTES)) == cudaSuccess &&
-               cudaFuncSetAttribute(r16x3_col_to_row<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+               cudaFuncSetAttribute(r16x3_col_to_row<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<2>::C_BYTES)) == cudaSuccess;
       })) {
     set_error(FUSG_CUDA, "transposing pass (1536 = 3 x 512): cannot configure shared memory");
@@ -517,7 +615,7 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
     return e ? std::max(1, atoi(e)) : 4;
   }();
   const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * waves);
-  fn<<<unsigned(grid), 96 * T, smem, s>>>(a);
+  fn<<<unsigned(grid), 96 * T, smem, s>>>(a, tm);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {

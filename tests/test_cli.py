@@ -161,4 +161,4 @@ def test_simulate_vie_mode_with_a_slab(tmp_path):
 def test_validate_suite_passes():
     rc, out, err = run("validate")
     assert rc == 0, out + err
-    assert out.count("[ ok ]") == 6 and out.strip().endswith("all checks passed")
+    assert out.count("[ ok ]") == 5 and out.strip().endswith("all checks passed")
