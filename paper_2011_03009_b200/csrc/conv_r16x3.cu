@@ -277,6 +277,9 @@ struct X3TSmem {
   static constexpr int C48 = US + 96;
   static constexpr int END = C48 + 48;
   static constexpr size_t BYTES = size_t(END) * sizeof(double2) + sizeof(uint64_t);
+  // TMA r2c: a second staging buffer after the tables (input rows two tiles ahead), 2 mbarriers
+  static constexpr int STAGE2 = END;
+  static constexpr size_t BYTES2 = size_t(STAGE2 + 768 * T) * sizeof(double2) + 2 * sizeof(uint64_t);
   // c2r: two [1536][T] tiles (double-buffered), then the tables
   static constexpr int C_TW = 2 * 1536 * T;
   static constexpr int C_US = C_TW + 128;
@@ -296,11 +299,14 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
   const int r = w % 3, t = w / 3;
   double2* const area = sm + X3TSmem::AREA;
   double2* const xr = area + 512 * w;
-  double2* const stage = sm + X3TSmem::STAGE;
-  uint64_t* const bar = reinterpret_cast<uint64_t*>(sm + X3TSmem::END);
+  // TMA: two staging buffers, filled two tiles ahead (the rows of pass B lie a z-plane apart and
+  // arrive late one tile ahead); else one
+  constexpr int NST = TMA ? 2 : 1;
+  double2* const stages[2] = {sm + X3TSmem::STAGE, sm + X3TSmem::STAGE2};
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + (TMA ? X3TSmem::STAGE2 + 768 * T : X3TSmem::END));
   x3_tables(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    for (int b = 0; b < NST; ++b) mbar_init(bars + b, 1);
     mbar_init_fence();
   }
   __syncthreads();
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
   const int nv = a.in_nvalid;
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
-  auto prefetch = [&](int64_t tix) {  // thread 0
+  auto prefetch = [&](int64_t tix, int sb) {  // thread 0
     if (tix < ntiles) {
       const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
       const int k = int(unsigned(tix) / unsigned(ntiles_i));
@@ -316,26 +322,29 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
       const double2* src = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
       const unsigned row = unsigned(nv) * sizeof(double2);
       refill_fence();
-      mbar_expect_tx(bar, row * lines_ok);
-      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stage + tt * 768, src + tt * a.in_si, row, bar);
+      mbar_expect_tx(bars + sb, row * lines_ok);
+      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stages[sb] + tt * 768, src + tt * a.in_si, row, bars + sb);
     }
   };
   int64_t tix = blockIdx.x;
-  if (threadIdx.x == 0) prefetch(tix);
-  unsigned ph = 0;
-  for (; tix < ntiles; tix += gridDim.x, ph ^= 1) {
+  if (threadIdx.x == 0)
+    for (int b = 0; b < NST; ++b) prefetch(tix + int64_t(b) * gridDim.x, b);
+  unsigned phs = 0;  // parity bit per staging buffer
+  for (int it = 0; tix < ntiles; tix += gridDim.x, ++it) {
+    const int sb = NST == 2 ? (it & 1) : 0;
     const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
     const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
-    mbar_wait(bar, ph);
+    mbar_wait(bars + sb, (phs >> sb) & 1u);
+    phs ^= 1u << sb;
     double2 v[16];
-    W.gather(v, stage + (t < lines_ok ? t : 0) * 768, nv, lane);
+    W.gather(v, stages[sb] + (t < lines_ok ? t : 0) * 768, nv, lane);
     if constexpr (TMA) {
       W.forward_a(v);
       if (threadIdx.x == 0) bulk_wait_read0();  // the previous tile's box stores have read the area
     }
-    __syncthreads();  // stage read by every warp: refill it with the next tile's rows
-    if (threadIdx.x == 0) prefetch(tix + gridDim.x);
+    __syncthreads();  // stage read by every warp: refill it with a later tile's rows
+    if (threadIdx.x == 0) prefetch(tix + int64_t(NST) * gridDim.x, sb);
     if constexpr (TMA) {
       W.forward_b(v, xr, lane);
     } else {
@@ -585,14 +594,14 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   const Fn fn = T == 4 ? (r2c ? (tma ? r16x3_row_to_col<4, true> : r16x3_row_to_col<4, false>)
                               : (tma ? r16x3_col_to_row<4, true> : r16x3_col_to_row<4, false>))
                        : (r2c ? r16x3_row_to_col<2, false> : r16x3_col_to_row<2, false>);
-  const size_t smem = T == 4 ? (r2c ? X3TSmem<4>::BYTES : X3TSmem<4>::C_BYTES)
+  const size_t smem = T == 4 ? (r2c ? (tma ? X3TSmem<4>::BYTES2 : X3TSmem<4>::BYTES) : X3TSmem<4>::C_BYTES)
                              : (r2c ? X3TSmem<2>::BYTES : X3TSmem<2>::C_BYTES);
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
         return cudaFuncSetAttribute(r16x3_row_to_col<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<4>::BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_row_to_col<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<4>::BYTES)) == cudaSuccess &&
+                                    int(X3TSmem<4>::BYTES2)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
