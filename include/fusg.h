@@ -191,8 +191,8 @@ fusg_status fusg_rhs_source(fusg_ctx* ctx, int32_t n, const double* const* lower
                             void* stream);
 /* The paper's full quadratic source (Eq. cascade_1) truncated at M harmonics:
  * out = coeff * [sum_{m=1}^{n-1} p_m p_{n-m} + 2 sum_{m=n+1}^{M} p_m conj(p_{m-n})], coeff as
- * fusg_rhs_source. fields_dev holds M device pointers p_1 .. p_M (entry n-1, p_n, is not read
- * and may be null). M = n-1 is bitwise fusg_rhs_source. The reference keeps only the first
+ * fusg_rhs_source. fields_dev holds M device pointers p_1 .. p_M (p_n, entry n-1, is read only
+ * through p_{2n} conj(p_n), so it may be null when 2n > M). M = n-1 is bitwise fusg_rhs_source. The reference keeps only the first
  * sum (src/cascade.cpp:36-39); this entry serves iterated sweeps. Parity: numpy restatement. */
 fusg_status fusg_rhs_source_full(fusg_ctx* ctx, int32_t n, const double* const* fields_dev, int32_t M,
                                  int64_t count, const fusg_medium* m, double omega, double* out_dev,

@@ -547,7 +547,15 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     return e ? std::max(1, atoi(e)) : 4;
   }();
   const int64_t grid = std::min<int64_t>(nl, int64_t(per_sm) * ctx->num_sms * waves);
-  fn<<<unsigned(grid), 96, smem, s>>>(a);
+  // FUSG_X3_QUAD (default 1): the (up to) four lines sharing a folded K^ row run consecutively,
+  // so each row is read from DRAM about once (cfg5 pass C reads 48.4 -> 40.1 GB, apply -1 %)
+  static const bool quad = [] {
+    const char* e = getenv("FUSG_X3_QUAD");
+    return !(e && atoi(e) == 0);
+  }();
+  WArgs b = a;
+  if (quad) b.ko.quad = 1;
+  fn<<<unsigned(grid), 96, smem, s>>>(b);
   ctx->launches++;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {

@@ -166,11 +166,14 @@ struct GLoadAt {
 };
 
 // Plain strided global store of positions < nvalid (pruned output), times scale.
+// first > 0 (kernel-spectrum build of an x-slab kernel): only positions [first, nvalid) are
+// stored, position pos at (pos - first) * sp.
 struct GStore {
   double2* p;
   int64_t si, sk, sp;
   int nvalid;
   double scale;  // 1.0 -> no multiply
+  int first = 0;
 };
 struct GStoreAt {
   static constexpr bool kSmem = false;
@@ -179,8 +182,9 @@ struct GStoreAt {
   int nvalid;
   bool ok;
   double scale;
+  int first;
   __device__ __forceinline__ void store(int pos, int, double2 v) const {
-    if (ok && pos < nvalid) base[pos * sp] = (scale == 1.0) ? v : cscale(v, scale);
+    if (ok && pos >= first && pos < nvalid) base[(pos - first) * sp] = (scale == 1.0) ? v : cscale(v, scale);
   }
 };
 

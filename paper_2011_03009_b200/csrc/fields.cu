@@ -792,9 +792,9 @@ fusg_status rhs_full_dev(fusg_ctx* ctx, int n, const double2* const* fields, int
   if (M < n - 1) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: need p_1 .. p_{n-1}");
   if (M > 32) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: at most 32 harmonics");
   LowerPtrs lp{};
-  for (int m = 0; m < M; ++m) {
-    if (m == n - 1) continue;  // p_n itself never enters its own source
-    if (!fields[m]) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: null harmonic field");
+  for (int m = 0; m < M; ++m) {  // p_n enters through p_{2n} conj(p_n) when 2n <= M
+    if (!fields[m] && m != n - 1) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: null harmonic field");
+    if (!fields[m] && 2 * n <= M) return set_error(FUSG_INVALID_ARGUMENT, "rhs_source_full: p_n is needed when 2n <= M");
     lp.p[m] = fields[m];
   }
   rhs_full_kernel<<<grid_stride_blocks(ctx, count, 256), 256, 0, s>>>(lp, n, M, count, coeff, out);

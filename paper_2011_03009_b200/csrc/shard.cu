@@ -27,6 +27,19 @@ constexpr size_t kC = sizeof(double2);
 
 int64_t row(const fusg_kernel* K) { return K->grid.dims[1]; }  // Ny: elements per (kx, z) row
 
+// The all-to-all staging buffer [p][nx][nz_p][Ny] of the NCCL transport, allocated on first use.
+fusg_status ensure_rbuf(fusg_kernel* K, cudaStream_t s) {
+  if (K->rbuf) return FUSG_OK;
+  const size_t n = size_t(K->nx) * K->grid.dims[2] * K->grid.dims[1];
+  if (cudaMallocAsync(&K->rbuf, std::max<size_t>(n, 1) * sizeof(double2), s) != cudaSuccess) {
+    cudaGetLastError();
+    K->rbuf = nullptr;
+    return set_error(FUSG_OOM, "slab apply: exchange buffer allocation failed");
+  }
+  K->bytes += n * sizeof(double2);
+  return FUSG_OK;
+}
+
 // The exchange plan (element offsets/counts per peer), shared by the NCCL and loopback
 // transports and exported as fusg_slab_exchange_plan:
 //   a_off/a_cnt[q]: block of A_r [Px][nz_r][Ny] holding rank q's kx columns (send in exchange 1,
@@ -284,6 +297,7 @@ fusg_status fusg_kernel_apply_slab(fusg_kernel* K, const double* f_dev, double* 
   FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
   std::lock_guard<std::mutex> lock(K->mu);
   cudaStream_t s = ctx->pick(stream);
+  FUSG_TRY(ensure_rbuf(K, s));
   FUSG_TRY(apply_phase_A(K, reinterpret_cast<const double2*>(f_dev), s));
   FUSG_TRY(nccl_alltoallv(ctx, K->bufA, [&](int q) { return a_off(K, q); }, [&](int q) { return a_cnt(K, q); },
                           K->rbuf, [&](int p) { return r_off(K, p); }, [&](int p) { return r_cnt(K, p); },
@@ -308,6 +322,7 @@ fusg_status fusg_kernel_apply_slab_loopback(fusg_kernel* const* ranks, int32_t n
   fusg_ctx* ctx = ranks[0]->ctx;
   FUSG_CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t s = ctx->stream;
+  for (int r = 0; r < nranks; ++r) FUSG_TRY(ensure_rbuf(ranks[r], s));
   const int G = nranks;
   for (int r = 0; r < G; ++r) FUSG_TRY(apply_phase_A(ranks[r], reinterpret_cast<const double2*>(f_dev[r]), s));
   for (int r = 0; r < G; ++r)  // exchange 1: p's A slice for r -> r's rbuf block p

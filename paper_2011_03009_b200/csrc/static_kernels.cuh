@@ -21,7 +21,7 @@ struct GLoadF {
 struct GStoreF {
   GStore g;
   __device__ __forceinline__ GStoreAt at(int i, int k, bool ok) const {
-    return GStoreAt{g.p + i * g.si + k * g.sk, g.sp, g.nvalid, ok, g.scale};
+    return GStoreAt{g.p + i * g.si + k * g.sk, g.sp, g.nvalid, ok, g.scale, g.first};
   }
 };
 

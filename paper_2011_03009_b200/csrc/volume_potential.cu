@@ -1492,15 +1492,16 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   if (alloc_ipc(&K->bufA, nA) != cudaSuccess ||
       cudaMallocAsync(&K->bufB, nB * sizeof(double2), as) != cudaSuccess ||
       cudaMallocAsync(&K->koct, nK * sizeof(double2), as) != cudaSuccess ||
-      (nX && alloc_ipc(&K->xbuf, nX) != cudaSuccess) ||
-      (nX && cudaMallocAsync(&K->rbuf, nX * sizeof(double2), as) != cudaSuccess)) {
+      (nX && alloc_ipc(&K->xbuf, nX) != cudaSuccess)) {
     cudaGetLastError();
     return set_error(FUSG_OOM, "GreenKernel: device allocation failed");
   }
   // build scratch: the apply workspaces are idle during the build, so G1/G2 live in bufA/bufB
   // whenever they fit (always unsharded) -- the peak stays at the apply's own footprint, which
   // is what lets a 1024^3 grid (2048^3 embedding) fit in one B200
-  const size_t n1 = size_t(Hx) * Ny * Nz, n2 = size_t(Hx) * Hy * Nz;  // (G2 only fills kx rows [kf0, kf0 + knf))
+  // G1 and G2 hold only the kx window [kf0, kf0 + knf) (compact, row stride knf; all Hx rows
+  // unsharded): the x pass still transforms every (oy, oz) line but stores the window
+  const size_t n1 = size_t(std::max(knf, 1)) * Ny * Nz, n2 = size_t(std::max(knf, 1)) * Hy * Nz;
   const bool g1_in_A = n1 <= nA, g2_in_B = n2 <= nB;
   g1 = g1_in_A ? K->bufA : nullptr;
   g2 = g2_in_B ? K->bufB : nullptr;
@@ -1510,24 +1511,26 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
     if (g1 && !g1_in_A) cudaFreeAsync(g1, as);
     return set_error(FUSG_OOM, "GreenKernel: build scratch allocation failed");
   }
-  K->bytes = (nA + nB + nK + 2 * nX) * sizeof(double2);
+  // (the all-to-all staging buffer rbuf, nX elements, is allocated by the first NCCL-transport
+  // apply: the fused peer-store transport never needs it)
+  K->bytes = (nA + nB + nK + nX) * sizeof(double2);
 
   fusg_ctx* ctx = K->ctx;
   cudaStream_t s = ctx->stream;
   const double dx = K->grid.dx;
   // G1: generate K along x for offsets (oy, oz) >= 0, forward x, keep kx <= Px/2
   KGenF gen{Nx, Ny, Px, dx, dx * dx * dx, K->k.k_re, K->k.k_im, self};
-  GStoreF s1{GStore{g1, Hx, 0, 1, Hx, 1.0}};
+  GStoreF s1{GStore{g1, std::max(knf, 1), 0, 1, kf0 + knf, 1.0, kf0}};
   FUSG_TRY(launch_axis<false>(ctx, K->plan[0], Ny * Nz, 1, gen, s1, s));
   // G2: even extension along y, forward y, keep ky <= Py/2 (kx rows [kf0, kf0 + knf) only:
   // the y and z transforms are independent per kx, so an x-slab kernel builds just its window;
   // the x pass above is the replicated part of a sharded build, and no collective is needed)
   if (knf > 0) {
-    FoldF l2{g1 + kf0, 1, int64_t(Ny) * Hx, Hx, Ny, Py};
-    GStoreF s2{GStore{g2 + kf0, 1, int64_t(Hy) * Hx, Hx, Hy, 1.0}};
+    FoldF l2{g1, 1, int64_t(Ny) * knf, knf, Ny, Py};
+    GStoreF s2{GStore{g2, 1, int64_t(Hy) * knf, knf, Hy, 1.0}};
     FUSG_TRY(launch_axis<false>(ctx, K->plan[1], knf, Nz, l2, s2, s));
     // G3: even extension along z, forward z, keep kz <= Pz/2 -> octant rows [kf0, kf0 + knf)
-    FoldF l3{g2 + kf0, 1, Hx, int64_t(Hy) * Hx, Nz, Pz};
+    FoldF l3{g2, 1, knf, int64_t(Hy) * knf, Nz, Pz};
     GStoreF s3{GStore{K->koct, int64_t(Hy) * Hz, Hz, 1, Hz, 1.0}};  // octant [kx - kf0][ky][kz]
     FUSG_TRY(launch_axis<false>(ctx, K->plan[2], knf, Hy, l3, s3, s));
   }

@@ -634,14 +634,15 @@ def rhs_source_full(n: int, fields: Sequence[HarmonicField], m: Medium, omega: f
                     ctx: Optional[Context] = None):
     """The paper's full quadratic source truncated at M = len(fields):
     coeff * [sum_{m<n} p_m p_{n-m} + 2 sum_{m=n+1}^{M} p_m conj(p_{m-n})]; fields = p_1 .. p_M on
-    one grid (fields[n-1] is not read). M = n - 1 reproduces rhs_source bit for bit."""
+    one grid (fields[n-1], p_n, enters only through p_{2n} conj(p_n) and may be None when
+    2n > M). M = n - 1 reproduces rhs_source bit for bit."""
     ctx = ctx or context()
     M = len(fields)
     if n < 2:
         raise ValueError("rhs_source: harmonic index must be >= 2")
     if M < n - 1:
         raise ValueError(f"rhs_source_full: missing lower harmonics for n = {n}")
-    vals = [None if (i == n - 1 or fields[i] is None) else _on_device(fields[i].values, ctx) for i in range(M)]
+    vals = [None if fields[i] is None else _on_device(fields[i].values, ctx) for i in range(M)]
     count = next(v for v in vals if v is not None).numel()
     if any(v is not None and v.numel() != count for v in vals):
         raise ValueError("rhs_source_full: harmonics live on different grids")

@@ -325,11 +325,15 @@ def test_rhs_source_full_conjugate_terms(ctx, orc):
         for M in range(n, 7):
             got = host(fus.rhs_source_full(n, hf[:M], w, omega))
             assert np.array_equal(got, orc.rhs_source_full(n, ho[:M], wo, omega)), (n, M)
-    # p_n itself is not read: passing None in its slot gives the same source
+    # p_n enters only through p_{2n} conj(p_n): with 2n > M its slot may be None
     withnone = list(hf[:5])
     withnone[2] = None
     assert np.array_equal(host(fus.rhs_source_full(3, withnone, w, omega)),
                           host(fus.rhs_source_full(3, hf[:5], w, omega)))
+    withnone = list(hf[:4])
+    withnone[1] = None
+    with pytest.raises(ValueError):  # n = 2, M = 4: p_4 conj(p_2) needs p_2
+        fus.rhs_source_full(2, withnone, w, omega)
     with pytest.raises(ValueError):
         fus.rhs_source_full(4, hf[:2], w, omega)
 
