@@ -115,6 +115,47 @@ struct X3Warp {
     dft16<false>(v);
     r16_twiddle_u<false>(v, u, w1, w2, w4, w8);
   }
+  // the exchange, stage B, and the last radix 2 fused with the folded-K^ multiply: the two K^
+  // values of step I + 1 are read from shared memory while step I shuffles, so their latency
+  // hides behind the half-exchange (the separate multiply loop stalled on each load)
+  __device__ __forceinline__ void forward_b_mulk(double2* v, double2* xr, int lane, const double2* kb,
+                                                 uint64_t* kbar, unsigned kph) const {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 16; ++h) v[h] = xr[r16_ex(k1, 2 * h + int(b))];
+    dft16<false>(v);
+    mbar_wait(kbar, kph);  // this line's K^ row has landed
+    // slot i holds X[3 k' + r] with k' = k1 + 16 (i + 8 b) (< 256) and slot i + 8 its k' + 256 twin,
+    // whose folded K^ index is 768 - j
+    const int jb = 3 * k1 + 384 * int(b) + r;
+    double2 ka = kb[jb], kz = kb[768 - jb];
+    r2_mulk<0>(v, kb, jb, ka, kz);
+    r2_mulk<1>(v, kb, jb, ka, kz);
+    r2_mulk<2>(v, kb, jb, ka, kz);
+    r2_mulk<3>(v, kb, jb, ka, kz);
+    r2_mulk<4>(v, kb, jb, ka, kz);
+    r2_mulk<5>(v, kb, jb, ka, kz);
+    r2_mulk<6>(v, kb, jb, ka, kz);
+    r2_mulk<7>(v, kb, jb, ka, kz);
+  }
+  template <int I>
+  __device__ __forceinline__ void r2_mulk(double2* v, const double2* kb, int jb, double2& ka, double2& kz) const {
+    double2 na, nz;
+    if constexpr (I + 1 < 8) {
+      const int j = jb + 48 * (I + 1);
+      na = kb[j];
+      nz = kb[768 - j];
+    }
+    r16_fwd_r2<I>(v, b);
+    v[I] = cmul(v[I], ka);
+    v[I + 8] = cmul(v[I + 8], kz);
+    if constexpr (I + 1 < 8) {
+      ka = na;
+      kz = nz;
+    }
+  }
   // the exchange through xr and stage B
   __device__ __forceinline__ void forward_b(double2* v, double2* xr, int lane) const {
 #pragma unroll
@@ -156,6 +197,47 @@ __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* 
     const double2 d = csub(t1, t2);
     const double2 o = make_double2(t0.x - 0.5 * s.x - kS3 * d.y, t0.y - 0.5 * s.y + kS3 * d.x);
     out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
+  }
+}
+
+// a thread's share (n = t0, t0 + NT, ... < 512) of the recombination, every shared load issued
+// before the arithmetic (the per-position loop waited on each load)
+template <int NT, int G>
+__device__ __forceinline__ void x3_recombine_group(const double2* x, int t0, int onv, double sc, double2* out);
+template <int NT, int G = 2>
+__device__ __forceinline__ void x3_recombine_all(const double2* x, int t0, int onv, double sc, double2* out) {
+  constexpr int J = (512 + NT - 1) / NT;
+#pragma unroll
+  for (int j0 = 0; j0 < J; j0 += G) x3_recombine_group<NT, G>(x, t0 + NT * j0, onv, sc, out);
+}
+template <int NT, int G>
+__device__ __forceinline__ void x3_recombine_group(const double2* x, int t0, int onv, double sc, double2* out) {
+  double2 a[G], b[G], c[G];
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const int n = t0 + NT * j;
+    if (n < 512) {
+      a[j] = x[n];
+      b[j] = x[512 + n];
+      c[j] = x[1024 + n];
+    }
+  }
+  constexpr double kS3 = 0.8660254037844386467637;
+#pragma unroll
+  for (int j = 0; j < G; ++j) {
+    const int n = t0 + NT * j;
+    if (n >= 512) break;
+    const double2 t0v = a[j], t1 = b[j], t2 = c[j];
+    const double2 s = cadd(t1, t2);
+    if (n < onv) {
+      const double2 o = cadd(t0v, s);
+      out[n] = sc == 1.0 ? o : cscale(o, sc);
+    }
+    if (n + 512 < onv) {
+      const double2 d = csub(t1, t2);
+      const double2 o = make_double2(t0v.x - 0.5 * s.x - kS3 * d.y, t0v.y - 0.5 * s.y + kS3 * d.x);
+      out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
+    }
   }
 }
 
@@ -239,15 +321,9 @@ __global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
     }
     __syncthreads();  // the staged row is read by all three warps: refill it
     if (threadIdx.x == 0) prefetch_in(line + stride);
-    W.forward(v, xr, lane);
-    // X[3k' + r] times the folded K^ row
-    mbar_wait(bars + 1, ph);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int j = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;  // < 768; its partner j + 768 folds to 768 - j
-      v[i] = cmul(v[i], kb[j]);
-      v[i + 8] = cmul(v[i + 8], kb[768 - j]);
-    }
+    // X[3k' + r] times the folded K^ row, fused into the last forward stage
+    W.forward_a(v);
+    W.forward_b_mulk(v, xr, lane, kb, bars + 1, ph);
     __syncthreads();  // K^ row read
     if (threadIdx.x == 0) prefetch_k(line + stride);
     W.inverse(v, xr, lane);
