@@ -113,7 +113,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     for (int h = 0; h < 16; ++h) v[h] = xb[r16_ex(k1, 2 * h + int(b))];
     // forward stage B and the cross-lane radix 2
     dft16<false>(v);
-    r16_r2_all<false>(v, b, I8);
+    if constexpr (!KL2) {
+      // the cross-lane radix 2 fused with the folded-K^ multiply (p < 256, mirror 256 - p)
+      mbar_wait(bars + 1, ph_k);
+      ph_k ^= 1;
+      r16_fwd_r2_mulk_all<16, 256>(v, b, kb, k1 + 128 * int(b), I8);
+      __syncwarp();  // K^ row consumed
+      prefetch_k(line + stride);
+    } else {
+      r16_r2_all<false>(v, b, I8);
+    }
     if constexpr (KL2) {
       int ky, kx;
       coords(line, ky, kx);
@@ -125,17 +134,6 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
         v[i] = cmul(v[i], __ldg(kl + p));
         v[i + 8] = cmul(v[i + 8], __ldg(kl + 256 - p));
       }
-    } else {
-      mbar_wait(bars + 1, ph_k);
-      ph_k ^= 1;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
-        v[i] = cmul(v[i], kb[p]);
-        v[i + 8] = cmul(v[i + 8], kb[256 - p]);
-      }
-      __syncwarp();  // K^ row consumed
-      prefetch_k(line + stride);
     }
     // inverse: radix 2 (in-lane) + half-exchange back, stage B, exchange, twiddle, stage A
     r16_r2_all<true>(v, b, I8);

@@ -129,32 +129,7 @@ struct X3Warp {
     mbar_wait(kbar, kph);  // this line's K^ row has landed
     // slot i holds X[3 k' + r] with k' = k1 + 16 (i + 8 b) (< 256) and slot i + 8 its k' + 256 twin,
     // whose folded K^ index is 768 - j
-    const int jb = 3 * k1 + 384 * int(b) + r;
-    double2 ka = kb[jb], kz = kb[768 - jb];
-    r2_mulk<0>(v, kb, jb, ka, kz);
-    r2_mulk<1>(v, kb, jb, ka, kz);
-    r2_mulk<2>(v, kb, jb, ka, kz);
-    r2_mulk<3>(v, kb, jb, ka, kz);
-    r2_mulk<4>(v, kb, jb, ka, kz);
-    r2_mulk<5>(v, kb, jb, ka, kz);
-    r2_mulk<6>(v, kb, jb, ka, kz);
-    r2_mulk<7>(v, kb, jb, ka, kz);
-  }
-  template <int I>
-  __device__ __forceinline__ void r2_mulk(double2* v, const double2* kb, int jb, double2& ka, double2& kz) const {
-    double2 na, nz;
-    if constexpr (I + 1 < 8) {
-      const int j = jb + 48 * (I + 1);
-      na = kb[j];
-      nz = kb[768 - j];
-    }
-    r16_fwd_r2<I>(v, b);
-    v[I] = cmul(v[I], ka);
-    v[I + 8] = cmul(v[I + 8], kz);
-    if constexpr (I + 1 < 8) {
-      ka = na;
-      kz = nz;
-    }
+    r16_fwd_r2_mulk_all<48, 768>(v, b, kb, 3 * k1 + 384 * int(b) + r, std::make_integer_sequence<int, 8>{});
   }
   // the exchange through xr and stage B
   __device__ __forceinline__ void forward_b(double2* v, double2* xr, int lane) const {

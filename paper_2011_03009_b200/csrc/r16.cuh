@@ -74,6 +74,35 @@ __device__ __forceinline__ void r16_inv_r2(double2* v, bool b) {
   v[I] = sel_d2(b, recv, z0);
   v[I + 8] = sel_d2(b, z1, recv);
 }
+// The forward cross-lane radix 2 fused with the spectral multiply by a folded K^ row in shared
+// memory: after step I, slot I is multiplied by kb[p0 + STEP I] and slot I + 8 by its mirror
+// kb[MIR - p0 - STEP I].  The two K^ values of step I + 1 are loaded before step I's
+// half-exchange, so their shared-load latency hides behind the shuffle (a separate multiply
+// loop waits on every load).
+template <int STEP, int MIR, int I>
+__device__ __forceinline__ void r16_fwd_r2_mulk(double2* v, bool b, const double2* kb, int p0, double2& ka,
+                                                double2& kz) {
+  double2 na, nz;
+  if constexpr (I + 1 < 8) {
+    const int p = p0 + STEP * (I + 1);
+    na = kb[p];
+    nz = kb[MIR - p];
+  }
+  r16_fwd_r2<I>(v, b);
+  v[I] = cmul(v[I], ka);
+  v[I + 8] = cmul(v[I + 8], kz);
+  if constexpr (I + 1 < 8) {
+    ka = na;
+    kz = nz;
+  }
+}
+template <int STEP, int MIR, int... Is>
+__device__ __forceinline__ void r16_fwd_r2_mulk_all(double2* v, bool b, const double2* kb, int p0,
+                                                    std::integer_sequence<int, Is...>) {
+  double2 ka = kb[p0], kz = kb[MIR - p0];
+  (r16_fwd_r2_mulk<STEP, MIR, Is>(v, b, kb, p0, ka, kz), ...);
+}
+
 template <bool INV, int... Is>
 __device__ __forceinline__ void r16_r2_all(double2* v, bool b, std::integer_sequence<int, Is...>) {
   if constexpr (INV) (r16_inv_r2<Is>(v, b), ...);
