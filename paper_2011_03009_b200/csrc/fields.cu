@@ -186,13 +186,19 @@ __device__ __forceinline__ void stage_sources(const double* src, int n_src, int 
 
 // kVPT adjacent voxels of one x-row per thread: the (y, z) part of the squared distance is
 // shared, the source loads are amortised and the thread carries kVPT independent chains.
-constexpr int kVPT = 4;
+#ifndef FUSG_MONO_VPT
+#define FUSG_MONO_VPT 4
+#endif
+#ifndef FUSG_MONO_THREADS
+#define FUSG_MONO_THREADS 256
+#endif
+constexpr int kVPT = FUSG_MONO_VPT;
 #ifndef FUSG_MONO_MINB
 #define FUSG_MONO_MINB 1  // CTAs per SM the grid kernel's register budget targets (4: 64 registers, measured equal: FP64-bound)
 #endif
 
 template <int ATT>
-__global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(const double* __restrict__ src, int n_src,
+__global__ void __launch_bounds__(FUSG_MONO_THREADS, FUSG_MONO_MINB) monopole_grid_kernel(const double* __restrict__ src, int n_src,
                                                             GridDev g, double k1, double kim,
                                                             double amp, double2* __restrict__ out,
                                                             int* flag, int n_eh = 0) {
@@ -225,6 +231,11 @@ __global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(cons
 #pragma unroll
   for (int v = 0; v < kVPT; ++v) acc[v] = make_double2(0.0, 0.0);
   bool bad = false;
+  // The bowl's points come ring by ring (distribute_points), and every point of a ring has the
+  // same x (one polar angle): the x part (x_v - s_x)^2 of the squared distance is recomputed only
+  // when s_x changes (a warp-uniform branch), one FP64 subtraction per term fewer.
+  double px[kVPT];
+  double s_prev = __longlong_as_double(0x7ff8000000000000LL);  // NaN: the first source differs
   for (int base = 0; base < n_src; base += kSrcChunk) {
     __syncthreads();
     stage_sources(src, n_src, base, sx, sy, sz, k1);
@@ -233,14 +244,20 @@ __global__ void __launch_bounds__(256, FUSG_MONO_MINB) monopole_grid_kernel(cons
       const int n = min(kSrcChunk, n_src - base);
       #pragma unroll 2
       for (int j = 0; j < n; ++j) {
+        const double s0 = sx[j];
+        if (s0 != s_prev) {
+          s_prev = s0;
+#pragma unroll
+          for (int v = 0; v < kVPT; ++v) {
+            const double ddx = x[v] - s0;
+            px[v] = ddx * ddx;
+          }
+        }
         const double ddy = y - sy[j], ddz = z - sz[j];
         const double q = fma(ddz, ddz, ddy * ddy);
-        const double s0 = sx[j];
 #pragma unroll
-        for (int v = 0; v < kVPT; ++v) {
-          const double ddx = x[v] - s0;
-          monopole_term_d2<ATT, true, kGridPhaseBits>(fma(ddx, ddx, q), k1, kim, tab, acc[v], bad, eh, tiny_bits);
-        }
+        for (int v = 0; v < kVPT; ++v)
+          monopole_term_d2<ATT, true, kGridPhaseBits>(px[v] + q, k1, kim, tab, acc[v], bad, eh, tiny_bits);
       }
     }
   }
@@ -679,7 +696,7 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   }
   const int64_t count = int64_t((gd.dims[0] + kVPT - 1) / kVPT) * gd.dims[1] * gd.dims[2];
   if (count == 0) return FUSG_OK;
-  const int threads = 256;
+  const int threads = FUSG_MONO_THREADS;
   const unsigned blocks = unsigned((count + threads - 1) / threads);
   const double k1 = phase_scale(kre, kGridPhaseBits);
   if (!(k1 > 0.0))  // the grid kernel measures distances in phase-table turns (Re k > 0)
