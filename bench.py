@@ -656,6 +656,10 @@ def run_gpu_sharded(args, world, rank, local):
 
 
 def main():
+    # NCCL prints its version banner on stdout at communicator creation when NCCL_DEBUG asks for
+    # it; the contract is one JSON line on rank 0's stdout, so keep NCCL's chatter at warnings
+    if not os.environ.get("FUSG_KEEP_NCCL_DEBUG") and os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
