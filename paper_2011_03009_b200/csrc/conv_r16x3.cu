@@ -58,34 +58,64 @@ __device__ __forceinline__ void r16_twiddle_u(double2* v, double2 u, double2 w1,
 }
 
 // shared-memory layout (double2 offsets) of one CTA
-template <bool STAGED = true>
+template <int MODE = 1>
 struct X3Smem {
+  static constexpr bool STAGED = MODE != 0;
   static constexpr int XB = 0;             // [3][512] exchange buffers, then the t_r rows
-  static constexpr int KB = 1536;          // folded K^ row (769, padded to 770)
+  static constexpr int KB = 1536;          // folded K^ row (769, padded to 770); MODE 2: also the input row
   static constexpr int TW = KB + 770;      // [4][32] W512^(lane 2^j)
   static constexpr int US = TW + 128;      // [3][32] W1536^(lane r)
   static constexpr int C48 = US + 96;      // [48] W48^j
-  static constexpr int SB = C48 + 48;      // staged input row (<= 768 positions), if staged
-  static constexpr int END = SB + (STAGED ? 768 : 0);
+  static constexpr int SB = MODE == 2 ? KB : C48 + 48;  // staged input row (<= 768 positions)
+  static constexpr int END = C48 + 48 + (MODE == 1 ? 768 : 0);
   static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
 };
 
-// Per-warp pieces of the 1536 = 3 x 512 transform (warp r owns residue r).
-struct X3Warp {
-  double2 u, w1, w2, w4, w8;  // W1536^(lane r); W512^(lane 2^j)
+// W48^j = W1536^(32 j) in the constant bank (the same long-double values as the twiddle table):
+// the residue-specialised slot twiddles below read them as constant operands, no shared loads
+__constant__ double2 c_w48[48];
+
+// shared load the compiler may not hoist out of the line loop (keeps loop-invariant twiddles out
+// of the register budget)
+__device__ __forceinline__ double2 lds_fresh(const double2* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+// Per-warp pieces of the 1536 = 3 x 512 transform (warp r owns residue r).  SMEMTW: the lane
+// twiddles W1536^(lane r), W512^(lane 2^j) are read from the CTA tables at each use instead of
+// living in 20 registers for the whole kernel (the 5-CTA pass C needs <= 136 registers).
+template <bool SMEMTW>
+struct X3W {
+  double2 u, w1, w2, w4, w8;  // W1536^(lane r); W512^(lane 2^j) (registers: !SMEMTW)
+  const double2* usp;         // &us[32 r + lane], &tws[lane] (SMEMTW)
+  const double2* twp;
   const double2* c48;         // W48^j (shared)
   int r, k1;
   bool b;
   double c3, s3;              // W3^r = c3 + i s3
-  __device__ __forceinline__ X3Warp(const double2* sm_us, const double2* tws, const double2* c48_, int r_, int lane)
+  __device__ __forceinline__ X3W(const double2* sm_us, const double2* tws, const double2* c48_, int r_, int lane)
       : c48(c48_), r(r_), k1(lane & 15), b(lane >= 16) {
-    u = sm_us[32 * r + lane];
-    w1 = tws[lane];
-    w2 = tws[32 + lane];
-    w4 = tws[64 + lane];
-    w8 = tws[96 + lane];
+    usp = sm_us + 32 * r + lane;
+    twp = tws + lane;
+    if constexpr (!SMEMTW) {
+      u = *usp;
+      w1 = twp[0];
+      w2 = twp[32];
+      w4 = twp[64];
+      w8 = twp[96];
+    }
     c3 = r == 0 ? 1.0 : -0.5;
     s3 = r == 0 ? 0.0 : r == 1 ? -0.8660254037844386467637 : 0.8660254037844386467637;
+  }
+  template <bool CONJ>
+  __device__ __forceinline__ void twiddle_u(double2* v) const {
+    if constexpr (SMEMTW) {
+      r16_twiddle_u<CONJ>(v, lds_fresh(usp), lds_fresh(twp), lds_fresh(twp + 32), lds_fresh(twp + 64), lds_fresh(twp + 96));
+    } else {
+      r16_twiddle_u<CONJ>(v, u, w1, w2, w4, w8);
+    }
   }
   // The three residues run the same instructions (residue 0 multiplies by exact ones), so the
   // warps of a CTA reach its barriers together.
@@ -110,10 +140,9 @@ struct X3Warp {
   }
   // stage A of the forward transform (registers only)
   __device__ __forceinline__ void forward_a(double2* v) const {
-#pragma unroll
-    for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmul(v[n1], c48[n1 * r]);  // W48^(n1 r), n1 r < 48
+    slot_twiddle<false>(v);  // W48^(n1 r), n1 r < 48
     dft16<false>(v);
-    r16_twiddle_u<false>(v, u, w1, w2, w4, w8);
+    twiddle_u<false>(v);
   }
   // the exchange, stage B, and the last radix 2 fused with the folded-K^ multiply: the two K^
   // values of step I + 1 are read from shared memory while step I shuffles, so their latency
@@ -151,12 +180,24 @@ struct X3Warp {
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = xr[r16_ex(k, lane)];
-    r16_twiddle_u<true>(v, u, w1, w2, w4, w8);
+    twiddle_u<true>(v);
     dft16<true>(v);
+    slot_twiddle<true>(v);
+  }
+  // v[n1] *= W48^(n1 r) (CONJ: its conjugate); residue 0 multiplies by ones and skips it
+  template <bool CONJ>
+  __device__ __forceinline__ void slot_twiddle(double2* v) const {
+    auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+    if (r == 1) {
 #pragma unroll
-    for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmulc(v[n1], c48[n1 * r]);
+      for (int n1 = 1; n1 < 16; ++n1) v[n1] = m(v[n1], c_w48[n1]);
+    } else if (r == 2) {
+#pragma unroll
+      for (int n1 = 1; n1 < 16; ++n1) v[n1] = m(v[n1], c_w48[2 * n1]);
+    }
   }
 };
+using X3Warp = X3W<false>;
 
 // cropped row from the three t_r rows: x[n'] = t0 + t1 + t2, x[n' + 512] = t0 + W3^-1 t1 + W3^-2 t2
 __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* t1r, const double2* t2r, int n,
@@ -172,47 +213,6 @@ __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* 
     const double2 d = csub(t1, t2);
     const double2 o = make_double2(t0.x - 0.5 * s.x - kS3 * d.y, t0.y - 0.5 * s.y + kS3 * d.x);
     out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
-  }
-}
-
-// a thread's share (n = t0, t0 + NT, ... < 512) of the recombination, every shared load issued
-// before the arithmetic (the per-position loop waited on each load)
-template <int NT, int G>
-__device__ __forceinline__ void x3_recombine_group(const double2* x, int t0, int onv, double sc, double2* out);
-template <int NT, int G = 2>
-__device__ __forceinline__ void x3_recombine_all(const double2* x, int t0, int onv, double sc, double2* out) {
-  constexpr int J = (512 + NT - 1) / NT;
-#pragma unroll
-  for (int j0 = 0; j0 < J; j0 += G) x3_recombine_group<NT, G>(x, t0 + NT * j0, onv, sc, out);
-}
-template <int NT, int G>
-__device__ __forceinline__ void x3_recombine_group(const double2* x, int t0, int onv, double sc, double2* out) {
-  double2 a[G], b[G], c[G];
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    const int n = t0 + NT * j;
-    if (n < 512) {
-      a[j] = x[n];
-      b[j] = x[512 + n];
-      c[j] = x[1024 + n];
-    }
-  }
-  constexpr double kS3 = 0.8660254037844386467637;
-#pragma unroll
-  for (int j = 0; j < G; ++j) {
-    const int n = t0 + NT * j;
-    if (n >= 512) break;
-    const double2 t0v = a[j], t1 = b[j], t2 = c[j];
-    const double2 s = cadd(t1, t2);
-    if (n < onv) {
-      const double2 o = cadd(t0v, s);
-      out[n] = sc == 1.0 ? o : cscale(o, sc);
-    }
-    if (n + 512 < onv) {
-      const double2 d = csub(t1, t2);
-      const double2 o = make_double2(t0v.x - 0.5 * s.x - kS3 * d.y, t0v.y - 0.5 * s.y + kS3 * d.x);
-      out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
-    }
   }
 }
 
@@ -232,10 +232,19 @@ __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.syn
 // 29.8 vs 32.8-33.6 ms at cfg5).
 // STAGED = false: the input row is read straight from global memory (prefetched into L2 one
 // line ahead), which frees 12 KB per CTA for a fifth CTA (15 warps) per SM.
-template <bool STAGED>
-__global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
+#ifndef FUSG_X3_MINB
+#define FUSG_X3_MINB 4  // CTAs per SM the staged pass C's register budget targets (4: <= 168 registers)
+#endif
+// MODE 1 (default): input row and K^ row in their own buffers, each refilled one line ahead.
+// MODE 2: one staging buffer holds the input row until the gather, then this line's K^ row
+// (loaded while the forward transform runs), then the next input row (loaded during the inverse
+// and the recombination); 41 KB of shared memory and lane twiddles read from the tables let 5
+// CTAs (15 warps) share an SM. MODE 0: input rows read from L2 (5 CTAs).
+template <int MODE>
+__global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(WArgs a) {
+  constexpr bool STAGED = MODE != 0;
   constexpr int HZ = 769;
-  using X3Smem = fusg::X3Smem<STAGED>;
+  using X3Smem = fusg::X3Smem<MODE>;
   extern __shared__ double2 sm[];
   const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + X3Smem::XB;
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
     mbar_init_fence();
   }
   __syncthreads();
-  const X3Warp W(sm + X3Smem::US, sm + X3Smem::TW, sm + X3Smem::C48, r, lane);
+  const X3W<MODE == 2> W(sm + X3Smem::US, sm + X3Smem::TW, sm + X3Smem::C48, r, lane);
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = gridDim.x;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
   int64_t line = blockIdx.x;
   if (threadIdx.x == 0) {
     prefetch_in(line);
-    prefetch_k(line);
+    if constexpr (MODE != 2) prefetch_k(line);
   }
   unsigned ph = 0;  // both staging barriers complete once per line
   for (; line < nlines; line += stride, ph ^= 1) {
@@ -295,12 +304,18 @@ __global__ void __launch_bounds__(96, STAGED ? 4 : 5) conv_r16x3(WArgs a) {
       W.gather(v, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, nv, lane);
     }
     __syncthreads();  // the staged row is read by all three warps: refill it
-    if (threadIdx.x == 0) prefetch_in(line + stride);
+    if (threadIdx.x == 0) {
+      if constexpr (MODE == 2) prefetch_k(line);  // this line's K^ row into the same buffer
+      else prefetch_in(line + stride);
+    }
     // X[3k' + r] times the folded K^ row, fused into the last forward stage
     W.forward_a(v);
     W.forward_b_mulk(v, xr, lane, kb, bars + 1, ph);
     __syncthreads();  // K^ row read
-    if (threadIdx.x == 0) prefetch_k(line + stride);
+    if (threadIdx.x == 0) {
+      if constexpr (MODE == 2) prefetch_in(line + stride);
+      else prefetch_k(line + stride);
+    }
     W.inverse(v, xr, lane);
     __syncwarp();  // every lane has read its exchange slots
 #pragma unroll
@@ -562,6 +577,19 @@ bool make_tile_map(CUtensorMap* map, const void* base, int64_t n_lines, int64_t 
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// c_w48 on the current device (once per device; the values do not depend on the grid)
+static bool load_w48() {
+  static std::atomic<uint64_t> mask{0};
+  return once_per_device(mask, [] {
+    double2 h[48];
+    for (int e = 0; e < 48; ++e) {  // the twiddle table's expression (upload_twiddles, L = 1536, m = 32 e)
+      const long double a = -2.0L * 3.141592653589793238462643383279502884L * (32 * e) / 1536;
+      h[e] = make_double2(double(cosl(a)), double(sinl(a)));
+    }
+    return cudaMemcpyToSymbol(c_w48, h, sizeof(h)) == cudaSuccess;
+  });
+}
+
 // pass C at L = 1536 (conv_r16x3): 1 launched, 0 not applicable, -1 error
 int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   static const bool on = [] {  // FUSG_CONV_R16X3=0 keeps the 64-lane radix (8, 8, 3, 8) pass C
@@ -571,19 +599,27 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   if (!on || a.in_nvalid < 1 || a.in_nvalid > 768 || a.out_nvalid > 768) return 0;
   const int64_t nl = int64_t(a.n_inner) * a.n_outer;
   if (nl >= (int64_t(1) << 31)) return 0;
-  static const bool staged = [] {  // FUSG_X3_STAGED=0: input rows from L2 (5 CTAs per SM)
-    const char* e = getenv("FUSG_X3_STAGED");
-    return !(e && atoi(e) == 0);
+  if (!load_w48()) {
+    set_error(FUSG_CUDA, "pass C (1536 = 3 x 512): cannot load the W48 table");
+    return -1;
+  }
+  // FUSG_X3_MODE: 1 (default) input and K^ rows in two staging buffers (4 CTAs per SM); 2 one
+  // shared staging buffer and lane twiddles from the tables (5 CTAs); 0 input rows from L2
+  static const int mode = [] {
+    const char* e = getenv("FUSG_X3_MODE");
+    const int m = e ? atoi(e) : 1;
+    return (m == 0 || m == 2) ? m : 1;
   }();
-  const auto fn = staged ? conv_r16x3<true> : conv_r16x3<false>;
-  // unstaged: the staging row is not allocated (it is the last region before the tables)
-  const size_t smem = staged ? X3Smem<true>::BYTES : X3Smem<false>::BYTES;
+  const auto fn = mode == 1 ? conv_r16x3<1> : mode == 2 ? conv_r16x3<2> : conv_r16x3<0>;
+  const size_t smem = mode == 1 ? X3Smem<1>::BYTES : mode == 2 ? X3Smem<2>::BYTES : X3Smem<0>::BYTES;
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
-        return cudaFuncSetAttribute(conv_r16x3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3Smem<true>::BYTES)) == cudaSuccess &&
-               cudaFuncSetAttribute(conv_r16x3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3Smem<false>::BYTES)) == cudaSuccess;
+        return cudaFuncSetAttribute(conv_r16x3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<1>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(conv_r16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<2>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(conv_r16x3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<0>::BYTES)) == cudaSuccess;
       })) {
     set_error(FUSG_CUDA, "pass C (1536 = 3 x 512): cannot configure shared memory");
     return -1;
@@ -637,6 +673,10 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   }();
   const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
   if (tiles >= (int64_t(1) << 31)) return 0;
+  if (!load_w48()) {
+    set_error(FUSG_CUDA, "transposing pass (1536 = 3 x 512): cannot load the W48 table");
+    return -1;
+  }
   // FUSG_X3_TMA=0: the column tiles move by per-thread stores / cp.async instead of tensor-map
   // box copies (T = 4, unit line stride, no peer stores, unscaled forward output)
   static const bool tma_on = [] {
