@@ -162,3 +162,17 @@ def test_validate_suite_passes():
     rc, out, err = run("validate")
     assert rc == 0, out + err
     assert out.count("[ ok ]") == 5 and out.strip().endswith("all checks passed")
+
+
+@pytest.mark.gpu
+def test_converge_quadrature_study(tmp_path):
+    # tools/fus_cli.cpp:191-228 on a small study: convergence.csv columns and the console lines
+    rc, out, err = run("converge", "--study", "quadrature", "--transducer", "H131", "--f0", "0.5e6",
+                       "--np", "128", "--nw-list", "3", "4", "--nw-ref", "6", "--length", "6e-3",
+                       "--width", "2e-3", "--out", str(tmp_path / "c"))
+    assert rc == 0, err
+    lines = (tmp_path / "c" / "convergence.csv").read_text().splitlines()
+    assert lines[0] == "harmonic,n_w,error_percent"
+    rows = [[float(x) for x in l.split(",")] for l in lines[1:]]
+    assert [r[1] for r in rows] == [3.0, 4.0] and all(r[2] >= 0 for r in rows)
+    assert "fitted log-log slope:" in out and out.count("error =") == 2
