@@ -308,7 +308,10 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
       const char* env_s = getenv("FUSG_HOST_SLOT_MB");
       const int hw = int(std::thread::hardware_concurrency());
       const int nt = env_t ? std::max(1, atoi(env_t)) : std::max(1, std::min(32, hw));
-      const size_t slot_mb = env_s ? size_t(std::max(1, atoi(env_s))) : 64;
+      // 16 MB slots: a thread's 1 MB share of a slot is still in the host caches when the DMA
+      // reads it (cfg5 pageable apply 368-414 ms with 64 MB slots, 308-312 with 8-16 MB, 458
+      // with 4 MB: per-slot overheads; pinned buffers 287 ms)
+      const size_t slot_mb = env_s ? size_t(std::max(1, atoi(env_s))) : 16;
       if (r->init(4, slot_mb << 20, nt) != cudaSuccess) {
         cudaGetLastError();
         r->destroy();
