@@ -303,16 +303,19 @@ fusg_status fusg_kernel_apply_host(fusg_kernel* K, const double* f_host, double*
     if (!K->ring) {
       auto* r = new PinnedRing;
       // FUSG_HOST_THREADS: copy threads (default: every hardware thread, up to 32);
-      // FUSG_HOST_SLOT_MB: pinned slot size (4 slots)
+      // FUSG_HOST_SLOT_MB / FUSG_HOST_SLOTS: pinned slot size and count (16 MB x 3)
       const char* env_t = getenv("FUSG_HOST_THREADS");
       const char* env_s = getenv("FUSG_HOST_SLOT_MB");
       const int hw = int(std::thread::hardware_concurrency());
       const int nt = env_t ? std::max(1, atoi(env_t)) : std::max(1, std::min(32, hw));
-      // 16 MB slots: a thread's 1 MB share of a slot is still in the host caches when the DMA
-      // reads it (cfg5 pageable apply 368-414 ms with 64 MB slots, 308-312 with 8-16 MB, 458
-      // with 4 MB: per-slot overheads; pinned buffers 287 ms)
+      // 3 slots of 16 MB: a thread's 1 MB share of a slot is still in the host caches when the
+      // DMA reads it, and the ring (48 MB) stays inside the box's 60 MB L3 (cfg5 pageable apply:
+      // 4 x 64 MB 368-414 ms, 4 x 16 MB 308-389 ms, 3 x 16 MB 307-312 ms, 4 x 4 MB 458 ms;
+      // pinned buffers 287 ms)
       const size_t slot_mb = env_s ? size_t(std::max(1, atoi(env_s))) : 16;
-      if (r->init(4, slot_mb << 20, nt) != cudaSuccess) {
+      const char* env_n = getenv("FUSG_HOST_SLOTS");
+      const int nslots = env_n ? std::max(2, atoi(env_n)) : 3;
+      if (r->init(nslots, slot_mb << 20, nt) != cudaSuccess) {
         cudaGetLastError();
         r->destroy();
         delete r;

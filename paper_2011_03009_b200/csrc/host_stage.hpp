@@ -7,7 +7,7 @@
 // the caller's vector into one slot of a ring of pinned buffers (several threads, so the copy
 // keeps up with PCIe), one cudaMemcpyAsync moves the slot, and the slot is reused once the
 // event recorded after its DMA has completed.  Device-to-host runs the same ring backwards.
-// Measured at cfg5 (7.25 GB each way, 16 host threads): 0.31 s per apply with 16 MB slots
+// Measured at cfg5 (7.25 GB each way, 16 host threads): 0.31 s per apply with 3 x 16 MB slots
 // against 0.287 s for pinned buffers (0.37-0.41 s with 64 MB slots: the staged path moves every
 // byte through host memory three times -- read the caller's vector, write the slot, DMA read --
 // unless the slot is still cached when the DMA reads it; non-temporal stores measured no faster).
