@@ -1,5 +1,5 @@
 // 16 x 16 x 2 warp transform pieces shared by the L = 512 kernels (conv_r16.cu) and the
-// L = 1536 = 3 x 512 kernels (conv_r16x3.cu).
+// L = 1536 = 3 x 512 (conv_r16x3.cu) and L = 1024 = 2 x 512 (conv_r16x2.cu) kernels.
 #pragma once
 #include <utility>
 
@@ -51,6 +51,39 @@ __device__ __forceinline__ double2 shfl_xor_d2(double2 x, int m) {
   return make_double2(__shfl_xor_sync(0xffffffffu, x.x, m), __shfl_xor_sync(0xffffffffu, x.y, m));
 }
 __device__ __forceinline__ double2 sel_d2(bool p, double2 a, double2 b) { return p ? a : b; }
+
+// v[k] *= u * W512^(lane k), k = 0..15, from u and the exact powers w1, w2, w4, w8 (CONJ: by the
+// conjugates)
+template <bool CONJ>
+__device__ __forceinline__ void r16_twiddle_u(double2* v, double2 u, double2 w1, double2 w2, double2 w4, double2 w8) {
+  auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+  // each power p_k = u W512^(lane k) is applied to v[k] and, times w8, to v[k + 8] as soon as it
+  // exists, so few products are live at once
+  v[0] = m(v[0], u);
+  const double2 p8 = cmul(u, w8);
+  v[8] = m(v[8], p8);
+  const double2 p1 = cmul(u, w1);
+  v[1] = m(v[1], p1);
+  v[9] = m(v[9], cmul(p1, w8));
+  const double2 p2 = cmul(u, w2);
+  v[2] = m(v[2], p2);
+  v[10] = m(v[10], cmul(p2, w8));
+  const double2 p4 = cmul(u, w4);
+  v[4] = m(v[4], p4);
+  v[12] = m(v[12], cmul(p4, w8));
+  const double2 p3 = cmul(p1, w2);
+  v[3] = m(v[3], p3);
+  v[11] = m(v[11], cmul(p3, w8));
+  const double2 p5 = cmul(p1, w4);
+  v[5] = m(v[5], p5);
+  v[13] = m(v[13], cmul(p5, w8));
+  const double2 p6 = cmul(p2, w4);
+  v[6] = m(v[6], p6);
+  v[14] = m(v[14], cmul(p6, w8));
+  const double2 p7 = cmul(p3, w4);
+  v[7] = m(v[7], p7);
+  v[15] = m(v[15], cmul(p7, w8));
+}
 
 // radix 2 over n2lo with twiddle W32^(q1 n2lo), q1 = i + 8 b (forward), and its adjoint
 template <int I>
