@@ -41,6 +41,8 @@ struct X3Smem {
 // W48^j = W1536^(32 j) in the constant bank (the same long-double values as the twiddle table):
 // the residue-specialised slot twiddles below read them as constant operands, no shared loads
 __constant__ double2 c_w48[48];
+// W32^j = W1024^(32 j) for the 2 x 512 transposing passes
+__constant__ double2 c_w32t[32];
 
 // shared load the compiler may not hoist out of the line loop (keeps loop-invariant twiddles out
 // of the register budget)
@@ -53,8 +55,9 @@ __device__ __forceinline__ double2 lds_fresh(const double2* p) {
 // Per-warp pieces of the 1536 = 3 x 512 transform (warp r owns residue r).  SMEMTW: the lane
 // twiddles W1536^(lane r), W512^(lane 2^j) are read from the CTA tables at each use instead of
 // living in 20 registers for the whole kernel (the 5-CTA pass C needs <= 136 registers).
-template <bool SMEMTW>
+template <bool SMEMTW, int R = 3>
 struct X3W {
+  static_assert(R == 2 || R == 3, "lines of 2 x 512 or 3 x 512");
   double2 u, w1, w2, w4, w8;  // W1536^(lane r); W512^(lane 2^j) (registers: !SMEMTW)
   const double2* usp;         // &us[32 r + lane], &tws[lane] (SMEMTW)
   const double2* twp;
@@ -86,13 +89,14 @@ struct X3W {
   }
   // The three residues run the same instructions (residue 0 multiplies by exact ones), so the
   // warps of a CTA reach its barriers together.
-  // y_r[32 n1 + lane] without its W1536 twiddle: x[m] + W3^r x[m + 512] (x zero beyond nv)
+  // y_r[32 n1 + lane] without its W1536 twiddle: x[m] + W3^r x[m + 512] (x zero beyond nv);
+  // R = 2 (nv <= 512): x[m]
   __device__ __forceinline__ void gather(double2* v, const double2* row, int nv, int lane) const {
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) {
       const int m = 32 * n1 + lane;
       double2 x0 = m < nv ? row[m] : make_double2(0.0, 0.0);
-      if (n1 < 8) {
+      if (R == 3 && n1 < 8) {
         const double2 x1 = m + 512 < nv ? row[m + 512] : make_double2(0.0, 0.0);
         x0 = make_double2(fma(c3, x1.x, fma(-s3, x1.y, x0.x)), fma(c3, x1.y, fma(s3, x1.x, x0.y)));
       }
@@ -155,6 +159,13 @@ struct X3W {
   template <bool CONJ>
   __device__ __forceinline__ void slot_twiddle(double2* v) const {
     auto m = [](double2 x, double2 t) { return CONJ ? cmulc(x, t) : cmul(x, t); };
+    if constexpr (R == 2) {  // W32^(n1 r)
+      if (r == 1) {
+#pragma unroll
+        for (int n1 = 1; n1 < 16; ++n1) v[n1] = m(v[n1], c_w32t[n1]);
+      }
+      return;
+    }
     if (r == 1) {
 #pragma unroll
       for (int n1 = 1; n1 < 16; ++n1) v[n1] = m(v[n1], c_w48[n1]);
@@ -184,10 +195,12 @@ __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* 
 }
 
 // the per-CTA twiddle tables: tws [4][32] W512^(lane 2^j), us [3][32] W1536^(lane r), c48 [48]
-__device__ __forceinline__ void x3_tables(const double2* tw1536, double2* tws, double2* us, double2* c48) {
-  for (int e = threadIdx.x; e < 128; e += blockDim.x) tws[e] = __ldg(tw1536 + (((3 * (e & 31)) << (e >> 5)) % 1536));
-  for (int e = threadIdx.x; e < 96; e += blockDim.x) us[e] = __ldg(tw1536 + (e & 31) * (e >> 5));
-  for (int e = threadIdx.x; e < 48; e += blockDim.x) c48[e] = __ldg(tw1536 + 32 * e);
+template <int R = 3>
+__device__ __forceinline__ void x3_tables(const double2* twL, double2* tws, double2* us, double2* c48) {
+  constexpr int L = 512 * R;  // twL: the W_L table; tws = W512^(lane 2^j), us = W_L^(lane r), c48 = W_L^(32 j)
+  for (int e = threadIdx.x; e < 128; e += blockDim.x) tws[e] = __ldg(twL + (((R * (e & 31)) << (e >> 5)) % L));
+  for (int e = threadIdx.x; e < 32 * R; e += blockDim.x) us[e] = __ldg(twL + (e & 31) * (e >> 5));
+  for (int e = threadIdx.x; e < 16 * R; e += blockDim.x) c48[e] = __ldg(twL + 32 * e);
 }
 
 __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -301,49 +314,51 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
 // lines (warp 3t + r: line t, residue r).  The T input rows (contiguous when the rows are
 // dense) arrive by 1-D bulk copy one tile ahead; the spectra meet in a swizzled [pos][T] tile
 // that aliases the twelve exchange buffers; the CTA stores 64-byte segments of T adjacent lines.
-template <int T>
+template <int T, int R = 3>
 struct X3TSmem {
-  static constexpr int AREA = 0;              // [1536][T] tile = 3T exchange buffers
-  static constexpr int STAGE = 1536 * T;      // [T][768] staged input rows (r2c)
-  static constexpr int TW = STAGE + 768 * T;  // tables as in X3Smem
+  static constexpr int L = 512 * R, H = 256 * R;
+  static constexpr int AREA = 0;            // [L][T] tile = R T exchange buffers
+  static constexpr int STAGE = L * T;       // [T][L/2] staged input rows (r2c)
+  static constexpr int TW = STAGE + H * T;  // tables as in X3Smem
   static constexpr int US = TW + 128;
-  static constexpr int C48 = US + 96;
-  static constexpr int END = C48 + 48;
+  static constexpr int C48 = US + 32 * R;
+  static constexpr int END = C48 + 16 * R;
   static constexpr size_t BYTES = size_t(END) * sizeof(double2) + sizeof(uint64_t);
   // TMA r2c: a second staging buffer after the tables (input rows two tiles ahead), 2 mbarriers
   static constexpr int STAGE2 = END;
-  static constexpr size_t BYTES2 = size_t(STAGE2 + 768 * T) * sizeof(double2) + 2 * sizeof(uint64_t);
-  // c2r: two [1536][T] tiles (double-buffered), then the tables
-  static constexpr int C_TW = 2 * 1536 * T;
+  static constexpr size_t BYTES2 = size_t(STAGE2 + H * T) * sizeof(double2) + 2 * sizeof(uint64_t);
+  // c2r: two [L][T] tiles (double-buffered), then the tables
+  static constexpr int C_TW = 2 * L * T;
   static constexpr int C_US = C_TW + 128;
-  static constexpr int C_C48 = C_US + 96;
-  static constexpr int C_END = C_C48 + 48;
+  static constexpr int C_C48 = C_US + 32 * R;
+  static constexpr int C_END = C_C48 + 16 * R;
   static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2) + 2 * sizeof(uint64_t);
 };
 
 // TMA (T = 4): the finished tile leaves by tensor-map box stores issued by one thread, and the
 // next tile's stage-A arithmetic overlaps them; the area is rewritten (first exchange) only after
 // the stores have read it.
-template <int T, bool TMA>
-__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
-  using X3TSmem = fusg::X3TSmem<T>;
+template <int T, bool TMA, int R = 3>
+__global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
+  using X3TSmem = fusg::X3TSmem<T, R>;
+  constexpr int H = X3TSmem::H;  // L / 2
   extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = w % 3, t = w / 3;
+  const int r = w % R, t = w / R;
   double2* const area = sm + X3TSmem::AREA;
   double2* const xr = area + 512 * w;
   // TMA: two staging buffers, filled two tiles ahead (the rows of pass B lie a z-plane apart and
   // arrive late one tile ahead); else one
   constexpr int NST = TMA ? 2 : 1;
   double2* const stages[2] = {sm + X3TSmem::STAGE, sm + X3TSmem::STAGE2};
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + (TMA ? X3TSmem::STAGE2 + 768 * T : X3TSmem::END));
-  x3_tables(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + (TMA ? X3TSmem::STAGE2 + H * T : X3TSmem::END));
+  x3_tables<R>(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
   if (threadIdx.x == 0) {
     for (int b = 0; b < NST; ++b) mbar_init(bars + b, 1);
     mbar_init_fence();
   }
   __syncthreads();
-  const X3Warp W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
+  const X3W<false, R> W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
   const int nv = a.in_nvalid;
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
@@ -356,7 +371,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
       const unsigned row = unsigned(nv) * sizeof(double2);
       refill_fence();
       mbar_expect_tx(bars + sb, row * lines_ok);
-      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stages[sb] + tt * 768, src + tt * a.in_si, row, bars + sb);
+      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stages[sb] + tt * H, src + tt * a.in_si, row, bars + sb);
     }
   };
   int64_t tix = blockIdx.x;
@@ -371,7 +386,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
     mbar_wait(bars + sb, (phs >> sb) & 1u);
     phs ^= 1u << sb;
     double2 v[16];
-    W.gather(v, stages[sb] + (t < lines_ok ? t : 0) * 768, nv, lane);
+    W.gather(v, stages[sb] + (t < lines_ok ? t : 0) * H, nv, lane);
     if constexpr (TMA) {
       W.forward_a(v);
       if (threadIdx.x == 0) bulk_wait_read0();  // the previous tile's box stores have read the area
@@ -386,9 +401,9 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
     __syncthreads();  // every exchange buffer is read out: the area becomes the tile
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int p = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
+      const int p = R * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
       area[mtile_at<T>(p, t)] = v[i];
-      area[mtile_at<T>(p + 768, t)] = v[i + 8];
+      area[mtile_at<T>(p + H, t)] = v[i + 8];
     }
     __syncthreads();  // all T spectra are in the tile
     if constexpr (TMA) {
@@ -401,7 +416,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
     }
     double2* const base = a.out + int64_t(i0) * a.out_si + int64_t(k) * a.out_sk;
 #pragma unroll 4
-    for (int e = threadIdx.x; e < a.out_nvalid * T; e += 96 * T) {
+    for (int e = threadIdx.x; e < a.out_nvalid * T; e += 32 * R * T) {
       const int pos = e / T, tt = e % T;
       if (tt < lines_ok) {
         const double2 x = area[mtile_at<T>(pos, tt)];
@@ -429,21 +444,23 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_row_to_col(WArgs a, const
 // writes the T cropped rows with coalesced stores.
 // TMA (T = 4): each column tile arrives by tensor-map box loads (one thread, one mbarrier per
 // buffer) instead of per-thread cp.async; positions and lines beyond the field are zero-filled.
-template <int T, bool TMA>
-__global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
-  using X3TSmem = fusg::X3TSmem<T>;
+template <int T, bool TMA, int R = 3>
+__global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
+  using X3TSmem = fusg::X3TSmem<T, R>;
+  constexpr int L = X3TSmem::L, H = X3TSmem::H;
+  constexpr int NT = 32 * R * T;
   extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = w % 3, t = w / 3;
+  const int r = w % R, t = w / R;
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + X3TSmem::C_END);  // [2], TMA only
-  x3_tables(a.tw, sm + X3TSmem::C_TW, sm + X3TSmem::C_US, sm + X3TSmem::C_C48);
+  x3_tables<R>(a.tw, sm + X3TSmem::C_TW, sm + X3TSmem::C_US, sm + X3TSmem::C_C48);
   if (TMA && threadIdx.x == 0) {
     mbar_init(bars, 1);
     mbar_init(bars + 1, 1);
     mbar_init_fence();
   }
   __syncthreads();
-  const X3Warp W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
+  const X3W<false, R> W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix, double2* tile) {
@@ -464,7 +481,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const
       const int k = int(unsigned(tix) / unsigned(ntiles_i));
       const int lines_ok = min(T, a.n_inner - i0);
       const double2* base = a.in + int64_t(i0) * a.in_si + int64_t(k) * a.in_sk;
-      for (int e = threadIdx.x; e < a.in_nvalid * T; e += 96 * T) {
+      for (int e = threadIdx.x; e < a.in_nvalid * T; e += NT) {
         const int pos = e / T, tt = e % T;
         cp_async16_zfill(&tile[mtile_at<T>(pos, tt)], tt < lines_ok ? base + tt * a.in_si + pos * a.in_sp : a.in,
                          tt < lines_ok);
@@ -476,7 +493,7 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const
   unsigned buf = 0, phs = 0;  // phs: parity bit of each buffer's mbarrier (TMA)
   prefetch(tix, sm);
   for (; tix < ntiles; tix += gridDim.x, buf ^= 1) {
-    double2* const tile = sm + buf * (1536 * T);
+    double2* const tile = sm + buf * (L * T);
     const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
     const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
@@ -491,18 +508,18 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int p = 3 * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
+      const int p = R * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
       v[i] = p < a.in_nvalid ? tile[mtile_at<T>(p, t)] : make_double2(0.0, 0.0);
-      v[i + 8] = p + 768 < a.in_nvalid ? tile[mtile_at<T>(p + 768, t)] : make_double2(0.0, 0.0);
+      v[i + 8] = p + H < a.in_nvalid ? tile[mtile_at<T>(p + H, t)] : make_double2(0.0, 0.0);
     }
     __syncthreads();  // tile read by every warp: it becomes the exchange area
-    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (1536 * T));
+    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (L * T));
     double2* const xr = tile + 512 * w;
     W.inverse(v, xr, lane);
     __syncwarp();
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
-    nbar_sync(1 + t, 96);  // line t's three t_r rows are in the area
+    nbar_sync(1 + t, 32 * R);  // line t's R t_r rows are in the area
     if (t < lines_ok) {
       const int line = i0 + t;
       double2* orow = a.out + int64_t(line) * a.out_si + int64_t(k) * a.out_sk;
@@ -510,9 +527,15 @@ __global__ void __launch_bounds__(96 * T, 4 / T) r16x3_col_to_row(WArgs a, const
         const int q = a.pm.owner(line);
         orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
       }
-      const double2* x = tile + 512 * 3 * t;
-      for (int n = threadIdx.x - 96 * t; n < 512; n += 96)
-        x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
+      const double2* x = tile + 512 * R * t;
+      for (int n = threadIdx.x - 32 * R * t; n < 512; n += 32 * R) {
+        if constexpr (R == 3) {
+          x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
+        } else if (n < a.out_nvalid) {  // x[n] = t0 + t1, n < 512
+          const double2 o = cadd(x[n], x[512 + n]);
+          orow[n] = a.scale == 1.0 ? o : cscale(o, a.scale);
+        }
+      }
     }
   }
   if constexpr (!TMA) cp_async_wait0();
@@ -695,6 +718,75 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) {
     cuda_error(err, "transposing pass (1536 = 3 x 512)");
+    return -1;
+  }
+  return 1;
+}
+
+// passes A/B (r2c) or D/E at L = 1024 = 2 x 512 (the 1536 kernels with R = 2: one CTA of 8 warps
+// on 4-line tiles, tensor-map TMA tiles): 1 launched, 0 not applicable, -1 error
+int launch_transpose_r16x2(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s) {
+  static const int mask = [] {  // FUSG_X2_T bitmask: 1 passes A/B, 2 passes D/E (default both)
+    const char* e = getenv("FUSG_X2_T");
+    return e ? atoi(e) : 3;
+  }();
+  if (!(mask & (r2c ? 1 : 2))) return 0;
+  if (r2c ? (a.in_nvalid > 512 || a.in_nvalid < 1 || a.in_sp != 1 || a.out_nvalid > 1024)
+          : (a.out_nvalid > 512 || a.out_sp != 1 || a.in_nvalid > 1024))
+    return 0;
+  constexpr int T = 4;
+  const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
+  if (tiles >= (int64_t(1) << 31)) return 0;
+  using SM2 = X3TSmem<T, 2>;
+  static std::atomic<uint64_t> attr_mask{0};
+  if (!once_per_device(attr_mask, [] {
+        double2 h[32];
+        for (int e = 0; e < 32; ++e) {  // the twiddle table's expression (L = 1024, m = 32 e)
+          const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (32 * e) / 1024;
+          h[e] = make_double2(double(cosl(ang)), double(sinl(ang)));
+        }
+        return cudaMemcpyToSymbol(c_w32t, h, sizeof(h)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_row_to_col<T, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(SM2::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_row_to_col<T, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(SM2::BYTES2)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<T, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(SM2::C_BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<T, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(SM2::C_BYTES)) == cudaSuccess;
+      })) {
+    set_error(FUSG_CUDA, "transposing pass (1024 = 2 x 512): cannot configure the kernels");
+    return -1;
+  }
+  static const bool tma_on = [] {
+    const char* e = getenv("FUSG_X3_TMA");
+    return !(e && atoi(e) == 0);
+  }();
+  CUtensorMap tm{};
+  const bool tma = tma_on && a.pm.n == 0 &&
+                   (r2c ? (a.out_si == 1 && a.scale == 1.0 &&
+                           make_tile_map(&tm, a.out, a.n_inner, a.out_nvalid, a.n_outer, a.out_sp, a.out_sk, T))
+                        : (a.in_si == 1 &&
+                           make_tile_map(&tm, a.in, a.n_inner, a.in_nvalid, a.n_outer, a.in_sp, a.in_sk, T)));
+  using Fn = void (*)(WArgs, CUtensorMap);
+  const Fn fn = r2c ? (tma ? r16x3_row_to_col<T, true, 2> : r16x3_row_to_col<T, false, 2>)
+                    : (tma ? r16x3_col_to_row<T, true, 2> : r16x3_col_to_row<T, false, 2>);
+  const size_t smem = r2c ? (tma ? SM2::BYTES2 : SM2::BYTES) : SM2::C_BYTES;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 * T, smem) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  static const int waves = [] {
+    const char* e = getenv("FUSG_X3T_WAVES");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(per_sm) * ctx->num_sms * waves);
+  fn<<<unsigned(grid), 64 * T, smem, s>>>(a, tm);
+  ctx->launches++;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    cuda_error(err, "transposing pass (1024 = 2 x 512)");
     return -1;
   }
   return 1;

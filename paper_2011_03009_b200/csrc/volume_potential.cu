@@ -1318,7 +1318,8 @@ static fusg_status launch_axis(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
       const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                      st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, KOct{}};
       int r = pl.L == 512 ? launch_transpose_r16(ctx, r2c, wa, s)
-              : pl.L == 1536 ? launch_transpose_r16x3(ctx, r2c, wa, s) : 0;
+              : pl.L == 1536 ? launch_transpose_r16x3(ctx, r2c, wa, s)
+              : pl.L == 1024 ? launch_transpose_r16x2(ctx, r2c, wa, s) : 0;
       if (r == 0) r = launch_mw(ctx, pl.L, r2c, wa, s);
       if (r == 0) r = launch_warp(ctx, pl.L, r2c ? kWRowToCol : kWColToRow, INV, wa, s);
       if (r < 0) return FUSG_CUDA;
@@ -1598,7 +1599,8 @@ fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap&
   WArgs a{f, Nx, int64_t(Ny) * Nx, 1, Nx, nullptr, 1, Ny, int64_t(Nz) * Ny, K->P[0], 1.0,
           Ny, K->nz, K->plan[0].tw, KOct{}, pm};
   int r = K->P[0] == 512 ? launch_transpose_r16(K->ctx, true, a, s)
-          : K->P[0] == 1536 ? launch_transpose_r16x3(K->ctx, true, a, s) : 0;
+          : K->P[0] == 1536 ? launch_transpose_r16x3(K->ctx, true, a, s)
+          : K->P[0] == 1024 ? launch_transpose_r16x2(K->ctx, true, a, s) : 0;
   if (r == 0) r = launch_mw(K->ctx, K->P[0], true, a, s);
   if (r == 0) r = launch_warp(K->ctx, K->P[0], kWRowToCol, false, a, s);
   if (r < 0) return FUSG_CUDA;
@@ -1612,7 +1614,8 @@ fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t 
   const int64_t PyNz = int64_t(Py) * Nz;
   WArgs a{K->bufB, 1, PyNz, Nz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
   int r = Py == 512 ? launch_transpose_r16(K->ctx, false, a, s)
-          : Py == 1536 ? launch_transpose_r16x3(K->ctx, false, a, s) : 0;
+          : Py == 1536 ? launch_transpose_r16x3(K->ctx, false, a, s)
+          : Py == 1024 ? launch_transpose_r16x2(K->ctx, false, a, s) : 0;
   if (r == 0) r = launch_mw(K->ctx, Py, false, a, s);
   if (r == 0) r = launch_warp(K->ctx, Py, kWColToRow, true, a, s);
   if (r < 0) return FUSG_CUDA;

@@ -85,6 +85,8 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
 int launch_conv_r16x2(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
 // pass C at L = 1536 (3 x 16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16x3.cu)
 int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
+// passes A/B (r2c) or D/E at L = 1024 = 2 x 512 (conv_r16x3.cu, R = 2)
+int launch_transpose_r16x2(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s);
 // passes A/B (r2c) or D/E at L = 1536 (conv_r16x3.cu)
 int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t s);
 // Passes A and B fused through an L2-resident ring of 8-plane z-slabs (conv_r16.cu)
