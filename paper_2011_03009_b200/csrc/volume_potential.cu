@@ -126,6 +126,18 @@ int device_padded_size(int n, int axis) {
       if (L <= pxy_warp && L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;
     return p;
   }
+  // x / y: the lengths with warp-transform transposing passes (512: 16x16x2; 1024, 1536: 2 / 3 x
+  // 512 with TMA tiles) when within FUSG_PXY_FAST (default 1.06) of the static length: cfg3's
+  // y 980 -> 1024 (passes B / D 4.8 -> ~2.5 ms)
+  static const double pxy_fast = [] {
+    const char* e = getenv("FUSG_PXY_FAST");
+    return e ? atof(e) : 1.06;
+  }();
+  if (axis != 2 && pxy_fast > 1.0) {
+    for (int L : {512, 1024, 1536})
+      if (L >= 2 * n - 1) return (L > p && L <= p * pxy_fast) ? L : p;
+    return p;
+  }
   if (axis != 2 || !pz_warp) return p;
   for (int L : {256, 512, 768, 1024, 1536, 2048})  // persistent pass C (warp / multi-warp lines)
     if (L <= pz_warp && L >= 2 * n - 1) return (L <= p * 1.35) ? L : p;

@@ -44,16 +44,17 @@ def _ladder(axis, env=None):
     return {int(L): v for L, v in json.loads(out.stdout.strip().splitlines()[-1]).items()}
 
 
-@pytest.mark.parametrize("axis,env", [(0, None), (1, None), (2, None), (2, {"FUSG_PZ_WARP": "0"})])
+@pytest.mark.parametrize("axis,env", [(0, {"FUSG_PXY_FAST": "0"}), (1, {"FUSG_PXY_FAST": "0"}), (0, None),
+                                      (2, None), (2, {"FUSG_PZ_WARP": "0"})])
 def test_static_ladder_every_length_vs_oracle(ctx, axis, env):
     res = _ladder(axis, env)
     lens = fus.static_lengths(axis == 2)
     assert sorted(res) == sorted(lens)
     reached = {L: v for L, v in res.items() if v[0] is not None}
-    if axis != 2 or env:  # every ladder length is reachable on x / y, and on z without the warp preference
+    if env:  # without the fast-length preference every ladder length is reachable
         assert sorted(reached) == sorted(lens), sorted(set(lens) - set(reached))
-    else:  # default z policy: at least the warp-engine and the largest lengths
-        assert {256, 512, 1536, 2048} <= set(reached)
+    else:  # default policies: at least the warp-engine and the largest lengths
+        assert {512, 1536, 2048} <= set(reached)
     bad = {L: v for L, v in reached.items() if not v[1] <= 1e-12}
     assert not bad, bad
 
