@@ -1400,7 +1400,9 @@ static fusg_status launch_conv(fusg_ctx* ctx, const AxisPlan& pl, int n_inner, i
   if (ld.g.sp == 1 && st.g.sp == 1 && ko.s_kz == 1) {
     const WArgs wa{ld.g.p, ld.g.si, ld.g.sk, ld.g.sp, ld.g.nvalid, st.g.p, st.g.si, st.g.sk,
                    st.g.sp, st.g.nvalid, st.g.scale, n_inner, n_outer, pl.tw, ko};
-    int r = pl.L == 1536 ? launch_conv_r16x3(ctx, wa, s) : pl.L == 1024 ? launch_conv_r16x2(ctx, wa, s) : 0;
+    int r = pl.L == 1536 ? launch_conv_r16x3(ctx, wa, s)
+            : pl.L == 1024 ? launch_conv_r16x2(ctx, wa, s)
+            : pl.L == 768 ? launch_conv_r16x3h(ctx, wa, s) : 0;
     if (r == 0) r = launch_conv64(ctx, pl.L, wa, s);
     if (r == 0) r = launch_warp(ctx, pl.L, kWConv, false, wa, s);
     if (r < 0) return FUSG_CUDA;

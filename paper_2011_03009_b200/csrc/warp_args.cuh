@@ -81,6 +81,8 @@ struct PPConvSmem {
 
 // pass C at L = 512 (16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16.cu)
 int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
+// pass C at L = 768 (3 x 16 x 16 on half-warps): 1 launched, 0 not applicable, -1 error (conv_r16x3h.cu)
+int launch_conv_r16x3h(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
 // pass C at L = 1024 (2 x 16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16x2.cu)
 int launch_conv_r16x2(fusg_ctx* ctx, const WArgs& a, cudaStream_t s);
 // pass C at L = 1536 (3 x 16 x 16 x 2): 1 launched, 0 not applicable, -1 error (conv_r16x3.cu)
