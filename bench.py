@@ -609,7 +609,7 @@ def run_gpu_sharded(args, world, rank, local):
     sent = max_over_ranks(float(sent), world, local)
     per_pass, total_bytes = algorithmic_bytes(g.dims, P)
     hbm, hbm_kind = peaks()
-    nvl = 900.0
+    nvl = 770.0  # measured peer copy per direction (B200_PROFILING.md); 900 GB/s nominal
     del K, fd, ud, fh, uh
     torch.cuda.empty_cache()
     # the nested 5-harmonic recursion sharded over the ranks (paper_2011_03009_b200/zslab.py):
@@ -644,7 +644,8 @@ def run_gpu_sharded(args, world, rank, local):
                          "frac": total_bytes / world / (ms * 1e-3) / 1e9 / hbm, "traffic": None,
                          "nvlink_bytes_sent_per_gpu": sent,
                          "nvlink_gbs_if_serialised": sent / (ms * 1e-3) / 1e9,
-                         "nvlink_peak_gbs": nvl, "nvlink_frac_if_serialised": sent / (ms * 1e-3) / 1e9 / nvl},
+                         "nvlink_peak_gbs": nvl, "nvlink_peak_kind": "measured peer copy (900 nominal)",
+                         "nvlink_frac_if_serialised": sent / (ms * 1e-3) / 1e9 / nvl},
             "kernel_build_s": build_s,
             "e2e": {"value": N / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 16 * N,
                     "d2h_bytes_per_step": 16 * N},
