@@ -60,6 +60,9 @@ constexpr int kPhaseBits = 11;
 constexpr int kPhaseN = 1 << kPhaseBits;
 constexpr double kTwoPi = 6.283185307179586476925;
 constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
+#ifndef FUSG_MONO_F2I
+#define FUSG_MONO_F2I 0  // phase rounding by F2I / I2F conversion (1) or the magic-number add (0)
+#endif
 
 // table scale: the host passes k1 = Re k * N / (2 pi)
 inline double phase_scale(double kre, int bits = kPhaseBits) { return kre * double(1 << bits) / kTwoPi; }
@@ -144,10 +147,20 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
   const double ir = rsqrt_refined(d2);
   const double d = d2 * ir;
   const double u = SC ? d : d * k1;
-  const double t = u + kRoundMagic;
   using PS = PhaseSpec<BITS>;
+#if FUSG_MONO_F2I
+  // j = rint(u) by conversion (F2I / I2F) instead of the magic-number add and subtract, off the
+  // FP64 pipe's add slots; v = u - j is exact either way (Sterbenz), so the terms are identical
+  const int ji = __double2int_rn(u);
+  const int j = ji & (PS::N - 1);
+  const double v = u - double(ji);
+  const int jhi = ji >> BITS;
+#else
+  const double t = u + kRoundMagic;
   const int j = __double2loint(t) & (PS::N - 1);
   const double v = u - (t - kRoundMagic);
+  const int jhi = __double2loint(t) >> BITS;
+#endif
   const double v2 = v * v;
   const double sn = v * fma(v2, PS::S3, PS::S1);
   const double cs = PS::kCos2 ? fma(v2, PS::C2, 1.0) : fma(v2, fma(v2, PS::C4, PS::C2), 1.0);
@@ -157,7 +170,7 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
     // tabulated attenuation: kim carries alpha = Im k / k1, the table rows already hold
     // e^{-alpha (j mod N)}, eh[m] = e^{-alpha N m}, and e^{-alpha v} = 1 - alpha v to
     // (alpha v)^2 / 2 < 1e-18
-    mag = ir * eh[__double2loint(t) >> BITS] * fma(-kim, v, 1.0);
+    mag = ir * eh[jhi] * fma(-kim, v, 1.0);
   } else {
     mag = ATT == 0 ? ir : ir * attenuation<ATT>(kim * d);
   }
