@@ -434,7 +434,10 @@ def test_cpp_dropin_api_all_cases(ctx):
 
 
 @pytest.mark.parametrize("dims,applies", [((106, 105, 105), 40), ((130, 105, 127), 40), ((256, 256, 256), 12),
-                                          ((64, 64, 700), 12), ((100, 100, 380), 12), ((200, 200, 490), 6)])
+                                          ((64, 64, 700), 12), ((100, 100, 380), 12), ((200, 200, 490), 6),
+                                          # the TMA-tiled transposing passes at 1536 and 1024 (x and y)
+                                          ((768, 64, 20), 10), ((64, 768, 20), 10), ((500, 37, 9), 20),
+                                          ((9, 500, 37), 20)])
 def test_repeated_applies_are_bitwise_identical(ctx, dims, applies):
     # Every staged pass C (L = 256 / 512 / 1536 / 768 / 1024) refills its shared buffers with bulk
     # copies while other lanes have just read them; without the async-proxy fence the refill
