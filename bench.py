@@ -444,6 +444,20 @@ def roofline_of(m):
             "unit": "GB/s", "frac": gbs / hbm, "traffic": traffic,
             "algorithmic_bytes_per_launch": per_pass[names[dom]],
             "launch_ms": m["pass_ms"][dom], "share_of_step": m["pass_ms"][dom] / sum(m["pass_ms"])}
+    # the dominant kernel against its binding floor, max(HBM floor, FP64 floor): the FP64 floor is
+    # the ncu-measured FP64-pipe time of the same kernel at 100 % (profiles/r2_apply_fp64.json)
+    try:
+        fp = json.load(open(os.path.join(ROOT, "profiles", "r2_apply_fp64.json")))
+        key = "x".join(str(p) for p in m["P"])
+        if key in fp and names[dom] in fp[key]:
+            hbm_floor = per_pass[names[dom]] / (hbm * 1e9) * 1e3
+            fp64_floor = fp[key][names[dom]]["fp64_floor_ms"]
+            roof["binding_floor"] = {"hbm_ms": hbm_floor, "fp64_ms": fp64_floor,
+                                     "bound": "fp64" if fp64_floor > hbm_floor else "hbm",
+                                     "frac": max(hbm_floor, fp64_floor) / m["pass_ms"][dom],
+                                     "source": "profiles/r2_apply_fp64.json"}
+    except Exception:
+        pass
     apply_roof = {"algorithmic_bytes": total, "achieved_gbs": total / (m["ms"] * 1e-3) / 1e9,
                   "frac": total / (m["ms"] * 1e-3) / 1e9 / hbm,
                   "per_pass_frac": {nm: per_pass[nm] / (t * 1e-3) / 1e9 / hbm
