@@ -92,6 +92,9 @@ def test_apply_linear_and_translation_covariant(ctx):
                                   (3, 2, 300), (2, 3, 341),
                                   # Nz = 490: Pz = 1024 (two-warp-line pass C)
                                   (2, 2, 490),
+                                  # Pz = 768 (3 x 256 half-warp pass C) with an odd line count
+                                  # (the last CTA pair holds one line), Pz = 1024 with odd lines
+                                  (5, 3, 333), (3, 3, 300), (5, 3, 500),
                                   # Nz = 768 / 1024: Pz = 1536 / 2048 (two- / four-warp lines)
                                   (3, 2, 768), (2, 3, 1024),
                                   # Nz = 600 / 900: Pz = 1536 / 2048 preferred over 1200 / 1800
