@@ -335,11 +335,20 @@ struct X3TSmem {
   static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2) + 2 * sizeof(uint64_t);
 };
 
+// CTAs per SM the transposing kernels' register budget targets: 1 per SM at T = 4 for 1536
+// (12 warps, <= 168 registers); R = 2 (1024) targets 2 CTAs of 8 warps (<= 128 registers) when
+// FUSG_X2T_MINB2 is set at compile time, else 1 CTA (8 warps, ~200 registers)
+#ifndef FUSG_X2T_MINB2
+#define FUSG_X2T_MINB2 1
+#endif
+#define X3T_MINB ((T == 4 && R == 2 && FUSG_X2T_MINB2) ? 2 : 4 / T)
+#define X3T_SMEMTW (T == 4 && R == 2 && FUSG_X2T_MINB2)  // lane twiddles from the CTA tables
+
 // TMA (T = 4): the finished tile leaves by tensor-map box stores issued by one thread, and the
 // next tile's stage-A arithmetic overlaps them; the area is rewritten (first exchange) only after
 // the stores have read it.
 template <int T, bool TMA, int R = 3>
-__global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
   using X3TSmem = fusg::X3TSmem<T, R>;
   constexpr int H = X3TSmem::H;  // L / 2
   extern __shared__ __align__(1024) double2 sm[];
@@ -358,7 +367,7 @@ __global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_row_to_col(WArgs a, c
     mbar_init_fence();
   }
   __syncthreads();
-  const X3W<false, R> W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
+  const X3W<X3T_SMEMTW, R> W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
   const int nv = a.in_nvalid;
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_row_to_col(WArgs a, c
 // TMA (T = 4): each column tile arrives by tensor-map box loads (one thread, one mbarrier per
 // buffer) instead of per-thread cp.async; positions and lines beyond the field are zero-filled.
 template <int T, bool TMA, int R = 3>
-__global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
+__global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
   using X3TSmem = fusg::X3TSmem<T, R>;
   constexpr int L = X3TSmem::L, H = X3TSmem::H;
   constexpr int NT = 32 * R * T;
@@ -460,7 +469,7 @@ __global__ void __launch_bounds__(32 * R * T, 4 / T) r16x3_col_to_row(WArgs a, c
     mbar_init_fence();
   }
   __syncthreads();
-  const X3W<false, R> W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
+  const X3W<X3T_SMEMTW, R> W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix, double2* tile) {

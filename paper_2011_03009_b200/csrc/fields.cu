@@ -67,10 +67,24 @@ constexpr double kRoundMagic = 6755399441055744.0;  // 1.5 * 2^52
 // table scale: the host passes k1 = Re k * N / (2 pi)
 inline double phase_scale(double kre, int bits = kPhaseBits) { return kre * double(1 << bits) / kTwoPi; }
 
-// Phase-table geometry for N = 2^BITS entries.  The grid kernel (the Rayleigh p1 sum) uses
-// 4096 entries in dynamic shared memory: the residual |2 pi v / N| <= 7.7e-4 lets cos drop to
-// degree 2 (error < 1.5e-14); the other kernels keep 2048 entries in static shared memory.
-constexpr int kGridPhaseBits = 12;
+// Phase-table geometry for N = 2^BITS entries.  The other kernels keep 2048 entries in static
+// shared memory.  The grid kernel (the Rayleigh p1 sum) reads its table once per term at an
+// effectively random index, and a warp's 32 random 16-byte reads cost ~10.4 wavefronts instead of
+// 4 (ncu: 6.3-way conflicts, the shared pipe as busy as the FP64 pipe).  FUSG_MONO_REP = 8: the
+// table holds 1024 entries, each replicated 8 times at [j][8] (128 KB), and lane L reads copy
+// L % 8, so the 8 lanes of a quarter-warp always hit 8 different 16-byte bank groups: exactly 4
+// wavefronts per warp.  The residual |2 pi v / N| <= 3.1e-3 keeps sin at degree 3 (error
+// < 2.2e-15) and takes cos to degree 4 (< 1.2e-18): one FP64 instruction more per term.
+// Measured on cfg4-desk p1: shared wavefronts 44.8e9 -> 19.3e9 and no bank conflicts, but
+// 200.8 vs 189.7 ms, the FP64 pipe at 74 % either way: the shared pipe was not the limit, so the
+// extra instruction costs time.  Default FUSG_MONO_REP = 1: 4096 entries, one copy (cos to
+// degree 2, error < 1.5e-14).
+#ifndef FUSG_MONO_REP
+#define FUSG_MONO_REP 1
+#endif
+constexpr int kGridRep = FUSG_MONO_REP;
+static_assert(kGridRep == 1 || kGridRep == 8, "phase-table copies: 1 or 8");
+constexpr int kGridPhaseBits = kGridRep == 8 ? 10 : 12;
 template <int BITS>
 struct PhaseSpec {
   static constexpr int N = 1 << BITS;
@@ -80,27 +94,30 @@ struct PhaseSpec {
   static constexpr bool kCos2 = BITS >= 12;  // cos to degree 2
 };
 
-template <int BITS = kPhaseBits>
+// REP copies of each entry, stored [j][REP]
+template <int BITS = kPhaseBits, int REP = 1>
 __device__ __forceinline__ void fill_phase_table(double2* tab) {
   constexpr int N = 1 << BITS;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+  for (int e = threadIdx.x; e < N * REP; e += blockDim.x) {
+    const int j = e / REP;
     double sn, cs;
     sincospi(2.0 * j / N, &sn, &cs);  // exact argument (power-of-two denominator)
-    tab[j] = make_double2(cs * kInv4Pi, sn * kInv4Pi);
+    tab[e] = make_double2(cs * kInv4Pi, sn * kInv4Pi);
   }
 }
 
 // ATT 3 tables (monopole_grid_kernel): rows e^{2 pi i j / N} e^{-alpha j} / (4 pi) and the
 // coarse factors eh[m] = e^{-alpha N m}, m < n_eh (the host bounds Re k d / (2 pi) N by N n_eh).
 constexpr int kEhMax = 512;
-template <int BITS = kPhaseBits>
+template <int BITS = kPhaseBits, int REP = 1>
 __device__ __forceinline__ void fill_att_tables(double2* tab, double* eh, double alpha, int n_eh) {
   constexpr int N = 1 << BITS;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+  for (int e = threadIdx.x; e < N * REP; e += blockDim.x) {
+    const int j = e / REP;
     double sn, cs;
     sincospi(2.0 * j / N, &sn, &cs);
     const double a = exp(-alpha * j) * kInv4Pi;
-    tab[j] = make_double2(cs * a, sn * a);
+    tab[e] = make_double2(cs * a, sn * a);
   }
   for (int m = threadIdx.x; m < n_eh; m += blockDim.x) eh[m] = exp(-alpha * double(N) * m);
 }
@@ -136,11 +153,12 @@ __device__ __forceinline__ double attenuation(double t) {  // e^{-t}, t = Im k *
 // SC (scaled coordinates, monopole_grid_kernel): coordinates arrive pre-multiplied by k1, so d2
 // is already in table turns squared, u = d, the magnitude 1/d carries a factor 1/k1 the caller
 // restores once per voxel, and the coincidence bound is (k1 1e-12)^2 (bits in tiny_bits).
-template <int ATT, bool SC = false, int BITS = kPhaseBits>
+// REP > 1: the table holds REP copies per entry ([j][REP]) and this lane reads copy `rep`
+template <int ATT, bool SC = false, int BITS = kPhaseBits, int REP = 1>
 __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double kim,
                                                  const double2* __restrict__ tab, double2& acc,
                                                  bool& bad, const double* __restrict__ eh = nullptr,
-                                                 long long tiny_bits = 0x3AF357C299A88EA7LL) {
+                                                 long long tiny_bits = 0x3AF357C299A88EA7LL, int rep = 0) {
   // dist < 1e-12 (src/transducer.cpp:112), i.e. d2 < 1e-24: for d2 >= +0 the IEEE order is the
   // integer order of the bit patterns, so the test runs on the integer pipe, exactly
   bad |= __double_as_longlong(d2) < tiny_bits;
@@ -164,7 +182,7 @@ __device__ __forceinline__ void monopole_term_d2(double d2, double k1, double ki
   const double v2 = v * v;
   const double sn = v * fma(v2, PS::S3, PS::S1);
   const double cs = PS::kCos2 ? fma(v2, PS::C2, 1.0) : fma(v2, fma(v2, PS::C4, PS::C2), 1.0);
-  const double2 w = tab[j];
+  const double2 w = tab[REP == 1 ? j : j * REP + rep];
   double mag;
   if constexpr (ATT == 3) {
     // tabulated attenuation: kim carries alpha = Im k / k1, the table rows already hold
@@ -203,7 +221,7 @@ __device__ __forceinline__ void stage_sources(const double* src, int n_src, int 
 #define FUSG_MONO_VPT 4
 #endif
 #ifndef FUSG_MONO_THREADS
-#define FUSG_MONO_THREADS 256
+#define FUSG_MONO_THREADS (kGridRep == 8 ? 512 : 256)  // 128 KB table: one CTA of 16 warps per SM
 #endif
 constexpr int kVPT = FUSG_MONO_VPT;
 #ifndef FUSG_MONO_MINB
@@ -219,10 +237,11 @@ __global__ void __launch_bounds__(FUSG_MONO_THREADS, FUSG_MONO_MINB) monopole_gr
   __shared__ double sx[kSrcChunk], sy[kSrcChunk], sz[kSrcChunk];
   extern __shared__ double2 dyn_tab[];  // phase table (2^kGridPhaseBits) + ATT 3 coarse table
   double2* const tab = dyn_tab;
-  double* const eh = reinterpret_cast<double*>(dyn_tab + (1 << kGridPhaseBits));
+  double* const eh = reinterpret_cast<double*>(dyn_tab + (kGridRep << kGridPhaseBits));
   // visible after the first barrier of the source loop
-  if constexpr (ATT == 3) fill_att_tables<kGridPhaseBits>(tab, eh, kim, n_eh);
-  else fill_phase_table<kGridPhaseBits>(tab);
+  if constexpr (ATT == 3) fill_att_tables<kGridPhaseBits, kGridRep>(tab, eh, kim, n_eh);
+  else fill_phase_table<kGridPhaseBits, kGridRep>(tab);
+  const int rep = threadIdx.x & (kGridRep - 1);  // this lane's table copy
   const int row_threads = (g.dims[0] + kVPT - 1) / kVPT;
   const int64_t count = int64_t(row_threads) * g.dims[1] * g.dims[2];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -270,7 +289,7 @@ __global__ void __launch_bounds__(FUSG_MONO_THREADS, FUSG_MONO_MINB) monopole_gr
         const double q = fma(ddz, ddz, ddy * ddy);
 #pragma unroll
         for (int v = 0; v < kVPT; ++v)
-          monopole_term_d2<ATT, true, kGridPhaseBits>(px[v] + q, k1, kim, tab, acc[v], bad, eh, tiny_bits);
+          monopole_term_d2<ATT, true, kGridPhaseBits, kGridRep>(px[v] + q, k1, kim, tab, acc[v], bad, eh, tiny_bits, rep);
       }
     }
   }
@@ -722,7 +741,7 @@ fusg_status monopole_grid(fusg_ctx* ctx, const double* src_dev, int n_src, const
   }();
   const double umax = dmax * k1;
   const int n_eh = dmax >= 0.0 ? int(umax / (1 << kGridPhaseBits)) + 2 : kEhMax + 1;
-  const size_t dsm = sizeof(double2) * (size_t(1) << kGridPhaseBits) + sizeof(double) * kEhMax;
+  const size_t dsm = sizeof(double2) * (size_t(kGridRep) << kGridPhaseBits) + sizeof(double) * kEhMax;
   static std::atomic<uint64_t> attr_mask{0};
   const bool attr = once_per_device(attr_mask, [&] {
     for (auto fn : {monopole_grid_kernel<0>, monopole_grid_kernel<1>, monopole_grid_kernel<2>, monopole_grid_kernel<3>})

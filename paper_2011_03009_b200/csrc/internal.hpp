@@ -119,6 +119,9 @@ struct fusg_kernel {
   // layout of the x-transformed intermediate A (and X): [kx][z][y] (az = Ny, akx = Nz Ny), or
   // [z][kx][y] for unsharded kernels with FUSG_A_ZKY (az = Px Ny, akx = Ny)
   int64_t az = 0, akx = 0;
+  // z pitch of the spectral intermediate B [kx][ky][z] (>= Nz): rounded up to 8 elements so every
+  // ky row starts on a 128-byte line (FUSG_B_PITCH=0: Nz)
+  int64_t bz = 0;
   int z0 = 0, nz = 0;  // this rank's z-planes of f/u
   int x0 = 0, nx = 0;  // this rank's spectral kx columns
   std::vector<int> zs, nzs, xs, nxs;  // all ranks' ranges (exchange offsets)

@@ -1458,6 +1458,14 @@ fusg_status kernel_init_geometry(fusg_kernel* K, int G, int rank) {
     const char* e = getenv("FUSG_A_ZKY");
     return !(e && atoi(e) == 0);
   }();
+  // B's z pitch: with Nz = 487 (cfg3) the 64-byte tile segments of passes B and D straddled
+  // 128-byte lines (pass B at 0.48 of HBM against 0.78 at Nz = 512)
+  static const bool bpitch = [] {
+    const char* e = getenv("FUSG_B_PITCH");
+    return !(e && atoi(e) == 0);
+  }();
+  const int64_t Nz = K->grid.dims[2];
+  K->bz = bpitch ? (Nz + 7) / 8 * 8 : Nz;
   const int64_t Ny = K->grid.dims[1];
   if (zky && G == 1 && !K->slab) {
     K->az = int64_t(K->P[0]) * Ny;
@@ -1479,7 +1487,7 @@ fusg_status volume_potential_build(fusg_kernel* K, double2 self) {
   const int Hx = K->H[0], Hy = K->H[1], Hz = K->H[2];
   // rank-local apply buffers (unsharded: nz = Nz, nx = Px and X aliases A); the full octant
   // is built on every rank (it depends only on the grid and k)
-  const size_t nA = size_t(Px) * Ny * K->nz, nB = size_t(K->nx) * Py * Nz;
+  const size_t nA = size_t(Px) * Ny * K->nz, nB = size_t(K->nx) * Py * K->bz;
   // folded kx rows this kernel's kx columns [x0, x0 + nx) need (all Hx when unsharded)
   {
     int lo = Hx, hi = -1;
@@ -1590,14 +1598,14 @@ static fusg_status phase_BC(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
   const int Hy = K->H[1], Hz = K->H[2];
   const int nx = K->nx;
-  const int64_t PyNz = int64_t(Py) * Nz;
+  const int64_t bz = K->bz, PyBz = int64_t(Py) * bz;
   // X: [kx][z][y] (x-slab) or A in the kernel's layout (unsharded)
   const int64_t xz = X == K->bufA ? K->az : Ny, xkx = X == K->bufA ? K->akx : int64_t(Nz) * Ny;
   FUSG_TRY(launch_axis<false>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{X, xz, xkx, 1, Ny}},
-                              GStoreF{GStore{K->bufB, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow));
+                              GStoreF{GStore{K->bufB, 1, PyBz, bz, Py, 1.0}}, s, kKindRow));
   if (ev) cudaEventRecord(ev[0], s);
-  FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
-                       GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
+  FUSG_TRY(launch_conv(K->ctx, K->plan[2], Py, nx, GLoadF{GLoad{K->bufB, bz, PyBz, 1, Nz}},
+                       GStoreF{GStore{K->bufB, bz, PyBz, 1, Nz, 1.0}},
                        KOct{K->koct, Px, Py, Pz, int64_t(Hy) * Hz, Hz, 1, K->x0, conv_quad(), K->kf0}, s));
   if (ev) cudaEventRecord(ev[1], s);
   return FUSG_OK;
@@ -1625,8 +1633,8 @@ fusg_status apply_phase_A_peers(fusg_kernel* K, const double2* f, const PeerMap&
 fusg_status apply_phase_D_peers(fusg_kernel* K, const PeerMap& pm, cudaStream_t s) {
   const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Py = K->P[1];
-  const int64_t PyNz = int64_t(Py) * Nz;
-  WArgs a{K->bufB, 1, PyNz, Nz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
+  const int64_t PyBz = int64_t(Py) * K->bz;
+  WArgs a{K->bufB, 1, PyBz, K->bz, Py, nullptr, Ny, 0, 1, Ny, 1.0, Nz, K->nx, K->plan[1].tw, KOct{}, pm};
   int r = Py == 512 ? launch_transpose_r16(K->ctx, false, a, s)
           : Py == 1536 ? launch_transpose_r16x3(K->ctx, false, a, s)
           : Py == 1024 ? launch_transpose_r16x2(K->ctx, false, a, s) : 0;
@@ -1642,11 +1650,11 @@ fusg_status apply_phase_BCD(fusg_kernel* K, double2* X, cudaStream_t s, cudaEven
   const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Py = K->P[1];
   const int nx = K->nx;
-  const int64_t PyNz = int64_t(Py) * Nz;
+  const int64_t PyBz = int64_t(Py) * K->bz;
   const int64_t xz = X == K->bufA ? K->az : Ny, xkx = X == K->bufA ? K->akx : int64_t(Nz) * Ny;
   FUSG_TRY(phase_BC(K, X, s, ev));
   // D: ky columns of B (lines z, tiled, contiguous; outer kx) -> y rows of X, keep Ny
-  return launch_axis<true>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{K->bufB, 1, PyNz, Nz, Py}},
+  return launch_axis<true>(K->ctx, K->plan[1], Nz, nx, GLoadF{GLoad{K->bufB, 1, PyBz, K->bz, Py}},
                            GStoreF{GStore{X, xz, xkx, 1, Ny, 1.0}}, s, kKindCol);
 }
 
@@ -1666,32 +1674,32 @@ fusg_status apply_phase_E(fusg_kernel* K, double2* u, double scale, cudaStream_t
 fusg_status apply_chunk_AB(fusg_kernel* K, const double2* f_z0, int z0, int nzc, cudaStream_t s) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1];
-  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
-  (void)NzNy;
+  const int64_t PyBz = int64_t(Py) * K->bz;
+  (void)Nz;
   double2* A = K->bufA + int64_t(z0) * K->az;
   FUSG_TRY(launch_axis<false>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{f_z0, Nx, int64_t(Ny) * Nx, 1, Nx}},
                               GStoreF{GStore{A, 1, K->az, K->akx, Px, 1.0}}, s, kKindRow));
   return launch_axis<false>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{A, K->az, K->akx, 1, Ny}},
-                            GStoreF{GStore{K->bufB + z0, 1, PyNz, Nz, Py, 1.0}}, s, kKindRow);
+                            GStoreF{GStore{K->bufB + z0, 1, PyBz, K->bz, Py, 1.0}}, s, kKindRow);
 }
 
 fusg_status apply_phase_C(fusg_kernel* K, cudaStream_t s) {
   const int Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1], Pz = K->P[2];
-  const int64_t PyNz = int64_t(Py) * Nz;
-  return launch_conv(K->ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, Nz, PyNz, 1, Nz}},
-                     GStoreF{GStore{K->bufB, Nz, PyNz, 1, Nz, 1.0}},
+  const int64_t bz = K->bz, PyBz = int64_t(Py) * bz;
+  return launch_conv(K->ctx, K->plan[2], Py, Px, GLoadF{GLoad{K->bufB, bz, PyBz, 1, Nz}},
+                     GStoreF{GStore{K->bufB, bz, PyBz, 1, Nz, 1.0}},
                      KOct{K->koct, Px, Py, Pz, int64_t(K->H[1]) * K->H[2], K->H[2], 1, 0, conv_quad(), K->kf0}, s);
 }
 
 fusg_status apply_chunk_DE(fusg_kernel* K, double2* u_z0, int z0, int nzc, double scale, cudaStream_t s) {
   const int Nx = K->grid.dims[0], Ny = K->grid.dims[1], Nz = K->grid.dims[2];
   const int Px = K->P[0], Py = K->P[1];
-  const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(Py) * Nz;
+  const int64_t PyBz = int64_t(Py) * K->bz;
   const double total = double(K->P[0]) * double(K->P[1]) * double(K->P[2]);
-  (void)NzNy;
+  (void)Nz;
   double2* A = K->bufA + int64_t(z0) * K->az;
-  FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{K->bufB + z0, 1, PyNz, Nz, Py}},
+  FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], nzc, Px, GLoadF{GLoad{K->bufB + z0, 1, PyBz, K->bz, Py}},
                              GStoreF{GStore{A, K->az, K->akx, 1, Ny, 1.0}}, s, kKindCol));
   return launch_axis<true>(K->ctx, K->plan[0], Ny, nzc, GLoadF{GLoad{A, 1, K->az, K->akx, Px}},
                            GStoreF{GStore{u_z0, Nx, int64_t(Ny) * Nx, 1, Nx, scale / total}}, s, kKindCol);
@@ -1714,10 +1722,10 @@ static int try_ab_fused(fusg_kernel* K, const double2* f, cudaStream_t s) {
     return 0;
   }
   if (slabs > 4096) return 0;
-  const int64_t PyNz = int64_t(Py) * Nz;
+  const int64_t PyBz = int64_t(Py) * K->bz;
   ABFused fa;
   fa.a = WArgs{f, Nx, int64_t(Ny) * Nx, 1, Nx, K->bufA, 1, Ny, 8 * int64_t(Ny), Px, 1.0, Ny, Nz, K->plan[0].tw, KOct{}};
-  fa.b = WArgs{K->bufA, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB, 1, PyNz, Nz, Py, 1.0, 8, Px, K->plan[1].tw, KOct{}};
+  fa.b = WArgs{K->bufA, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB, 1, PyBz, K->bz, Py, 1.0, 8, Px, K->plan[1].tw, KOct{}};
   fa.nz = Nz;
   fa.slabs = slabs;
   fa.ring = kRing;
@@ -1755,7 +1763,7 @@ static int try_ab_chunks(fusg_kernel* K, const double2* f, cudaStream_t s) {
   // the B stream starts after everything already queued on s (e.g. the previous apply)
   if (cudaEventRecord(K->ab_ev[2 * C], s) != cudaSuccess || cudaStreamWaitEvent(K->ab_stream, K->ab_ev[2 * C], 0))
     return -1;
-  const int64_t PyNz = int64_t(Py) * Nz;
+  const int64_t PyBz = int64_t(Py) * K->bz;
   for (int c = 0; c < C; ++c) {
     const int z0 = 8 * c, nzc = std::min(8, Nz - z0);
     double2* const sl = K->bufA + int64_t(c % kRing) * slot;
@@ -1765,7 +1773,7 @@ static int try_ab_chunks(fusg_kernel* K, const double2* f, cudaStream_t s) {
     if (launch_r16_chunk(K->ctx, false, wa, s) < 0) return -1;
     if (cudaEventRecord(evA[2 * c], s) != cudaSuccess || cudaStreamWaitEvent(K->ab_stream, evA[2 * c], 0))
       return -1;
-    const WArgs wb{sl, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB + z0, 1, PyNz, Nz, Py, 1.0, nzc, Px, K->plan[1].tw,
+    const WArgs wb{sl, Ny, 8 * int64_t(Ny), 1, Ny, K->bufB + z0, 1, PyBz, K->bz, Py, 1.0, nzc, Px, K->plan[1].tw,
                    KOct{}};
     if (launch_r16_chunk(K->ctx, true, wb, K->ab_stream) < 0) return -1;
     if (cudaEventRecord(evA[2 * c + 1], K->ab_stream) != cudaSuccess) return -1;
@@ -1786,13 +1794,12 @@ fusg_status volume_potential_apply(fusg_kernel* K, const double2* f, double2* u,
   if (fused < 0) return FUSG_CUDA;
   if (fused) {  // A+B in one launch (both marks after it), then C, D, E
     const int Ny = K->grid.dims[1], Nz = K->grid.dims[2];
-    const int64_t NzNy = int64_t(Nz) * Ny, PyNz = int64_t(K->P[1]) * Nz;
+    const int64_t PyBz = int64_t(K->P[1]) * K->bz;
     mark(1);
     mark(2);
     FUSG_TRY(apply_phase_C(K, s));
     mark(3);
-    (void)NzNy;
-    FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], Nz, K->P[0], GLoadF{GLoad{K->bufB, 1, PyNz, Nz, K->P[1]}},
+    FUSG_TRY(launch_axis<true>(K->ctx, K->plan[1], Nz, K->P[0], GLoadF{GLoad{K->bufB, 1, PyBz, K->bz, K->P[1]}},
                                GStoreF{GStore{K->bufA, K->az, K->akx, 1, Ny, 1.0}}, s, kKindCol));
     mark(4);
     FUSG_TRY(apply_phase_E(K, u, scale, s));
