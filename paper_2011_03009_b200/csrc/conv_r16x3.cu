@@ -336,10 +336,12 @@ struct X3TSmem {
 };
 
 // CTAs per SM the transposing kernels' register budget targets: 1 per SM at T = 4 for 1536
-// (12 warps, <= 168 registers); R = 2 (1024) targets 2 CTAs of 8 warps (<= 128 registers) when
-// FUSG_X2T_MINB2 is set at compile time, else 1 CTA (8 warps, ~200 registers)
+// (12 warps, <= 168 registers); R = 2 (1024): 1 CTA (8 warps, ~200 registers), or with
+// FUSG_X2T_MINB2 set at compile time a 128-register budget with the lane twiddles read from the
+// CTA tables (no spills) -- but the double-buffered tiles (~130 KB) still allow one CTA per SM,
+// so it only adds shared loads
 #ifndef FUSG_X2T_MINB2
-#define FUSG_X2T_MINB2 1
+#define FUSG_X2T_MINB2 0
 #endif
 #define X3T_MINB ((T == 4 && R == 2 && FUSG_X2T_MINB2) ? 2 : 4 / T)
 #define X3T_SMEMTW (T == 4 && R == 2 && FUSG_X2T_MINB2)  // lane twiddles from the CTA tables
