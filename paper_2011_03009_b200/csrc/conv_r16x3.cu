@@ -309,6 +309,219 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
   }
 }
 
+// ---------------------------------------------------------------------------- pass C, quad CTA + TMEM
+// One CTA of twelve warps per SM runs the (up to) four lines (+-ky, +-kx) that read one folded
+// K^ row: warp 4 r + j owns residue r of line j.  The three warps of a line sit in the same
+// tensor-memory lane quarter (warp index mod 4 = j) and lane l of each holds position
+// 32 n1 + l of its t_r, so the recombination x[n'] = t0 + t1 + t2 is lane-local: every warp
+// parks its t_r in tensor memory (tcgen05.st, 64 columns), and after a 96-thread named barrier
+// reads back the slots it combines (tcgen05.ld) and stores them -- no shared-memory round trip
+// (384 of ~2290 LSU wavefronts per line), on a data path separate from the shared-memory pipe
+// (tools/mb/tmem_ldst.cu: >= 184 B/clk/SM written, >= 236 B/clk/SM read with 12 warps).
+// The K^ row is staged once per CTA (three buffers, two rows ahead; each warp arrives on the
+// buffer's "read" mbarrier and thread 0 waits on it before the refill, so no CTA-wide barrier
+// runs in the loop); each line's input row is staged per line group one row ahead.
+// Measured (cfg5, B200): 30.5 ms against 29.4 ms for the three-warp kernel -- the lane twiddles
+// have to come from the shared tables to stay under 168 registers (+120 wavefronts per line),
+// the three warps of a line share one scheduler (their lane quarter) and hit the FP64 pipe
+// together, and neither a CTA barrier taken at staggered points (38.1 ms) nor mbarriers waited
+// on late with t_r double-buffered (31.7 ms) helped.  Opt-in: FUSG_X3_QUADTM=1.
+struct X3QSmem {
+  static constexpr int XB = 0;              // [12][512] exchange buffers, one per warp
+  static constexpr int KB = 12 * 512;       // [3][770] folded K^ rows
+  static constexpr int SB = KB + 3 * 770;   // [4][768] staged input rows, one per line
+  static constexpr int TW = SB + 4 * 768;   // [4][32] W512^(lane 2^j)
+  static constexpr int US = TW + 128;       // [3][32] W1536^(lane r)
+  static constexpr int C48 = US + 96;       // [48]
+  static constexpr int END = C48 + 48;
+  // + 3 + 3 K^ barriers (landed / read), 4 row barriers, the tensor-memory base address
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 11 * sizeof(uint64_t);
+};
+
+// 4 complex128 values of this lane -> 16 tensor-memory columns at taddr (four of them park a
+// t_r: one 64-column store needs 64 consecutive registers, which made the allocator spill)
+__device__ __forceinline__ void tm_st_c4(uint32_t taddr, const double2* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(taddr),
+      "r"(__double2loint(v[0].x)), "r"(__double2hiint(v[0].x)), "r"(__double2loint(v[0].y)), "r"(__double2hiint(v[0].y)),
+      "r"(__double2loint(v[1].x)), "r"(__double2hiint(v[1].x)), "r"(__double2loint(v[1].y)), "r"(__double2hiint(v[1].y)),
+      "r"(__double2loint(v[2].x)), "r"(__double2hiint(v[2].x)), "r"(__double2loint(v[2].y)), "r"(__double2hiint(v[2].y)),
+      "r"(__double2loint(v[3].x)), "r"(__double2hiint(v[3].x)), "r"(__double2loint(v[3].y)), "r"(__double2hiint(v[3].y))
+      : "memory");
+}
+__device__ __forceinline__ void tm_st_c16(uint32_t taddr, const double2* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tm_st_c4(taddr + 16u * unsigned(i), v + 4 * i);
+}
+// 4 complex128 values (16 columns) of this lane from taddr
+__device__ __forceinline__ void tm_ld_c4(uint32_t taddr, double2* v) {
+  uint32_t w[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+        "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    v[i] = make_double2(__hiloint2double(int(w[4 * i + 1]), int(w[4 * i])), __hiloint2double(int(w[4 * i + 3]), int(w[4 * i + 2])));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// x[n'] = t0 + t1 + t2 and x[n' + 512] = t0 + W3^-1 t1 + W3^-2 t2 (the expressions of x3_recombine)
+__device__ __forceinline__ void x3_combine(double2 t0, double2 t1, double2 t2, double2& lo, double2& hi) {
+  constexpr double kS3 = 0.8660254037844386467637;
+  const double2 s = cadd(t1, t2), d = csub(t1, t2);
+  lo = cadd(t0, s);
+  hi = make_double2(t0.x - 0.5 * s.x - kS3 * d.y, t0.y - 0.5 * s.y + kS3 * d.x);
+}
+
+#ifndef FUSG_X3Q_SMEMTW
+#define FUSG_X3Q_SMEMTW 1
+#endif
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__global__ void __launch_bounds__(384, 1) conv_r16x3q(WArgs a) {
+  constexpr int HZ = 769;
+  extern __shared__ double2 sm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = wid & 3, r = wid >> 2;  // line of the quad (tensor-memory lane quarter), residue
+  double2* const xr = sm + X3QSmem::XB + 512 * wid;
+  double2* const xs = sm + X3QSmem::SB + 768 * j;
+  uint64_t* const kfull = reinterpret_cast<uint64_t*>(sm + X3QSmem::END);  // [3] K^ row landed
+  uint64_t* const kfree = kfull + 3;                                        // [3] K^ row read by the 12 warps
+  uint64_t* const xbar = kfull + 6 + j;
+  uint32_t* const tm_slot = reinterpret_cast<uint32_t*>(kfull + 10);
+  x3_tables(a.tw, sm + X3QSmem::TW, sm + X3QSmem::US, sm + X3QSmem::C48);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(kfull + i, 1);
+    for (int i = 0; i < 3; ++i) mbar_init(kfree + i, 12);
+    for (int i = 0; i < 4; ++i) mbar_init(kfull + 6 + i, 1);
+    mbar_init_fence();
+  }
+  if (wid == 0) {  // 256 columns: t_r at columns 64 r (192 used)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(smem_u32(tm_slot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tm_fence_before_sync();
+  __syncthreads();
+  tm_fence_after_sync();
+  const uint32_t tm_base = *tm_slot;
+  const uint32_t tm_lane = tm_base + (uint32_t(32 * j) << 16);
+  const int Py = a.ko.Py, Px = a.ko.Px;
+  const int Hy = Py / 2 + 1, Hx = Px / 2 + 1;
+  const int nrows = Hy * Hx;  // folded K^ rows (< 2^31, host-checked)
+  const int stride = int(gridDim.x);
+  const int nv = a.in_nvalid, onv = a.out_nvalid;
+  // line j of folded row q = fx Hy + fy: ky = fy or Py - fy (odd j), kx = fx or Px - fx (j >= 2);
+  // false when that mirror is the line itself
+  auto line_of = [&](int q, int& ky, int& kx) {
+    const int fx = q / Hy, fy = q - fx * Hy;
+    ky = fy, kx = fx;
+    bool on = true;
+    if (j & 1) {
+      ky = Py - fy;
+      on = fy > 0 && ky != fy;
+    }
+    if (j & 2) {
+      kx = Px - fx;
+      on = on && fx > 0 && kx != fx;
+    }
+    return on;
+  };
+  auto stage_k = [&](int q, int buf) {  // thread 0
+    if (q < nrows) {
+      const int fx = q / Hy, fy = q - fx * Hy;
+      bulk_stage(sm + X3QSmem::KB + 770 * buf, a.ko.line(fy, fx), HZ * sizeof(double2), kfull + buf);
+    }
+  };
+  auto stage_row = [&](int q) {  // residue 0, lane 0 of the line group, after the group's reads
+    int ky, kx;
+    if (q < nrows && line_of(q, ky, kx))
+      bulk_stage(xs, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(nv) * sizeof(double2), xbar);
+  };
+  int q = int(blockIdx.x);
+  if (threadIdx.x == 0) {
+    stage_k(q, 0);
+    stage_k(q + stride, 1);
+  }
+  if (r == 0 && lane == 0) stage_row(q);
+  unsigned xph = 0;
+#pragma unroll 1
+  for (unsigned it = 0; q < nrows; q += stride, ++it) {
+    const int buf = int(it % 3u);
+    const double2* kb = sm + X3QSmem::KB + 770 * buf;
+    int ky, kx;
+    if (!line_of(q, ky, kx)) {  // the row's mirror line is the line itself: nothing to do
+      if (lane == 0) {
+        if (r == 0) stage_row(q + stride);
+        // wait for the row like a working warp: an idle warp running ahead would arrive on this
+        // buffer's next phase before the others have finished this one
+        mbar_wait(kfull + buf, (it / 3u) & 1u);
+        mbar_arrive(kfree + buf);
+      }
+      __syncwarp();
+      continue;
+    }
+    // lane-derived shared-memory addresses are rebuilt every row instead of living in (spilled)
+    // registers across the loop
+    int ln = lane;
+    asm volatile("" : "+r"(ln));
+    const X3W<FUSG_X3Q_SMEMTW != 0> W(sm + X3QSmem::US, sm + X3QSmem::TW, sm + X3QSmem::C48, r, ln);
+    double2 v[16];
+    mbar_wait(xbar, xph);  // this line's row has landed
+    xph ^= 1u;
+    W.gather(v, xs, nv, ln);
+    nbar_sync(1 + j, 96);  // the staged row is read by the line's three warps: refill it
+    if (r == 0 && lane == 0) stage_row(q + stride);
+    W.forward_a(v);
+    W.forward_b_mulk(v, xr, ln, kb, kfull + buf, (it / 3u) & 1u);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(kfree + buf);  // this warp has read the K^ row
+    if (threadIdx.x == 0 && q + 2 * stride < nrows) {
+      // the buffer of the previous row takes the row two ahead once all twelve warps have read it
+      // (line 0 is never its own mirror, so this thread runs every row)
+      const unsigned pb = (it + 2u) % 3u;
+      if (it > 0) mbar_wait(kfree + pb, ((it - 1u) / 3u) & 1u);
+      stage_k(q + 2 * stride, int(pb));
+    }
+    W.inverse(v, xr, ln);
+    __syncwarp();  // every lane has read its exchange slots
+    tm_st_c16(tm_lane + 64u * unsigned(r), v);
+    tm_wait_st();
+    tm_fence_before_sync();
+    nbar_sync(1 + j, 96);  // the three t_r are in tensor memory
+    tm_fence_after_sync();
+    // warp r combines slots 4 r .. 4 r + 3 (r < 2: x[n'] and x[n' + 512]) or 8 .. 15 (x[n'] only)
+    double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    const double sc = a.scale;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && r < 2) break;
+      const int s0 = r < 2 ? 4 * r : 8 + 4 * h;
+      double2 t0[4], t1[4], t2[4];
+      tm_ld_c4(tm_lane + 4u * unsigned(s0), t0);
+      tm_ld_c4(tm_lane + 64u + 4u * unsigned(s0), t1);
+      tm_ld_c4(tm_lane + 128u + 4u * unsigned(s0), t2);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2 lo, hi;
+        x3_combine(t0[i], t1[i], t2[i], lo, hi);
+        const int m = 32 * (s0 + i) + ln;
+        if (m < onv) out[m] = sc == 1.0 ? lo : cscale(lo, sc);
+        if (r < 2 && m + 512 < onv) out[m + 512] = sc == 1.0 ? hi : cscale(hi, sc);
+      }
+    }
+    tm_fence_before_sync();  // these reads are ordered before the next row's tcgen05.st by its first group barrier
+  }
+  __syncthreads();
+  if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tm_base) : "memory");
+}
+
 // ---------------------------------------------------------------------------- passes A / B
 // Row -> column (forward, pruned input <= 768 of 1536): a CTA of 3T warps transforms T adjacent
 // lines (warp 3t + r: line t, residue r).  The T input rows (contiguous when the rows are
@@ -603,6 +816,34 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
   if (!load_w48()) {
     set_error(FUSG_CUDA, "pass C (1536 = 3 x 512): cannot load the W48 table");
     return -1;
+  }
+  // Unsharded applies, opt-in (FUSG_X3_QUADTM=1): the quad-CTA kernel with the recombination
+  // through tensor memory.  Bitwise the three-warp kernel's result; measured 30.5 ms against
+  // 29.4 ms at cfg5, so the three-warp kernel stays the default.
+  static const bool quadtm = [] {
+    const char* e = getenv("FUSG_X3_QUADTM");
+    return e && atoi(e) != 0;
+  }();
+  if (quadtm && a.n_outer == a.ko.Px && a.n_inner == a.ko.Py && a.ko.kx_off == 0 && a.ko.kx_base == 0 &&
+      a.in_sp == 1 && a.out_sp == 1 && a.ko.s_kz == 1) {
+    static std::atomic<uint64_t> qattr{0};
+    if (!once_per_device(qattr, [&] {
+          return cudaFuncSetAttribute(conv_r16x3q, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(X3QSmem::BYTES)) == cudaSuccess;
+        })) {
+      set_error(FUSG_CUDA, "pass C (1536, quad CTA): cannot configure shared memory");
+      return -1;
+    }
+    const int64_t rows = int64_t(a.ko.Py / 2 + 1) * (a.ko.Px / 2 + 1);
+    const int64_t grid = std::min<int64_t>(rows, ctx->num_sms);
+    conv_r16x3q<<<unsigned(grid), 384, X3QSmem::BYTES, s>>>(a);
+    ctx->launches++;
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+      cuda_error(err, "pass C (1536, quad CTA)");
+      return -1;
+    }
+    return 1;
   }
   // FUSG_X3_MODE: 1 (default) input and K^ rows in two staging buffers (4 CTAs per SM); 2 one
   // shared staging buffer and lane twiddles from the tables (5 CTAs); 0 input rows from L2

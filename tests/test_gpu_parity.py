@@ -591,6 +591,46 @@ def test_ab_fused_ring_path_is_bitwise_two_pass(tmp_path, fused):
         assert np.array_equal(res["0"][key], res[fused][key])
 
 
+_QUADTM_CHILD = """
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2011_03009_b200 import fus
+w = fus.medium_preset("water")
+out = []
+# Pz = 1536 with full and partial rows, odd / even / tiny Px, Py (self-mirror lines, idle warps)
+for dims in [(5, 4, 768), (1, 1, 700), (12, 9, 650), (33, 2, 601), (40, 37, 768)]:
+    g = fus.make_grid([0, 0, 0], [d * 1e-4 for d in dims], 1e-4, 2)
+    assert fus.padded_dims(g)[2] == 1536
+    k = fus.complex_wavenumber(w, 1.1e6, 2)
+    f = fus.random_vector(g.count(), 23)
+    K = fus.GreenKernel(g, k)
+    out.append(K.apply(f, -0.5).cpu().numpy())
+    out.append(K.apply(f).cpu().numpy())
+np.savez(sys.argv[2], *out)
+"""
+
+
+@pytest.mark.gpu
+def test_quad_cta_tensor_memory_pass_c_is_bitwise_three_warp_kernel(tmp_path):
+    # FUSG_X3_QUADTM=1 (opt-in): pass C at 1536 with one 12-warp CTA per folded K^ row and the
+    # recombination of the three residues through tensor memory (tcgen05.st / tcgen05.ld) runs
+    # the same transforms and the same recombination expressions: bit for bit the default.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for v in ("0", "1"):
+        p = tmp_path / f"u{v}.npz"
+        env = dict(os.environ, FUSG_X3_QUADTM=v)
+        r = subprocess.run([sys.executable, "-c", _QUADTM_CHILD, root, str(p)], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[v] = np.load(p)
+    for key in res["0"].files:
+        assert np.array_equal(res["0"][key], res["1"][key]), key
+
+
 @pytest.mark.parametrize("G", [1, 2, 3, 5])
 def test_incident_field_zslabs_are_bitwise_the_full_field(ctx, G):
     # SURVEY.md 8(e): p1 shards by z-planes with no collective; ragged slabs of any split must
