@@ -142,23 +142,64 @@ __device__ __forceinline__ double2 w16(double2 a) {
   }
 }
 
+// (a + w16^E b, a - w16^E b) in 6 FMAs: w = wr (1 + i t) with the compile-time t = wi / wr, so
+// w b = wr ((b.x - t b.y) + i (b.y + t b.x)) and the scale by wr rides on the butterfly's adds
+// (a separate complex multiply plus the adds take 8).  Quarter turns cost 4 adds.
+template <bool INV, int E>
+__device__ __forceinline__ void pm16(double2 a, double2 b, double2& p, double2& m) {
+  constexpr int e = E & 15;
+  if constexpr (e == 0) {
+    p = cadd(a, b);
+    m = csub(a, b);
+  } else if constexpr (e == 8) {
+    p = csub(a, b);
+    m = cadd(a, b);
+  } else if constexpr (e == 4 || e == 12) {
+    const double2 r = e == 4 ? rot90<INV>(b) : rot90<!INV>(b);
+    p = cadd(a, r);
+    m = csub(a, r);
+  } else {
+    constexpr double cs[16] = {1.0, c::kC16, c::kR2, c::kS16, 0.0, -c::kS16, -c::kR2, -c::kC16,
+                               -1.0, -c::kC16, -c::kR2, -c::kS16, 0.0, c::kS16, c::kR2, c::kC16};
+    constexpr double wr = cs[e];
+    constexpr double sn = cs[(e + 12) & 15];  // sin(2 pi e / 16) = cos(2 pi (e - 4) / 16)
+    constexpr double t = (INV ? sn : -sn) / wr;
+    const double u = fma(-t, b.y, b.x), v = fma(t, b.x, b.y);
+    p = make_double2(fma(wr, u, a.x), fma(wr, v, a.y));
+    m = make_double2(fma(-wr, u, a.x), fma(-wr, v, a.y));
+  }
+}
+// dft4 of (a0, w16^E1 a1, w16^E2 a2, w16^E3 a3) with the twiddles folded into the butterflies:
+// w^E1 a1 +- w^E3 a3 = w^E1 (a1 +- w^(E3 - E1) a3).  20-24 FP64 instructions instead of 24-28.
+template <bool INV, int E1, int E2, int E3>
+__device__ __forceinline__ void dft4_tw16(double2& a0, double2& a1, double2& a2, double2& a3) {
+  double2 t0, t1, s, d, o0, o1, o2, o3;
+  pm16<INV, E2>(a0, a2, t0, t1);
+  pm16<INV, E3 - E1 + 16>(a1, a3, s, d);
+  pm16<INV, E1>(t0, s, o0, o2);
+  pm16<INV, E1 + 4>(t1, d, o1, o3);  // rot90<INV>(w^E1 d) = w^(E1 + 4) d
+  a0 = o0;
+  a1 = o1;
+  a2 = o2;
+  a3 = o3;
+}
+// the outer level of the 4 x 4 radix 16: a[4 q1 + r2] holds B[r2][q1] before its twiddle
+// w16^(r2 q1)
+template <bool INV>
+__device__ __forceinline__ void dft16_outer(double2* a) {
+  dft4<INV>(a[0], a[1], a[2], a[3]);
+  dft4_tw16<INV, 1, 2, 3>(a[4], a[5], a[6], a[7]);
+  dft4_tw16<INV, 2, 4, 6>(a[8], a[9], a[10], a[11]);
+  dft4_tw16<INV, 3, 6, 9>(a[12], a[13], a[14], a[15]);
+}
+
 template <bool INV>
 __device__ __forceinline__ void dft16(double2* a) {
   // 4 x 4: inner DFT4 over stride-4 inputs, twiddle, outer DFT4
 #pragma unroll
   for (int r2 = 0; r2 < 4; ++r2) dft4<INV>(a[r2], a[r2 + 4], a[r2 + 8], a[r2 + 12]);
-  // a[r2 + 4*q1] now holds B[r2][q1]; twiddle by w16^(r2*q1)
-  a[5] = w16<INV, 1>(a[5]);
-  a[9] = w16<INV, 2>(a[9]);
-  a[13] = w16<INV, 3>(a[13]);
-  a[6] = w16<INV, 2>(a[6]);
-  a[10] = w16<INV, 4>(a[10]);
-  a[14] = w16<INV, 6>(a[14]);
-  a[7] = w16<INV, 3>(a[7]);
-  a[11] = w16<INV, 6>(a[11]);
-  a[15] = w16<INV, 9>(a[15]);
-#pragma unroll
-  for (int q1 = 0; q1 < 4; ++q1) dft4<INV>(a[4 * q1], a[4 * q1 + 1], a[4 * q1 + 2], a[4 * q1 + 3]);
+  // a[r2 + 4*q1] now holds B[r2][q1]; the twiddles w16^(r2*q1) ride on the outer butterflies
+  dft16_outer<INV>(a);
   // X[q1 + 4 q2] = a[4 q1 + q2]  -> transpose 4x4
   double2 t[16];
 #pragma unroll
@@ -181,17 +222,7 @@ __device__ __forceinline__ void dft16_half_in(double2* a) {
     a[r2 + 8] = csub(x0, x1);
     a[r2 + 12] = csub(x0, x1r);
   }
-  a[5] = w16<INV, 1>(a[5]);
-  a[9] = w16<INV, 2>(a[9]);
-  a[13] = w16<INV, 3>(a[13]);
-  a[6] = w16<INV, 2>(a[6]);
-  a[10] = w16<INV, 4>(a[10]);
-  a[14] = w16<INV, 6>(a[14]);
-  a[7] = w16<INV, 3>(a[7]);
-  a[11] = w16<INV, 6>(a[11]);
-  a[15] = w16<INV, 9>(a[15]);
-#pragma unroll
-  for (int q1 = 0; q1 < 4; ++q1) dft4<INV>(a[4 * q1], a[4 * q1 + 1], a[4 * q1 + 2], a[4 * q1 + 3]);
+  dft16_outer<INV>(a);
   double2 t[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) t[i] = a[i];
@@ -206,23 +237,14 @@ template <bool INV>
 __device__ __forceinline__ void dft16_half_out(double2* a) {
 #pragma unroll
   for (int r2 = 0; r2 < 4; ++r2) dft4<INV>(a[r2], a[r2 + 4], a[r2 + 8], a[r2 + 12]);
-  a[5] = w16<INV, 1>(a[5]);
-  a[9] = w16<INV, 2>(a[9]);
-  a[13] = w16<INV, 3>(a[13]);
-  a[6] = w16<INV, 2>(a[6]);
-  a[10] = w16<INV, 4>(a[10]);
-  a[14] = w16<INV, 6>(a[14]);
-  a[7] = w16<INV, 3>(a[7]);
-  a[11] = w16<INV, 6>(a[11]);
-  a[15] = w16<INV, 9>(a[15]);
-  // outer DFT4 over a[4 q1 .. 4 q1 + 3], outputs q2 = 0, 1 only: X[q1 + 4 q2]
+  // outer DFT4 over a[4 q1 .. 4 q1 + 3], outputs q2 = 0, 1 only: X[q1 + 4 q2] (the unused
+  // differences of the fused butterflies are dead code)
+  dft16_outer<INV>(a);
   double2 x[8];
 #pragma unroll
   for (int q1 = 0; q1 < 4; ++q1) {
-    const double2 t0 = cadd(a[4 * q1], a[4 * q1 + 2]), t1 = csub(a[4 * q1], a[4 * q1 + 2]);
-    const double2 t2 = cadd(a[4 * q1 + 1], a[4 * q1 + 3]), t3 = rot90<INV>(csub(a[4 * q1 + 1], a[4 * q1 + 3]));
-    x[q1] = cadd(t0, t2);
-    x[q1 + 4] = cadd(t1, t3);
+    x[q1] = a[4 * q1];
+    x[q1 + 4] = a[4 * q1 + 1];
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) a[i] = x[i];
