@@ -92,10 +92,22 @@ __device__ __forceinline__ void r16_fwd_r2(double2* v, bool b) {
   const double2 recv = shfl_xor_d2(send, 16);
   const double2 z0 = sel_d2(b, recv, v[I]);
   const double2 z1 = sel_d2(b, v[I + 8], recv);
-  double2 t = w32<false, I>(z1);
-  t = sel_d2(b, rot90<false>(t), t);  // W32^8 = -i
-  v[I] = cadd(z0, t);
-  v[I + 8] = csub(z0, t);
+  if constexpr (I == 0) {
+    const double2 t = sel_d2(b, rot90<false>(z1), z1);  // W32^8 = -i
+    v[I] = cadd(z0, t);
+    v[I + 8] = csub(z0, t);
+  } else {
+    // z0 +- w z1, w = W32^(I + 8 b) = wr (1 + i t): the two compile-time (wr, t) pairs are picked
+    // by the lane half and the scale rides on the butterfly (6 FMAs; multiply then add: 8)
+    constexpr double cs[9] = {1.0, 0.98078528040323044912618, c::kC16, 0.83146961230254523707879, c::kR2,
+                              0.55557023301960222474283, c::kS16, 0.19509032201612826784828, 0.0};
+    constexpr double co = cs[I], si = cs[8 - I];  // cos, sin of 2 pi I / 32; w(b = 0) = (co, -si), w(b = 1) = (-si, -co)
+    const double wr = b ? -si : co;
+    const double t = b ? co / si : -si / co;
+    const double u = fma(-t, z1.y, z1.x), w = fma(t, z1.x, z1.y);
+    v[I] = make_double2(fma(wr, u, z0.x), fma(wr, w, z0.y));
+    v[I + 8] = make_double2(fma(-wr, u, z0.x), fma(-wr, w, z0.y));
+  }
 }
 template <int I>
 __device__ __forceinline__ void r16_inv_r2(double2* v, bool b) {
