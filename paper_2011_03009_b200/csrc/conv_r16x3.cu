@@ -220,7 +220,9 @@ __device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.syn
 // (loaded while the forward transform runs), then the next input row (loaded during the inverse
 // and the recombination); 41 KB of shared memory and lane twiddles read from the tables let 5
 // CTAs (15 warps) share an SM. MODE 0: input rows read from L2 (5 CTAs).
-template <int MODE>
+// FULL: every row holds 768 valid inputs and outputs (cfg5): the bounds are compile-time, so the
+// gather and the recombination carry no predicates or zero fills.
+template <int MODE, bool FULL = false>
 __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(WArgs a) {
   constexpr bool STAGED = MODE != 0;
   constexpr int HZ = 769;
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
       bulk_stage(kb, a.ko.line(ky, kx), HZ * sizeof(double2), bars + 1);
     }
   };
-  const int nv = a.in_nvalid, onv = a.out_nvalid;
+  const int nv = FULL ? 768 : a.in_nvalid, onv = FULL ? 768 : a.out_nvalid;
   int64_t line = blockIdx.x;
   if (threadIdx.x == 0) {
     prefetch_in(line);
@@ -852,11 +854,14 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     const int m = e ? atoi(e) : 1;
     return (m == 0 || m == 2) ? m : 1;
   }();
-  const auto fn = mode == 1 ? conv_r16x3<1> : mode == 2 ? conv_r16x3<2> : conv_r16x3<0>;
+  const bool full = mode == 1 && a.in_nvalid == 768 && a.out_nvalid == 768;
+  const auto fn = full ? conv_r16x3<1, true> : mode == 1 ? conv_r16x3<1> : mode == 2 ? conv_r16x3<2> : conv_r16x3<0>;
   const size_t smem = mode == 1 ? X3Smem<1>::BYTES : mode == 2 ? X3Smem<2>::BYTES : X3Smem<0>::BYTES;
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
         return cudaFuncSetAttribute(conv_r16x3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3Smem<1>::BYTES)) == cudaSuccess &&
+               cudaFuncSetAttribute(conv_r16x3<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3Smem<1>::BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(conv_r16x3<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     int(X3Smem<2>::BYTES)) == cudaSuccess &&

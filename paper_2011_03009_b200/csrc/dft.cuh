@@ -185,8 +185,25 @@ __device__ __forceinline__ void dft4_tw16(double2& a0, double2& a1, double2& a2,
 }
 // the outer level of the 4 x 4 radix 16: a[4 q1 + r2] holds B[r2][q1] before its twiddle
 // w16^(r2 q1)
+#ifndef FUSG_DFT16_TAN
+#define FUSG_DFT16_TAN 1  // 0: multiply by the inner twiddles, then plain radix-4 butterflies
+#endif
 template <bool INV>
 __device__ __forceinline__ void dft16_outer(double2* a) {
+  if constexpr (!FUSG_DFT16_TAN) {
+    a[5] = w16<INV, 1>(a[5]);
+    a[6] = w16<INV, 2>(a[6]);
+    a[7] = w16<INV, 3>(a[7]);
+    a[9] = w16<INV, 2>(a[9]);
+    a[10] = w16<INV, 4>(a[10]);
+    a[11] = w16<INV, 6>(a[11]);
+    a[13] = w16<INV, 3>(a[13]);
+    a[14] = w16<INV, 6>(a[14]);
+    a[15] = w16<INV, 9>(a[15]);
+#pragma unroll
+    for (int q1 = 0; q1 < 4; ++q1) dft4<INV>(a[4 * q1], a[4 * q1 + 1], a[4 * q1 + 2], a[4 * q1 + 3]);
+    return;
+  }
   dft4<INV>(a[0], a[1], a[2], a[3]);
   dft4_tw16<INV, 1, 2, 3>(a[4], a[5], a[6], a[7]);
   dft4_tw16<INV, 2, 4, 6>(a[8], a[9], a[10], a[11]);
