@@ -24,12 +24,16 @@
 
 namespace fusg {
 
+#ifndef FUSG_X3_PAD
+#define FUSG_X3_PAD 1  // pass C exchange buffers as 16 rows of 33 entries (0: XOR-swizzled [16][32])
+#endif
 // shared-memory layout (double2 offsets) of one CTA
 template <int MODE = 1>
 struct X3Smem {
   static constexpr bool STAGED = MODE != 0;
-  static constexpr int XB = 0;             // [3][512] exchange buffers, then the t_r rows
-  static constexpr int KB = 1536;          // folded K^ row (769, padded to 770); MODE 2: also the input row
+  static constexpr int XS = FUSG_X3_PAD ? 16 * 33 : 512;  // exchange buffer of one warp (X3W<.., PAD>)
+  static constexpr int XB = 0;             // [3][XS] exchange buffers, then the t_r rows
+  static constexpr int KB = 3 * XS;        // folded K^ row (769, padded to 770); MODE 2: also the input row
   static constexpr int TW = KB + 770;      // [4][32] W512^(lane 2^j)
   static constexpr int US = TW + 128;      // [3][32] W1536^(lane r)
   static constexpr int C48 = US + 96;      // [48] W48^j
@@ -55,9 +59,14 @@ __device__ __forceinline__ double2 lds_fresh(const double2* p) {
 // Per-warp pieces of the 1536 = 3 x 512 transform (warp r owns residue r).  SMEMTW: the lane
 // twiddles W1536^(lane r), W512^(lane 2^j) are read from the CTA tables at each use instead of
 // living in 20 registers for the whole kernel (the 5-CTA pass C needs <= 136 registers).
-template <bool SMEMTW, int R = 3>
+template <bool SMEMTW, int R = 3, bool PAD = false>
 struct X3W {
   static_assert(R == 2 || R == 3, "lines of 2 x 512 or 3 x 512");
+  // exchange buffer index of (row, col): XOR-swizzled [16][32], or (PAD) rows of 33 entries --
+  // also conflict-free for both access patterns and affine in the lane, so every offset folds
+  // into the instruction's immediate (the XOR costs a LOP3 per access, 5 % of pass C's instructions)
+  static constexpr int XSTRIDE = PAD ? 16 * 33 : 512;
+  static __device__ __forceinline__ int ex(int row, int col) { return PAD ? row * 33 + col : r16_ex(row, col); }
   double2 u, w1, w2, w4, w8;  // W1536^(lane r); W512^(lane 2^j) (registers: !SMEMTW)
   const double2* usp;         // &us[32 r + lane], &tws[lane] (SMEMTW)
   const double2* twp;
@@ -121,10 +130,10 @@ struct X3W {
   __device__ __forceinline__ void forward_b_mulk(double2* v, double2* xr, int lane, const double2* kb,
                                                  uint64_t* kbar, unsigned kph) const {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
+    for (int k = 0; k < 16; ++k) xr[ex(k, lane)] = v[k];
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 16; ++h) v[h] = xr[r16_ex(k1, 2 * h + int(b))];
+    for (int h = 0; h < 16; ++h) v[h] = xr[ex(k1, 2 * h + int(b))];
     dft16<false>(v);
     mbar_wait(kbar, kph);  // this line's K^ row has landed
     // slot i holds X[3 k' + r] with k' = k1 + 16 (i + 8 b) (< 256) and slot i + 8 its k' + 256 twin,
@@ -134,10 +143,10 @@ struct X3W {
   // the exchange through xr and stage B
   __device__ __forceinline__ void forward_b(double2* v, double2* xr, int lane) const {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
+    for (int k = 0; k < 16; ++k) xr[ex(k, lane)] = v[k];
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 16; ++h) v[h] = xr[r16_ex(k1, 2 * h + int(b))];
+    for (int h = 0; h < 16; ++h) v[h] = xr[ex(k1, 2 * h + int(b))];
     dft16<false>(v);
     r16_r2_all<false>(v, b, std::make_integer_sequence<int, 8>{});
   }
@@ -147,10 +156,10 @@ struct X3W {
     r16_r2_all<true>(v, b, std::make_integer_sequence<int, 8>{});
     dft16<true>(v);
 #pragma unroll
-    for (int h = 0; h < 16; ++h) xr[r16_ex(k1, 2 * h + int(b))] = v[h];
+    for (int h = 0; h < 16; ++h) xr[ex(k1, 2 * h + int(b))] = v[h];
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = xr[r16_ex(k, lane)];
+    for (int k = 0; k < 16; ++k) v[k] = xr[ex(k, lane)];
     twiddle_u<true>(v);
     dft16<true>(v);
     slot_twiddle<true>(v);
@@ -230,7 +239,7 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
   extern __shared__ double2 sm[];
   const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + X3Smem::XB;
-  double2* const xr = xb + 512 * r;
+  double2* const xr = xb + X3Smem::XS * r;
   double2* const sb = sm + X3Smem::SB;
   double2* const kb = sm + X3Smem::KB;
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + X3Smem::END);
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
     mbar_init_fence();
   }
   __syncthreads();
-  const X3W<MODE == 2> W(sm + X3Smem::US, sm + X3Smem::TW, sm + X3Smem::C48, r, lane);
+  const X3W<MODE == 2, 3, FUSG_X3_PAD != 0> W(sm + X3Smem::US, sm + X3Smem::TW, sm + X3Smem::C48, r, lane);
   const int64_t nlines = int64_t(a.n_inner) * a.n_outer;
   const int64_t stride = gridDim.x;
   const bool mirror = a.n_outer == a.ko.Px;
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
     int ky, kx;
     coords(line, ky, kx);
     double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
-    for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + 512, xb + 1024, n, onv, a.scale, out);
+    for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + X3Smem::XS, xb + 2 * X3Smem::XS, n, onv, a.scale, out);
     // (the next line's staging barrier orders these reads before its exchange writes)
   }
 }
