@@ -21,10 +21,18 @@ namespace fusg {
 // X[k1 + 16 (i + 8 b)] and, in slot i + 8, X[k1 + 16 (i + 8 b) + 256].
 // Exchange buffer: row k1 (32 entries), column n2 ^ (k1 & 7): both access patterns are
 // bank-conflict-free (8 lanes of each 128-byte phase hit 8 distinct 16-byte bank groups).
+// Pass C (FUSG_R16_PAD, default on): the exchange buffer as 16 rows of 33 entries instead, also
+// conflict-free for both patterns and affine in the lane, so every offset folds into the
+// instruction's immediate (the XOR costs a LOP3 per access).
+#ifndef FUSG_R16_PAD
+#define FUSG_R16_PAD 1
+#endif
+constexpr int kR16XL = FUSG_R16_PAD ? 16 * 33 : 512;  // exchange buffer entries per warp (pass C)
+__device__ __forceinline__ int r16_exc(int row, int col) { return FUSG_R16_PAD ? row * 33 + col : r16_ex(row, col); }
 // per-warp buffers of the radix-8 kernel + the CTA's twiddle bases
 template <bool TAB>
 constexpr size_t r16_smem_bytes(int nw, bool kl2 = false) {
-  return size_t(nw) * (kl2 ? 512 + PPConvSmem<512, true>::STAGE : PPConvSmem<512, true>::PER_WARP) * sizeof(double2) +
+  return size_t(nw) * (kR16XL - 512 + (kl2 ? 512 + PPConvSmem<512, true>::STAGE : PPConvSmem<512, true>::PER_WARP)) * sizeof(double2) +
          nw * 2 * sizeof(uint64_t) + (TAB ? 16 : 4) * 32 * sizeof(double2);
 }
 
@@ -36,11 +44,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   constexpr int L = 512;
   constexpr int HZ = L / 2 + 1;
   using SM = PPConvSmem<L, true>;
-  constexpr int PW = KL2 ? L + SM::STAGE : SM::PER_WARP;  // double2 per warp
+  constexpr int PW = kR16XL - L + (KL2 ? L + SM::STAGE : SM::PER_WARP);  // double2 per warp
   extern __shared__ double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + size_t(w) * PW;
-  double2* const sb = xb + L;
+  double2* const sb = xb + kR16XL;
   double2* const kb = sb + SM::STAGE;  // (unused when KL2)
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + size_t(NW) * PW) + 2 * w;
   if (lane == 0) {
@@ -107,10 +115,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     dft16_half_in<false>(v);
     tw.apply<false>(v);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) xb[r16_ex(k, lane)] = v[k];
+    for (int k = 0; k < 16; ++k) xb[r16_exc(k, lane)] = v[k];
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 16; ++h) v[h] = xb[r16_ex(k1, 2 * h + int(b))];
+    for (int h = 0; h < 16; ++h) v[h] = xb[r16_exc(k1, 2 * h + int(b))];
     // forward stage B and the cross-lane radix 2
     dft16<false>(v);
     if constexpr (!KL2) {
@@ -139,10 +147,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     r16_r2_all<true>(v, b, I8);
     dft16<true>(v);
 #pragma unroll
-    for (int h = 0; h < 16; ++h) xb[r16_ex(k1, 2 * h + int(b))] = v[h];
+    for (int h = 0; h < 16; ++h) xb[r16_exc(k1, 2 * h + int(b))] = v[h];
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = xb[r16_ex(k, lane)];
+    for (int k = 0; k < 16; ++k) v[k] = xb[r16_exc(k, lane)];
     tw.apply<true>(v);
     dft16_half_out<true>(v);
     int ky, kx;

@@ -23,9 +23,18 @@ namespace fusg {
 // W32^j = W1024^(32 j) (the twiddle table's long-double values) for the slot twiddles
 __constant__ double2 c_w32[32];
 
+// FUSG_X2_PAD=1: exchange buffers as 16 rows of 33 entries (conflict-free for both patterns, every
+// offset an immediate) instead of the XOR-swizzled [16][32].  A gain at 1536, 768 and 512; here
+// (six 2-warp CTAs per SM at 168 registers) it spills 24 bytes and measures 7.44 vs 7.32 ms at
+// cfg3, so it is off.
+#ifndef FUSG_X2_PAD
+#define FUSG_X2_PAD 0
+#endif
+__device__ __forceinline__ int x2_ex(int row, int col) { return FUSG_X2_PAD ? row * 33 + col : r16_ex(row, col); }
 struct X2Smem {
-  static constexpr int XB = 0;          // [2][512] exchange buffers, then the t_r rows
-  static constexpr int KB = 1024;       // folded K^ row (513, padded to 514)
+  static constexpr int XS = FUSG_X2_PAD ? 16 * 33 : 512;  // exchange buffer of one warp
+  static constexpr int XB = 0;          // [2][XS] exchange buffers, then the t_r rows
+  static constexpr int KB = 2 * XS;     // folded K^ row (513, padded to 514)
   static constexpr int TW = KB + 514;   // [4][32] W512^(lane 2^j)
   static constexpr int US = TW + 128;   // [2][32] W1024^(lane r)
   static constexpr int SB = US + 64;    // staged input row (<= 512 positions)
@@ -60,10 +69,10 @@ struct X2W {
     dft16<false>(v);
     r16_twiddle_u<false>(v, u, w1, w2, w4, w8);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) xr[r16_ex(k, lane)] = v[k];
+    for (int k = 0; k < 16; ++k) xr[x2_ex(k, lane)] = v[k];
     __syncwarp();
 #pragma unroll
-    for (int h = 0; h < 16; ++h) v[h] = xr[r16_ex(k1, 2 * h + int(b))];
+    for (int h = 0; h < 16; ++h) v[h] = xr[x2_ex(k1, 2 * h + int(b))];
     dft16<false>(v);
     mbar_wait(kbar, kph);  // this line's K^ row has landed
     // j = 2 k' + r < 512; slot i + 8 holds index j + 512, which folds to 512 - j
@@ -74,10 +83,10 @@ struct X2W {
     r16_r2_all<true>(v, b, std::make_integer_sequence<int, 8>{});
     dft16<true>(v);
 #pragma unroll
-    for (int h = 0; h < 16; ++h) xr[r16_ex(k1, 2 * h + int(b))] = v[h];
+    for (int h = 0; h < 16; ++h) xr[x2_ex(k1, 2 * h + int(b))] = v[h];
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = xr[r16_ex(k, lane)];
+    for (int k = 0; k < 16; ++k) v[k] = xr[x2_ex(k, lane)];
     r16_twiddle_u<true>(v, u, w1, w2, w4, w8);
     dft16<true>(v);
     slot_twiddle<true>(v);
@@ -90,7 +99,7 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
   extern __shared__ double2 sm[];
   const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* const xb = sm + X2Smem::XB;
-  double2* const xr = xb + 512 * r;
+  double2* const xr = xb + X2Smem::XS * r;
   double2* const sb = sm + X2Smem::SB;
   double2* const kb = sm + X2Smem::KB;
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + X2Smem::END);
@@ -151,7 +160,7 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
     coords(line, ky, kx);
     double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
     for (int n = threadIdx.x; n < onv; n += NT) {
-      const double2 o = cadd(xb[n], xb[512 + n]);
+      const double2 o = cadd(xb[n], xb[X2Smem::XS + n]);
       out[n] = a.scale == 1.0 ? o : cscale(o, a.scale);
     }
     // (the next line's staging barrier orders these reads before its exchange writes)

@@ -22,9 +22,15 @@ namespace fusg {
 
 __constant__ double2 c_w48h[48];  // W48^j = W768^(16 j) (the twiddle table's long-double values)
 
+// exchange buffers as 16 rows of 17 entries (conflict-free for both patterns, every offset an
+// immediate) instead of the XOR-swizzled [16][16] (FUSG_H3_PAD=0)
+#ifndef FUSG_H3_PAD
+#define FUSG_H3_PAD 1
+#endif
 struct H3Smem {
-  static constexpr int XB = 0;            // [2 r + h][256] exchange buffers, then the t_r rows
-  static constexpr int KB = 6 * 256;      // folded K^ rows of the two lines (385 each, stride 386)
+  static constexpr int XH = FUSG_H3_PAD ? 16 * 17 : 256;  // exchange buffer of one half-warp
+  static constexpr int XB = 0;            // [2 r + h][XH] exchange buffers, then the t_r rows
+  static constexpr int KB = 6 * XH;       // folded K^ rows of the two lines (385 each, stride 386)
   static constexpr int TW = KB + 2 * 386; // [4][16] W256^(l 2^j)
   static constexpr int US = TW + 64;      // [3][16] W768^(l r)
   static constexpr int SB = US + 48;      // staged input rows of the two lines (<= 384 each)
@@ -32,7 +38,7 @@ struct H3Smem {
   static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
 };
 
-__device__ __forceinline__ int ex16(int row, int col) { return row * 16 + (col ^ (row & 7)); }
+__device__ __forceinline__ int ex16(int row, int col) { return FUSG_H3_PAD ? row * 17 + col : row * 16 + (col ^ (row & 7)); }
 
 __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
   constexpr int HZ = 385;
@@ -40,7 +46,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
   const int r = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = lane & 15, h = lane >> 4;
   double2* const xb = sm + H3Smem::XB;
-  double2* const xr = xb + 256 * (2 * r + h);  // this half-warp's exchange buffer / t_r row
+  double2* const xr = xb + H3Smem::XH * (2 * r + h);  // this half-warp's exchange buffer / t_r row
   double2* const kb = sm + H3Smem::KB + 386 * h;
   double2* const sb = sm + H3Smem::SB;
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + H3Smem::END);
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
       const int t = e >> 8, n = e & 255;
       if (t == 1 && !ok1) break;
       double2* out = outs[t];
-      const double2 t0 = xb[256 * t + n], t1 = xb[256 * (2 + t) + n], t2 = xb[256 * (4 + t) + n];
+      const double2 t0 = xb[H3Smem::XH * t + n], t1 = xb[H3Smem::XH * (2 + t) + n], t2 = xb[H3Smem::XH * (4 + t) + n];
       const double2 s = cadd(t1, t2);
       if (n < onv) {
         const double2 o = cadd(t0, s);
