@@ -538,11 +538,21 @@ __global__ void __launch_bounds__(384, 1) conv_r16x3q(WArgs a) {
 // lines (warp 3t + r: line t, residue r).  The T input rows (contiguous when the rows are
 // dense) arrive by 1-D bulk copy one tile ahead; the spectra meet in a swizzled [pos][T] tile
 // that aliases the twelve exchange buffers; the CTA stores 64-byte segments of T adjacent lines.
-template <int T, int R = 3>
+// FUSG_X3T_PAD bit 1: passes A / B (row -> column), bit 2: passes D / E.  Same-box A/B at cfg5:
+// D / E 8.55 / 4.23 -> 8.41 / 4.16 ms padded, A / B 4.25 / 8.45 -> 4.30 / 8.57 ms, so only D / E.
+#ifndef FUSG_X3T_PAD
+#define FUSG_X3T_PAD 2
+#endif
+template <int T, int R = 3, bool PAD = false>
 struct X3TSmem {
   static constexpr int L = 512 * R, H = 256 * R;
+  // PAD: the warps' exchange buffers as 16 rows of 33 entries (X3W<.., PAD>) instead of the
+  // XOR-swizzled [16][32]; the R T buffers then need a little more than the [L][T] tile they alias
+  // (R = 3, T = 4: 6336 entries = 99 KB, still 1024-byte aligned for the second TMA tile)
+  static constexpr int XS = PAD ? 16 * 33 : 512;
+  static constexpr int TILE = L * T > R * T * XS ? L * T : R * T * XS;
   static constexpr int AREA = 0;            // [L][T] tile = R T exchange buffers
-  static constexpr int STAGE = L * T;       // [T][L/2] staged input rows (r2c)
+  static constexpr int STAGE = TILE;        // [T][L/2] staged input rows (r2c)
   static constexpr int TW = STAGE + H * T;  // tables as in X3Smem
   static constexpr int US = TW + 128;
   static constexpr int C48 = US + 32 * R;
@@ -552,12 +562,17 @@ struct X3TSmem {
   static constexpr int STAGE2 = END;
   static constexpr size_t BYTES2 = size_t(STAGE2 + H * T) * sizeof(double2) + 2 * sizeof(uint64_t);
   // c2r: two [L][T] tiles (double-buffered), then the tables
-  static constexpr int C_TW = 2 * L * T;
+  static constexpr int C_TW = 2 * TILE;
   static constexpr int C_US = C_TW + 128;
   static constexpr int C_C48 = C_US + 32 * R;
   static constexpr int C_END = C_C48 + 16 * R;
   static constexpr size_t C_BYTES = size_t(C_END) * sizeof(double2) + 2 * sizeof(uint64_t);
 };
+
+template <int T, int R = 3>
+using X3TSmemA = X3TSmem<T, R, (FUSG_X3T_PAD & 1) != 0>;  // passes A / B
+template <int T, int R = 3>
+using X3TSmemD = X3TSmem<T, R, (FUSG_X3T_PAD & 2) != 0>;  // passes D / E
 
 // CTAs per SM the transposing kernels' register budget targets: 1 per SM at T = 4 for 1536
 // (12 warps, <= 168 registers); R = 2 (1024): 1 CTA (8 warps, ~200 registers), or with
@@ -573,15 +588,17 @@ struct X3TSmem {
 // TMA (T = 4): the finished tile leaves by tensor-map box stores issued by one thread, and the
 // next tile's stage-A arithmetic overlaps them; the area is rewritten (first exchange) only after
 // the stores have read it.
-template <int T, bool TMA, int R = 3>
+// FULL: every row holds L / 2 valid inputs (no predicates or zero fills in the gather)
+template <int T, bool TMA, int R = 3, bool FULL = false>
 __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a, const __grid_constant__ CUtensorMap tm) {
-  using X3TSmem = fusg::X3TSmem<T, R>;
+  constexpr bool PAD = (FUSG_X3T_PAD & 1) != 0;
+  using X3TSmem = fusg::X3TSmem<T, R, PAD>;
   constexpr int H = X3TSmem::H;  // L / 2
   extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = w % R, t = w / R;
   double2* const area = sm + X3TSmem::AREA;
-  double2* const xr = area + 512 * w;
+  double2* const xr = area + X3TSmem::XS * w;
   // TMA: two staging buffers, filled two tiles ahead (the rows of pass B lie a z-plane apart and
   // arrive late one tile ahead); else one
   constexpr int NST = TMA ? 2 : 1;
@@ -593,8 +610,8 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
     mbar_init_fence();
   }
   __syncthreads();
-  const X3W<X3T_SMEMTW, R> W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
-  const int nv = a.in_nvalid;
+  const X3W<X3T_SMEMTW, R, PAD> W(sm + X3TSmem::US, sm + X3TSmem::TW, sm + X3TSmem::C48, r, lane);
+  const int nv = FULL ? H : a.in_nvalid;
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix, int sb) {  // thread 0
@@ -679,10 +696,12 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
 // writes the T cropped rows with coalesced stores.
 // TMA (T = 4): each column tile arrives by tensor-map box loads (one thread, one mbarrier per
 // buffer) instead of per-thread cp.async; positions and lines beyond the field are zero-filled.
-template <int T, bool TMA, int R = 3>
+// FULL: full spectra in (L positions), L / 2 valid outputs per row
+template <int T, bool TMA, int R = 3, bool FULL = false>
 __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a, const __grid_constant__ CUtensorMap tm) {
-  using X3TSmem = fusg::X3TSmem<T, R>;
-  constexpr int L = X3TSmem::L, H = X3TSmem::H;
+  constexpr bool PAD = (FUSG_X3T_PAD & 2) != 0;
+  using X3TSmem = fusg::X3TSmem<T, R, PAD>;
+  constexpr int H = X3TSmem::H;
   constexpr int NT = 32 * R * T;
   extern __shared__ __align__(1024) double2 sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -695,7 +714,7 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a
     mbar_init_fence();
   }
   __syncthreads();
-  const X3W<X3T_SMEMTW, R> W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
+  const X3W<X3T_SMEMTW, R, PAD> W(sm + X3TSmem::C_US, sm + X3TSmem::C_TW, sm + X3TSmem::C_C48, r, lane);
   const int ntiles_i = (a.n_inner + T - 1) / T;
   const int64_t ntiles = int64_t(ntiles_i) * a.n_outer;
   auto prefetch = [&](int64_t tix, double2* tile) {
@@ -728,7 +747,7 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a
   unsigned buf = 0, phs = 0;  // phs: parity bit of each buffer's mbarrier (TMA)
   prefetch(tix, sm);
   for (; tix < ntiles; tix += gridDim.x, buf ^= 1) {
-    double2* const tile = sm + buf * (L * T);
+    double2* const tile = sm + buf * X3TSmem::TILE;
     const int i0 = int(unsigned(tix) % unsigned(ntiles_i)) * T;
     const int k = int(unsigned(tix) / unsigned(ntiles_i));
     const int lines_ok = min(T, a.n_inner - i0);
@@ -744,12 +763,12 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int p = R * (W.k1 + 16 * (i + 8 * int(W.b))) + r;
-      v[i] = p < a.in_nvalid ? tile[mtile_at<T>(p, t)] : make_double2(0.0, 0.0);
-      v[i + 8] = p + H < a.in_nvalid ? tile[mtile_at<T>(p + H, t)] : make_double2(0.0, 0.0);
+      v[i] = (FULL || p < a.in_nvalid) ? tile[mtile_at<T>(p, t)] : make_double2(0.0, 0.0);
+      v[i + 8] = (FULL || p + H < a.in_nvalid) ? tile[mtile_at<T>(p + H, t)] : make_double2(0.0, 0.0);
     }
     __syncthreads();  // tile read by every warp: it becomes the exchange area
-    prefetch(tix + gridDim.x, sm + (buf ^ 1) * (L * T));
-    double2* const xr = tile + 512 * w;
+    prefetch(tix + gridDim.x, sm + (buf ^ 1) * X3TSmem::TILE);
+    double2* const xr = tile + X3TSmem::XS * w;
     W.inverse(v, xr, lane);
     __syncwarp();
 #pragma unroll
@@ -762,12 +781,13 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a
         const int q = a.pm.owner(line);
         orow = a.pm.base[q] + (a.pm.off[q] + int64_t(line) * a.out_si + int64_t(k) * a.pm.sk[q]);
       }
-      const double2* x = tile + 512 * R * t;
+      constexpr int XS = X3TSmem::XS;
+      const double2* x = tile + XS * R * t;
       for (int n = threadIdx.x - 32 * R * t; n < 512; n += 32 * R) {
         if constexpr (R == 3) {
-          x3_recombine(x, x + 512, x + 1024, n, a.out_nvalid, a.scale, orow);
-        } else if (n < a.out_nvalid) {  // x[n] = t0 + t1, n < 512
-          const double2 o = cadd(x[n], x[512 + n]);
+          x3_recombine(x, x + XS, x + 2 * XS, n, FULL ? H : a.out_nvalid, a.scale, orow);
+        } else if (FULL || n < a.out_nvalid) {  // x[n] = t0 + t1, n < 512
+          const double2 o = cadd(x[n], x[XS + n]);
           orow[n] = a.scale == 1.0 ? o : cscale(o, a.scale);
         }
       }
@@ -946,25 +966,31 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
                         : (a.in_si == 1 &&
                            make_tile_map(&tm, a.in, a.n_inner, a.in_nvalid, a.n_outer, a.in_sp, a.in_sk, T)));
   using Fn = void (*)(WArgs, CUtensorMap);
-  const Fn fn = T == 4 ? (r2c ? (tma ? r16x3_row_to_col<4, true> : r16x3_row_to_col<4, false>)
-                              : (tma ? r16x3_col_to_row<4, true> : r16x3_col_to_row<4, false>))
+  // full rows (768 valid positions on the pruned side, the whole spectrum on the other: cfg5)
+  const bool full = tma && (r2c ? a.in_nvalid == 768 : (a.in_nvalid == 1536 && a.out_nvalid == 768));
+  const Fn fn = T == 4 ? (r2c ? (full ? r16x3_row_to_col<4, true, 3, true> : tma ? r16x3_row_to_col<4, true> : r16x3_row_to_col<4, false>)
+                              : (full ? r16x3_col_to_row<4, true, 3, true> : tma ? r16x3_col_to_row<4, true> : r16x3_col_to_row<4, false>))
                        : (r2c ? r16x3_row_to_col<2, false> : r16x3_col_to_row<2, false>);
-  const size_t smem = T == 4 ? (r2c ? (tma ? X3TSmem<4>::BYTES2 : X3TSmem<4>::BYTES) : X3TSmem<4>::C_BYTES)
-                             : (r2c ? X3TSmem<2>::BYTES : X3TSmem<2>::C_BYTES);
+  const size_t smem = T == 4 ? (r2c ? (tma ? X3TSmemA<4>::BYTES2 : X3TSmemA<4>::BYTES) : X3TSmemD<4>::C_BYTES)
+                             : (r2c ? X3TSmemA<2>::BYTES : X3TSmemD<2>::C_BYTES);
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [&] {
         return cudaFuncSetAttribute(r16x3_row_to_col<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<4>::BYTES)) == cudaSuccess &&
+                                    int(X3TSmemA<4>::BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_row_to_col<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<4>::BYTES2)) == cudaSuccess &&
+                                    int(X3TSmemA<4>::BYTES2)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_row_to_col<4, true, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmemA<4>::BYTES2)) == cudaSuccess &&
+               cudaFuncSetAttribute(r16x3_col_to_row<4, true, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(X3TSmemD<4>::C_BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
+                                    int(X3TSmemD<4>::C_BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<4>::C_BYTES)) == cudaSuccess &&
+                                    int(X3TSmemD<4>::C_BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_row_to_col<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<2>::BYTES)) == cudaSuccess &&
+                                    int(X3TSmemA<2>::BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(X3TSmem<2>::C_BYTES)) == cudaSuccess;
+                                    int(X3TSmemD<2>::C_BYTES)) == cudaSuccess;
       })) {
     set_error(FUSG_CUDA, "transposing pass (1536 = 3 x 512): cannot configure shared memory");
     return -1;
@@ -1003,7 +1029,8 @@ int launch_transpose_r16x2(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   constexpr int T = 4;
   const int64_t tiles = int64_t((a.n_inner + T - 1) / T) * a.n_outer;
   if (tiles >= (int64_t(1) << 31)) return 0;
-  using SM2 = X3TSmem<T, 2>;
+  using SM2A = X3TSmemA<T, 2>;
+  using SM2D = X3TSmemD<T, 2>;
   static std::atomic<uint64_t> attr_mask{0};
   if (!once_per_device(attr_mask, [] {
         double2 h[32];
@@ -1013,13 +1040,13 @@ int launch_transpose_r16x2(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
         }
         return cudaMemcpyToSymbol(c_w32t, h, sizeof(h)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_row_to_col<T, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(SM2::BYTES)) == cudaSuccess &&
+                                    int(SM2A::BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_row_to_col<T, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(SM2::BYTES2)) == cudaSuccess &&
+                                    int(SM2A::BYTES2)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<T, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(SM2::C_BYTES)) == cudaSuccess &&
+                                    int(SM2D::C_BYTES)) == cudaSuccess &&
                cudaFuncSetAttribute(r16x3_col_to_row<T, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(SM2::C_BYTES)) == cudaSuccess;
+                                    int(SM2D::C_BYTES)) == cudaSuccess;
       })) {
     set_error(FUSG_CUDA, "transposing pass (1024 = 2 x 512): cannot configure the kernels");
     return -1;
@@ -1037,7 +1064,7 @@ int launch_transpose_r16x2(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
   using Fn = void (*)(WArgs, CUtensorMap);
   const Fn fn = r2c ? (tma ? r16x3_row_to_col<T, true, 2> : r16x3_row_to_col<T, false, 2>)
                     : (tma ? r16x3_col_to_row<T, true, 2> : r16x3_col_to_row<T, false, 2>);
-  const size_t smem = r2c ? (tma ? SM2::BYTES2 : SM2::BYTES) : SM2::C_BYTES;
+  const size_t smem = r2c ? (tma ? SM2A::BYTES2 : SM2A::BYTES) : SM2D::C_BYTES;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 64 * T, smem) != cudaSuccess || per_sm < 1) {
     cudaGetLastError();
