@@ -967,7 +967,10 @@ int launch_transpose_r16x3(fusg_ctx* ctx, bool r2c, const WArgs& a, cudaStream_t
                            make_tile_map(&tm, a.in, a.n_inner, a.in_nvalid, a.n_outer, a.in_sp, a.in_sk, T)));
   using Fn = void (*)(WArgs, CUtensorMap);
   // full rows (768 valid positions on the pruned side, the whole spectrum on the other: cfg5)
-  const bool full = tma && (r2c ? a.in_nvalid == 768 : (a.in_nvalid == 1536 && a.out_nvalid == 768));
+#ifndef FUSG_X3T_FULL
+#define FUSG_X3T_FULL 1
+#endif
+  const bool full = FUSG_X3T_FULL && tma && (r2c ? a.in_nvalid == 768 : (a.in_nvalid == 1536 && a.out_nvalid == 768));
   const Fn fn = T == 4 ? (r2c ? (full ? r16x3_row_to_col<4, true, 3, true> : tma ? r16x3_row_to_col<4, true> : r16x3_row_to_col<4, false>)
                               : (full ? r16x3_col_to_row<4, true, 3, true> : tma ? r16x3_col_to_row<4, true> : r16x3_col_to_row<4, false>))
                        : (r2c ? r16x3_row_to_col<2, false> : r16x3_col_to_row<2, false>);
