@@ -24,6 +24,9 @@
 
 namespace fusg {
 
+#ifndef FUSG_X3_OROW
+#define FUSG_X3_OROW 1  // pass C: the staging thread leaves each line's output-row offset in shared memory
+#endif
 #ifndef FUSG_X3_PAD
 #define FUSG_X3_PAD 1  // pass C exchange buffers as 16 rows of 33 entries (0: XOR-swizzled [16][32])
 #endif
@@ -39,7 +42,9 @@ struct X3Smem {
   static constexpr int C48 = US + 96;      // [48] W48^j
   static constexpr int SB = MODE == 2 ? KB : C48 + 48;  // staged input row (<= 768 positions)
   static constexpr int END = C48 + 48 + (MODE == 1 ? 768 : 0);
-  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
+  // + 2 mbarriers + 2 output-row offsets (MODE 1: thread 0 leaves the row offset of the line it
+  // stages for the other threads, which then skip the line -> (ky, kx) divisions)
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 4 * sizeof(uint64_t);
 };
 
 // W48^j = W1536^(32 j) in the constant bank (the same long-double values as the twiddle table):
@@ -257,11 +262,13 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
   auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
     conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
-  auto prefetch_in = [&](int64_t line) {
+  int64_t* const orow = reinterpret_cast<int64_t*>(bars + 2);  // [2] output-row offsets by line parity
+  auto prefetch_in = [&](int64_t line, unsigned slot) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
       const double2* src = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
+      if constexpr (MODE == 1 && FUSG_X3_OROW) orow[slot] = ky * a.out_si + int64_t(kx) * a.out_sk;
       if constexpr (STAGED) {
         bulk_stage(sb, src, unsigned(a.in_nvalid) * sizeof(double2), bars);
       } else {
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
   const int nv = FULL ? 768 : a.in_nvalid, onv = FULL ? 768 : a.out_nvalid;
   int64_t line = blockIdx.x;
   if (threadIdx.x == 0) {
-    prefetch_in(line);
+    prefetch_in(line, 0);
     if constexpr (MODE != 2) prefetch_k(line);
   }
   unsigned ph = 0;  // both staging barriers complete once per line
@@ -297,14 +304,14 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
     __syncthreads();  // the staged row is read by all three warps: refill it
     if (threadIdx.x == 0) {
       if constexpr (MODE == 2) prefetch_k(line);  // this line's K^ row into the same buffer
-      else prefetch_in(line + stride);
+      else prefetch_in(line + stride, ph ^ 1u);
     }
     // X[3k' + r] times the folded K^ row, fused into the last forward stage
     W.forward_a(v);
     W.forward_b_mulk(v, xr, lane, kb, bars + 1, ph);
     __syncthreads();  // K^ row read
     if (threadIdx.x == 0) {
-      if constexpr (MODE == 2) prefetch_in(line + stride);
+      if constexpr (MODE == 2) prefetch_in(line + stride, ph ^ 1u);
       else prefetch_k(line + stride);
     }
     W.inverse(v, xr, lane);
@@ -312,9 +319,14 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
     __syncthreads();
-    int ky, kx;
-    coords(line, ky, kx);
-    double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    double2* out;
+    if constexpr (MODE == 1 && FUSG_X3_OROW) {
+      out = a.out + orow[ph];  // left by thread 0 when it staged this line (barriers in between)
+    } else {
+      int ky, kx;
+      coords(line, ky, kx);
+      out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    }
     for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + X3Smem::XS, xb + 2 * X3Smem::XS, n, onv, a.scale, out);
     // (the next line's staging barrier orders these reads before its exchange writes)
   }
