@@ -192,6 +192,9 @@ struct X3W {
 using X3Warp = X3W<false>;
 
 // cropped row from the three t_r rows: x[n'] = t0 + t1 + t2, x[n' + 512] = t0 + W3^-1 t1 + W3^-2 t2
+// SCALED = false: the caller knows sc == 1 (pass C always; the per-element test-and-select costs
+// issue slots)
+template <bool SCALED = true>
 __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* t1r, const double2* t2r, int n,
                                              int onv, double sc, double2* out) {
   constexpr double kS3 = 0.8660254037844386467637;
@@ -199,12 +202,12 @@ __device__ __forceinline__ void x3_recombine(const double2* t0r, const double2* 
   const double2 s = cadd(t1, t2);
   if (n < onv) {
     const double2 o = cadd(t0, s);
-    out[n] = sc == 1.0 ? o : cscale(o, sc);
+    out[n] = (!SCALED || sc == 1.0) ? o : cscale(o, sc);
   }
   if (n + 512 < onv) {
     const double2 d = csub(t1, t2);
     const double2 o = make_double2(t0.x - 0.5 * s.x - kS3 * d.y, t0.y - 0.5 * s.y + kS3 * d.x);
-    out[n + 512] = sc == 1.0 ? o : cscale(o, sc);
+    out[n + 512] = (!SCALED || sc == 1.0) ? o : cscale(o, sc);
   }
 }
 
@@ -327,7 +330,11 @@ __global__ void __launch_bounds__(96, MODE == 1 ? FUSG_X3_MINB : 5) conv_r16x3(W
       coords(line, ky, kx);
       out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
     }
-    for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + X3Smem::XS, xb + 2 * X3Smem::XS, n, onv, a.scale, out);
+    if (a.scale == 1.0) {  // (always, from the apply: the scale rides on pass E)
+      for (int n = threadIdx.x; n < 512; n += 96) x3_recombine<false>(xb, xb + X3Smem::XS, xb + 2 * X3Smem::XS, n, onv, 1.0, out);
+    } else {
+      for (int n = threadIdx.x; n < 512; n += 96) x3_recombine(xb, xb + X3Smem::XS, xb + 2 * X3Smem::XS, n, onv, a.scale, out);
+    }
     // (the next line's staging barrier orders these reads before its exchange writes)
   }
 }
@@ -795,6 +802,10 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_col_to_row(WArgs a
       }
       constexpr int XS = X3TSmem::XS;
       const double2* x = tile + XS * R * t;
+      if (R == 3 && a.scale == 1.0) {
+        for (int n = threadIdx.x - 32 * R * t; n < 512; n += 32 * R)
+          x3_recombine<false>(x, x + XS, x + 2 * XS, n, FULL ? H : a.out_nvalid, 1.0, orow);
+      } else
       for (int n = threadIdx.x - 32 * R * t; n < 512; n += 32 * R) {
         if constexpr (R == 3) {
           x3_recombine(x, x + XS, x + 2 * XS, n, FULL ? H : a.out_nvalid, a.scale, orow);
