@@ -196,9 +196,9 @@ int launch_conv_r16x2(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     cudaGetLastError();
     return 0;
   }
-  static const int waves = [] {  // CTAs per resident slot (1 = fully persistent)
+  static const int waves = [] {  // CTAs per resident slot (1 = fully persistent); cfg3: 4 / 16 / 64 -> 7.31 / 7.21 / 7.31 ms
     const char* e = getenv("FUSG_X2_WAVES");
-    return e ? std::max(1, atoi(e)) : 4;
+    return e ? std::max(1, atoi(e)) : 16;
   }();
   const int64_t grid = std::min<int64_t>(nl, int64_t(per_sm) * ctx->num_sms * waves);
   WArgs b = a;

@@ -928,9 +928,11 @@ int launch_conv_r16x3(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
     cudaGetLastError();
     return 0;
   }
-  static const int waves = [] {  // CTAs per resident slot (1 = fully persistent)
+  // CTAs per resident slot (1 = fully persistent).  cfg5, one box: 1 / 2 / 4 / 8 / 16 / 32 / 64 / 128
+  // -> 27.4 / 27.0 / 26.4 / 26.2 / 25.9 / 25.8 / 25.7 / 26.0 ms
+  static const int waves = [] {
     const char* e = getenv("FUSG_X3_WAVES");
-    return e ? std::max(1, atoi(e)) : 4;
+    return e ? std::max(1, atoi(e)) : 64;
   }();
   const int64_t grid = std::min<int64_t>(nl, int64_t(per_sm) * ctx->num_sms * waves);
   // FUSG_X3_QUAD (default 1): the (up to) four lines sharing a folded K^ row run consecutively,
