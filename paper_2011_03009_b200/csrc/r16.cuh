@@ -85,19 +85,22 @@ __device__ __forceinline__ void r16_twiddle_u(double2* v, double2 u, double2 w1,
   v[15] = m(v[15], cmul(p7, w8));
 }
 
+#ifndef FUSG_R2_TAN_MULK
+#define FUSG_R2_TAN_MULK 1  // the tan form inside pass C's fused radix 2 + K^ multiply only
+#endif
 #ifndef FUSG_R2_TAN
 #define FUSG_R2_TAN 0  // 1: z0 +- w z1 in tan form (6 FP64 instructions per step instead of 8, but the
                        // per-lane-half (wr, t) selects cost issue slots: cfg5 passes A / B 4.19 / 8.36 -> 4.33 / 8.63 ms,
                        // pass C unchanged)
 #endif
 // radix 2 over n2lo with twiddle W32^(q1 n2lo), q1 = i + 8 b (forward), and its adjoint
-template <int I>
+template <int I, bool TAN = (FUSG_R2_TAN != 0)>
 __device__ __forceinline__ void r16_fwd_r2(double2* v, bool b) {
   const double2 send = sel_d2(b, v[I], v[I + 8]);  // lane b keeps q1 in [8b, 8b + 8)
   const double2 recv = shfl_xor_d2(send, 16);
   const double2 z0 = sel_d2(b, recv, v[I]);
   const double2 z1 = sel_d2(b, v[I + 8], recv);
-  if constexpr (I == 0 || !FUSG_R2_TAN) {
+  if constexpr (I == 0 || !TAN) {
     double2 t = w32<false, I>(z1);
     t = sel_d2(b, rot90<false>(t), t);  // W32^8 = -i
     v[I] = cadd(z0, t);
@@ -139,7 +142,7 @@ __device__ __forceinline__ void r16_fwd_r2_mulk(double2* v, bool b, const double
     na = kb[p];
     nz = kb[MIR - p];
   }
-  r16_fwd_r2<I>(v, b);
+  r16_fwd_r2<I, (FUSG_R2_TAN_MULK != 0)>(v, b);
   v[I] = cmul(v[I], ka);
   v[I + 8] = cmul(v[I + 8], kz);
   if constexpr (I + 1 < 8) {
