@@ -16,6 +16,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+// the tan-form radix 2 inside the fused K^ multiply is a gain at 1536 only: here 7.35 vs 7.68 ms at cfg3 (spills)
+#ifndef FUSG_R2_TAN_MULK
+#define FUSG_R2_TAN_MULK 0
+#endif
 #include "r16.cuh"
 
 namespace fusg {
