@@ -621,7 +621,9 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
   // TMA: two staging buffers, filled two tiles ahead (the rows of pass B lie a z-plane apart and
   // arrive late one tile ahead); else one
   constexpr int NST = TMA ? 2 : 1;
-  double2* const stages[2] = {sm + X3TSmem::STAGE, sm + X3TSmem::STAGE2};
+  // (addressed arithmetically from the shared base: a runtime-indexed pointer array turns the
+  // gather's shared loads into generic LD)
+  auto stage_of = [&](int sb) { return sm + (sb ? X3TSmem::STAGE2 : X3TSmem::STAGE); };
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + (TMA ? X3TSmem::STAGE2 + H * T : X3TSmem::END));
   x3_tables<R>(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
   if (threadIdx.x == 0) {
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
       const unsigned row = unsigned(nv) * sizeof(double2);
       refill_fence();
       mbar_expect_tx(bars + sb, row * lines_ok);
-      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stages[sb] + tt * H, src + tt * a.in_si, row, bars + sb);
+      for (int tt = 0; tt < lines_ok; ++tt) bulk_g2s(stage_of(sb) + tt * H, src + tt * a.in_si, row, bars + sb);
     }
   };
   int64_t tix = blockIdx.x;
@@ -657,7 +659,7 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
     mbar_wait(bars + sb, (phs >> sb) & 1u);
     phs ^= 1u << sb;
     double2 v[16];
-    W.gather(v, stages[sb] + (t < lines_ok ? t : 0) * H, nv, lane);
+    W.gather(v, stage_of(sb) + (t < lines_ok ? t : 0) * H, nv, lane);
     if constexpr (TMA) {
       W.forward_a(v);
       if (threadIdx.x == 0) bulk_wait_read0();  // the previous tile's box stores have read the area
