@@ -623,7 +623,15 @@ __global__ void __launch_bounds__(32 * R * T, X3T_MINB) r16x3_row_to_col(WArgs a
   constexpr int NST = TMA ? 2 : 1;
   // (addressed arithmetically from the shared base: a runtime-indexed pointer array turns the
   // gather's shared loads into generic LD)
+#ifndef FUSG_X3T_STAGEPTR
+#define FUSG_X3T_STAGEPTR 0
+#endif
+#if FUSG_X3T_STAGEPTR
+  double2* const stages_[2] = {sm + X3TSmem::STAGE, sm + X3TSmem::STAGE2};
+  auto stage_of = [&](int sb) { return stages_[sb]; };
+#else
   auto stage_of = [&](int sb) { return sm + (sb ? X3TSmem::STAGE2 : X3TSmem::STAGE); };
+#endif
   uint64_t* const bars = reinterpret_cast<uint64_t*>(sm + (TMA ? X3TSmem::STAGE2 + H * T : X3TSmem::END));
   x3_tables<R>(a.tw, sm + X3TSmem::TW, sm + X3TSmem::US, sm + X3TSmem::C48);
   if (threadIdx.x == 0) {
