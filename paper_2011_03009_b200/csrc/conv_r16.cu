@@ -68,17 +68,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   auto coords = [&](int64_t line, int& ky, int& kx) {  // line < 2^31 (host-checked)
     conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
-  auto prefetch_in = [&](int64_t line) {
-    if (line < nlines && lane == 0) {
-      int ky, kx;
-      coords(line, ky, kx);
+  // (ky, kx) of a line costs ~45 instructions (divisions); each line's pair is computed once, one
+  // line ahead, and serves both refills and the output row
+  auto prefetch_in = [&](bool ok, int ky, int kx) {
+    if (ok && lane == 0)
       bulk_stage(sb, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(a.in_nvalid) * sizeof(double2), bars);
-    }
   };
-  auto prefetch_k = [&](int64_t line) {
-    if (line < nlines && lane == 0) {
-      int ky, kx;
-      coords(line, ky, kx);
+  auto prefetch_k = [&](bool ok, int ky, int kx) {
+    if (ok && lane == 0) {
       if constexpr (KL2) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.ko.line(ky, kx)), "r"(unsigned(HZ * sizeof(double2)))
                      : "memory");
@@ -102,9 +99,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   const int k1 = lane & 15;
   const auto I8 = std::make_integer_sequence<int, 8>{};
   int64_t line = int64_t(blockIdx.x) * NW + w;
-  prefetch_in(line);
-  prefetch_k(line);
+  int ky = 0, kx = 0;
+  if (line < nlines) coords(line, ky, kx);
+  prefetch_in(line < nlines, ky, kx);
+  prefetch_k(line < nlines, ky, kx);
   for (; line < nlines; line += stride) {
+    const bool more = line + stride < nlines;
+    int kyn = 0, kxn = 0;
+    if (more) coords(line + stride, kyn, kxn);
     mbar_wait(bars, ph_in);
     ph_in ^= 1;
     double2 v[16];
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
       v[e] = pos < a.in_nvalid ? sb[pos] : make_double2(0.0, 0.0);
     }
     __syncwarp();  // S consumed: refill it with the next line while this one is transformed
-    prefetch_in(line + stride);
+    prefetch_in(more, kyn, kxn);
     // forward stage A (upper half zero) and its twiddle
     dft16_half_in<false>(v);
     tw.apply<false>(v);
@@ -131,15 +133,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
       ph_k ^= 1;
       r16_fwd_r2_mulk_all<16, 256>(v, b, kb, k1 + 128 * int(b), I8);
       __syncwarp();  // K^ row consumed
-      prefetch_k(line + stride);
+      prefetch_k(more, kyn, kxn);
     } else {
       r16_r2_all<false>(v, b, I8);
     }
     if constexpr (KL2) {
-      int ky, kx;
-      coords(line, ky, kx);
       const double2* kl = a.ko.line(ky, kx);
-      prefetch_k(line + stride);
+      prefetch_k(more, kyn, kxn);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int p = k1 + 16 * (i + 8 * int(b));  // < 256; its mirror p + 256 folds to 256 - p
@@ -157,9 +157,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
     for (int k = 0; k < 16; ++k) v[k] = xb[r16_exc(k, lane)];
     tw.apply<true>(v);
     dft16_half_out<true>(v);
-    int ky, kx;
-    coords(line, ky, kx);
     double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    ky = kyn;
+    kx = kxn;
     if (a.scale == 1.0) {  // (always, inside the apply: the scale rides on pass E)
 #pragma unroll
       for (int e = 0; e < 8; ++e) {

@@ -43,7 +43,9 @@ struct X2Smem {
   static constexpr int US = TW + 128;   // [2][32] W1024^(lane r)
   static constexpr int SB = US + 64;    // staged input row (<= 512 positions)
   static constexpr int END = SB + 512;
-  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
+  // + 2 mbarriers + 2 output-row offsets (left by the staging thread: the other threads skip the
+  // line -> (ky, kx) divisions)
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 4 * sizeof(uint64_t);
 };
 
 struct X2W {
@@ -121,10 +123,11 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
   const int64_t stride = gridDim.x;
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) { conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx); };
-  auto prefetch_in = [&](int64_t line) {
+  auto prefetch_in = [&](int64_t line, unsigned slot) {
     if (line < nlines) {
       int ky, kx;
       coords(line, ky, kx);
+      reinterpret_cast<int64_t*>(bars + 2)[slot] = ky * a.out_si + int64_t(kx) * a.out_sk;
       bulk_stage(sb, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, unsigned(a.in_nvalid) * sizeof(double2), bars);
     }
   };
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
   const int nv = a.in_nvalid, onv = a.out_nvalid;
   int64_t line = blockIdx.x;
   if (threadIdx.x == 0) {
-    prefetch_in(line);
+    prefetch_in(line, 0);
     prefetch_k(line);
   }
   unsigned ph = 0;  // both staging barriers complete once per line
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
       v[n1] = m < nv ? sb[m] : make_double2(0.0, 0.0);
     }
     __syncthreads();  // the staged row is read by both warps: refill it
-    if (threadIdx.x == 0) prefetch_in(line + stride);
+    if (threadIdx.x == 0) prefetch_in(line + stride, ph ^ 1u);
     W.forward_mulk(v, xr, lane, kb, bars + 1, ph);
     __syncthreads();  // K^ row read
     if (threadIdx.x == 0) prefetch_k(line + stride);
@@ -160,9 +163,7 @@ __global__ void __launch_bounds__(64, 6) conv_r16x2(WArgs a) {
 #pragma unroll
     for (int n1 = 0; n1 < 16; ++n1) xr[32 * n1 + lane] = v[n1];
     __syncthreads();
-    int ky, kx;
-    coords(line, ky, kx);
-    double2* out = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
+    double2* out = a.out + reinterpret_cast<const int64_t*>(bars + 2)[ph];  // (barriers in between)
     for (int n = threadIdx.x; n < onv; n += NT) {
       const double2 o = cadd(xb[n], xb[X2Smem::XS + n]);
       out[n] = a.scale == 1.0 ? o : cscale(o, a.scale);

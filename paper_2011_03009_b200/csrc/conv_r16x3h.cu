@@ -35,7 +35,9 @@ struct H3Smem {
   static constexpr int US = TW + 64;      // [3][16] W768^(l r)
   static constexpr int SB = US + 48;      // staged input rows of the two lines (<= 384 each)
   static constexpr int END = SB + 2 * 384;
-  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 2 * sizeof(uint64_t);  // + 2 mbarriers
+  // + 2 mbarriers + [2][2] output-row offsets (the staging thread leaves them for the pair it stages:
+  // the other threads skip the line -> (ky, kx) divisions)
+  static constexpr size_t BYTES = size_t(END) * sizeof(double2) + 6 * sizeof(uint64_t);
 };
 
 __device__ __forceinline__ int ex16(int row, int col) { return FUSG_H3_PAD ? row * 17 + col : row * 16 + (col ^ (row & 7)); }
@@ -69,7 +71,8 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
   const bool mirror = a.n_outer == a.ko.Px;
   auto coords = [&](int64_t line, int& ky, int& kx) { conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx); };
   const int nv = a.in_nvalid, onv = a.out_nvalid;
-  auto prefetch_in = [&](int64_t pr) {  // thread 0: both rows of pair pr, one barrier
+  auto prefetch_in = [&](int64_t pr, unsigned slot) {  // thread 0: both rows of pair pr, one barrier
+    int64_t* const orow = reinterpret_cast<int64_t*>(bars + 2);  // [slot][t] output-row offsets
     if (pr < npairs) {
       const int nl = (2 * pr + 1 < nlines) ? 2 : 1;
       const unsigned row = unsigned(nv) * sizeof(double2);
@@ -78,6 +81,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
       for (int t = 0; t < nl; ++t) {
         int ky, kx;
         coords(2 * pr + t, ky, kx);
+        orow[2 * slot + t] = ky * a.out_si + int64_t(kx) * a.out_sk;
         bulk_g2s(sb + 384 * t, a.in + ky * a.in_si + int64_t(kx) * a.in_sk, row, bars);
       }
     }
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
   };
   int64_t pr = blockIdx.x;
   if (threadIdx.x == 0) {
-    prefetch_in(pr);
+    prefetch_in(pr, 0);
     prefetch_k(pr);
   }
   unsigned ph = 0;
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
       }
     }
     __syncthreads();  // both staged rows read by all three warps: refill
-    if (threadIdx.x == 0) prefetch_in(pr + stride);
+    if (threadIdx.x == 0) prefetch_in(pr + stride, ph ^ 1u);
     // forward: slot twiddle, stage A, lane twiddle, exchange, stage B
     if (r == 1) {
 #pragma unroll
@@ -169,11 +173,8 @@ __global__ void __launch_bounds__(96, 4) conv_r16x3h(WArgs a) {
     constexpr double kS3 = 0.8660254037844386467637;
     double2* outs[2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      int ky = 0, kx = 0;
-      if (t == 0 || ok1) coords(2 * pr + t, ky, kx);
-      outs[t] = a.out + ky * a.out_si + int64_t(kx) * a.out_sk;
-    }
+    for (int t = 0; t < 2; ++t)  // offsets left by thread 0 when it staged this pair (barriers in between)
+      outs[t] = a.out + ((t == 0 || ok1) ? reinterpret_cast<const int64_t*>(bars + 2)[2 * ph + t] : 0);
     for (int e = threadIdx.x; e < 512; e += 96) {
       const int t = e >> 8, n = e & 255;
       if (t == 1 && !ok1) break;
