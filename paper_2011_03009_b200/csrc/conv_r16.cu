@@ -43,7 +43,8 @@ constexpr size_t r16_smem_bytes(int nw, bool kl2 = false) {
 // KL2: the K^ row is not staged in shared memory; it is prefetched into L2 one line ahead
 // (cp.async.bulk.prefetch) and read at the multiply with read-only loads.  12 KB per warp
 // instead of 16 lets 16 warps share an SM (MINB 4, 128 registers).
-template <int NW, int MINB, bool TAB, bool KL2 = false>
+// FULL: every row holds 256 valid inputs and outputs (cfg2): no predicates or zero fills
+template <int NW, int MINB, bool TAB, bool KL2 = false, bool FULL = false>
 __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
   constexpr int L = 512;
   constexpr int HZ = L / 2 + 1;
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int pos = lane + 32 * e;
-      v[e] = pos < a.in_nvalid ? sb[pos] : make_double2(0.0, 0.0);
+      v[e] = (FULL || pos < a.in_nvalid) ? sb[pos] : make_double2(0.0, 0.0);
     }
     __syncwarp();  // S consumed: refill it with the next line while this one is transformed
     prefetch_in(more, kyn, kxn);
@@ -164,13 +165,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) warp_row_conv_r16(WArgs a) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int pos = lane + 32 * e;
-        if (pos < a.out_nvalid) out[pos] = v[e];
+        if (FULL || pos < a.out_nvalid) out[pos] = v[e];
       }
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int pos = lane + 32 * e;
-        if (pos < a.out_nvalid) out[pos] = cscale(v[e], a.scale);
+        if (FULL || pos < a.out_nvalid) out[pos] = cscale(v[e], a.scale);
       }
     }
     __syncwarp();  // every lane has read the exchange buffer before the next line writes it
@@ -204,6 +205,7 @@ int launch_conv_r16(fusg_ctx* ctx, const WArgs& a, cudaStream_t s) {
                 : nw == 2 ? (tab ? warp_row_conv_r16<2, 6, true> : warp_row_conv_r16<2, 6, false>)
                 : nw == 3 ? (tab ? warp_row_conv_r16<3, 4, true> : warp_row_conv_r16<3, 4, false>)
                 : nw == 6 ? (tab ? warp_row_conv_r16<6, 2, true> : warp_row_conv_r16<6, 2, false>)
+                : (!tab && a.in_nvalid == 256 && a.out_nvalid == 256) ? warp_row_conv_r16<4, FUSG_PP_MINB, false, false, true>
                           : (tab ? warp_row_conv_r16<4, FUSG_PP_MINB, true> : warp_row_conv_r16<4, FUSG_PP_MINB, false>);
   const size_t smem = kl2 ? r16_smem_bytes<false>(4, true) : tab ? r16_smem_bytes<true>(nw) : r16_smem_bytes<false>(nw);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
