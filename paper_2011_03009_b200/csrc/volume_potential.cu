@@ -570,10 +570,10 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
     conv_line_coords(unsigned(line), a.ko, a.n_inner, mirror, ky, kx);
   };
   // staged position p lives at S[swz(p)] (PRUNED: p < L/2, so the swizzle stays inside S)
-  auto prefetch_in = [&](int64_t line) {
-    if (line < nlines) {
-      int ky, kx;
-      coords(line, ky, kx);
+  // (each line's (ky, kx) -- ~45 instructions of divisions -- is computed once, one line ahead, and
+  // serves both refills and the output row)
+  auto prefetch_in = [&](bool ok, int ky, int kx) {
+    if (ok) {
       const double2* in = a.in + ky * a.in_si + int64_t(kx) * a.in_sk;
       if constexpr (BULK) {
         if (lane == 0) bulk_stage(sb, in, unsigned(a.in_nvalid) * sizeof(double2), bars);
@@ -583,10 +583,8 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
     }
     if constexpr (!BULK) cp_async_commit();
   };
-  auto prefetch_k = [&](int64_t line) {
-    if (line < nlines) {
-      int ky, kx;
-      coords(line, ky, kx);
+  auto prefetch_k = [&](bool ok, int ky, int kx) {
+    if (ok) {
       const double2* kl = a.ko.line(ky, kx);
       if constexpr (BULK) {
         if (lane == 0) bulk_stage(kb, kl, HZ * sizeof(double2), bars + 1);
@@ -602,9 +600,14 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
   constexpr int kPin = PRUNED ? 1 : 0, kPout = PRUNED ? 2 : 0;
   const PrivEx ex{xb};
   int64_t line = int64_t(blockIdx.x) * kPPWarps + w;
-  prefetch_in(line);
-  prefetch_k(line);
+  int ky = 0, kx = 0;
+  if (line < nlines) coords(line, ky, kx);
+  prefetch_in(line < nlines, ky, kx);
+  prefetch_k(line < nlines, ky, kx);
   for (; line < nlines; line += stride) {
+    const bool more = line + stride < nlines;
+    int kyn = 0, kxn = 0;
+    if (more) coords(line + stride, kyn, kxn);
     if constexpr (BULK) {
       mbar_wait(bars, ph_in);  // this line's staged input has landed
       ph_in ^= 1;
@@ -620,7 +623,7 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
       v[e] = pos < a.in_nvalid ? sb[BULK ? pos : swz(pos)] : make_double2(0.0, 0.0);
     }
     __syncwarp();  // S consumed: refill it with the next line while this one is transformed
-    prefetch_in(line + stride);
+    prefetch_in(more, kyn, kxn);
     RegsIn vin{v};
     RegsOut mid{v};
     warp_fft<RL, LANES, false, kPin>(v, ex, lane, tw, vin, mid);
@@ -631,10 +634,10 @@ __global__ void __launch_bounds__(kPPWarps * 32, pp_min_blocks<RL::len()>()) war
 #pragma unroll
     for (int e = 0; e < E; ++e) v[e] = cmul(v[e], kb[fold_index(in_pos<RL, LANES, 0>(lane, e), L)]);
     __syncwarp();  // K^ row consumed
-    prefetch_k(line + stride);
-    int ky, kx;
-    coords(line, ky, kx);
+    prefetch_k(more, kyn, kxn);
     RowOut dst{a.out + ky * a.out_si + int64_t(kx) * a.out_sk, 1, a.out_nvalid, true, a.scale};
+    ky = kyn;
+    kx = kxn;
     warp_fft<RL, LANES, true, kPout>(v, ex, lane, tw, vin, dst);
   }
   if constexpr (!BULK) cp_async_wait0();
